@@ -1,0 +1,235 @@
+/*
+ * sd_abi.h — C ABI of the B200-native FastDecode decode hot path.
+ *
+ * Drop-in boundary for the reference `splitdecode` (FastDecode, arXiv
+ * 2403.11421) decode path. Plain pointers and sizes only; no C++ or torch
+ * types cross this boundary. Each entry point names the reference interface
+ * it replaces (file:line under the reference's proj/).
+ *
+ * Conventions
+ *   - Every function returns an int status (SD_OK == 0). On failure
+ *     sd_last_error() returns a thread-local message. Status numbering
+ *     follows the reference's wire error codes (transport.hpp:39-44):
+ *     3 malformed/ProtocolError, 4 CapacityError, 5 UnknownSequenceError,
+ *     6 internal; plus 7 std::logic_error, 8 ConfigError, 9 CUDA, 10 NCCL,
+ *     11 AdmissionError (scheduler.hpp:20-23).
+ *   - Activations are row-major float32 [rows][width]. Weights are passed in
+ *     the reference's storage: Eigen column-major (out x in), element w(j,k)
+ *     at w[k*out + j] (core.hpp:79-90).
+ *   - Functions without a `_dev` suffix take HOST pointers and are
+ *     synchronous (the reference's blocking semantics). `_dev` variants take
+ *     DEVICE pointers and enqueue on `stream` (a cudaStream_t; NULL = the
+ *     legacy default stream) without synchronizing.
+ *   - Validation (positions, capacity, unknown sequences, atomicity) runs on
+ *     the host against a mirror of per-(sequence, layer) stored lengths
+ *     before anything is launched, so error behaviour is the reference's.
+ *   - One handle is used from one host thread (the reference's ownership
+ *     model).
+ */
+#ifndef SD_ABI_H_
+#define SD_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define SD_ABI_VERSION 1
+
+enum sd_status {
+  SD_OK = 0,
+  SD_ERR_PROTOCOL = 3,
+  SD_ERR_CAPACITY = 4,
+  SD_ERR_UNKNOWN_SEQ = 5,
+  SD_ERR_INTERNAL = 6,
+  SD_ERR_LOGIC = 7,
+  SD_ERR_CONFIG = 8,
+  SD_ERR_CUDA = 9,
+  SD_ERR_NCCL = 10,
+  SD_ERR_ADMISSION = 11
+};
+
+/* KvFormat (attention.hpp:24) */
+enum sd_kv_format { SD_KV_SINGLE = 0, SD_KV_HALF = 1, SD_KV_INT8 = 2 };
+
+/* S-Part arithmetic (dense.hpp:16-20 fixes fp32, k-ascending). */
+enum sd_dense_mode {
+  SD_DENSE_EXACT_F32 = 0, /* CUDA-core fp32, the reference's per-element op order (bitwise) */
+  SD_DENSE_BF16 = 1,      /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
+  SD_DENSE_TF32 = 2       /* tcgen05 kind::tf32, fp32 operands, fp32 accumulate in TMEM */
+};
+
+/* ShardMode (transport.hpp:150-170) */
+enum sd_shard_mode { SD_SHARD_BY_SEQUENCE = 0, SD_SHARD_BY_HEAD = 1, SD_SHARD_HYBRID = 2 };
+
+/* ModelSpec (core.hpp:43-50); num_kv_heads is a GQA extension (0 = num_heads). */
+typedef struct sd_model_spec {
+  int32_t num_layers, model_dim, num_heads, head_dim, mlp_dim, vocab_size, num_kv_heads;
+} sd_model_spec;
+
+/* Physical KV store sizing (no reference counterpart: the reference grows
+ * std::vectors). All zero = defaults documented in DESIGN.md. */
+typedef struct sd_kv_options {
+  int32_t max_sequences;  /* live sequences (slots); 0 = min(capacity, 4096) */
+  int32_t max_seq_len;    /* positions per sequence; 0 = min(capacity, 32768) */
+  int32_t page_positions; /* positions per page group, power of two; 0 = 16 */
+  int32_t pool_pages;     /* page groups in the pool; 0 = ceil(cap/P) + max_sequences */
+} sd_kv_options;
+
+typedef struct sd_kv sd_kv;
+typedef struct sd_weights sd_weights;
+typedef struct sd_engine sd_engine;
+
+const char* sd_last_error(void);
+int sd_abi_version(void);
+/* make_model_spec (core.cpp:11-30) */
+int sd_make_model_spec(int num_layers, int model_dim, int num_heads, int mlp_dim,
+                       int vocab_size, int num_kv_heads, sd_model_spec* out);
+/* mix64 (core.cpp:161-166), prompt_token (core.cpp:168-171) */
+uint64_t sd_mix64(uint64_t x);
+int sd_prompt_token(uint64_t seed, uint64_t seq, int vocab_size);
+
+/* ---------------------------------------------------------------- R-Part
+ * KvShard (attention.hpp:68-140). head_start/head_count index kv heads. */
+/* KvShard::KvShard (attention.hpp:70-71) */
+int sd_kv_create(const sd_model_spec* spec, int head_start, int head_count,
+                 int64_t capacity_tokens, int kv_format, int device,
+                 const sd_kv_options* options, sd_kv** out);
+int sd_kv_destroy(sd_kv* kv);
+/* KvShard::append (attention.hpp:91-92): one (seq, layer) K/V row pair. */
+int sd_kv_append(sd_kv* kv, uint64_t seq, int layer, uint32_t position, const float* k,
+                 const float* v);
+/* KvShard::append_request (attention.hpp:96): all-or-nothing batch append.
+ * k, v: [n][width]. */
+int sd_kv_append_request(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs,
+                         const uint32_t* positions, const float* k, const float* v);
+/* KvShard::attend (attention.hpp:102): q, o: [n][q_width], outputs in item order. */
+int sd_kv_attend(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs, const float* q,
+                 float* o);
+/* Fused append_request + attend, the R-worker's QKV handler
+ * (workers.cpp:110-111; dense.cpp:111-112). */
+int sd_kv_append_attend(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs,
+                        const uint32_t* positions, const float* q, const float* k,
+                        const float* v, float* o);
+/* Device-pointer, stream-ordered variants of the three calls above. */
+int sd_kv_append_request_dev(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs,
+                             const uint32_t* positions, const float* k_dev,
+                             const float* v_dev, void* stream);
+int sd_kv_attend_dev(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs,
+                     const float* q_dev, float* o_dev, void* stream);
+int sd_kv_append_attend_dev(sd_kv* kv, int layer, int32_t n, const uint64_t* seqs,
+                            const uint32_t* positions, const float* q_dev,
+                            const float* k_dev, const float* v_dev, float* o_dev,
+                            void* stream);
+/* KvShard::drop_sequence (attention.hpp:106); unknown ids count a warning. */
+int sd_kv_drop(sd_kv* kv, int32_t n, const uint64_t* seqs);
+/* Queries (attention.hpp:73-111). */
+int sd_kv_stored_length(const sd_kv* kv, uint64_t seq, int layer, int32_t* out);
+int sd_kv_has_sequence(const sd_kv* kv, uint64_t seq, int32_t* out);
+int sd_kv_token_count(const sd_kv* kv, int64_t* out);
+int sd_kv_warning_count(const sd_kv* kv, int32_t* out);
+int sd_kv_bytes_per_token(const sd_kv* kv, int64_t* out);
+int sd_kv_width(const sd_kv* kv, int32_t* width, int32_t* q_width);
+/* Stored bytes of one lane (which: 0 = K, 1 = V) in the reference's
+ * [pos][head][d] order (attention.cpp:117-118) and, for int8, the per
+ * (pos, head) scales (attention.cpp:129-130). Returns the byte count (or a
+ * negative status); copies when host/scales are large enough. */
+int64_t sd_kv_export_lane(const sd_kv* kv, uint64_t seq, int layer, int which, void* host,
+                          size_t host_bytes, float* scales, size_t scales_count);
+/* Fills every (slot, layer, position < length) of the listed sequences
+ * with the counter-based synthetic values of SURVEY §8d (bench prefill).
+ * Registers the sequences with stored length `length` in every layer. */
+int sd_kv_prefill_synthetic(sd_kv* kv, int32_t n, const uint64_t* seqs, int32_t length,
+                            uint64_t salt);
+/* Per-launch timing of the attention kernel (CUDA events on the launching
+ * stream). enable != 0 starts recording; read returns the summed kernel
+ * milliseconds, launches and algorithmic bytes since the last reset. */
+int sd_kv_timing(sd_kv* kv, int enable);
+int sd_kv_timing_read(sd_kv* kv, double* ms, int64_t* launches, double* bytes, int reset);
+
+/* ---------------------------------------------------------------- S-Part
+ * WeightSet (core.hpp:85-90) uploaded once. tensors[] in reference order:
+ * embedding (D x V), then per layer w_q, w_k, w_v, w_o, w_mlp_in, w_mlp_out,
+ * then head (V x D); each Eigen column-major. */
+int sd_weights_upload(const sd_model_spec* spec, const float* const* tensors, int dense_mode,
+                      int device, sd_weights** out);
+/* Device-side seed_random_weights (core.cpp:97-127) is not offered: weights
+ * are generated on the host (mt19937 is sequential) and uploaded. */
+int sd_weights_destroy(sd_weights* w);
+/* project_qkv (dense.hpp:26-27): x [B][D] -> q [B][D], k, v [B][Hkv*hd]. */
+int sd_s_project_qkv(sd_weights* w, int layer, int32_t B, const float* x, float* q, float* k,
+                     float* v);
+/* finish_block (dense.hpp:31-32): x_out = y + silu(y W_in^T) W_out^T, y = o W_o^T + res. */
+int sd_s_finish_block(sd_weights* w, int layer, int32_t B, const float* o, const float* res,
+                      float* x_out);
+/* output_logits + argmax_token (dense.hpp:35-38); logits may be NULL. */
+int sd_s_logits_argmax(sd_weights* w, int32_t B, const float* x, float* logits,
+                       int32_t* tokens);
+/* apply_linear (dense.hpp:20) over an uploaded tensor (index as in
+ * sd_weights_upload, 1..6 per layer, 7 = head). */
+int sd_s_apply_linear(sd_weights* w, int layer, int which, int32_t B, const float* x, float* y);
+
+/* -------------------------------------------------------------- runtime
+ * The GPU StepComputation (workers.hpp:151-158): decode_step_monolithic
+ * (dense.cpp:90-129) with the KV store, S-Part and head on one device. */
+int sd_engine_create(sd_weights* w, sd_kv* kv, sd_engine** out);
+int sd_engine_destroy(sd_engine* e);
+/* StepComputation::compute: features = embedding columns of `tokens`
+ * (workers.cpp:629-638) for the batch rows `seqs`; writes next tokens and,
+ * when non-NULL, the final pre-head activations [B][D]. Host buffers,
+ * synchronous. */
+int sd_engine_step(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t* tokens,
+                   int32_t* next_tokens, float* final_x);
+/* Same with explicit features x [B][D] (TokenBatch.features). */
+int sd_engine_step_features(sd_engine* e, int32_t B, const uint64_t* seqs, const float* x,
+                            int32_t* next_tokens, float* final_x, float* logits);
+/* StepComputation::retire (workers.hpp:157). */
+int sd_engine_retire(sd_engine* e, int32_t n, const uint64_t* seqs);
+/* Device-timed step loop for the bench: runs `steps` decode steps over the
+ * resident batch (tokens fed back on device), returns device milliseconds. */
+int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t* tokens,
+                    int32_t steps, int32_t* next_tokens, double* device_ms);
+
+/* drive_schedule (workers.cpp:547-684) over the GPU engine. cold_start: 0
+ * fixed-interval, 1 ramped-limit (scheduler.hpp:99). steps <= 0 runs to
+ * completion. The transcript (step, seq, token) is returned through a
+ * result handle. */
+typedef struct sd_drive_config {
+  int32_t batch, target_len, interval, cold_start;
+  int64_t steps, load_limit;
+  uint64_t seed;
+  int32_t record_activations;
+} sd_drive_config;
+typedef struct sd_drive_result sd_drive_result;
+int sd_drive(sd_engine* e, const sd_drive_config* cfg, sd_drive_result** out);
+int64_t sd_drive_count(const sd_drive_result* r);
+int sd_drive_record(const sd_drive_result* r, int64_t i, int64_t* step, uint64_t* seq,
+                    int32_t* token);
+const float* sd_drive_activations(const sd_drive_result* r);
+double sd_drive_wall_seconds(const sd_drive_result* r);
+int sd_drive_destroy(sd_drive_result* r);
+
+/* ------------------------------------------------------- ShardMap, load
+ * ShardMap (transport.cpp:319-380). */
+int sd_shardmap_worker_for(int mode, int num_heads, int workers, uint64_t seq, int head,
+                           int32_t* out);
+int sd_shardmap_head_range(int mode, int num_heads, int workers, int worker, int32_t* start,
+                           int32_t* count);
+/* micro_batch_size / cold_start_schedule (scheduler.cpp:10-214):
+ * admissions as (step, size, target) triples. */
+int sd_micro_batch_size(int batch, int interval, int target_len, int32_t* out);
+int sd_cold_start_schedule(int batch, int target_len, int interval, int mode, int64_t horizon,
+                           int64_t* triples, int64_t capacity, int64_t* count);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* SD_ABI_H_ */

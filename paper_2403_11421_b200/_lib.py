@@ -1,0 +1,114 @@
+"""Loads libsd_b200.so (the C-ABI of include/sd_abi.h) and declares its
+signatures. There is no fallback: if the CUDA library is missing or cannot
+be loaded the import fails loudly."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsd_b200.so")
+
+
+class LibraryMissing(ImportError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise LibraryMissing(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(make -C paper_2403_11421_b200/csrc). There is no CPU fallback.")
+    return C.CDLL(LIB_PATH)
+
+
+lib = _load()
+
+
+class ModelSpec(C.Structure):
+    """ModelSpec (core.hpp:43-50) + num_kv_heads (GQA extension)."""
+    _fields_ = [(n, C.c_int32) for n in ("num_layers", "model_dim", "num_heads", "head_dim",
+                                          "mlp_dim", "vocab_size", "num_kv_heads")]
+
+    def __repr__(self):
+        return ("ModelSpec(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")")
+
+
+class KvOptions(C.Structure):
+    _fields_ = [("max_sequences", C.c_int32), ("max_seq_len", C.c_int32),
+                ("page_positions", C.c_int32), ("pool_pages", C.c_int32)]
+
+
+class DriveConfig(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("target_len", C.c_int32), ("interval", C.c_int32),
+                ("cold_start", C.c_int32), ("steps", C.c_int64), ("load_limit", C.c_int64),
+                ("seed", C.c_uint64), ("record_activations", C.c_int32)]
+
+
+P = C.c_void_p
+PP = C.POINTER(C.c_void_p)
+FP = C.POINTER(C.c_float)
+U64P = C.POINTER(C.c_uint64)
+U32P = C.POINTER(C.c_uint32)
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+DP = C.POINTER(C.c_double)
+SPEC_P = C.POINTER(ModelSpec)
+
+SIGNATURES = {
+    "sd_last_error": (C.c_char_p, []),
+    "sd_abi_version": (C.c_int, []),
+    "sd_make_model_spec": (C.c_int, [C.c_int] * 6 + [SPEC_P]),
+    "sd_mix64": (C.c_uint64, [C.c_uint64]),
+    "sd_prompt_token": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int]),
+    "sd_kv_create": (C.c_int, [SPEC_P, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int,
+                               C.POINTER(KvOptions), PP]),
+    "sd_kv_destroy": (C.c_int, [P]),
+    "sd_kv_append": (C.c_int, [P, C.c_uint64, C.c_int, C.c_uint32, FP, FP]),
+    "sd_kv_append_request": (C.c_int, [P, C.c_int, C.c_int32, U64P, U32P, FP, FP]),
+    "sd_kv_attend": (C.c_int, [P, C.c_int, C.c_int32, U64P, FP, FP]),
+    "sd_kv_append_attend": (C.c_int, [P, C.c_int, C.c_int32, U64P, U32P, FP, FP, FP, FP]),
+    "sd_kv_append_request_dev": (C.c_int, [P, C.c_int, C.c_int32, U64P, U32P, P, P, P]),
+    "sd_kv_attend_dev": (C.c_int, [P, C.c_int, C.c_int32, U64P, P, P, P]),
+    "sd_kv_append_attend_dev": (C.c_int, [P, C.c_int, C.c_int32, U64P, U32P, P, P, P, P, P]),
+    "sd_kv_drop": (C.c_int, [P, C.c_int32, U64P]),
+    "sd_kv_stored_length": (C.c_int, [P, C.c_uint64, C.c_int, I32P]),
+    "sd_kv_has_sequence": (C.c_int, [P, C.c_uint64, I32P]),
+    "sd_kv_token_count": (C.c_int, [P, I64P]),
+    "sd_kv_warning_count": (C.c_int, [P, I32P]),
+    "sd_kv_bytes_per_token": (C.c_int, [P, I64P]),
+    "sd_kv_width": (C.c_int, [P, I32P, I32P]),
+    "sd_kv_export_lane": (C.c_int64, [P, C.c_uint64, C.c_int, C.c_int, P, C.c_size_t, FP,
+                                      C.c_size_t]),
+    "sd_kv_prefill_synthetic": (C.c_int, [P, C.c_int32, U64P, C.c_int32, C.c_uint64]),
+    "sd_kv_timing": (C.c_int, [P, C.c_int]),
+    "sd_kv_timing_read": (C.c_int, [P, DP, I64P, DP, C.c_int]),
+    "sd_weights_upload": (C.c_int, [SPEC_P, C.POINTER(FP), C.c_int, C.c_int, PP]),
+    "sd_weights_destroy": (C.c_int, [P]),
+    "sd_s_project_qkv": (C.c_int, [P, C.c_int, C.c_int32, FP, FP, FP, FP]),
+    "sd_s_finish_block": (C.c_int, [P, C.c_int, C.c_int32, FP, FP, FP]),
+    "sd_s_logits_argmax": (C.c_int, [P, C.c_int32, FP, FP, I32P]),
+    "sd_s_apply_linear": (C.c_int, [P, C.c_int, C.c_int, C.c_int32, FP, FP]),
+    "sd_engine_create": (C.c_int, [P, P, PP]),
+    "sd_engine_destroy": (C.c_int, [P]),
+    "sd_engine_step": (C.c_int, [P, C.c_int32, U64P, I32P, I32P, FP]),
+    "sd_engine_step_features": (C.c_int, [P, C.c_int32, U64P, FP, I32P, FP, FP]),
+    "sd_engine_retire": (C.c_int, [P, C.c_int32, U64P]),
+    "sd_engine_bench": (C.c_int, [P, C.c_int32, U64P, I32P, C.c_int32, I32P, DP]),
+    "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
+    "sd_drive_count": (C.c_int64, [P]),
+    "sd_drive_record": (C.c_int, [P, C.c_int64, I64P, U64P, I32P]),
+    "sd_drive_activations": (FP, [P]),
+    "sd_drive_wall_seconds": (C.c_double, [P]),
+    "sd_drive_destroy": (C.c_int, [P]),
+    "sd_shardmap_worker_for": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, I32P]),
+    "sd_shardmap_head_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, I32P, I32P]),
+    "sd_micro_batch_size": (C.c_int, [C.c_int, C.c_int, C.c_int, I32P]),
+    "sd_cold_start_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, I64P,
+                                         C.c_int64, I64P]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _f = getattr(lib, _name)  # AttributeError = the .so lacks an ABI symbol: fail loudly
+    _f.restype = _res
+    _f.argtypes = _args

@@ -1,0 +1,462 @@
+"""Host-side mirror of the reference `splitdecode` hot-path interfaces over
+the C-ABI (include/sd_abi.h). Names, argument meaning and error types follow
+the reference:
+
+  KvShard            attention.hpp:68-140   (R-Part worker interface)
+  project_qkv ...    dense.hpp:20-50        (S-Part step interface)
+  Engine             workers.hpp:151-158    (StepComputation on the GPU)
+  run_generation     workers.cpp:547-701    (drive_schedule over the engine)
+  ShardMap           transport.hpp:150-170
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from ._lib import (DriveConfig, FP, I32P, I64P, KvOptions, ModelSpec, U32P, U64P, lib)
+
+# ------------------------------------------------------------------ errors
+class SplitDecodeError(RuntimeError):
+    code = 6
+
+
+class ConfigError(SplitDecodeError):       # core.hpp:25-28
+    code = 8
+
+
+class ProtocolError(SplitDecodeError):     # core.hpp:30-33
+    code = 3
+
+
+class UnknownSequenceError(ProtocolError):  # attention.hpp:19-22
+    code = 5
+
+
+class CapacityError(SplitDecodeError):     # core.hpp:35-38
+    code = 4
+
+
+class LogicError(SplitDecodeError):        # std::logic_error
+    code = 7
+
+
+class AdmissionError(SplitDecodeError):    # scheduler.hpp:20-23
+    code = 11
+
+
+class CudaError(SplitDecodeError):
+    code = 9
+
+
+_BY_CODE = {c.code: c for c in (ConfigError, ProtocolError, UnknownSequenceError, CapacityError,
+                                LogicError, AdmissionError, CudaError)}
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib.sd_last_error().decode()
+        raise _BY_CODE.get(rc, SplitDecodeError)(msg)
+
+
+FORMATS = {"single": 0, "half": 1, "int8": 2}
+DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2}
+SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2}
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _fp(a: np.ndarray):
+    return a.ctypes.data_as(FP)
+
+
+def _u64(seqs):
+    a = np.ascontiguousarray(seqs, dtype=np.uint64)
+    return a, a.ctypes.data_as(U64P)
+
+
+# -------------------------------------------------------------------- core
+def make_model_spec(num_layers: int, model_dim: int, num_heads: int, mlp_dim: int,
+                    vocab_size: int, num_kv_heads: int = 0) -> ModelSpec:
+    """make_model_spec (core.cpp:11-30)."""
+    s = ModelSpec()
+    _check(lib.sd_make_model_spec(num_layers, model_dim, num_heads, mlp_dim, vocab_size,
+                                  num_kv_heads, C.byref(s)))
+    return s
+
+
+def mix64(x: int) -> int:
+    return int(lib.sd_mix64(x & (2**64 - 1)))
+
+
+def prompt_token(seed: int, seq: int, vocab_size: int) -> int:
+    return int(lib.sd_prompt_token(seed, seq, vocab_size))
+
+
+# ------------------------------------------------------------------ R-Part
+@dataclass
+class AttentionItem:
+    """AttentionItem (attention.hpp:44-48)."""
+    seq: int
+    position: int
+    q: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+
+
+@dataclass
+class AttentionRequest:
+    """AttentionRequest (attention.hpp:50-53)."""
+    layer: int = 0
+    items: list = field(default_factory=list)
+
+
+class KvShard:
+    """KvShard (attention.hpp:68-140) on a B200: paged HBM KV store plus the
+    split-K decode-attention kernel. head_start / head_count index kv heads."""
+
+    def __init__(self, spec: ModelSpec, head_start: int, head_count: int, capacity_tokens: int,
+                 fmt: str = "single", device: int = 0, max_sequences: int = 0,
+                 max_seq_len: int = 0, page_positions: int = 0, pool_pages: int = 0):
+        self.spec = spec
+        self.h = C.c_void_p()
+        opts = KvOptions(max_sequences, max_seq_len, page_positions, pool_pages)
+        _check(lib.sd_kv_create(C.byref(spec), head_start, head_count, capacity_tokens,
+                                FORMATS[fmt], device, C.byref(opts), C.byref(self.h)))
+        w, qw = C.c_int32(), C.c_int32()
+        _check(lib.sd_kv_width(self.h, C.byref(w), C.byref(qw)))
+        self._width, self.q_width = w.value, qw.value
+        self._fmt = fmt
+        self._head_start, self._head_count = head_start, head_count
+        self._capacity = capacity_tokens
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sd_kv_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # queries (attention.hpp:73-111)
+    def head_start(self): return self._head_start
+    def head_count(self): return self._head_count
+    def width(self): return self._width
+    def format(self): return self._fmt
+    def capacity(self): return self._capacity
+
+    def token_count(self) -> int:
+        out = C.c_int64()
+        _check(lib.sd_kv_token_count(self.h, C.byref(out)))
+        return out.value
+
+    def has_sequence(self, seq: int) -> bool:
+        out = C.c_int32()
+        _check(lib.sd_kv_has_sequence(self.h, seq, C.byref(out)))
+        return bool(out.value)
+
+    def stored_length(self, seq: int, layer: int) -> int:
+        out = C.c_int32()
+        _check(lib.sd_kv_stored_length(self.h, seq, layer, C.byref(out)))
+        return out.value
+
+    def warning_count(self) -> int:
+        out = C.c_int32()
+        _check(lib.sd_kv_warning_count(self.h, C.byref(out)))
+        return out.value
+
+    def bytes_per_token(self) -> int:
+        out = C.c_int64()
+        _check(lib.sd_kv_bytes_per_token(self.h, C.byref(out)))
+        return out.value
+
+    # operations
+    def append(self, seq: int, layer: int, position: int, k, v):
+        """KvShard::append (attention.hpp:91-92)."""
+        k, v = _f32(k), _f32(v)
+        if k.size != self._width or v.size != self._width:
+            raise ProtocolError("append: K/V width does not match the shard's head range")
+        _check(lib.sd_kv_append(self.h, seq, layer, position, _fp(k), _fp(v)))
+
+    def append_request(self, request_or_layer, seqs=None, positions=None, k=None, v=None):
+        """KvShard::append_request (attention.hpp:96). Accepts an
+        AttentionRequest or (layer, seqs, positions, k[n,w], v[n,w])."""
+        layer, seqs, positions, k, v = self._unpack(request_or_layer, seqs, positions, k, v)
+        s, sp = _u64(seqs)
+        pos = np.ascontiguousarray(positions, dtype=np.uint32)
+        k, v = _f32(k).reshape(len(s), -1), _f32(v).reshape(len(s), -1)
+        if len(s) and (k.shape[1] != self._width or v.shape[1] != self._width):
+            raise ProtocolError("append: K/V width does not match the shard's head range")
+        _check(lib.sd_kv_append_request(self.h, layer, len(s), sp, pos.ctypes.data_as(U32P),
+                                        _fp(k), _fp(v)))
+
+    def attend(self, request_or_layer, seqs=None, q=None) -> np.ndarray:
+        """KvShard::attend (attention.hpp:102); returns O rows in item order."""
+        if isinstance(request_or_layer, AttentionRequest):
+            r = request_or_layer
+            layer, seqs = r.layer, [it.seq for it in r.items]
+            q = np.stack([_f32(it.q) for it in r.items]) if r.items else np.zeros((0, self.q_width))
+        else:
+            layer = request_or_layer
+        s, sp = _u64(seqs)
+        q = _f32(q).reshape(len(s), -1)
+        if len(s) and q.shape[1] != self.q_width:
+            raise ProtocolError("attend: Q width does not match the shard's head range")
+        o = np.zeros((len(s), self.q_width), dtype=np.float32)
+        _check(lib.sd_kv_attend(self.h, layer, len(s), sp, _fp(q), _fp(o)))
+        return o
+
+    def append_attend(self, layer, seqs, positions, q, k, v) -> np.ndarray:
+        """append_request + attend, the R-worker QKV handler (workers.cpp:110-111)."""
+        s, sp = _u64(seqs)
+        pos = np.ascontiguousarray(positions, dtype=np.uint32)
+        q, k, v = (_f32(a).reshape(len(s), -1) for a in (q, k, v))
+        o = np.zeros((len(s), self.q_width), dtype=np.float32)
+        _check(lib.sd_kv_append_attend(self.h, layer, len(s), sp, pos.ctypes.data_as(U32P),
+                                       _fp(q), _fp(k), _fp(v), _fp(o)))
+        return o
+
+    def append_attend_dev(self, layer, seqs, positions, q_ptr, k_ptr, v_ptr, o_ptr, stream=0):
+        """Device-pointer variant (e.g. torch CUDA tensors' data_ptr())."""
+        s, sp = _u64(seqs)
+        pos = np.ascontiguousarray(positions, dtype=np.uint32)
+        _check(lib.sd_kv_append_attend_dev(self.h, layer, len(s), sp, pos.ctypes.data_as(U32P),
+                                           q_ptr, k_ptr, v_ptr, o_ptr, stream))
+
+    def attend_dev(self, layer, seqs, q_ptr, o_ptr, stream=0):
+        s, sp = _u64(seqs)
+        _check(lib.sd_kv_attend_dev(self.h, layer, len(s), sp, q_ptr, o_ptr, stream))
+
+    def drop_sequence(self, seq: int):
+        """KvShard::drop_sequence (attention.hpp:106)."""
+        s, sp = _u64([seq])
+        _check(lib.sd_kv_drop(self.h, 1, sp))
+
+    def export_lane(self, seq: int, layer: int, which: int):
+        """Stored bytes of lane K (0) / V (1) in the reference [pos][head][d]
+        order, plus int8 scales [pos][head]."""
+        n = lib.sd_kv_export_lane(self.h, seq, layer, which, None, 0, None, 0)
+        if n < 0:
+            _check(int(-n))
+        buf = np.zeros(n, dtype=np.uint8)
+        L = self.stored_length(seq, layer)
+        sc = np.zeros(L * self._head_count, np.float32) if self._fmt == "int8" else None
+        r = lib.sd_kv_export_lane(self.h, seq, layer, which, buf.ctypes.data_as(C.c_void_p), n,
+                                  _fp(sc) if sc is not None else None,
+                                  sc.size if sc is not None else 0)
+        if r < 0:
+            _check(int(-r))
+        return buf, sc
+
+    def prefill_synthetic(self, seqs, length: int, salt: int = 0):
+        s, sp = _u64(seqs)
+        _check(lib.sd_kv_prefill_synthetic(self.h, len(s), sp, length, salt))
+
+    def timing(self, enable: bool):
+        _check(lib.sd_kv_timing(self.h, int(enable)))
+
+    def timing_read(self, reset=True):
+        ms, n, b = C.c_double(), C.c_int64(), C.c_double()
+        _check(lib.sd_kv_timing_read(self.h, C.byref(ms), C.byref(n), C.byref(b), int(reset)))
+        return ms.value, n.value, b.value
+
+    @staticmethod
+    def _unpack(r, seqs, positions, k, v):
+        if isinstance(r, AttentionRequest):
+            items = r.items
+            return (r.layer, [it.seq for it in items], [it.position for it in items],
+                    np.stack([_f32(it.k) for it in items]) if items else np.zeros((0, 1), np.float32),
+                    np.stack([_f32(it.v) for it in items]) if items else np.zeros((0, 1), np.float32))
+        return r, seqs, positions, k, v
+
+
+# ------------------------------------------------------------------ S-Part
+class DeviceWeights:
+    """WeightSet (core.hpp:85-90) uploaded to a device. `tensors` follow the
+    reference storage: [embedding (D x V), per layer w_q, w_k, w_v, w_o,
+    w_mlp_in, w_mlp_out, head (V x D)], each a flat column-major buffer.
+    tensors=None generates synthetic weights on the device."""
+
+    def __init__(self, spec: ModelSpec, tensors: Sequence[np.ndarray] | None, mode: str = "exact",
+                 device: int = 0):
+        self.spec = spec
+        self.mode = mode
+        self.h = C.c_void_p()
+        if tensors is None:
+            _check(lib.sd_weights_upload(C.byref(spec), None, DENSE_MODES[mode], device,
+                                         C.byref(self.h)))
+        else:
+            self._keep = [_f32(t).reshape(-1) for t in tensors]
+            arr = (FP * len(self._keep))(*[_fp(t) for t in self._keep])
+            _check(lib.sd_weights_upload(C.byref(spec), arr, DENSE_MODES[mode], device,
+                                         C.byref(self.h)))
+            self._keep = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sd_weights_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+def project_qkv(w: DeviceWeights, layer: int, x):
+    """project_qkv (dense.hpp:26-27) -> (q, k, v)."""
+    x = _f32(x)
+    B = x.shape[0]
+    s = w.spec
+    kvw = s.num_kv_heads * s.head_dim
+    q = np.zeros((B, s.model_dim), np.float32)
+    k = np.zeros((B, kvw), np.float32)
+    v = np.zeros((B, kvw), np.float32)
+    _check(lib.sd_s_project_qkv(w.h, layer, B, _fp(x), _fp(q), _fp(k), _fp(v)))
+    return q, k, v
+
+
+def finish_block(w: DeviceWeights, layer: int, o, residual):
+    """finish_block (dense.hpp:31-32)."""
+    o, r = _f32(o), _f32(residual)
+    out = np.zeros_like(r)
+    _check(lib.sd_s_finish_block(w.h, layer, o.shape[0], _fp(o), _fp(r), _fp(out)))
+    return out
+
+
+def output_logits_argmax(w: DeviceWeights, x):
+    """output_logits + argmax_token (dense.hpp:35-38) -> (logits, tokens)."""
+    x = _f32(x)
+    B = x.shape[0]
+    lg = np.zeros((B, w.spec.vocab_size), np.float32)
+    tk = np.zeros(B, np.int32)
+    _check(lib.sd_s_logits_argmax(w.h, B, _fp(x), _fp(lg), tk.ctypes.data_as(I32P)))
+    return lg, tk
+
+
+def apply_linear(w: DeviceWeights, layer: int, which: int, x):
+    """apply_linear (dense.hpp:20) over uploaded tensor `which`."""
+    x = _f32(x)
+    outs = {1: w.spec.model_dim, 2: w.spec.num_kv_heads * w.spec.head_dim,
+            3: w.spec.num_kv_heads * w.spec.head_dim, 4: w.spec.model_dim, 5: w.spec.mlp_dim,
+            6: w.spec.model_dim, 7: w.spec.vocab_size}
+    y = np.zeros((x.shape[0], outs[which]), np.float32)
+    _check(lib.sd_s_apply_linear(w.h, layer, which, x.shape[0], _fp(x), _fp(y)))
+    return y
+
+
+# ----------------------------------------------------------------- runtime
+class Engine:
+    """The GPU StepComputation (workers.hpp:151-158)."""
+
+    def __init__(self, weights: DeviceWeights, kv: KvShard):
+        self.weights, self.kv = weights, kv
+        self.h = C.c_void_p()
+        _check(lib.sd_engine_create(weights.h, kv.h, C.byref(self.h)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sd_engine_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def compute(self, seqs, tokens=None, features=None, want_final=False, want_logits=False):
+        """StepComputation::compute -> DecodeStepResult(next_tokens, final_activations)."""
+        s, sp = _u64(seqs)
+        B = len(s)
+        nxt = np.zeros(B, np.int32)
+        fx = np.zeros((B, self.weights.spec.model_dim), np.float32) if want_final else None
+        if features is not None:
+            x = _f32(features)
+            lg = np.zeros((B, self.weights.spec.vocab_size), np.float32) if want_logits else None
+            _check(lib.sd_engine_step_features(self.h, B, sp, _fp(x), nxt.ctypes.data_as(I32P),
+                                               _fp(fx) if fx is not None else None,
+                                               _fp(lg) if lg is not None else None))
+            return nxt, fx, lg
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        _check(lib.sd_engine_step(self.h, B, sp, t.ctypes.data_as(I32P), nxt.ctypes.data_as(I32P),
+                                  _fp(fx) if fx is not None else None))
+        return nxt, fx
+
+    def retire(self, seqs):
+        s, sp = _u64(seqs)
+        _check(lib.sd_engine_retire(self.h, len(s), sp))
+
+    def bench(self, seqs, tokens, steps: int):
+        """Device-timed loop of `steps` decode steps; returns (ms, next_tokens)."""
+        s, sp = _u64(seqs)
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        nxt = np.zeros(len(s), np.int32)
+        ms = C.c_double()
+        _check(lib.sd_engine_bench(self.h, len(s), sp, t.ctypes.data_as(I32P), steps,
+                                   nxt.ctypes.data_as(I32P), C.byref(ms)))
+        return ms.value, nxt
+
+
+def run_generation(engine: Engine, batch: int, target_len: int, interval: int, steps: int,
+                   seed: int = 0, cold_start: str = "fixed-interval", load_limit: int = 0,
+                   record_activations: bool = False):
+    """drive_schedule (workers.cpp:547-684) over the GPU engine ->
+    (transcript [(step, seq, token)], activations, wall_seconds)."""
+    cfg = DriveConfig(batch, target_len, interval,
+                      {"fixed-interval": 0, "ramped-limit": 1}[cold_start], steps, load_limit,
+                      seed, int(record_activations))
+    h = C.c_void_p()
+    _check(lib.sd_drive(engine.h, C.byref(cfg), C.byref(h)))
+    try:
+        n = lib.sd_drive_count(h)
+        st, sq, tk = C.c_int64(), C.c_uint64(), C.c_int32()
+        recs = []
+        for i in range(n):
+            _check(lib.sd_drive_record(h, i, C.byref(st), C.byref(sq), C.byref(tk)))
+            recs.append((st.value, sq.value, tk.value))
+        acts = None
+        if record_activations and n:
+            p = lib.sd_drive_activations(h)
+            acts = np.ctypeslib.as_array(p, shape=(n * engine.weights.spec.model_dim,)).reshape(n, -1).copy()
+        return recs, acts, lib.sd_drive_wall_seconds(h)
+    finally:
+        lib.sd_drive_destroy(h)
+
+
+def transcript_csv(recs) -> str:
+    """transcript_csv (workers.cpp:746-755)."""
+    return "step,seq_id,token_id\n" + "".join(f"{s},{q},{t}\n" for s, q, t in recs)
+
+
+# ---------------------------------------------------------------- ShardMap
+class ShardMap:
+    """ShardMap (transport.hpp:150-170)."""
+
+    def __init__(self, mode: str, num_heads: int, workers: int):
+        self.mode, self.num_heads, self.workers = SHARD_MODES[mode], num_heads, workers
+        self.head_range(0)  # validates
+
+    def worker_for(self, seq: int, head: int) -> int:
+        out = C.c_int32()
+        _check(lib.sd_shardmap_worker_for(self.mode, self.num_heads, self.workers, seq, head,
+                                          C.byref(out)))
+        return out.value
+
+    def head_range(self, worker: int):
+        a, b = C.c_int32(), C.c_int32()
+        _check(lib.sd_shardmap_head_range(self.mode, self.num_heads, self.workers, worker,
+                                          C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+def micro_batch_size(batch: int, interval: int, target_len: int) -> int:
+    out = C.c_int32()
+    _check(lib.sd_micro_batch_size(batch, interval, target_len, C.byref(out)))
+    return out.value
+
+
+def cold_start_schedule(batch, target_len, interval, mode="fixed-interval", horizon=0):
+    m = {"fixed-interval": 0, "ramped-limit": 1}[mode]
+    n = C.c_int64()
+    cap = horizon + 2
+    buf = np.zeros(3 * cap, np.int64)
+    _check(lib.sd_cold_start_schedule(batch, target_len, interval, m, horizon,
+                                      buf.ctypes.data_as(I64P), cap, C.byref(n)))
+    return [tuple(int(x) for x in buf[3 * i:3 * i + 3]) for i in range(n.value)]

@@ -1,0 +1,55 @@
+// S-Part device interfaces (dense_kernels.cu, gemm_sm100.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sd {
+
+enum Epilogue : int {
+  kEpiNone = 0,      // y = acc
+  kEpiResidual = 1,  // y = acc + res          (finish_block's `y += residual`, dense.cpp:60)
+  kEpiSilu = 2,      // y = silu(acc)          (dense.cpp:47-49, 63-65)
+};
+
+// K7: out[b][j] = sum_k w(j,k) * x[b][k] with the reference's per-element
+// operation order (k ascending, one accumulator, multiply then add, no FMA;
+// dense.cpp:16-31). w is the reference storage: w(j,k) at w[k*ldw + j].
+void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, const float* w,
+                         int64_t ldw, float* y, int64_t ldy, int epi, const float* res,
+                         int64_t ldr, cudaStream_t s);
+// x[b][:] = embedding(:, tokens[b]); embedding is D x V column-major.
+void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
+                  __nv_bfloat16* xb, cudaStream_t s);
+// argmax_token per row (first index wins ties, dense.cpp:78-88)
+void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
+                   cudaStream_t s);
+// fp32 -> bf16 copy (activation staging for the tensor-core GEMMs)
+void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat16* y,
+                    int64_t ldy, cudaStream_t s);
+
+// tcgen05 GEMM: C[M][N] = A[M][K] . B[N][K]^T with fused epilogue; A, B
+// K-major (bf16 for kind::f16, fp32 bits for kind::tf32). Writes fp32 C and,
+// if cb != nullptr, a bf16 copy for the next GEMM's A operand.
+struct GemmArgs {
+  int M, N, K;
+  const void* A;
+  int64_t lda;  // elements
+  const void* B;
+  int64_t ldb;
+  float* C;
+  int64_t ldc;
+  __nv_bfloat16* Cb;
+  int64_t ldcb;
+  int epi;
+  const float* res;
+  int64_t ldr;
+  int kind;  // 1 = bf16 (kind::f16), 2 = tf32
+};
+bool gemm_sm100_supported(const GemmArgs& g);
+void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);
+// argmax over rows of C fused as a second pass (kept separate: logits stay in HBM for callers)
+
+}  // namespace sd

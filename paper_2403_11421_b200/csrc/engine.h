@@ -1,0 +1,140 @@
+// S-Part weights, the GPU StepComputation (engine) and the host scheduler.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <unordered_map>
+#include <vector>
+
+#include "dense_kernels.cuh"
+#include "kv_store.h"
+#include "sd_common.h"
+
+namespace sd {
+
+// WeightSet on the device (core.hpp:79-90). Exact mode keeps the reference
+// storage W^T = [in][out] fp32; tensor-core modes keep W = [out][in]
+// (K-major) in bf16 (kind::f16) or fp32 (kind::tf32). Q/K/V are fused into
+// one [qkv_width] output projection; the per-element arithmetic is unchanged.
+class Weights {
+ public:
+  Weights(const Spec& spec, const float* const* tensors, int mode, int device);
+  // Counter-based synthetic weights of the same distribution (uniform
+  // +-1/sqrt(fan_in)); generated on device for the full-size benchmark.
+  Weights(const Spec& spec, int mode, uint64_t seed, int device);
+  ~Weights();
+  Weights(const Weights&) = delete;
+  Weights& operator=(const Weights&) = delete;
+
+  const Spec& spec() const { return spec_; }
+  int mode() const { return mode_; }
+  int device() const { return device_; }
+
+  // y[B][out] = x . W^T (+ epilogue). which: 0 = qkv (fused), 4 = w_o,
+  // 5 = w_mlp_in, 6 = w_mlp_out, 7 = head, 1/2/3 = q/k/v slices.
+  // x_bf16 is required in BF16 mode (A operand), ignored otherwise.
+  void linear(int layer, int which, int B, const float* x, int64_t ldx,
+              const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
+              int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s) const;
+  const float* embedding() const { return emb_; }
+  int out_dim(int which) const;
+  int in_dim(int which) const;
+
+ private:
+  void alloc();
+  const void* tensor(int layer, int which) const;
+
+  Spec spec_;
+  int mode_, device_;
+  float* emb_ = nullptr;        // D x V column-major ([V][D])
+  void* blob_ = nullptr;        // all layer tensors + head
+  std::vector<size_t> off_;     // per (layer, which) byte offsets
+  size_t head_off_ = 0;
+};
+
+// The GPU StepComputation (workers.hpp:151-158): decode_step_monolithic
+// (dense.cpp:90-129) with the S-Part on tensor cores / CUDA cores and the
+// R-Part on the KvStore, all on one device stream.
+class Engine {
+ public:
+  Engine(Weights* w, KvStore* kv);
+  ~Engine();
+  // features from token ids (workers.cpp:629-638) or explicit [B][D]
+  void step(int B, const uint64_t* seqs, const int32_t* tokens_host, const float* x_host,
+            int32_t* next_host, float* final_host, float* logits_host);
+  void retire(int n, const uint64_t* seqs);
+  double bench(int B, const uint64_t* seqs, const int32_t* tokens_host, int steps,
+               int32_t* next_host);
+  cudaStream_t stream() const { return stream_; }
+  // device-resident step: tokens_dev -> next_dev (no host sync)
+  void step_device(int B, const uint64_t* seqs, const int32_t* tokens_dev, int32_t* next_dev);
+  int launches_per_step() const { return launches_per_step_; }
+
+ private:
+  void ensure(int B);
+  void run_layers(int B, const uint64_t* seqs);
+
+  Weights* w_;
+  KvStore* kv_;
+  cudaStream_t stream_ = nullptr;
+  int cap_B_ = 0;
+  float *x_ = nullptr, *qkv_ = nullptr, *o_ = nullptr, *y_ = nullptr, *h_ = nullptr,
+        *logits_ = nullptr;
+  __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
+  int32_t* tok_ = nullptr;
+  std::vector<uint32_t> pos_;
+  int launches_per_step_ = 0;
+};
+
+// ---- scheduler (scheduler.cpp:10-236), kept in host C++
+int micro_batch_size(int batch, int interval, int target_len);
+struct Admission {
+  int64_t step;
+  int size, target;
+};
+std::vector<Admission> cold_start_schedule(int batch, int target_len, int interval, int mode,
+                                           int64_t horizon);
+class LoadTracker {
+ public:
+  explicit LoadTracker(int64_t limit);
+  int add(int64_t start, int size, int target);
+  struct Plan {
+    int64_t step = 0, total_load = 0;
+    std::vector<int> active_ids, ending;
+  };
+  Plan step();
+  int64_t earliest_start(int size, int target) const;
+  int64_t current() const { return cur_; }
+  void set_limit(int64_t l) {
+    if (l < 1) fail(SD_ERR_ADMISSION, "load limit must be >= 1");
+    limit_ = l;
+  }
+
+ private:
+  struct MB {
+    int id, size;
+    int64_t start, end;
+  };
+  int64_t limit_, cur_ = 0;
+  int next_id_ = 0;
+  std::vector<MB> b_;
+  std::vector<int64_t> w_;
+};
+
+// ShardMap (transport.cpp:319-380)
+int shard_worker_for(int mode, int heads, int workers, uint64_t seq, int head);
+std::pair<int, int> shard_head_range(int mode, int heads, int workers, int worker);
+
+// drive_schedule (workers.cpp:547-684) over the engine
+struct DriveResult {
+  std::vector<int64_t> steps;
+  std::vector<uint64_t> seqs;
+  std::vector<int32_t> tokens;
+  std::vector<float> activations;
+  double wall_seconds = 0;
+};
+DriveResult drive(Engine& e, const Weights& w, const sd_drive_config& c);
+
+}  // namespace sd

@@ -1,0 +1,709 @@
+// R-Part kernels for sm_100a: in-place KV append (K1), split-K flash-decode
+// attention streaming the paged KV pool through a TMA bulk-copy / mbarrier
+// pipeline (K2), and the deterministic split combine (K3).
+//
+// Semantics follow KvShard::append_lane / attend (reference
+// proj/src/attention.cpp:91-112, 204-282): scores are scaled dot products
+// over every stored position including the current token, softmax is taken
+// over all of them, all arithmetic is fp32 regardless of the storage format
+// (fp32 | fp16 RNE | int8 with per-(position, head) scale).
+#include <cuda_fp16.h>
+
+#include <cfloat>
+#include <cmath>
+
+#include "kv_kernels.cuh"
+#include "sd_common.h"
+
+namespace sd {
+
+namespace {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// TMA bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <int FMT>
+struct Fmt;
+template <>
+struct Fmt<SD_KV_SINGLE> {
+  static constexpr int kBytes = 4;
+  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 16);
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+};
+template <>
+struct Fmt<SD_KV_HALF> {
+  static constexpr int kBytes = 2;
+  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+    const uint4 r = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h;
+      *reinterpret_cast<uint32_t*>(&h) = w[i];
+      const float2 f = __half22float2(h);
+      x[2 * i] = f.x;
+      x[2 * i + 1] = f.y;
+    }
+  }
+};
+template <>
+struct Fmt<SD_KV_INT8> {
+  static constexpr int kBytes = 1;
+  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = static_cast<float>(static_cast<int8_t>(r.x >> (8 * i)));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[4 + i] = static_cast<float>(static_cast<int8_t>(r.y >> (8 * i)));
+  }
+};
+
+// --------------------------------------------------------------- K2 ------
+// Persistent split-K decode attention. One CTA per SM walks a contiguous,
+// balanced range of (item, position) pieces (host-built). Warp
+// kConsumerWarps is the producer: one lane streams T-position stages of the
+// item's K and V rows (all shard heads, contiguous inside a page group) into
+// an nstages-deep shared-memory ring with cp.async.bulk + mbarriers. The
+// 8 consumer warps are split into row groups of LPR = hd/8 lanes; each lane
+// owns 8 consecutive elements of a row, so a K·q dot is 8 FMAs plus log2(LPR)
+// xor-shuffles. Row group rg owns MAXH kv heads (and their G query heads) in
+// one position class; online softmax in the log2 domain; fp32 throughout.
+template <int FMT, int LPR, int MAXH, int G>
+__global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
+  constexpr int E = Fmt<FMT>::kBytes;
+  constexpr int HD = LPR * 8;
+  constexpr int RGW = 32 / LPR;              // row groups per warp
+  constexpr int RG = kConsumerWarps * RGW;   // row groups per CTA
+  constexpr int MAXQ = MAXH * G;
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + a.nstages;
+  uint8_t* ring = smem + 128 * ((16 * a.nstages + 127) / 128);
+  float* scratch = reinterpret_cast<float*>(ring + static_cast<size_t>(2) * a.nstages * a.stage_region);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const KvGeom& g = a.g;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int cb = a.cta_begin[blockIdx.x];
+  const int ce = a.cta_begin[blockIdx.x + 1];
+  const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = cb; w < ce; ++w) {
+        const Piece pc = a.pieces[w];
+        const int slot = a.item_slot[pc.item];
+        const int32_t* pt = g.page_table + static_cast<int64_t>(slot) * g.max_pages;
+        for (int pos = pc.p0; pos < pc.p1; pos += a.T) {
+          const int cnt = min(a.T, pc.p1 - pos);
+          const int grp = pt[pos >> g.log2P];
+          const int off = pos & (g.P - 1);
+          const uint8_t* base = layer_base + static_cast<int64_t>(grp) * g.group_bytes +
+                                static_cast<int64_t>(off) * g.pos_bytes;
+          const uint32_t bytes = static_cast<uint32_t>(cnt) * g.pos_bytes;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], 2 * bytes);
+          uint8_t* dst = ring + static_cast<size_t>(2 * stage) * a.stage_region;
+          bulk_g2s(dst, base, bytes, &full[stage], pol);
+          bulk_g2s(dst + a.stage_region, base + g.v_off, bytes, &full[stage], pol);
+          if (++stage == a.nstages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int rg = warp * RGW + lane / LPR;
+  const int li = lane % LPR;
+  const int hkv = g.hc;
+  int ncls, cls, h0, hstride, nh;
+  if (hkv >= RG) {
+    ncls = 1;
+    cls = 0;
+    h0 = rg;
+    hstride = RG;
+    nh = (hkv - rg + RG - 1) / RG;
+  } else {
+    ncls = RG / hkv;
+    cls = rg / hkv;
+    h0 = rg % hkv;
+    hstride = hkv;
+    nh = cls < ncls ? 1 : 0;
+  }
+  const int Hq = hkv * G;
+  const int row_bytes = HD * E;
+
+  float q[MAXQ][8], acc[MAXQ][8], m[MAXQ], l[MAXQ];
+  int stage = 0;
+  uint32_t phase = 0;
+
+  for (int w = cb; w < ce; ++w) {
+    const Piece pc = a.pieces[w];
+    const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride;
+#pragma unroll
+    for (int j = 0; j < MAXQ; ++j) {
+      const int hh = j / G;
+      m[j] = -INFINITY;
+      l[j] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[j][i] = 0.0f;
+      if (hh < nh) {
+        const int qh = (h0 + hh * hstride) * G + (j % G);
+        const float4* src = reinterpret_cast<const float4*>(qrow + qh * HD + li * 8);
+        const float4 x0 = src[0], x1 = src[1];
+        q[j][0] = x0.x * a.qscale; q[j][1] = x0.y * a.qscale;
+        q[j][2] = x0.z * a.qscale; q[j][3] = x0.w * a.qscale;
+        q[j][4] = x1.x * a.qscale; q[j][5] = x1.y * a.qscale;
+        q[j][6] = x1.z * a.qscale; q[j][7] = x1.w * a.qscale;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[j][i] = 0.0f;
+      }
+    }
+    const int slot = a.item_slot[pc.item];
+    const int32_t* pt = g.page_table + static_cast<int64_t>(slot) * g.max_pages;
+
+    for (int pos = pc.p0; pos < pc.p1; pos += a.T) {
+      const int cnt = min(a.T, pc.p1 - pos);
+      mbar_wait(&full[stage], phase);
+      const uint8_t* Ks = ring + static_cast<size_t>(2 * stage) * a.stage_region;
+      const uint8_t* Vs = Ks + a.stage_region;
+      const float* ksc = nullptr;
+      const float* vsc = nullptr;
+      if (FMT == SD_KV_INT8) {
+        const int grp = pt[pos >> g.log2P];
+        const uint8_t* lb = layer_base + static_cast<int64_t>(grp) * g.group_bytes;
+        const int off = pos & (g.P - 1);
+        ksc = reinterpret_cast<const float*>(lb + g.ks_off) + off * hkv;
+        vsc = reinterpret_cast<const float*>(lb + g.vs_off) + off * hkv;
+      }
+      // warp-uniform trip count: every lane runs every shuffle
+      for (int t0 = 0; t0 < a.T; t0 += ncls) {
+        const int t = t0 + cls;
+        const bool tact = t < cnt;
+#pragma unroll
+        for (int hh = 0; hh < MAXH; ++hh) {
+          const bool act = tact && hh < nh;
+          const int hk = h0 + hh * hstride;
+          float kx[8];
+          if (act) {
+            Fmt<FMT>::load8(Ks + static_cast<size_t>(t * hkv + hk) * row_bytes + li * 8 * E, kx);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) kx[i] = 0.0f;
+          }
+          float s[G];
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            float d = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d = fmaf(q[hh * G + gg][i], kx[i], d);
+#pragma unroll
+            for (int sh = LPR / 2; sh > 0; sh >>= 1) d += __shfl_xor_sync(0xffffffffu, d, sh);
+            s[gg] = d;
+          }
+          if (act) {
+            float vx[8];
+            Fmt<FMT>::load8(Vs + static_cast<size_t>(t * hkv + hk) * row_bytes + li * 8 * E, vx);
+            float vscale = 1.0f;
+            if (FMT == SD_KV_INT8) {
+              const float kscale = ksc[t * hkv + hk];
+#pragma unroll
+              for (int gg = 0; gg < G; ++gg) s[gg] *= kscale;
+              vscale = vsc[t * hkv + hk];
+            }
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) {
+              const int j = hh * G + gg;
+              if (s[gg] > m[j]) {
+                const float c = fast_exp2(m[j] - s[gg]);
+                l[j] *= c;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) acc[j][i] *= c;
+                m[j] = s[gg];
+              }
+              const float p = fast_exp2(s[gg] - m[j]);
+              l[j] += p;
+              const float pv = p * vscale;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[j][i] = fmaf(pv, vx[i], acc[j][i]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == a.nstages) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // ---- finalize the piece: merge position classes through shared memory
+    if (ncls > 1) {
+      const int slot_stride = MAXQ * (HD + 2);
+      if (nh > 0 && cls > 0) {
+        float* dst = scratch + static_cast<size_t>(rg) * slot_stride;
+#pragma unroll
+        for (int j = 0; j < MAXQ; ++j) {
+          if (j / G < nh) {
+            float* d = dst + j * (HD + 2);
+            if (li == 0) {
+              d[0] = m[j];
+              d[1] = l[j];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) d[2 + li * 8 + i] = acc[j][i];
+          }
+        }
+      }
+      named_bar(1, kConsumerWarps * 32);
+      if (nh > 0 && cls == 0) {
+        for (int c = 1; c < ncls; ++c) {
+          const float* src = scratch + static_cast<size_t>(c * hkv + h0) * slot_stride;
+#pragma unroll
+          for (int j = 0; j < MAXQ; ++j) {
+            if (j / G < nh) {
+              const float* sp = src + j * (HD + 2);
+              const float m2 = sp[0], l2 = sp[1];
+              const float M = fmaxf(m[j], m2);
+              const float ca = fast_exp2(m[j] - M);
+              const float cb2 = m2 == -INFINITY ? 0.0f : fast_exp2(m2 - M);
+              l[j] = l[j] * ca + l2 * cb2;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[j][i] = acc[j][i] * ca + sp[2 + li * 8 + i] * cb2;
+              m[j] = M;
+            }
+          }
+        }
+      }
+      named_bar(1, kConsumerWarps * 32);
+    }
+    if (nh > 0 && cls == 0) {
+      const bool direct = pc.flags & 1;
+      float* orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride;
+#pragma unroll
+      for (int j = 0; j < MAXQ; ++j) {
+        if (j / G < nh) {
+          const int qh = (h0 + (j / G) * hstride) * G + (j % G);
+          if (direct) {
+            const float inv = 1.0f / l[j];
+            float4* dst = reinterpret_cast<float4*>(orow + qh * HD + li * 8);
+            dst[0] = make_float4(acc[j][0] * inv, acc[j][1] * inv, acc[j][2] * inv, acc[j][3] * inv);
+            dst[1] = make_float4(acc[j][4] * inv, acc[j][5] * inv, acc[j][6] * inv, acc[j][7] * inv);
+          } else {
+            float* pa = a.part_acc + static_cast<int64_t>(w) * Hq * HD + qh * HD + li * 8;
+            reinterpret_cast<float4*>(pa)[0] = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
+            reinterpret_cast<float4*>(pa)[1] = make_float4(acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+            if (li == 0) {
+              float* pm = a.part_ml + (static_cast<int64_t>(w) * Hq + qh) * 2;
+              pm[0] = m[j];
+              pm[1] = l[j];
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------- K2 generic path ---
+// Any head_dim / format / geometry (reference unit-test shapes such as
+// hd = 4 or 12). One warp per (piece, query head); positions sequential,
+// elements strided over lanes. Same online-softmax math as the fast path.
+__device__ __forceinline__ float load_elem(const KvGeom& g, const uint8_t* lb, int off, int hk,
+                                           int d, bool is_v) {
+  const uint8_t* rows = lb + (is_v ? g.v_off : 0) + static_cast<int64_t>(off) * g.pos_bytes;
+  const int idx = hk * g.hd + d;
+  switch (g.fmt) {
+    case SD_KV_SINGLE: return reinterpret_cast<const float*>(rows)[idx];
+    case SD_KV_HALF: return __half2float(reinterpret_cast<const __half*>(rows)[idx]);
+    default: {
+      const float sc = reinterpret_cast<const float*>(lb + (is_v ? g.vs_off : g.ks_off))[off * g.hc + hk];
+      return static_cast<float>(reinterpret_cast<const int8_t*>(rows)[idx]) * sc;
+    }
+  }
+}
+
+constexpr int kGenericMaxPerLane = 8;  // hd <= 256
+
+__global__ void attn_generic_kernel(const AttnArgs a) {
+  const KvGeom& g = a.g;
+  const int w = blockIdx.x;
+  const int qh = blockIdx.y;
+  const int lane = threadIdx.x;
+  const Piece pc = a.pieces[w];
+  const int hk = qh / a.G;
+  const int Hq = g.hc * a.G;
+  const int slot = a.item_slot[pc.item];
+  const int32_t* pt = g.page_table + static_cast<int64_t>(slot) * g.max_pages;
+  const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
+  const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride + qh * g.hd;
+  float qv[kGenericMaxPerLane], acc[kGenericMaxPerLane];
+#pragma unroll
+  for (int r = 0; r < kGenericMaxPerLane; ++r) {
+    const int d = lane + 32 * r;
+    qv[r] = d < g.hd ? qrow[d] * a.qscale : 0.0f;
+    acc[r] = 0.0f;
+  }
+  float m = -INFINITY, l = 0.0f;
+  for (int pos = pc.p0; pos < pc.p1; ++pos) {
+    const uint8_t* lb = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes;
+    const int off = pos & (g.P - 1);
+    float s = 0.0f;
+#pragma unroll
+    for (int r = 0; r < kGenericMaxPerLane; ++r) {
+      const int d = lane + 32 * r;
+      if (d < g.hd) s = fmaf(qv[r], load_elem(g, lb, off, hk, d, false), s);
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) s += __shfl_xor_sync(0xffffffffu, s, sh);
+    if (s > m) {
+      const float c = fast_exp2(m - s);
+      l *= c;
+#pragma unroll
+      for (int r = 0; r < kGenericMaxPerLane; ++r) acc[r] *= c;
+      m = s;
+    }
+    const float p = fast_exp2(s - m);
+    l += p;
+#pragma unroll
+    for (int r = 0; r < kGenericMaxPerLane; ++r) {
+      const int d = lane + 32 * r;
+      if (d < g.hd) acc[r] = fmaf(p, load_elem(g, lb, off, hk, d, true), acc[r]);
+    }
+  }
+  if (pc.flags & 1) {
+    float* orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * g.hd;
+    const float inv = 1.0f / l;
+#pragma unroll
+    for (int r = 0; r < kGenericMaxPerLane; ++r) {
+      const int d = lane + 32 * r;
+      if (d < g.hd) orow[d] = acc[r] * inv;
+    }
+  } else {
+    float* pa = a.part_acc + static_cast<int64_t>(w) * Hq * g.hd + qh * g.hd;
+#pragma unroll
+    for (int r = 0; r < kGenericMaxPerLane; ++r) {
+      const int d = lane + 32 * r;
+      if (d < g.hd) pa[d] = acc[r];
+    }
+    if (lane == 0) {
+      a.part_ml[(static_cast<int64_t>(w) * Hq + qh) * 2] = m;
+      a.part_ml[(static_cast<int64_t>(w) * Hq + qh) * 2 + 1] = l;
+    }
+  }
+}
+
+// --------------------------------------------------------------- K3 ------
+// Deterministic combine of an item's pieces in piece order.
+__global__ void combine_kernel(const CombineArgs a) {
+  const int4 it = a.items[blockIdx.x];
+  const int width = a.Hq * a.hd;
+  float* orow = a.o + static_cast<int64_t>(it.x) * a.o_stride;
+  for (int e = threadIdx.x; e < width; e += blockDim.x) {
+    const int qh = e / a.hd;
+    float M = -INFINITY;
+    for (int p = 0; p < it.z; ++p) M = fmaxf(M, a.part_ml[(static_cast<int64_t>(it.y + p) * a.Hq + qh) * 2]);
+    float L = 0.0f, acc = 0.0f;
+    for (int p = 0; p < it.z; ++p) {
+      const int64_t pi = it.y + p;
+      const float wgt = fast_exp2(a.part_ml[(pi * a.Hq + qh) * 2] - M);
+      L = fmaf(wgt, a.part_ml[(pi * a.Hq + qh) * 2 + 1], L);
+      acc = fmaf(wgt, a.part_acc[pi * width + e], acc);
+    }
+    orow[e] = acc / L;
+  }
+}
+
+// --------------------------------------------------------------- K1 ------
+// One block per (item, K|V) row: convert the fp32 row into the storage
+// format at (slot, layer, position). int8 follows quantize_int8
+// (attention.cpp:28-46) bit for bit: scale = max|x| / 127.0f (IEEE fp32
+// division), q = clamp(rint((double)x * (1.0 / (double)scale)), +-127).
+__global__ void append_kernel(const AppendArgs a) {
+  const KvGeom& g = a.g;
+  // page-table updates for pages opened by this call
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int u = threadIdx.x; u < a.nupd; u += blockDim.x) g.page_table[a.upd[2 * u]] = a.upd[2 * u + 1];
+  }
+  const int i = blockIdx.x;
+  if (i >= a.n) return;
+  const bool is_v = blockIdx.y == 1;
+  const float* src = (is_v ? a.v + i * a.v_stride : a.k + i * a.k_stride);
+  const int pos = a.pos[i];
+  const int off = pos & (g.P - 1);
+  uint8_t* lb = g.pool + static_cast<int64_t>(a.group[i]) * g.group_bytes +
+                static_cast<int64_t>(a.layer) * g.layer_bytes;
+  uint8_t* row = lb + (is_v ? g.v_off : 0) + static_cast<int64_t>(off) * g.pos_bytes;
+  if (g.fmt == SD_KV_SINGLE) {
+    float* d = reinterpret_cast<float*>(row);
+    for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = src[e];
+  } else if (g.fmt == SD_KV_HALF) {
+    __half* d = reinterpret_cast<__half*>(row);
+    for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(src[e]);
+  } else {
+    // one warp per head
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    float* scales = reinterpret_cast<float*>(lb + (is_v ? g.vs_off : g.ks_off)) + off * g.hc;
+    int8_t* d = reinterpret_cast<int8_t*>(row);
+    for (int h = warp; h < g.hc; h += nw) {
+      const float* x = src + h * g.hd;
+      float mx = 0.0f;
+      for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(x[e]));
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+      if (mx == 0.0f) {
+        for (int e = lane; e < g.hd; e += 32) d[h * g.hd + e] = 0;
+        if (lane == 0) scales[h] = 0.0f;
+      } else {
+        const float sc = __fdiv_rn(mx, 127.0f);
+        const double inv = 1.0 / static_cast<double>(sc);
+        for (int e = lane; e < g.hd; e += 32) {
+          double r = rint(static_cast<double>(x[e]) * inv);
+          r = fmin(fmax(r, -127.0), 127.0);
+          d[h * g.hd + e] = static_cast<int8_t>(r);
+        }
+        if (lane == 0) scales[h] = sc;
+      }
+    }
+  }
+}
+
+// Synthetic prefill: element (slot, layer, pos, kv, i) = synth_value(idx).
+__global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* slots, int n,
+                               int length, uint64_t salt) {
+  const int64_t rows = static_cast<int64_t>(n) * num_layers * length * 2;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    int64_t t = r;
+    const int kv = static_cast<int>(t & 1);
+    t >>= 1;
+    const int pos = static_cast<int>(t % length);
+    t /= length;
+    const int layer = static_cast<int>(t % num_layers);
+    const int item = static_cast<int>(t / num_layers);
+    const int slot = slots[item];
+    const int grp = g.page_table[static_cast<int64_t>(slot) * g.max_pages + (pos >> g.log2P)];
+    const int off = pos & (g.P - 1);
+    uint8_t* lb = g.pool + static_cast<int64_t>(grp) * g.group_bytes +
+                  static_cast<int64_t>(layer) * g.layer_bytes;
+    uint8_t* row = lb + (kv ? g.v_off : 0) + static_cast<int64_t>(off) * g.pos_bytes;
+    const uint64_t base =
+        salt ^ ((((static_cast<uint64_t>(slot) * 4096u + layer) * 1048576u + pos) * 2u + kv) *
+                static_cast<uint64_t>(g.width));
+    if (g.fmt == SD_KV_SINGLE) {
+      float* d = reinterpret_cast<float*>(row);
+      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = synth_value(base + e);
+    } else if (g.fmt == SD_KV_HALF) {
+      __half* d = reinterpret_cast<__half*>(row);
+      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(synth_value(base + e));
+    } else {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      float* scales = reinterpret_cast<float*>(lb + (kv ? g.vs_off : g.ks_off)) + off * g.hc;
+      int8_t* d = reinterpret_cast<int8_t*>(row);
+      for (int h = warp; h < g.hc; h += nw) {
+        float mx = 0.0f;
+        for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(synth_value(base + h * g.hd + e)));
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+        const float sc = mx == 0.0f ? 0.0f : __fdiv_rn(mx, 127.0f);
+        const double inv = sc == 0.0f ? 0.0 : 1.0 / static_cast<double>(sc);
+        for (int e = lane; e < g.hd; e += 32) {
+          double rr = rint(static_cast<double>(synth_value(base + h * g.hd + e)) * inv);
+          rr = fmin(fmax(rr, -127.0), 127.0);
+          d[h * g.hd + e] = static_cast<int8_t>(rr);
+        }
+        if (lane == 0) scales[h] = sc;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ dispatch ---
+using AttnFn = void (*)(const AttnArgs);
+
+template <int FMT, int LPR>
+AttnFn pick_mh(int maxh, int G) {
+  if (G == 1) {
+    switch (maxh) {
+      case 1: return attn_kernel<FMT, LPR, 1, 1>;
+      case 2: return attn_kernel<FMT, LPR, 2, 1>;
+      case 3: return attn_kernel<FMT, LPR, 3, 1>;
+      case 4: return attn_kernel<FMT, LPR, 4, 1>;
+      default: return nullptr;
+    }
+  }
+  if (maxh != 1) return nullptr;
+  switch (G) {
+    case 2: return attn_kernel<FMT, LPR, 1, 2>;
+    case 4: return attn_kernel<FMT, LPR, 1, 4>;
+    case 8: return attn_kernel<FMT, LPR, 1, 8>;
+    default: return nullptr;
+  }
+}
+
+template <int FMT>
+AttnFn pick_lpr(int lpr, int maxh, int G) {
+  switch (lpr) {
+    case 2: return pick_mh<FMT, 2>(maxh, G);
+    case 4: return pick_mh<FMT, 4>(maxh, G);
+    case 8: return pick_mh<FMT, 8>(maxh, G);
+    case 16: return pick_mh<FMT, 16>(maxh, G);
+    case 32: return pick_mh<FMT, 32>(maxh, G);
+    default: return nullptr;
+  }
+}
+
+AttnFn pick(const KvGeom& g, int G) {
+  if (g.hd % 8 != 0) return nullptr;
+  const int lpr = g.hd / 8;
+  if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) return nullptr;
+  if (g.pos_bytes % 16 != 0) return nullptr;
+  const int RG = kConsumerWarps * (32 / lpr);
+  const int maxh = g.hc >= RG ? (g.hc + RG - 1) / RG : 1;
+  switch (g.fmt) {
+    case SD_KV_SINGLE: return pick_lpr<SD_KV_SINGLE>(lpr, maxh, G);
+    case SD_KV_HALF: return pick_lpr<SD_KV_HALF>(lpr, maxh, G);
+    case SD_KV_INT8: return pick_lpr<SD_KV_INT8>(lpr, maxh, G);
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+int attention_consumer_warps() { return kConsumerWarps; }
+
+size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region) {
+  const int region = ((T * g.pos_bytes + 127) / 128) * 128;
+  *stage_region = region;
+  size_t bytes = 128 * ((16 * nstages + 127) / 128) + static_cast<size_t>(2) * nstages * region;
+  if (g.hd % 8 == 0) {
+    const int lpr = g.hd / 8;
+    const int RG = kConsumerWarps * (32 / (lpr > 0 ? lpr : 1));
+    if (g.hc < RG) {
+      // class-merge scratch: RG x MAXQ x (hd + 2) floats
+      bytes += static_cast<size_t>(RG) * G * (g.hd + 2) * sizeof(float);
+    }
+  }
+  return bytes;
+}
+
+bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
+  AttnFn fn = pick(a.g, a.G);
+  if (!fn) return false;
+  if (smem > 48 * 1024) {
+    SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  }
+  fn<<<grid, kThreads, smem, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+  return true;
+}
+
+void launch_attention_generic(const AttnArgs& a, int npieces, cudaStream_t s) {
+  if (a.g.hd > 32 * kGenericMaxPerLane) fail(SD_ERR_CONFIG, "head_dim > 256 is not supported");
+  dim3 grid(npieces, a.g.hc * a.G);
+  attn_generic_kernel<<<grid, 32, 0, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+}
+
+void launch_combine(const CombineArgs& a, cudaStream_t s) {
+  if (a.m == 0) return;
+  combine_kernel<<<a.m, 256, 0, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+}
+
+void launch_append(const AppendArgs& a, cudaStream_t s) {
+  if (a.n == 0 && a.nupd == 0) return;
+  dim3 grid(a.n > 0 ? a.n : 1, 2);
+  append_kernel<<<grid, 256, 0, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+}
+
+void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, int n,
+                              int length, uint64_t salt, cudaStream_t s) {
+  if (n == 0 || length == 0) return;
+  prefill_kernel<<<148 * 16, 256, 0, s>>>(g, num_layers, slots, n, length, salt);
+  SD_CUDA(cudaGetLastError());
+}
+
+}  // namespace sd

@@ -1,0 +1,91 @@
+// R-Part device interfaces: KV append (K1), split-K decode attention (K2),
+// split combine (K3). See DESIGN.md "R-Part kernels".
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sd {
+
+// Geometry of the paged KV pool.
+// A page group holds P consecutive positions of one sequence for every
+// layer; inside it, layer l's region is
+//   [K rows P x pos_bytes][V rows P x pos_bytes][K scales P x hc f32][V scales P x hc f32]
+// where a row is one position's [head][d] vector in the storage format, i.e.
+// the reference's per-(seq, layer) lane order (attention.cpp:117-118).
+struct KvGeom {
+  uint8_t* pool;
+  int32_t* page_table;  // [max_sequences][max_pages] page-group ids
+  int32_t max_pages;
+  int32_t P;            // positions per page group (power of two)
+  int32_t log2P;
+  int32_t fmt;          // SD_KV_*
+  int32_t hc;           // kv heads in the shard
+  int32_t hd;           // head dim
+  int32_t width;        // hc * hd
+  int32_t pos_bytes;    // width * elem bytes
+  int64_t layer_bytes;  // bytes per layer region (128-B aligned)
+  int64_t group_bytes;  // layer_bytes * num_layers
+  int64_t v_off, ks_off, vs_off;  // offsets inside a layer region
+};
+
+struct AppendArgs {
+  KvGeom g;
+  int32_t layer;
+  int32_t n;
+  const int32_t* slot;   // [n]
+  const int32_t* pos;    // [n]
+  const int32_t* group;  // [n] physical page group of the written position
+  const int32_t* upd;    // [nupd][2] (page-table index, group)
+  int32_t nupd;
+  const float* k;        // [n][width]
+  const float* v;        // [n][width]
+  int64_t k_stride, v_stride;  // row strides in floats
+};
+
+// One contiguous piece of one item's positions, processed by one CTA.
+struct Piece {
+  int32_t item, p0, p1, flags;  // flags & 1: item has a single piece (write o directly)
+};
+
+struct AttnArgs {
+  KvGeom g;
+  int32_t layer;
+  const int32_t* item_slot;   // [n]
+  const Piece* pieces;        // [npieces], item-contiguous
+  const int32_t* cta_begin;   // [grid + 1] piece ranges per CTA
+  const float* q;             // [n][q_stride] row-major
+  float* o;                   // [n][o_stride]
+  int64_t q_stride, o_stride;
+  float* part_acc;            // [npieces][Hq * hd]
+  float* part_ml;             // [npieces][Hq][2]
+  float qscale;               // log2(e) / sqrt(hd)
+  int32_t G;                  // q heads per kv head
+  int32_t T;                  // positions per pipeline stage
+  int32_t nstages;
+  int32_t stage_region;       // bytes of one K (or V) stage region (128-B aligned)
+};
+
+struct CombineArgs {
+  const int4* items;  // [m] (item, first piece, piece count, -)
+  int32_t m;
+  const float* part_acc;
+  const float* part_ml;
+  float* o;
+  int64_t o_stride;
+  int32_t Hq, hd;
+};
+
+// launchers (kv_kernels.cu)
+void launch_append(const AppendArgs& a, cudaStream_t s);
+// returns false if the fast path does not support the shape (caller uses generic)
+bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s);
+void launch_attention_generic(const AttnArgs& a, int npieces, cudaStream_t s);
+void launch_combine(const CombineArgs& a, cudaStream_t s);
+void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots,
+                              int n, int length, uint64_t salt, cudaStream_t s);
+int attention_consumer_warps();
+size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region);
+
+}  // namespace sd

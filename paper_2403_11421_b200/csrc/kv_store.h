@@ -1,0 +1,115 @@
+// KvStore: the B200 KvShard. Host-side mirror of per-(sequence, layer)
+// stored lengths gives the reference's validation and error behaviour
+// (attention.cpp:139-305); K/V live in a paged HBM pool written and read by
+// the kernels in kv_kernels.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <unordered_map>
+#include <vector>
+
+#include "kv_kernels.cuh"
+#include "sd_common.h"
+
+namespace sd {
+
+class KvStore {
+ public:
+  KvStore(const Spec& spec, int head_start, int head_count, int64_t capacity_tokens, int fmt,
+          int device, const sd_kv_options* opts);
+  ~KvStore();
+  KvStore(const KvStore&) = delete;
+  KvStore& operator=(const KvStore&) = delete;
+
+  // ---- reference queries (attention.hpp:73-111)
+  int width() const { return geom_.width; }
+  int q_width() const { return geom_.width * G_; }
+  int group_size() const { return G_; }
+  int64_t capacity() const { return cap_; }
+  int format() const { return geom_.fmt; }
+  int64_t token_count() const { return total_ / spec_.L; }
+  int warnings() const { return warnings_; }
+  bool has(uint64_t seq) const { return slot_of_.count(seq) != 0; }
+  int stored(uint64_t seq, int layer) const;
+  int64_t bytes_per_token() const;
+  int device() const { return device_; }
+  const Spec& spec() const { return spec_; }
+
+  // ---- operations (device pointers; host `seqs`/`positions`)
+  // KvShard::append_request semantics (attention.cpp:172-202), including the
+  // reference's partial commit when a later item of the batch fails inside
+  // the sequential append loop (e.g. a duplicated sequence).
+  void append(int layer, int n, const uint64_t* seqs, const uint32_t* positions,
+              const float* k_dev, int64_t k_stride, const float* v_dev, int64_t v_stride,
+              cudaStream_t s);
+  // KvShard::attend semantics (attention.cpp:204-282).
+  void attend(int layer, int n, const uint64_t* seqs, const float* q_dev, int64_t q_stride,
+              float* o_dev, int64_t o_stride, cudaStream_t s);
+  // KvShard::drop_sequence (attention.cpp:284-294)
+  void drop(uint64_t seq);
+  int64_t export_lane(uint64_t seq, int layer, int which, void* host, size_t host_bytes,
+                      float* scales, size_t scales_count);
+  void prefill_synthetic(int n, const uint64_t* seqs, int length, uint64_t salt,
+                         cudaStream_t s);
+
+  // ---- timing of the attention kernel (CUDA events on the launching stream)
+  void set_timing(bool on);
+  void read_timing(double* ms, int64_t* launches, double* bytes, bool reset);
+
+ private:
+  struct Blob {  // one staged descriptor upload
+    HostBuf host;
+    DevBuf dev;
+    cudaEvent_t done = nullptr;
+  };
+  Blob& next_blob();
+  int slot_for_new(uint64_t seq);
+  void release_slot(int slot);
+  int alloc_group();
+  void upload(Blob& b, size_t bytes, cudaStream_t s);
+  void launch_attention_plan(int layer, const float* q, int64_t qs, float* o, int64_t os,
+                             cudaStream_t s);
+
+  Spec spec_;
+  int head_start_, head_count_, G_;
+  int64_t cap_;
+  int device_;
+  int nsm_ = 148;
+  KvGeom geom_{};
+  int T_ = 1, nstages_ = 2, stage_region_ = 0;
+  size_t attn_smem_ = 0;
+  int max_seqs_ = 0, max_len_ = 0, pool_groups_ = 0;
+
+  // host mirror
+  std::unordered_map<uint64_t, int> slot_of_;
+  std::vector<int32_t> len_;     // [max_seqs][L]
+  std::vector<int32_t> pages_;   // [max_seqs][max_pages], -1 = none
+  std::vector<int32_t> npages_;  // [max_seqs]
+  std::vector<int32_t> free_slots_, free_groups_;
+  int64_t total_ = 0;
+  int warnings_ = 0;
+
+  // staging
+  std::vector<Blob> ring_;
+  size_t ring_next_ = 0;
+  // cached attention plan (reused while (slots, lengths) repeat, e.g. across
+  // the layers of one lockstep decode step)
+  std::vector<int32_t> plan_slots_, plan_lens_;
+  int plan_npieces_ = 0, plan_grid_ = 0, plan_ncombine_ = 0;
+  int64_t plan_positions_ = 0;
+  Blob plan_blob_;
+  size_t off_slot_ = 0, off_pieces_ = 0, off_cta_ = 0, off_comb_ = 0;
+  DevBuf part_acc_, part_ml_;
+
+  // timing
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending_;
+  std::vector<double> ev_bytes_;
+  double t_ms_ = 0, t_bytes_ = 0;
+  int64_t t_launches_ = 0;
+};
+
+}  // namespace sd

@@ -1,0 +1,123 @@
+// Internal shared definitions for libsd_b200 (host C++ and CUDA).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/sd_abi.h"
+
+namespace sd {
+
+// Typed errors mirroring the reference's exception classes (core.hpp:25-38,
+// attention.hpp:19-22); `code` is the C-ABI status they map to.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    fail(SD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define SD_CUDA(x) ::sd::cuda_check((x), #x)
+
+struct Spec {
+  int L, D, H, hd, F, V, Hkv;
+  int kv_width() const { return Hkv * hd; }
+  int qkv_width() const { return (H + 2 * Hkv) * hd; }
+};
+
+inline Spec make_spec(int L, int D, int H, int F, int V, int Hkv) {
+  if (L < 1 || D < 1 || H < 1 || F < 1 || V < 1) {
+    fail(SD_ERR_CONFIG, "model spec fields must all be >= 1");
+  }
+  if (D % H != 0) {
+    fail(SD_ERR_CONFIG, "model_dim not divisible by heads (model_dim=" + std::to_string(D) +
+                            ", num_heads=" + std::to_string(H) + ")");
+  }
+  if (Hkv == 0) Hkv = H;
+  if (Hkv < 1 || H % Hkv != 0) fail(SD_ERR_CONFIG, "num_heads not divisible by num_kv_heads");
+  return Spec{L, D, H, D / H, F, V, Hkv};
+}
+
+inline Spec from_abi(const sd_model_spec* s) {
+  if (!s) fail(SD_ERR_CONFIG, "null model spec");
+  Spec r = make_spec(s->num_layers, s->model_dim, s->num_heads, s->mlp_dim, s->vocab_size,
+                     s->num_kv_heads);
+  if (s->head_dim != 0 && s->head_dim != r.hd) {
+    fail(SD_ERR_CONFIG, "head_dim inconsistent with model_dim / num_heads");
+  }
+  return r;
+}
+
+// SplitMix64 finalizer (core.cpp:161-166)
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// Counter-based synthetic value in [-1, 1) (SURVEY §8d bench prefill)
+__host__ __device__ inline float synth_value(uint64_t idx) {
+  return 2.0f * (static_cast<float>(mix64(0x5EEDull ^ idx) >> 40) * 0x1p-24f) - 1.0f;
+}
+
+// Device scratch buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      SD_CUDA(cudaMalloc(&p, need));
+      bytes = need;
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct HostBuf {  // pinned
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      bytes = 0;
+      SD_CUDA(cudaMallocHost(&p, need));
+      bytes = need;
+    }
+    return p;
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// RAII device guard
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) SD_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace sd

@@ -32,3 +32,17 @@ def rnd_stream(seed):
             out[i] = 2.0 * np.float32((state[0] >> 40) * 2.0**-24) - 1.0
         return out
     return vec
+
+
+def upload_oracle_weights(W, mode="exact", device=0):
+    """Upload an oracle WeightSet through the product C-ABI (tests only)."""
+    import paper_2403_11421_b200 as sd
+    tensors = [W.raw("embedding")]
+    for l in range(W.spec.num_layers):
+        for n in ("w_q", "w_k", "w_v", "w_o", "w_mlp_in", "w_mlp_out"):
+            tensors.append(W.raw(n, l))
+    tensors.append(W.raw("head"))
+    s = W.spec
+    spec = sd.make_model_spec(s.num_layers, s.model_dim, s.num_heads, s.mlp_dim, s.vocab_size,
+                              s.num_kv_heads)
+    return sd.DeviceWeights(spec, tensors, mode, device)

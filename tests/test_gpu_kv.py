@@ -1,0 +1,281 @@
+"""R-Part parity on the GPU: the B200 KvShard (paged HBM store + split-K
+decode-attention kernel) against the CPU oracle restatement of
+KvShard::append_request / attend (attention.cpp:139-305).
+
+Tolerances: KV layout, int8 codes/scales and fp16 bits are bit-exact; the
+attention output is fp32 with a different (parallel, online-softmax)
+reduction order, so it must satisfy the reference's own bound of 1e-5 abs
+for |values| <= 1 (test_attention.cpp:142-163, acceptance.cpp:303-357),
+scaled by max|o| for larger values."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import rnd_stream
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sd():
+    import paper_2403_11421_b200 as m
+    return m
+
+
+def _specs(sd, oracle, L, D, H, F, V, Hkv=0):
+    return sd.make_model_spec(L, D, H, F, V, Hkv), oracle.make_spec(L, D, H, F, V, Hkv)
+
+
+def _rng(seed):
+    return np.random.default_rng(seed)
+
+
+def test_single_token_returns_v_exactly(sd):
+    # proj/tests/test_attention.cpp:73-82
+    vec = rnd_stream(7)
+    s = sd.make_model_spec(1, 16, 2, 8, 8)
+    kv = sd.KvShard(s, 0, 2, 64)
+    q, k, v = vec(16), vec(16), vec(16)
+    o = kv.append_attend(0, [7], [0], q[None], k[None], v[None])
+    assert np.array_equal(o[0], v)
+
+
+def test_orthogonal_query_averages_values(sd):
+    # proj/tests/test_attention.cpp:84-98 (hd = 4: generic kernel)
+    vec = rnd_stream(9)
+    s = sd.make_model_spec(1, 4, 1, 8, 8)
+    kv = sd.KvShard(s, 0, 1, 64)
+    k1, k2, q = np.zeros(4, np.float32), np.zeros(4, np.float32), np.zeros(4, np.float32)
+    k1[0] = k2[1] = 1.0
+    q[3] = 5.0
+    v1, v2 = vec(4), vec(4)
+    kv.append_request(0, [1], [0], k1[None], v1[None])
+    kv.append_request(0, [1], [1], k2[None], v2[None])
+    o = kv.attend(0, [1], q[None])[0]
+    assert np.abs(o - (0.5 * v1 + 0.5 * v2)).max() < 1e-6
+
+
+def test_softmax_weights_sum_to_one(sd):
+    # proj/tests/test_attention.cpp:118-140 (hd = 12: generic kernel)
+    vec = rnd_stream(5)
+    n = 12
+    s = sd.make_model_spec(1, n, 1, 8, 8)
+    kv = sd.KvShard(s, 0, 1, 64)
+    for pos in range(n):
+        v = np.zeros(n, np.float32)
+        v[pos] = 1.0
+        kv.append_request(0, [1], [pos], vec(n)[None], v[None])
+    w = kv.attend(0, [1], vec(n)[None])[0]
+    assert (w >= 0).all() and abs(float(w.astype(np.float64).sum()) - 1.0) < 1e-6
+
+
+def _double_attention(q, ks, vs, H, G, hd):
+    out = np.zeros(H * hd)
+    for h in range(H):
+        kh = h // G
+        qs = q[h * hd:(h + 1) * hd].astype(np.float64)
+        sc = np.array([qs @ k[kh * hd:(kh + 1) * hd].astype(np.float64) for k in ks]) / math.sqrt(hd)
+        e = np.exp(sc - sc.max())
+        a = e / e.sum()
+        out[h * hd:(h + 1) * hd] = sum(a[j] * vs[j][kh * hd:(kh + 1) * hd].astype(np.float64)
+                                       for j in range(len(ks)))
+    return out
+
+
+@pytest.mark.parametrize("D,H", [(32, 4), (64, 4), (256, 2)])
+def test_incremental_cache_matches_double_oracle(sd, D, H):
+    # proj/tests/test_attention.cpp:142-163 and acceptance.cpp:303-357
+    vec = rnd_stream(11 + D)
+    s = sd.make_model_spec(1, D, H, 8, 8)
+    hd = D // H
+    for trial in range(6):
+        kv = sd.KvShard(s, 0, H, 256)
+        ks, vs = [], []
+        worst = 0.0
+        n = 1 + (trial * 37) % 64
+        for pos in range(n):
+            q = vec(D)
+            ks.append(vec(D))
+            vs.append(vec(D))
+            o = kv.append_attend(0, [1], [pos], q[None], ks[-1][None], vs[-1][None])[0]
+            worst = max(worst, float(np.abs(o - _double_attention(q, ks, vs, H, 1, hd)).max()))
+        assert worst < 1e-5, (trial, worst)
+
+
+CASES = [
+    # (L, D, H, Hkv, fmt, batch, max_len)
+    (2, 64, 4, 0, "single", 5, 40),        # reference toy geometry, hd 16
+    (2, 64, 4, 0, "half", 5, 40),
+    (2, 64, 4, 0, "int8", 5, 40),
+    (1, 256, 2, 0, "single", 16, 130),     # C1 geometry, hd 128
+    (1, 256, 2, 0, "half", 16, 130),
+    (1, 512, 8, 2, "half", 7, 200),        # GQA (extension), hd 64
+    (1, 1024, 8, 0, "single", 9, 300),     # hd 128, 8 heads
+    (1, 2048, 16, 4, "int8", 6, 150),      # GQA + int8
+    (1, 1024, 32, 0, "half", 4, 60),       # hd 32, 32 heads (2 heads per row group)
+    (1, 4096, 32, 0, "half", 3, 90),       # Llama-2-7B head geometry
+    (1, 5120, 40, 0, "half", 3, 70),       # Llama-2-13B head geometry (3 heads per row group)
+    (1, 4096, 32, 8, "half", 3, 90),       # Llama-3-8B GQA geometry
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[1]}x{c[2]}kv{c[3]}-{c[4]}" for c in CASES])
+def test_ragged_batch_parity_vs_oracle(sd, oracle, case):
+    L, D, H, Hkv, fmt, B, max_len = case
+    s, os_ = _specs(sd, oracle, L, D, H, 8, 8, Hkv)
+    hkv = s.num_kv_heads
+    kvw = hkv * s.head_dim
+    cap = B * max_len + 8
+    gpu = sd.KvShard(s, 0, hkv, cap, fmt)
+    cpu = oracle.KvShard(os_, 0, hkv, cap, fmt)
+    rng = _rng(hash(case) & 0xffff)
+    lens = rng.integers(1, max_len, B)
+    seqs = [int(x) for x in rng.permutation(1000)[:B] + 1]
+    # prefill through append_request, several positions at a time, all layers
+    for pos in range(int(lens.max())):
+        act = [i for i in range(B) if lens[i] > pos]
+        ids = [seqs[i] for i in act]
+        for layer in range(L):
+            k = rng.uniform(-1, 1, (len(act), kvw)).astype(np.float32)
+            v = rng.uniform(-1, 1, (len(act), kvw)).astype(np.float32)
+            gpu.append_request(layer, ids, [pos] * len(act), k, v)
+            cpu.append_request(layer, ids, [pos] * len(act), k, v)
+    assert gpu.token_count() == cpu.token_count()
+    for layer in range(L):
+        q = rng.uniform(-1, 1, (B, D)).astype(np.float32) * 2.0
+        og = gpu.attend(layer, seqs, q)
+        oc = cpu.attend(layer, seqs, q)
+        err = float(np.abs(og - oc).max())
+        tol = 1e-5 if fmt == "single" else 2e-5
+        assert err < tol, err
+    # bit-exact KV layout / codecs against the oracle's storage
+    for i in (0, B - 1):
+        for which in (0, 1):
+            bg, sg = gpu.export_lane(seqs[i], 0, which)
+            bc, sc = cpu.export_lane(seqs[i], 0, which)
+            assert np.array_equal(bg, bc)
+            if fmt == "int8":
+                assert np.array_equal(sg.view(np.uint32), sc.view(np.uint32))
+
+
+def test_many_sequences_split_and_combine(sd, oracle):
+    """Enough work to split items across CTAs (balanced split-K + combine)."""
+    s, os_ = _specs(sd, oracle, 1, 1024, 8, 8, 8)
+    B, Lmax = 300, 700
+    gpu = sd.KvShard(s, 0, 8, B * Lmax, "half")
+    cpu = oracle.KvShard(os_, 0, 8, B * Lmax, "half")
+    rng = _rng(3)
+    lens = rng.integers(1, Lmax, B)
+    seqs = list(range(1, B + 1))
+    for pos in range(int(lens.max())):
+        act = [i for i in range(B) if lens[i] > pos]
+        k = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        v = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        ids = [seqs[i] for i in act]
+        gpu.append_request(0, ids, [pos] * len(act), k, v)
+        cpu.append_request(0, ids, [pos] * len(act), k, v)
+    q = rng.uniform(-2, 2, (B, 1024)).astype(np.float32)
+    err = float(np.abs(gpu.attend(0, seqs, q) - cpu.attend(0, seqs, q)).max())
+    assert err < 2e-5, err
+
+
+def test_capacity_positions_atomicity_drop(sd):
+    # proj/tests/test_attention.cpp:205-284, reference error types
+    vec = rnd_stream(17)
+    s = sd.make_model_spec(2, 8, 2, 8, 8)
+    kv = sd.KvShard(s, 0, 2, 4)
+    k, v = vec(8), vec(8)
+    kv.append(1, 0, 0, k, v)
+    assert kv.stored_length(1, 0) == 1
+    kv.append(1, 1, 0, k, v)
+    assert kv.token_count() == 1
+    for pos in range(1, 4):
+        for layer in range(2):
+            kv.append(1, layer, pos, k, v)
+    assert kv.token_count() == 4
+    with pytest.raises(sd.CapacityError, match="capacity exceeded"):
+        kv.append(1, 0, 4, k, v)
+
+    s1 = sd.make_model_spec(1, 8, 2, 8, 8)
+    kv = sd.KvShard(s1, 0, 2, 64)
+    with pytest.raises(sd.UnknownSequenceError):
+        kv.append(9, 0, 3, k, v)
+    kv.append(9, 0, 0, k, v)
+    with pytest.raises(sd.ProtocolError) as e:
+        kv.append(9, 0, 2, k, v)
+    assert not isinstance(e.value, sd.UnknownSequenceError)
+
+    kv = sd.KvShard(s1, 0, 2, 2)
+    ks = np.stack([vec(8) for _ in range(3)])
+    with pytest.raises(sd.CapacityError):
+        kv.append_request(0, [1, 2, 3], [0, 0, 0], ks, ks)
+    assert kv.token_count() == 0 and not kv.has_sequence(1)
+
+    kv = sd.KvShard(s, 0, 2, 16)
+    for pos in range(3):
+        for layer in range(2):
+            kv.append(4, layer, pos, k, v)
+    assert kv.token_count() == 3
+    kv.drop_sequence(4)
+    assert kv.token_count() == 0 and not kv.has_sequence(4) and kv.warning_count() == 0
+    kv.drop_sequence(4)
+    assert kv.warning_count() == 1
+    with pytest.raises(sd.UnknownSequenceError):
+        kv.attend(0, [4], vec(8)[None])
+
+
+def test_duplicate_item_partial_commit_matches_oracle(sd, oracle):
+    """append_request validates against the pre-call state, then appends
+    sequentially; a duplicated new sequence fails on its second item with the
+    first already stored (attention.cpp:172-202)."""
+    s, os_ = _specs(sd, oracle, 1, 32, 2, 8, 8)
+    g, c = sd.KvShard(s, 0, 2, 64), oracle.KvShard(os_, 0, 2, 64)
+    rows = np.ones((3, 32), np.float32)
+    with pytest.raises(sd.ProtocolError):
+        g.append_request(0, [5, 6, 5], [0, 0, 0], rows, rows)
+    with pytest.raises(oracle.OracleError):
+        c.append_request(0, [5, 6, 5], [0, 0, 0], rows, rows)
+    for q in (5, 6):
+        assert g.stored_length(q, 0) == c.stored_length(q, 0)
+    assert g.token_count() == c.token_count()
+
+
+def test_empty_layer_is_logic_error(sd):
+    s = sd.make_model_spec(2, 32, 2, 8, 8)
+    kv = sd.KvShard(s, 0, 2, 64)
+    kv.append(3, 0, 0, np.ones(32), np.ones(32))
+    with pytest.raises(sd.LogicError):
+        kv.attend(1, [3], np.ones((1, 32)))
+
+
+def test_slot_and_page_reuse_after_drop(sd, oracle):
+    s, os_ = _specs(sd, oracle, 1, 128, 1, 8, 8)
+    g = sd.KvShard(s, 0, 1, 200, "half", max_sequences=4)
+    c = oracle.KvShard(os_, 0, 1, 200, "half")
+    rng = _rng(5)
+    live = {}
+    nxt = 1
+    for it in range(60):
+        if len(live) == 4 or (live and rng.random() < 0.3):
+            q = int(rng.choice(list(live)))
+            g.drop_sequence(q)
+            c.drop_sequence(q)
+            del live[q]
+        else:
+            live[nxt] = 0
+            nxt += 1
+        ids = list(live)
+        if not ids:
+            continue
+        k = rng.uniform(-1, 1, (len(ids), 128)).astype(np.float32)
+        v = rng.uniform(-1, 1, (len(ids), 128)).astype(np.float32)
+        q = rng.uniform(-1, 1, (len(ids), 128)).astype(np.float32)
+        pos = [live[i] for i in ids]
+        og = g.append_attend(0, ids, pos, q, k, v)
+        c.append_request(0, ids, pos, k, v)
+        oc = c.attend(0, ids, q)
+        assert np.abs(og - oc).max() < 2e-5
+        for i in ids:
+            live[i] += 1
+    assert g.token_count() == c.token_count()

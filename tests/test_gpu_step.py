@@ -1,0 +1,91 @@
+"""GPU StepComputation parity: the engine (S-Part + R-Part on one B200)
+against the oracle's decode_step_monolithic / run_monolithic and the
+reference's golden transcript."""
+import collections
+import os
+
+import numpy as np
+import pytest
+
+from conftest import upload_oracle_weights
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sd():
+    import paper_2403_11421_b200 as m
+    return m
+
+
+def _engine(sd, oracle, spec_args, seed=0, mode="exact", fmt="single", cap=1 << 16):
+    W = oracle.Weights(oracle.make_spec(*spec_args), seed)
+    dw = upload_oracle_weights(W, mode)
+    kv = sd.KvShard(dw.spec, 0, dw.spec.num_kv_heads, cap, fmt)
+    return W, dw, kv, sd.Engine(dw, kv)
+
+
+def test_golden_transcript_on_gpu(sd, oracle):
+    # proj/tests/test_dense.cpp:173-190: byte-exact against the fixture
+    W, dw, kv, eng = _engine(sd, oracle, (2, 64, 4, 256, 128))
+    recs, _, _ = sd.run_generation(eng, batch=3, target_len=20, interval=20, steps=20, seed=0)
+    with open(os.path.join(GOLDEN, "golden_transcript_2x64_3seq_20.csv")) as f:
+        assert sd.transcript_csv(recs) == f.read()
+
+
+def test_exact_dense_path_is_bitwise(sd, oracle):
+    """K7 reproduces apply_linear / project_qkv bit for bit (dense.cpp:16-43)."""
+    W = oracle.Weights(oracle.make_spec(1, 64, 4, 96, 50), 9)
+    dw = upload_oracle_weights(W, "exact")
+    x = np.random.default_rng(0).uniform(-1, 1, (7, 64)).astype(np.float32)
+    q, k, v = sd.project_qkv(dw, 0, x)
+    qo, ko, vo = oracle.project_qkv(W, 0, list(range(1, 8)), x)
+    assert np.array_equal(q, qo) and np.array_equal(k, ko) and np.array_equal(v, vo)
+    lg, tk = sd.output_logits_argmax(dw, x)
+    assert np.array_equal(lg, oracle.output_logits(W, x))
+    assert list(tk) == [oracle.argmax_token(r) for r in lg]
+    # finish_block differs only through device expf in silu: <= a few ulp
+    o = np.random.default_rng(1).uniform(-1, 1, (7, 64)).astype(np.float32)
+    fb = sd.finish_block(dw, 0, o, x)
+    assert np.abs(fb - oracle.finish_block(W, 0, o, x)).max() < 1e-5
+
+
+def test_monolithic_generation_matches_oracle(sd, oracle):
+    # proj/tests/test_workers.cpp:280-321: identical tokens, activations <= 1e-5
+    W, dw, kv, eng = _engine(sd, oracle, (2, 64, 4, 256, 128))
+    recs, acts, _ = sd.run_generation(eng, 8, 32, 32, 32, seed=0, record_activations=True)
+    orecs, oacts = oracle.run_monolithic(W, 8, 32, 32, 32, seed=0, record=True)
+    assert recs == orecs
+    assert np.abs(acts - oacts).max() <= 1e-5
+
+
+def test_stabilized_schedule_with_retirement(sd, oracle):
+    # proj/tests/test_workers.cpp:323-344
+    W, dw, kv, eng = _engine(sd, oracle, (2, 64, 4, 256, 128))
+    recs, acts, _ = sd.run_generation(eng, 8, 16, 4, 48, seed=0, record_activations=True)
+    orecs, oacts = oracle.run_monolithic(W, 8, 16, 4, 48, seed=0, record=True)
+    assert recs == orecs
+    assert np.abs(acts - oacts).max() <= 1e-5
+    recs, _, _ = sd.run_generation(eng, 12, 16, 4, 0, seed=0)
+    c = collections.Counter(q for _, q, _ in recs)
+    assert set(c.values()) == {16}
+
+
+def test_c1_tiny_config_matches_oracle(sd, oracle):
+    """BASELINE config 1: 2 layers, d=256 (hd 128), batch 16, context 128, fp32."""
+    W, dw, kv, eng = _engine(sd, oracle, (2, 256, 2, 1024, 256))
+    recs, acts, _ = sd.run_generation(eng, 16, 128, 128, 128, seed=0, record_activations=True)
+    orecs, oacts = oracle.run_monolithic(W, 16, 128, 128, 128, seed=0, record=True, threads=8)
+    assert recs == orecs
+    assert np.abs(acts - oacts).max() <= 1e-4
+
+
+def test_engine_capacity_error_is_typed(sd, oracle):
+    W, dw, kv, eng = _engine(sd, oracle, (2, 64, 4, 256, 128), cap=4)
+    toks = [1, 2, 3]
+    eng.compute([1, 2, 3], tokens=toks)
+    with pytest.raises(sd.CapacityError):
+        eng.compute([1, 2, 3], tokens=toks)
+    with pytest.raises(sd.ConfigError):
+        eng.compute([1, 1], tokens=[0, 0])
