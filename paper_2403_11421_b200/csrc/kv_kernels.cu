@@ -122,25 +122,31 @@ struct Fmt<SD_KV_INT8> {
 // Persistent split-K decode attention. One CTA per SM walks a contiguous,
 // balanced range of (item, position) pieces (host-built). Warp
 // kConsumerWarps is the producer: one lane streams T-position stages of the
-// item's K and V rows (all shard heads, contiguous inside a page group) into
-// an nstages-deep shared-memory ring with cp.async.bulk + mbarriers. The
-// 8 consumer warps are split into row groups of LPR = hd/8 lanes; each lane
-// owns 8 consecutive elements of a row, so a K·q dot is 8 FMAs plus log2(LPR)
-// xor-shuffles. Row group rg owns MAXH kv heads (and their G query heads) in
-// one position class; online softmax in the log2 domain; fp32 throughout.
-template <int FMT, int LPR, int MAXH, int G>
+// item's K and V rows (all shard heads, contiguous inside a page group; plus
+// the int8 scales) into an nstages-deep shared-memory ring with
+// cp.async.bulk + mbarriers. The consumer warps are split into row groups
+// of LPR lanes; each lane owns EPL consecutive elements of a head row, so a
+// K.q dot is EPL FMAs plus log2(LPR) xor-shuffles. Row group rg owns MAXH kv
+// heads (and their G query heads) in one position class. Rows are processed
+// in batches of PB positions per head: all K dots of a batch are issued
+// before any reduction (ILP), the online softmax rescales once per batch, in
+// the log2 domain, fp32 throughout.
+template <int FMT, int LPR, int EPL, int MAXH, int G>
 __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
   constexpr int E = Fmt<FMT>::kBytes;
-  constexpr int HD = LPR * 8;
+  constexpr int HD = LPR * EPL;
   constexpr int RGW = 32 / LPR;              // row groups per warp
   constexpr int RG = kConsumerWarps * RGW;   // row groups per CTA
   constexpr int MAXQ = MAXH * G;
+  constexpr int PB = 4;                      // positions per batch
+  constexpr int NC = EPL / 8;                // 8-element chunks per lane
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + a.nstages;
   uint8_t* ring = smem + 128 * ((16 * a.nstages + 127) / 128);
-  float* scratch = reinterpret_cast<float*>(ring + static_cast<size_t>(2) * a.nstages * a.stage_region);
+  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + 2 * a.sc_region;
+  float* scratch = reinterpret_cast<float*>(ring + stage_bytes * a.nstages);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -173,14 +179,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
           const int cnt = min(a.T, pc.p1 - pos);
           const int grp = pt[pos >> g.log2P];
           const int off = pos & (g.P - 1);
-          const uint8_t* base = layer_base + static_cast<int64_t>(grp) * g.group_bytes +
-                                static_cast<int64_t>(off) * g.pos_bytes;
+          const uint8_t* lb = layer_base + static_cast<int64_t>(grp) * g.group_bytes;
+          const uint8_t* base = lb + static_cast<int64_t>(off) * g.pos_bytes;
           const uint32_t bytes = static_cast<uint32_t>(cnt) * g.pos_bytes;
+          const uint32_t sbytes = a.sc_region ? static_cast<uint32_t>(cnt) * g.hc * 4u : 0u;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], 2 * bytes);
-          uint8_t* dst = ring + static_cast<size_t>(2 * stage) * a.stage_region;
+          mbar_expect_tx(&full[stage], 2 * bytes + 2 * sbytes);
+          uint8_t* dst = ring + stage * stage_bytes;
           bulk_g2s(dst, base, bytes, &full[stage], pol);
           bulk_g2s(dst + a.stage_region, base + g.v_off, bytes, &full[stage], pol);
+          if (sbytes) {
+            const uint8_t* sb = lb + static_cast<int64_t>(off) * g.hc * 4;
+            bulk_g2s(dst + 2 * a.stage_region, sb + g.ks_off, sbytes, &full[stage], pol);
+            bulk_g2s(dst + 2 * a.stage_region + a.sc_region, sb + g.vs_off, sbytes, &full[stage], pol);
+          }
           if (++stage == a.nstages) {
             stage = 0;
             phase ^= 1;
@@ -210,9 +222,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
     nh = cls < ncls ? 1 : 0;
   }
   const int Hq = hkv * G;
-  const int row_bytes = HD * E;
+  constexpr int row_bytes = HD * E;
+  const int tstep = ncls * PB;
 
-  float q[MAXQ][8], acc[MAXQ][8], m[MAXQ], l[MAXQ];
+  float q[MAXQ][EPL], acc[MAXQ][EPL], m[MAXQ], l[MAXQ];
   int stage = 0;
   uint32_t phase = 0;
 
@@ -225,18 +238,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
       m[j] = -INFINITY;
       l[j] = 0.0f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[j][i] = 0.0f;
+      for (int i = 0; i < EPL; ++i) acc[j][i] = 0.0f;
       if (hh < nh) {
         const int qh = (h0 + hh * hstride) * G + (j % G);
-        const float4* src = reinterpret_cast<const float4*>(qrow + qh * HD + li * 8);
-        const float4 x0 = src[0], x1 = src[1];
-        q[j][0] = x0.x * a.qscale; q[j][1] = x0.y * a.qscale;
-        q[j][2] = x0.z * a.qscale; q[j][3] = x0.w * a.qscale;
-        q[j][4] = x1.x * a.qscale; q[j][5] = x1.y * a.qscale;
-        q[j][6] = x1.z * a.qscale; q[j][7] = x1.w * a.qscale;
+        const float4* src = reinterpret_cast<const float4*>(qrow + qh * HD + li * EPL);
+#pragma unroll
+        for (int c = 0; c < EPL / 4; ++c) {
+          const float4 x = src[c];
+          q[j][4 * c + 0] = x.x * a.qscale;
+          q[j][4 * c + 1] = x.y * a.qscale;
+          q[j][4 * c + 2] = x.z * a.qscale;
+          q[j][4 * c + 3] = x.w * a.qscale;
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) q[j][i] = 0.0f;
+        for (int i = 0; i < EPL; ++i) q[j][i] = 0.0f;
       }
     }
     const int slot = a.item_slot[pc.item];
@@ -245,67 +261,125 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
     for (int pos = pc.p0; pos < pc.p1; pos += a.T) {
       const int cnt = min(a.T, pc.p1 - pos);
       mbar_wait(&full[stage], phase);
-      const uint8_t* Ks = ring + static_cast<size_t>(2 * stage) * a.stage_region;
+      const uint8_t* Ks = ring + stage * stage_bytes;
       const uint8_t* Vs = Ks + a.stage_region;
       const float* ksc = nullptr;
       const float* vsc = nullptr;
       if (FMT == SD_KV_INT8) {
-        const int grp = pt[pos >> g.log2P];
-        const uint8_t* lb = layer_base + static_cast<int64_t>(grp) * g.group_bytes;
-        const int off = pos & (g.P - 1);
-        ksc = reinterpret_cast<const float*>(lb + g.ks_off) + off * hkv;
-        vsc = reinterpret_cast<const float*>(lb + g.vs_off) + off * hkv;
+        if (a.sc_region) {
+          ksc = reinterpret_cast<const float*>(Ks + 2 * a.stage_region);
+          vsc = reinterpret_cast<const float*>(Ks + 2 * a.stage_region + a.sc_region);
+        } else {
+          const int grp = pt[pos >> g.log2P];
+          const uint8_t* lb = layer_base + static_cast<int64_t>(grp) * g.group_bytes;
+          const int off = pos & (g.P - 1);
+          ksc = reinterpret_cast<const float*>(lb + g.ks_off) + off * hkv;
+          vsc = reinterpret_cast<const float*>(lb + g.vs_off) + off * hkv;
+        }
       }
       // warp-uniform trip count: every lane runs every shuffle
-      for (int t0 = 0; t0 < a.T; t0 += ncls) {
-        const int t = t0 + cls;
-        const bool tact = t < cnt;
+      for (int t0 = 0; t0 < a.T; t0 += tstep) {
+        float sc[MAXH][PB][G];
+        // (A) all K dots of the batch, independent chains
 #pragma unroll
         for (int hh = 0; hh < MAXH; ++hh) {
-          const bool act = tact && hh < nh;
           const int hk = h0 + hh * hstride;
-          float kx[8];
-          if (act) {
-            Fmt<FMT>::load8(Ks + static_cast<size_t>(t * hkv + hk) * row_bytes + li * 8 * E, kx);
-          } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) kx[i] = 0.0f;
+          for (int i = 0; i < PB; ++i) {
+            const int t = t0 + cls + ncls * i;
+            const bool act = t < cnt && hh < nh;
+#pragma unroll
+            for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] = 0.0f;
+            if (act) {
+              const uint8_t* kr = Ks + static_cast<size_t>(t * hkv + hk) * row_bytes + li * EPL * E;
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                float kx[8];
+                Fmt<FMT>::load8(kr + c * 8 * E, kx);
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) sc[hh][i][gg] = fmaf(q[hh * G + gg][c * 8 + e], kx[e], sc[hh][i][gg]);
+                }
+              }
+            }
           }
-          float s[G];
+        }
+        // (B) reductions over the LPR lanes of each row, pipelined
 #pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            float d = 0.0f;
+        for (int sh = LPR / 2; sh > 0; sh >>= 1) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) d = fmaf(q[hh * G + gg][i], kx[i], d);
+          for (int hh = 0; hh < MAXH; ++hh)
 #pragma unroll
-            for (int sh = LPR / 2; sh > 0; sh >>= 1) d += __shfl_xor_sync(0xffffffffu, d, sh);
-            s[gg] = d;
-          }
-          if (act) {
-            float vx[8];
-            Fmt<FMT>::load8(Vs + static_cast<size_t>(t * hkv + hk) * row_bytes + li * 8 * E, vx);
-            float vscale = 1.0f;
-            if (FMT == SD_KV_INT8) {
-              const float kscale = ksc[t * hkv + hk];
+            for (int i = 0; i < PB; ++i)
 #pragma unroll
-              for (int gg = 0; gg < G; ++gg) s[gg] *= kscale;
-              vscale = vsc[t * hkv + hk];
+              for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] += __shfl_xor_sync(0xffffffffu, sc[hh][i][gg], sh);
+        }
+        // (C) block online softmax per (head, query)
+        float p[MAXH][PB][G];
+        float vs[MAXH][PB];
+#pragma unroll
+        for (int hh = 0; hh < MAXH; ++hh) {
+          const int hk = h0 + hh * hstride;
+#pragma unroll
+          for (int i = 0; i < PB; ++i) {
+            const int t = t0 + cls + ncls * i;
+            const bool act = t < cnt && hh < nh;
+            float ks = 1.0f;
+            vs[hh][i] = 1.0f;
+            if (FMT == SD_KV_INT8 && act) {
+              ks = ksc[t * hkv + hk];
+              vs[hh][i] = vsc[t * hkv + hk];
             }
 #pragma unroll
-            for (int gg = 0; gg < G; ++gg) {
-              const int j = hh * G + gg;
-              if (s[gg] > m[j]) {
-                const float c = fast_exp2(m[j] - s[gg]);
-                l[j] *= c;
+            for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] = act ? sc[hh][i][gg] * ks : -INFINITY;
+          }
 #pragma unroll
-                for (int i = 0; i < 8; ++i) acc[j][i] *= c;
-                m[j] = s[gg];
+          for (int gg = 0; gg < G; ++gg) {
+            const int j = hh * G + gg;
+            float mb = sc[hh][0][gg];
+#pragma unroll
+            for (int i = 1; i < PB; ++i) mb = fmaxf(mb, sc[hh][i][gg]);
+            const float mn = fmaxf(m[j], mb);
+            if (mn == -INFINITY) {
+#pragma unroll
+              for (int i = 0; i < PB; ++i) p[hh][i][gg] = 0.0f;
+              continue;
+            }
+            const float c = fast_exp2(m[j] - mn);
+            float ps = 0.0f;
+#pragma unroll
+            for (int i = 0; i < PB; ++i) {
+              p[hh][i][gg] = fast_exp2(sc[hh][i][gg] - mn);
+              ps += p[hh][i][gg];
+            }
+            l[j] = fmaf(l[j], c, ps);
+            m[j] = mn;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) acc[j][e] *= c;
+          }
+        }
+        // (D) V accumulation
+#pragma unroll
+        for (int hh = 0; hh < MAXH; ++hh) {
+          const int hk = h0 + hh * hstride;
+#pragma unroll
+          for (int i = 0; i < PB; ++i) {
+            const int t = t0 + cls + ncls * i;
+            const bool act = t < cnt && hh < nh;
+            if (act) {
+              const uint8_t* vr = Vs + static_cast<size_t>(t * hkv + hk) * row_bytes + li * EPL * E;
+#pragma unroll
+              for (int c = 0; c < NC; ++c) {
+                float vx[8];
+                Fmt<FMT>::load8(vr + c * 8 * E, vx);
+#pragma unroll
+                for (int gg = 0; gg < G; ++gg) {
+                  const float pv = FMT == SD_KV_INT8 ? p[hh][i][gg] * vs[hh][i] : p[hh][i][gg];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) acc[hh * G + gg][c * 8 + e] = fmaf(pv, vx[e], acc[hh * G + gg][c * 8 + e]);
+                }
               }
-              const float p = fast_exp2(s[gg] - m[j]);
-              l[j] += p;
-              const float pv = p * vscale;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[j][i] = fmaf(pv, vx[i], acc[j][i]);
             }
           }
         }
@@ -332,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
               d[1] = l[j];
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) d[2 + li * 8 + i] = acc[j][i];
+            for (int i = 0; i < EPL; ++i) d[2 + li * EPL + i] = acc[j][i];
           }
         }
       }
@@ -346,11 +420,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
               const float* sp = src + j * (HD + 2);
               const float m2 = sp[0], l2 = sp[1];
               const float M = fmaxf(m[j], m2);
-              const float ca = fast_exp2(m[j] - M);
+              const float ca = m[j] == -INFINITY ? 0.0f : fast_exp2(m[j] - M);
               const float cb2 = m2 == -INFINITY ? 0.0f : fast_exp2(m2 - M);
               l[j] = l[j] * ca + l2 * cb2;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) acc[j][i] = acc[j][i] * ca + sp[2 + li * 8 + i] * cb2;
+              for (int i = 0; i < EPL; ++i) acc[j][i] = acc[j][i] * ca + sp[2 + li * EPL + i] * cb2;
               m[j] = M;
             }
           }
@@ -367,13 +441,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
           const int qh = (h0 + (j / G) * hstride) * G + (j % G);
           if (direct) {
             const float inv = 1.0f / l[j];
-            float4* dst = reinterpret_cast<float4*>(orow + qh * HD + li * 8);
-            dst[0] = make_float4(acc[j][0] * inv, acc[j][1] * inv, acc[j][2] * inv, acc[j][3] * inv);
-            dst[1] = make_float4(acc[j][4] * inv, acc[j][5] * inv, acc[j][6] * inv, acc[j][7] * inv);
+            float4* dst = reinterpret_cast<float4*>(orow + qh * HD + li * EPL);
+#pragma unroll
+            for (int c = 0; c < EPL / 4; ++c) {
+              dst[c] = make_float4(acc[j][4 * c] * inv, acc[j][4 * c + 1] * inv,
+                                   acc[j][4 * c + 2] * inv, acc[j][4 * c + 3] * inv);
+            }
           } else {
-            float* pa = a.part_acc + static_cast<int64_t>(w) * Hq * HD + qh * HD + li * 8;
-            reinterpret_cast<float4*>(pa)[0] = make_float4(acc[j][0], acc[j][1], acc[j][2], acc[j][3]);
-            reinterpret_cast<float4*>(pa)[1] = make_float4(acc[j][4], acc[j][5], acc[j][6], acc[j][7]);
+            float4* pa = reinterpret_cast<float4*>(a.part_acc + static_cast<int64_t>(w) * Hq * HD + qh * HD + li * EPL);
+#pragma unroll
+            for (int c = 0; c < EPL / 4; ++c) {
+              pa[c] = make_float4(acc[j][4 * c], acc[j][4 * c + 1], acc[j][4 * c + 2], acc[j][4 * c + 3]);
+            }
             if (li == 0) {
               float* pm = a.part_ml + (static_cast<int64_t>(w) * Hq + qh) * 2;
               pm[0] = m[j];
@@ -601,68 +680,94 @@ __global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* sl
 // ------------------------------------------------------------ dispatch ---
 using AttnFn = void (*)(const AttnArgs);
 
-template <int FMT, int LPR>
+template <int FMT, int LPR, int EPL>
 AttnFn pick_mh(int maxh, int G) {
   if (G == 1) {
     switch (maxh) {
-      case 1: return attn_kernel<FMT, LPR, 1, 1>;
-      case 2: return attn_kernel<FMT, LPR, 2, 1>;
-      case 3: return attn_kernel<FMT, LPR, 3, 1>;
-      case 4: return attn_kernel<FMT, LPR, 4, 1>;
+      case 1: return attn_kernel<FMT, LPR, EPL, 1, 1>;
+      case 2: return attn_kernel<FMT, LPR, EPL, 2, 1>;
+      case 3: return attn_kernel<FMT, LPR, EPL, 3, 1>;
       default: return nullptr;
     }
   }
-  if (maxh != 1) return nullptr;
+  if (maxh != 1 || EPL != 8) return nullptr;
   switch (G) {
-    case 2: return attn_kernel<FMT, LPR, 1, 2>;
-    case 4: return attn_kernel<FMT, LPR, 1, 4>;
-    case 8: return attn_kernel<FMT, LPR, 1, 8>;
+    case 2: return attn_kernel<FMT, LPR, 8, 1, 2>;
+    case 4: return attn_kernel<FMT, LPR, 8, 1, 4>;
     default: return nullptr;
   }
 }
 
 template <int FMT>
-AttnFn pick_lpr(int lpr, int maxh, int G) {
-  switch (lpr) {
-    case 2: return pick_mh<FMT, 2>(maxh, G);
-    case 4: return pick_mh<FMT, 4>(maxh, G);
-    case 8: return pick_mh<FMT, 8>(maxh, G);
-    case 16: return pick_mh<FMT, 16>(maxh, G);
-    case 32: return pick_mh<FMT, 32>(maxh, G);
+AttnFn pick_fmt(const AttnConfig& c, int G) {
+  if (c.epl == 16) {
+    switch (c.lpr) {
+      case 8: return pick_mh<FMT, 8, 16>(c.maxh, G);
+      case 16: return pick_mh<FMT, 16, 16>(c.maxh, G);
+      default: return nullptr;
+    }
+  }
+  switch (c.lpr) {
+    case 2: return pick_mh<FMT, 2, 8>(c.maxh, G);
+    case 4: return pick_mh<FMT, 4, 8>(c.maxh, G);
+    case 8: return pick_mh<FMT, 8, 8>(c.maxh, G);
+    case 16: return pick_mh<FMT, 16, 8>(c.maxh, G);
+    case 32: return pick_mh<FMT, 32, 8>(c.maxh, G);
     default: return nullptr;
   }
 }
 
 AttnFn pick(const KvGeom& g, int G) {
-  if (g.hd % 8 != 0) return nullptr;
-  const int lpr = g.hd / 8;
-  if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) return nullptr;
-  if (g.pos_bytes % 16 != 0) return nullptr;
-  const int RG = kConsumerWarps * (32 / lpr);
-  const int maxh = g.hc >= RG ? (g.hc + RG - 1) / RG : 1;
+  const AttnConfig c = choose_attn_config(g, G);
+  if (!c.supported) return nullptr;
   switch (g.fmt) {
-    case SD_KV_SINGLE: return pick_lpr<SD_KV_SINGLE>(lpr, maxh, G);
-    case SD_KV_HALF: return pick_lpr<SD_KV_HALF>(lpr, maxh, G);
-    case SD_KV_INT8: return pick_lpr<SD_KV_INT8>(lpr, maxh, G);
+    case SD_KV_SINGLE: return pick_fmt<SD_KV_SINGLE>(c, G);
+    case SD_KV_HALF: return pick_fmt<SD_KV_HALF>(c, G);
+    case SD_KV_INT8: return pick_fmt<SD_KV_INT8>(c, G);
     default: return nullptr;
   }
 }
 
 }  // namespace
 
+// Lanes per head row (LPR) and elements per lane (EPL): EPL = 16 when it
+// balances the heads over the row groups at least as well as EPL = 8 (fewer
+// shuffles per element), else 8. Heads per row group MAXH <= 3, G <= 4.
+AttnConfig choose_attn_config(const KvGeom& g, int G) {
+  AttnConfig best{false, 0, 0, 0, 0};
+  if (g.hd % 8 != 0 || g.pos_bytes % 16 != 0) return best;
+  double best_eff = -1.0;
+  for (int epl : {16, 8}) {
+    if (g.hd % epl != 0) continue;
+    const int lpr = g.hd / epl;
+    if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) continue;
+    if (epl == 16 && (G != 1 || (lpr != 8 && lpr != 16))) continue;
+    const int rg = kConsumerWarps * (32 / lpr);
+    const int maxh = g.hc >= rg ? (g.hc + rg - 1) / rg : 1;
+    if (maxh > 3 || (G > 1 && maxh != 1) || (G != 1 && G != 2 && G != 4)) continue;
+    const double eff = g.hc >= rg ? static_cast<double>(g.hc) / (rg * maxh) : 1.0;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = AttnConfig{true, lpr, epl, maxh, rg};
+    }
+  }
+  return best;
+}
+
 int attention_consumer_warps() { return kConsumerWarps; }
 
-size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region) {
+size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region,
+                            int* sc_region) {
   const int region = ((T * g.pos_bytes + 127) / 128) * 128;
   *stage_region = region;
-  size_t bytes = 128 * ((16 * nstages + 127) / 128) + static_cast<size_t>(2) * nstages * region;
-  if (g.hd % 8 == 0) {
-    const int lpr = g.hd / 8;
-    const int RG = kConsumerWarps * (32 / (lpr > 0 ? lpr : 1));
-    if (g.hc < RG) {
-      // class-merge scratch: RG x MAXQ x (hd + 2) floats
-      bytes += static_cast<size_t>(RG) * G * (g.hd + 2) * sizeof(float);
-    }
+  *sc_region = 0;
+  if (g.fmt == SD_KV_INT8 && g.hc % 4 == 0) *sc_region = ((T * g.hc * 4 + 127) / 128) * 128;
+  size_t bytes = 128 * ((16 * nstages + 127) / 128) +
+                 static_cast<size_t>(nstages) * (2 * region + 2 * *sc_region);
+  const AttnConfig c = choose_attn_config(g, G);
+  if (c.supported && g.hc < c.rg) {
+    // class-merge scratch: RG x MAXQ x (hd + 2) floats
+    bytes += static_cast<size_t>(c.rg) * G * (g.hd + 2) * sizeof(float);
   }
   return bytes;
 }

@@ -65,7 +65,15 @@ struct AttnArgs {
   int32_t T;                  // positions per pipeline stage
   int32_t nstages;
   int32_t stage_region;       // bytes of one K (or V) stage region (128-B aligned)
+  int32_t sc_region;          // bytes of one int8 scale region per stage (0: scales read from L2)
 };
+
+// Static shape of the fast attention kernel for a geometry (kv_kernels.cu).
+struct AttnConfig {
+  bool supported;
+  int lpr, epl, maxh, rg;
+};
+AttnConfig choose_attn_config(const KvGeom& g, int G);
 
 struct CombineArgs {
   const int4* items;  // [m] (item, first piece, piece count, -)
@@ -86,6 +94,7 @@ void launch_combine(const CombineArgs& a, cudaStream_t s);
 void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots,
                               int n, int length, uint64_t salt, cudaStream_t s);
 int attention_consumer_warps();
-size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region);
+size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region,
+                            int* sc_region);
 
 }  // namespace sd

@@ -95,11 +95,13 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   // pipeline geometry for the attention kernel: T positions per stage,
   // 2*T*pos_bytes <= 32 KB, as many stages as fit ~200 KB of shared memory
   T_ = 1;
-  while (T_ * 2 <= P && 2 * (T_ * 2) * g.pos_bytes <= 32 * 1024) T_ *= 2;
-  int region = 0;
+  while (T_ * 2 <= P && 2 * (T_ * 2) * g.pos_bytes <= 64 * 1024) T_ *= 2;
+  int region = 0, sregion = 0;
   nstages_ = 8;
-  while (nstages_ > 2 && attention_smem_bytes(g, T_, nstages_, G_, &region) > 220 * 1024) --nstages_;
-  attn_smem_ = attention_smem_bytes(g, T_, nstages_, G_, &stage_region_);
+  while (nstages_ > 2 && attention_smem_bytes(g, T_, nstages_, G_, &region, &sregion) > 210 * 1024) {
+    --nstages_;
+  }
+  attn_smem_ = attention_smem_bytes(g, T_, nstages_, G_, &stage_region_, &sc_region_);
 
   ring_.resize(8);
   for (Blob& b : ring_) SD_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
@@ -408,6 +410,7 @@ void KvStore::launch_attention_plan(int layer, const float* q, int64_t qs, float
   a.T = T_;
   a.nstages = nstages_;
   a.stage_region = stage_region_;
+  a.sc_region = sc_region_;
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timing_) {

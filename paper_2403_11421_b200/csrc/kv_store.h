@@ -78,7 +78,7 @@ class KvStore {
   int device_;
   int nsm_ = 148;
   KvGeom geom_{};
-  int T_ = 1, nstages_ = 2, stage_region_ = 0;
+  int T_ = 1, nstages_ = 2, stage_region_ = 0, sc_region_ = 0;
   size_t attn_smem_ = 0;
   int max_seqs_ = 0, max_len_ = 0, pool_groups_ = 0;
 
