@@ -1,0 +1,335 @@
+"""Decode benchmark for the B200 FastDecode hot path (BASELINE.json metric:
+decode tokens/sec at 1/2/4/8 B200; R-Part HBM GB/s as % of peak).
+
+One "step" = one full decode step (all layers: QKV GEMM, KV append,
+split-K attention over the KV cache, W_o + MLP GEMMs, head + argmax) over the
+resident batch, exactly StepComputation::compute (workers.hpp:151-158).
+
+Default workload (N=1): BASELINE config 5, Llama-3-8B GQA shape at batch 512,
+context 2048 — the largest BASELINE config whose full 32-layer KV cache fits
+one B200 (config 2, Llama-2-7B at B=1024 / ctx 1024, needs 550 GB of fp16 KV;
+its R-Part is measured per layer and reported as `r_part_c2`). Synthetic
+counter-hash weights and KV prefill; inputs (137 GB of KV) exceed the 126 MB
+L2 by 1000x, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (layers, model_dim, heads, kv_heads, mlp_dim, vocab, batch/GPU, context, kv fmt, dense)
+    "c5-llama3-8b-gqa-b512-ctx2048": (32, 4096, 32, 8, 14336, 128256, 512, 2048, "half", "bf16"),
+    "c5-llama3-8b-gqa-b512-ctx1024": (32, 4096, 32, 8, 14336, 128256, 512, 1024, "half", "bf16"),
+    "c1-tiny-b16-ctx128": (2, 256, 2, 2, 1024, 256, 16, 128, "single", "exact"),
+}
+DEFAULT = "c5-llama3-8b-gqa-b512-ctx2048"
+METRIC = "decode tokens/sec at 1/2/4/8 B200; R-Part HBM GB/s as % of peak"
+
+
+def peaks():
+    p = {"hbm_gbs": 6524.0, "bf16_tflops": 1657.6, "bf16_tflops_sustained": 1413.6, "src": "measured"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: float(m[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+    except (OSError, ValueError, KeyError):
+        p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+    return p
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.p = None
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [s for s in sm if s > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_estimate(wl, threads, reps=1):
+    """Reference CPU path (the oracle port of KvShard::attend and
+    apply_linear/finish_block, built -O2 -ffp-contract=off) timed on this
+    host on a bounded sample, turned into decode tokens/s with the
+    reference's own performance model: step = N*(T(B) + R(B)) + head
+    (serial S then R, as in decode_step_monolithic; dense.cpp:90-129)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    L, D, H, Hkv, F, V, B, ctx, fmt, _ = wl
+    spec = oracle.make_spec(1, D, H, F, 8, Hkv)
+    n_s = max(2 * threads, 8)
+    b_s = 16
+    t0 = time.perf_counter()
+    t_att = oracle.bench_attend(spec, n_s, ctx, fmt, threads, reps)
+    t_dense = oracle.bench_dense(spec, b_s, threads, reps)
+    wall = time.perf_counter() - t0
+    kvw = Hkv * (D // H)
+    flop_tok_layer = 2 * D * (D + 2 * kvw) + 2 * D * D + 4 * D * F
+    dense_flops = b_s * flop_tok_layer / t_dense
+    r_layer = t_att * B / n_s
+    s_layer = t_dense * B / b_s
+    head = 2.0 * D * V * B / dense_flops
+    step = L * (s_layer + r_layer) + head
+    kv_bytes = n_s * ctx * 2 * kvw * {"single": 4, "half": 2, "int8": 1}[fmt]
+    return {"value": B / step, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle KvShard::attend over {n_s} seqs x ctx {ctx} ({fmt} KV, 1 layer) + "
+                       f"project_qkv/finish_block at B={b_s} (1 layer), {threads} host threads; "
+                       f"scaled by the reference model B/(N*(T(B)+R)+head) to B={B}, N={L}"),
+            "r_part_gbs": kv_bytes / t_att / 1e9, "dense_gflops": dense_flops / 1e9,
+            "sample_wall_s": wall}
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, wl, rank, world, dev, dist):
+    import numpy as np
+    import torch
+    import paper_2403_11421_b200 as sd
+
+    L, D, H, Hkv, F, V, B, ctx, fmt, dense = wl
+    pk = peaks()
+    spec = sd.make_model_spec(L, D, H, F, V, Hkv)
+    steps_total = args.warmup + args.steps + args.e2e_steps + 8
+    weights = sd.DeviceWeights(spec, None, dense, dev, seed=rank)
+    kv = sd.KvShard(spec, 0, spec.num_kv_heads, B * (ctx + steps_total), fmt, dev,
+                    max_sequences=B, max_seq_len=ctx + steps_total + 16)
+    eng = sd.Engine(weights, kv)
+    # sequence ids of this rank's shard: ids whose mix64 hash lands here
+    # (ShardMap by-sequence, transport.cpp:352-353), B per GPU
+    seqs, q = [], 1
+    while len(seqs) < B:
+        if world == 1 or sd.mix64(q) % world == rank:
+            seqs.append(q)
+        q += 1
+    kv.prefill_synthetic(seqs, ctx, salt=rank)
+    tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
+
+    # warm-up (untimed)
+    _, tok = eng.bench(seqs, tokens, args.warmup)
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed region: K steps, CUDA events on the engine stream
+    kv.timing(True)
+    eng.timing(True)
+    kv.timing_read(reset=True)
+    eng.timing_read(reset=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = Clocks(dev)
+    l0 = sd.launch_count()
+    ms, tok = eng.bench(seqs, tok, args.steps)
+    l1 = sd.launch_count()
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    a_ms, a_n, a_bytes = kv.timing_read()
+    g_ms, g_flops, g_n = eng.timing_read()
+    kv.timing(False)
+    eng.timing(False)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tokens_total = B * world * args.steps
+    value = tokens_total / (ms / 1e3)
+
+    # ---- end to end through the public C-ABI with host buffers: every step
+    # copies the step's token ids H2D from pinned memory and reads the next
+    # tokens back D2H (sd_engine_step is synchronous)
+    pin_in = torch.empty(B, dtype=torch.int32).pin_memory().numpy()
+    pin_in[:] = tok
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        nxt, _ = eng.compute(seqs, tokens=pin_in)
+        pin_in[:] = nxt
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": B * world * args.e2e_steps / e2e_s, "unit": "tokens/s",
+           "h2d_bytes_per_step": int(B * 4), "d2h_bytes_per_step": int(B * 4),
+           "steps": args.e2e_steps, "api": "sd_engine_step (include/sd_abi.h)"}
+
+    eng.close()
+    kv.close()
+    weights.close()
+
+    extra = {}
+    if rank == 0 and world == 1 and not args.no_c2:
+        extra["r_part_c2"] = rpart_c2(sd, torch, dev, pk)
+    achieved = a_bytes / (a_ms / 1e3) / 1e9 if a_ms > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                traffic = json.load(f).get(args.workload)
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-hash weights and KV prefill; no checkpoint)",
+        "config": {"workload": args.workload, "model": "Llama-3-8B GQA shape (reference 2-matrix SiLU MLP)",
+                   "layers": L, "model_dim": D, "heads": H, "kv_heads": Hkv, "mlp_dim": F, "vocab": V,
+                   "batch_per_gpu": B, "global_batch": B * world, "context": ctx, "kv_format": fmt,
+                   "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
+                   "parallelism": f"kv-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
+        "roofline": {"bound": "hbm", "kernel": "attn_kernel (split-K decode attention)",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "launches": a_n, "ms_per_launch": a_ms / max(a_n, 1),
+                     "share_of_step": a_ms / ms if ms else None,
+                     "peak_src": pk["src"] + " (MEASURED_PEAKS.json hbm_gbs)"},
+        "s_part": {"bound": "tensor", "achieved": g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0,
+                   "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                   "frac": (g_flops / (g_ms / 1e3) / 1e12) / pk["bf16_tflops_sustained"] if g_ms else 0.0,
+                   "share_of_step": g_ms / ms if ms else None, "launches": g_n},
+        "e2e": e2e,
+        "gpu_launches": int(l1 - l0),
+        "clocks": clocks,
+    }
+    line.update(extra)
+    return line
+
+
+def rpart_c2(sd, torch, dev, pk):
+    """BASELINE config 2 R-Part: Llama-2-7B heads (32 x 128, MHA), B=1024,
+    ctx 1024, fp16 KV, one layer resident (full depth needs 550 GB)."""
+    spec = sd.make_model_spec(1, 4096, 32, 11008, 32000)
+    B, ctx = 1024, 1024
+    kv = sd.KvShard(spec, 0, 32, B * (ctx + 1), "half", dev, max_sequences=B, max_seq_len=ctx + 16)
+    seqs = list(range(1, B + 1))
+    kv.prefill_synthetic(seqs, ctx)
+    q = torch.randn(B, 4096, device=f"cuda:{dev}")
+    o = torch.empty_like(q)
+    for _ in range(3):
+        kv.attend_dev(0, seqs, q.data_ptr(), o.data_ptr())
+    torch.cuda.synchronize(dev)
+    kv.timing(True)
+    kv.timing_read(reset=True)
+    for _ in range(10):
+        kv.attend_dev(0, seqs, q.data_ptr(), o.data_ptr())
+    ms, n, byt = kv.timing_read()
+    kv.close()
+    gbs = byt / (ms / 1e3) / 1e9
+    return {"workload": "c2 Llama-2-7B MHA heads, B=1024, ctx 1024, fp16 KV, 1 layer",
+            "ms_per_layer": ms / n, "achieved_gbs": gbs, "frac": gbs / pk["hbm_gbs"],
+            "projected_32_layer_r_ms": 32 * ms / n}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=DEFAULT, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        # the reference CPU path (oracle port), rank 0 only, all host threads
+        if rank != 0:
+            return
+        threads = host_threads()
+        vals, last = [], None
+        for _ in range(args.warmup if args.warmup < 2 else 1):
+            cpu_estimate(wl, threads)
+        for _ in range(args.steps):
+            last = cpu_estimate(wl, threads)
+            vals.append(last["value"])
+        v = statistics.median(vals)
+        L, D, H, Hkv, F, V, B, ctx, fmt, dense = wl
+        out = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * B / v,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic", "impl": "reference",
+               "config": {"workload": args.workload, "batch_per_gpu": B, "context": ctx,
+                          "kv_format": fmt, "layers": L},
+               "cpu_baseline": {k: last[k] for k in ("kind", "cores", "sample")} | {"value": v, "unit": "tokens/s"},
+               "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        torch.cuda.set_device(local)
+        tdist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist = tdist
+    torch.cuda.set_device(local)
+    line = run_ours(args, wl, rank, world, local, dist)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_estimate(wl, host_threads())
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

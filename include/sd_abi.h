@@ -194,6 +194,16 @@ int sd_engine_retire(sd_engine* e, int32_t n, const uint64_t* seqs);
  * resident batch (tokens fed back on device), returns device milliseconds. */
 int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t* tokens,
                     int32_t steps, int32_t* next_tokens, double* device_ms);
+/* CUDA-event timing of the engine's S-Part GEMM launches (sum of kernel
+ * milliseconds and algorithmic flops since the last reset). */
+int sd_engine_timing(sd_engine* e, int enable);
+int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* launches, int reset);
+/* Kernel launches issued by this library in this process (all devices). */
+int64_t sd_launch_count(void);
+/* Synthetic device-generated weights (uniform +-1/sqrt(fan_in), counter
+ * hash of `seed`) in the requested dense mode: the full-size bench. */
+int sd_weights_synthetic(const sd_model_spec* spec, int dense_mode, uint64_t seed, int device,
+                         sd_weights** out);
 
 /* drive_schedule (workers.cpp:547-684) over the GPU engine. cold_start: 0
  * fixed-interval, 1 ramped-limit (scheduler.hpp:99). steps <= 0 runs to

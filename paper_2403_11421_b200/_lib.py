@@ -95,6 +95,10 @@ SIGNATURES = {
     "sd_engine_step_features": (C.c_int, [P, C.c_int32, U64P, FP, I32P, FP, FP]),
     "sd_engine_retire": (C.c_int, [P, C.c_int32, U64P]),
     "sd_engine_bench": (C.c_int, [P, C.c_int32, U64P, I32P, C.c_int32, I32P, DP]),
+    "sd_engine_timing": (C.c_int, [P, C.c_int]),
+    "sd_engine_timing_read": (C.c_int, [P, DP, DP, I64P, C.c_int]),
+    "sd_launch_count": (C.c_int64, []),
+    "sd_weights_synthetic": (C.c_int, [SPEC_P, C.c_int, C.c_uint64, C.c_int, PP]),
     "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_drive_count": (C.c_int64, [P]),
     "sd_drive_record": (C.c_int, [P, C.c_int64, I64P, U64P, I32P]),

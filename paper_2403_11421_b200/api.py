@@ -89,6 +89,11 @@ def make_model_spec(num_layers: int, model_dim: int, num_heads: int, mlp_dim: in
     return s
 
 
+def launch_count() -> int:
+    """Kernel launches issued by libsd_b200 in this process."""
+    return int(lib.sd_launch_count())
+
+
 def mix64(x: int) -> int:
     return int(lib.sd_mix64(x & (2**64 - 1)))
 
@@ -281,13 +286,13 @@ class DeviceWeights:
     tensors=None generates synthetic weights on the device."""
 
     def __init__(self, spec: ModelSpec, tensors: Sequence[np.ndarray] | None, mode: str = "exact",
-                 device: int = 0):
+                 device: int = 0, seed: int = 0):
         self.spec = spec
         self.mode = mode
         self.h = C.c_void_p()
         if tensors is None:
-            _check(lib.sd_weights_upload(C.byref(spec), None, DENSE_MODES[mode], device,
-                                         C.byref(self.h)))
+            _check(lib.sd_weights_synthetic(C.byref(spec), DENSE_MODES[mode], seed, device,
+                                            C.byref(self.h)))
         else:
             self._keep = [_f32(t).reshape(-1) for t in tensors]
             arr = (FP * len(self._keep))(*[_fp(t) for t in self._keep])
@@ -382,6 +387,15 @@ class Engine:
     def retire(self, seqs):
         s, sp = _u64(seqs)
         _check(lib.sd_engine_retire(self.h, len(s), sp))
+
+    def timing(self, enable: bool):
+        """CUDA-event timing of the S-Part GEMMs."""
+        _check(lib.sd_engine_timing(self.h, int(enable)))
+
+    def timing_read(self, reset=True):
+        ms, fl, n = C.c_double(), C.c_double(), C.c_int64()
+        _check(lib.sd_engine_timing_read(self.h, C.byref(ms), C.byref(fl), C.byref(n), int(reset)))
+        return ms.value, fl.value, n.value
 
     def bench(self, seqs, tokens, steps: int):
         """Device-timed loop of `steps` decode steps; returns (ms, next_tokens)."""

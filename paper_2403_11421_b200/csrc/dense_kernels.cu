@@ -140,6 +140,7 @@ void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, co
   dim3 grid((out + kCols - 1) / kCols, (B + kRows - 1) / kRows);
   linear_exact_kernel<<<grid, kCols, 0, s>>>(B, in, out, x, ldx, w, ldw, y, ldy, epi, res, ldr);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
@@ -147,6 +148,7 @@ void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* 
   if (B == 0) return;
   embed_kernel<<<B, 256, 0, s>>>(B, D, tokens, emb, x, ldx, xb);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
@@ -154,6 +156,7 @@ void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* token
   if (B == 0) return;
   argmax_kernel<<<B, 512, 0, s>>>(V, logits, ld, tokens);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat16* y,
@@ -162,6 +165,7 @@ void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat
   dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, rows);
   to_bf16_kernel<<<grid, 256, 0, s>>>(rows, cols, x, ldx, y, ldy);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 }  // namespace sd

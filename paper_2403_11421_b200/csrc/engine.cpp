@@ -144,6 +144,7 @@ Weights::Weights(const Spec& spec, const float* const* tensors, int mode, int de
     dim3 grid((out + 31) / 32, (in + 31) / 32);
     pack_kernel<<<grid, dim3(32, 8)>>>(static_cast<const float*>(tmp.p), in, out, dst, ld, off, mode_);
     SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
   };
   uint8_t* b = static_cast<uint8_t*>(blob_);
   for (int l = 0; l < spec.L; ++l) {
@@ -173,6 +174,7 @@ Weights::Weights(const Spec& spec, int mode, uint64_t seed, int device)
   auto gen = [&](int in, int out, void* dst, int64_t ld, int off, float scale) {
     synth_weight_kernel<<<148 * 8, 256>>>(in, out, dst, ld, off, mode_, salt, scale);
     SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
     salt = mix64(salt);
   };
   synth_embedding_kernel<<<148 * 8, 256>>>(static_cast<int64_t>(D) * V, emb_, salt);
@@ -300,24 +302,66 @@ void Engine::ensure(int B) {
   pos_.resize(b);
 }
 
+void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
+                  const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
+                  int64_t ldyb, int epi, const float* res, int64_t ldr) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing_) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (ev_pool_.empty()) {
+        SD_CUDA(cudaEventCreate(e));
+      } else {
+        *e = ev_pool_.back();
+        ev_pool_.pop_back();
+      }
+    }
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_);
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    ev_flops_.push_back(2.0 * B * w_->out_dim(which) * w_->in_dim(which));
+  }
+}
+
+void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool reset) {
+  for (size_t i = 0; i < ev_.size(); ++i) {
+    SD_CUDA(cudaEventSynchronize(ev_[i].second));
+    float t = 0;
+    SD_CUDA(cudaEventElapsedTime(&t, ev_[i].first, ev_[i].second));
+    t_ms_ += t;
+    t_flops_ += ev_flops_[i];
+    t_n_ += 1;
+    ev_pool_.push_back(ev_[i].first);
+    ev_pool_.push_back(ev_[i].second);
+  }
+  ev_.clear();
+  ev_flops_.clear();
+  if (ms) *ms = t_ms_;
+  if (flops) *flops = t_flops_;
+  if (launches) *launches = t_n_;
+  if (reset) {
+    t_ms_ = t_flops_ = 0;
+    t_n_ = 0;
+  }
+}
+
 // decode_step_monolithic body after the features are in x_ (dense.cpp:95-122)
 void Engine::run_layers(int B, const uint64_t* seqs) {
   const Spec& s = w_->spec();
   const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
   const bool bf = w_->mode() == SD_DENSE_BF16;
-  int launches = 0;
   for (int l = 0; l < s.L; ++l) {
-    w_->linear(l, 0, B, x_, D, xb_, D, qkv_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    gemm(l, 0, B, x_, D, xb_, D, qkv_, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
     for (int i = 0; i < B; ++i) pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(seqs[i], l));
     kv_->append(l, B, seqs, pos_.data(), qkv_ + D, qkvw, qkv_ + D + kvw, qkvw, stream_);
     kv_->attend(l, B, seqs, qkv_, qkvw, o_, D, stream_);
     if (bf) launch_to_bf16(B, D, o_, D, ob_, D, stream_);
-    w_->linear(l, 4, B, o_, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
-    w_->linear(l, 5, B, y_, D, yb_, D, h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0, stream_);
-    w_->linear(l, 6, B, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D, stream_);
-    launches += 4 + 2 + (bf ? 1 : 0);
+    gemm(l, 4, B, o_, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D);
+    gemm(l, 5, B, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0);
+    gemm(l, 6, B, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D);
   }
-  launches_per_step_ = launches + 2;  // + head GEMM + argmax
 }
 
 void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const float* x_host,
@@ -346,7 +390,7 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
     if (bf) launch_to_bf16(B, s.D, x_, s.D, xb_, s.D, stream_);
   }
   run_layers(B, seqs);
-  w_->linear(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+  gemm(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0);
   launch_argmax(B, s.V, logits_, s.V, tok_, stream_);
   if (next_host) {
     SD_CUDA(cudaMemcpyAsync(next_host, tok_, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
@@ -366,7 +410,7 @@ void Engine::step_device(int B, const uint64_t* seqs, const int32_t* tokens_dev,
   const bool bf = w_->mode() == SD_DENSE_BF16;
   launch_embed(B, s.D, tokens_dev, w_->embedding(), x_, s.D, bf ? xb_ : nullptr, stream_);
   run_layers(B, seqs);
-  w_->linear(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+  gemm(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0);
   launch_argmax(B, s.V, logits_, s.V, next_dev, stream_);
 }
 

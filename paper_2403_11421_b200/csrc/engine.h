@@ -70,11 +70,23 @@ class Engine {
   cudaStream_t stream() const { return stream_; }
   // device-resident step: tokens_dev -> next_dev (no host sync)
   void step_device(int B, const uint64_t* seqs, const int32_t* tokens_dev, int32_t* next_dev);
-  int launches_per_step() const { return launches_per_step_; }
+  // CUDA-event timing of the S-Part GEMMs (on the engine stream)
+  void set_timing(bool on) { timing_ = on; }
+  void read_timing(double* ms, double* flops, int64_t* launches, bool reset);
 
  private:
   void ensure(int B);
   void run_layers(int B, const uint64_t* seqs);
+  void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
+            int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+            const float* res, int64_t ldr);
+
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
+  std::vector<double> ev_flops_;
+  double t_ms_ = 0, t_flops_ = 0;
+  int64_t t_n_ = 0;
 
   Weights* w_;
   KvStore* kv_;
@@ -85,7 +97,6 @@ class Engine {
   __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
   int32_t* tok_ = nullptr;
   std::vector<uint32_t> pos_;
-  int launches_per_step_ = 0;
 };
 
 // ---- scheduler (scheduler.cpp:10-236), kept in host C++

@@ -370,6 +370,7 @@ void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s) {
   const int grid = tiles < num_sms() ? tiles : num_sms();
   gemm_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(ta, tb, p);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 }  // namespace sd

@@ -781,6 +781,7 @@ bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) 
   }
   fn<<<grid, kThreads, smem, s>>>(a);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
   return true;
 }
 
@@ -789,12 +790,14 @@ void launch_attention_generic(const AttnArgs& a, int npieces, cudaStream_t s) {
   dim3 grid(npieces, a.g.hc * a.G);
   attn_generic_kernel<<<grid, 32, 0, s>>>(a);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_combine(const CombineArgs& a, cudaStream_t s) {
   if (a.m == 0) return;
   combine_kernel<<<a.m, 256, 0, s>>>(a);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_append(const AppendArgs& a, cudaStream_t s) {
@@ -802,6 +805,7 @@ void launch_append(const AppendArgs& a, cudaStream_t s) {
   dim3 grid(a.n > 0 ? a.n : 1, 2);
   append_kernel<<<grid, 256, 0, s>>>(a);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, int n,
@@ -809,6 +813,7 @@ void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* sl
   if (n == 0 || length == 0) return;
   prefill_kernel<<<148 * 16, 256, 0, s>>>(g, num_layers, slots, n, length, salt);
   SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
 }
 
 }  // namespace sd

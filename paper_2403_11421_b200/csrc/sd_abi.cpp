@@ -453,6 +453,33 @@ int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t
   });
 }
 
+int sd_engine_timing(sd_engine* e, int enable) {
+  return guard([&] {
+    need(e, "engine");
+    e->e->set_timing(enable != 0);
+  });
+}
+
+int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* launches, int reset) {
+  return guard([&] {
+    need(e, "engine");
+    e->e->read_timing(ms, flops, launches, reset != 0);
+  });
+}
+
+int64_t sd_launch_count(void) { return sd::g_launches.load(); }
+
+int sd_weights_synthetic(const sd_model_spec* spec, int mode, uint64_t seed, int device,
+                         sd_weights** out) {
+  return guard([&] {
+    need(out, "out");
+    sd::Spec s = sd::from_abi(spec);
+    auto h = std::make_unique<sd_weights>();
+    h->w = std::make_unique<sd::Weights>(s, mode, seed, device);
+    *out = h.release();
+  });
+}
+
 int sd_drive(sd_engine* e, const sd_drive_config* cfg, sd_drive_result** out) {
   return guard([&] {
     need(e, "engine");

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -26,6 +27,11 @@ inline void cuda_check(cudaError_t e, const char* what) {
   }
 }
 #define SD_CUDA(x) ::sd::cuda_check((x), #x)
+
+// Every kernel launch of this library bumps one process-wide counter
+// (sd_launch_count in the C-ABI): the bench's "gpu_launches" evidence.
+inline std::atomic<long long> g_launches{0};
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 struct Spec {
   int L, D, H, hd, F, V, Hkv;
