@@ -241,14 +241,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
       for (int i = 0; i < EPL; ++i) acc[j][i] = 0.0f;
       if (hh < nh) {
         const int qh = (h0 + hh * hstride) * G + (j % G);
-        const float4* src = reinterpret_cast<const float4*>(qrow + qh * HD + li * EPL);
 #pragma unroll
-        for (int c = 0; c < EPL / 4; ++c) {
-          const float4 x = src[c];
-          q[j][4 * c + 0] = x.x * a.qscale;
-          q[j][4 * c + 1] = x.y * a.qscale;
-          q[j][4 * c + 2] = x.z * a.qscale;
-          q[j][4 * c + 3] = x.w * a.qscale;
+        for (int c = 0; c < NC; ++c) {
+          const float4* src = reinterpret_cast<const float4*>(qrow + qh * HD + (c * LPR + li) * 8);
+          const float4 x0 = src[0], x1 = src[1];
+          q[j][8 * c + 0] = x0.x * a.qscale;
+          q[j][8 * c + 1] = x0.y * a.qscale;
+          q[j][8 * c + 2] = x0.z * a.qscale;
+          q[j][8 * c + 3] = x0.w * a.qscale;
+          q[j][8 * c + 4] = x1.x * a.qscale;
+          q[j][8 * c + 5] = x1.y * a.qscale;
+          q[j][8 * c + 6] = x1.z * a.qscale;
+          q[j][8 * c + 7] = x1.w * a.qscale;
         }
       } else {
 #pragma unroll
@@ -291,11 +295,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
 #pragma unroll
             for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] = 0.0f;
             if (act) {
-              const uint8_t* kr = Ks + static_cast<size_t>(t * hkv + hk) * row_bytes + li * EPL * E;
+              const uint8_t* kr = Ks + static_cast<size_t>(t * hkv + hk) * row_bytes;
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
                 float kx[8];
-                Fmt<FMT>::load8(kr + c * 8 * E, kx);
+                Fmt<FMT>::load8(kr + (c * LPR + li) * 8 * E, kx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
@@ -340,17 +344,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
             float mb = sc[hh][0][gg];
 #pragma unroll
             for (int i = 1; i < PB; ++i) mb = fmaxf(mb, sc[hh][i][gg]);
+            // branchless: an all-masked batch with no history gives c = p = 0
             const float mn = fmaxf(m[j], mb);
-            if (mn == -INFINITY) {
-#pragma unroll
-              for (int i = 0; i < PB; ++i) p[hh][i][gg] = 0.0f;
-              continue;
-            }
-            const float c = fast_exp2(m[j] - mn);
+            const float ms = mn == -INFINITY ? 0.0f : mn;
+            const float c = fast_exp2(m[j] - ms);
             float ps = 0.0f;
 #pragma unroll
             for (int i = 0; i < PB; ++i) {
-              p[hh][i][gg] = fast_exp2(sc[hh][i][gg] - mn);
+              p[hh][i][gg] = fast_exp2(sc[hh][i][gg] - ms);
               ps += p[hh][i][gg];
             }
             l[j] = fmaf(l[j], c, ps);
@@ -368,11 +369,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
             const int t = t0 + cls + ncls * i;
             const bool act = t < cnt && hh < nh;
             if (act) {
-              const uint8_t* vr = Vs + static_cast<size_t>(t * hkv + hk) * row_bytes + li * EPL * E;
+              const uint8_t* vr = Vs + static_cast<size_t>(t * hkv + hk) * row_bytes;
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
                 float vx[8];
-                Fmt<FMT>::load8(vr + c * 8 * E, vx);
+                Fmt<FMT>::load8(vr + (c * LPR + li) * 8 * E, vx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                   const float pv = FMT == SD_KV_INT8 ? p[hh][i][gg] * vs[hh][i] : p[hh][i][gg];
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
               d[1] = l[j];
             }
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) d[2 + li * EPL + i] = acc[j][i];
+            for (int i = 0; i < EPL; ++i) d[2 + ((i / 8) * LPR + li) * 8 + (i % 8)] = acc[j][i];
           }
         }
       }
@@ -424,7 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
               const float cb2 = m2 == -INFINITY ? 0.0f : fast_exp2(m2 - M);
               l[j] = l[j] * ca + l2 * cb2;
 #pragma unroll
-              for (int i = 0; i < EPL; ++i) acc[j][i] = acc[j][i] * ca + sp[2 + li * EPL + i] * cb2;
+              for (int i = 0; i < EPL; ++i) {
+                acc[j][i] = acc[j][i] * ca + sp[2 + ((i / 8) * LPR + li) * 8 + (i % 8)] * cb2;
+              }
               m[j] = M;
             }
           }
@@ -441,17 +444,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
           const int qh = (h0 + (j / G) * hstride) * G + (j % G);
           if (direct) {
             const float inv = 1.0f / l[j];
-            float4* dst = reinterpret_cast<float4*>(orow + qh * HD + li * EPL);
 #pragma unroll
-            for (int c = 0; c < EPL / 4; ++c) {
-              dst[c] = make_float4(acc[j][4 * c] * inv, acc[j][4 * c + 1] * inv,
-                                   acc[j][4 * c + 2] * inv, acc[j][4 * c + 3] * inv);
+            for (int c = 0; c < NC; ++c) {
+              float4* dst = reinterpret_cast<float4*>(orow + qh * HD + (c * LPR + li) * 8);
+              dst[0] = make_float4(acc[j][8 * c] * inv, acc[j][8 * c + 1] * inv,
+                                   acc[j][8 * c + 2] * inv, acc[j][8 * c + 3] * inv);
+              dst[1] = make_float4(acc[j][8 * c + 4] * inv, acc[j][8 * c + 5] * inv,
+                                   acc[j][8 * c + 6] * inv, acc[j][8 * c + 7] * inv);
             }
           } else {
-            float4* pa = reinterpret_cast<float4*>(a.part_acc + static_cast<int64_t>(w) * Hq * HD + qh * HD + li * EPL);
+            float* pbase = a.part_acc + static_cast<int64_t>(w) * Hq * HD + qh * HD;
 #pragma unroll
-            for (int c = 0; c < EPL / 4; ++c) {
-              pa[c] = make_float4(acc[j][4 * c], acc[j][4 * c + 1], acc[j][4 * c + 2], acc[j][4 * c + 3]);
+            for (int c = 0; c < NC; ++c) {
+              float4* pa = reinterpret_cast<float4*>(pbase + (c * LPR + li) * 8);
+              pa[0] = make_float4(acc[j][8 * c], acc[j][8 * c + 1], acc[j][8 * c + 2], acc[j][8 * c + 3]);
+              pa[1] = make_float4(acc[j][8 * c + 4], acc[j][8 * c + 5], acc[j][8 * c + 6], acc[j][8 * c + 7]);
             }
             if (li == 0) {
               float* pm = a.part_ml + (static_cast<int64_t>(w) * Hq + qh) * 2;
@@ -741,6 +748,8 @@ AttnConfig choose_attn_config(const KvGeom& g, int G) {
     if (g.hd % epl != 0) continue;
     const int lpr = g.hd / epl;
     if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) continue;
+    // EPL 16 with grouped heads needs ~220 registers: over the 168 a thread
+    // may hold when 9 warps share 4 SM sub-partitions
     if (epl == 16 && (G != 1 || (lpr != 8 && lpr != 16))) continue;
     const int rg = kConsumerWarps * (32 / lpr);
     const int maxh = g.hc >= rg ? (g.hc + rg - 1) / rg : 1;
@@ -780,7 +789,15 @@ bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) 
                                  static_cast<int>(smem)));
   }
   fn<<<grid, kThreads, smem, s>>>(a);
-  SD_CUDA(cudaGetLastError());
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fn);
+    fail(SD_ERR_CUDA, std::string("attention launch: ") + cudaGetErrorString(e) + " (regs " +
+                          std::to_string(fa.numRegs) + ", max threads " + std::to_string(fa.maxThreadsPerBlock) +
+                          ", dyn smem " + std::to_string(smem) + ", static smem " +
+                          std::to_string(fa.sharedSizeBytes) + ", grid " + std::to_string(grid) + ")");
+  }
   ::sd::count_launch();
   return true;
 }
