@@ -1,0 +1,333 @@
+// K2 for grouped-query attention over fp16 KV (BASELINE config 5): the G
+// query heads that share a kv head make the R-Part a thin GEMM, so the dot
+// products and the value sum run on tensor cores (mma.sync m16n8k16, fp32
+// accumulate) instead of CUDA-core FMAs.
+//
+//   S^T[pos][q] = K[pos][:] . Q^T[:][q]     M = 16 positions, N = 8 (G <= 8 heads), K = hd
+//   O^T[d][q]  += V^T[d][pos] . P^T[pos][q]  M = 16 head-dims,  N = 8 heads,         K = 16 pos
+//
+// K rows are the A operand (ldmatrix), V rows the transposed A operand
+// (ldmatrix.trans); Q^T is a register-resident B operand; P^T is built from
+// the S^T accumulators with movmatrix.trans. fp16 K/V are exact tensor-core
+// operands; q and p are split into fp16 hi + lo parts (two MMAs each), so the
+// products carry ~22 significant bits — fp32-level agreement with the
+// reference's fp32 attend (attention.cpp:204-282), not fp16 rounding.
+//
+// Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
+// protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
+// positions and each position row is copied to a 16-B padded pitch so the
+// eight ldmatrix row addresses of a warp fall in distinct bank groups.
+#include <cuda_fp16.h>
+
+#include "kv_kernels.cuh"
+#include "sd_common.h"
+
+namespace sd {
+
+namespace {
+
+constexpr int kWarps = 8;                 // consumer warps = kv heads per CTA
+constexpr int kThreads = (kWarps + 1) * 32;
+constexpr int kT = 16;                    // positions per stage
+constexpr int kHD = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+// D (+)= A . B, m16n8k16, fp16 in, fp32 accumulate
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_h2(float lo_col, float hi_col) {
+  __half2 h = __floats2half2_rn(lo_col, hi_col);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// split (x0, x1) into fp16 hi pair + fp16 lo pair (residuals)
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack_h2(x0 - hf.x, x1 - hf.y);
+}
+
+template <int G>
+__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int nst = a.nstages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + nst;
+  uint8_t* ring = smem + 128 * ((16 * nst + 127) / 128);
+  const int pitch = a.stage_region / kT;  // padded bytes per position row
+  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region;
+  const KvGeom& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // rows past a stage's valid count are read (and masked): keep them finite
+  for (size_t i = threadIdx.x * 16; i < stage_bytes * nst; i += kThreads * 16) {
+    *reinterpret_cast<uint4*>(ring + i) = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
+  const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
+
+  if (warp == kWarps) {
+    // producer warp: lane 0 arms the stage barrier, then lanes 0-15 copy the
+    // K rows and lanes 16-31 the V rows of the stage in parallel
+    const uint64_t pol = evict_first_policy();
+    int stage = 0;
+    uint32_t phase = 0;
+    const int t = lane & 15;
+    for (int w = cb; w < ce; ++w) {
+      const Piece pc = a.pieces[w];
+      const int32_t* pt = g.page_table + static_cast<int64_t>(a.item_slot[pc.item]) * g.max_pages;
+      for (int pos = pc.p0; pos < pc.p1; pos += kT) {
+        const int cnt = min(kT, pc.p1 - pos);
+        const uint8_t* base = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes +
+                              static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes);
+        }
+        __syncwarp();
+        if (t < cnt) {
+          uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + t * pitch;
+          bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + t * g.pos_bytes, g.pos_bytes, &full[stage], pol);
+        }
+        if (++stage == nst) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumer
+  // warp = kv head; fragment coordinates: gq = lane/4 (row group), tq = lane%4
+  const int hk = warp;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int Hq = g.hc * G;
+  float o[8][4];      // O^T fragments: hd rows 16*mt + {gq, gq+8}, heads {2tq, 2tq+1}
+  float m[2], l[2];   // per head 2tq, 2tq+1 (replicated over gq lanes; l partial per lane)
+  uint32_t qb[8][2][2];  // Q^T B-fragments: [k-step][b0|b1][hi|lo]
+  int stage = 0;
+  uint32_t phase = 0;
+  // ldmatrix lane address components
+  const int lm = lane >> 3, lr = lane & 7;
+
+  for (int w = cb; w < ce; ++w) {
+    const Piece pc = a.pieces[w];
+    {
+      const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride + static_cast<int64_t>(hk) * G * kHD;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2 x = make_float2(0.0f, 0.0f);
+          if (gq < G) x = *reinterpret_cast<const float2*>(qrow + gq * kHD + 16 * kk + 8 * h + 2 * tq);
+          split2(x.x * a.qscale, x.y * a.qscale, qb[kk][h][0], qb[kk][h][1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[mt][i] = 0.0f;
+    m[0] = m[1] = -INFINITY;
+    l[0] = l[1] = 0.0f;
+
+    for (int pos = pc.p0; pos < pc.p1; pos += kT) {
+      const int cnt = min(kT, pc.p1 - pos);
+      mbar_wait(&full[stage], phase);
+      __syncwarp();
+      const uint32_t Ks = smem_u32(ring + stage * stage_bytes) + hk * kHD * 2;
+      const uint32_t Vs = Ks + a.stage_region;
+      // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
+      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t ka[4];
+        // matrices: (pos 0-7, d 0-7), (pos 8-15, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 8-15)
+        ldsm_x4(Ks + (lr + 8 * (lm & 1)) * pitch + (16 * kk + 8 * (lm >> 1)) * 2, ka);
+        mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
+        mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+      }
+      // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
+      const bool v0 = gq < cnt, v1 = gq + 8 < cnt;
+      if (!v0) s[0] = s[1] = -INFINITY;
+      if (!v1) s[2] = s[3] = -INFINITY;
+      float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
+#pragma unroll
+      for (int sh = 4; sh < 32; sh <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
+      }
+      const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: position 0 of a piece is valid
+      const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
+      m[0] = mn0;
+      m[1] = mn1;
+      const float p0 = fast_exp2(s[0] - mn0), p1 = fast_exp2(s[1] - mn1);
+      const float p2 = fast_exp2(s[2] - mn0), p3 = fast_exp2(s[3] - mn1);
+      l[0] = fmaf(l[0], c0, p0 + p2);
+      l[1] = fmaf(l[1], c1, p1 + p3);
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] *= c0;
+        o[mt][2] *= c0;
+        o[mt][1] *= c1;
+        o[mt][3] *= c1;
+      }
+      // ---- P^T B-fragments via transposes of the S^T accumulator layout
+      uint32_t h01, l01, h23, l23;
+      split2(p0, p1, h01, l01);  // (pos gq, heads 2tq..): rows = pos
+      split2(p2, p3, h23, l23);  // (pos gq+8, ...)
+      const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
+      const uint32_t bl0 = movm_t(l01), bl1 = movm_t(l23);
+      // ---- O^T += V^T . P^T  (8 tiles of 16 head-dims)
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t va[4];
+        // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
+        ldsm_x4_t(Vs + (lr + 8 * (lm >> 1)) * pitch + (16 * mt + 8 * (lm & 1)) * 2, va);
+        mma16816(o[mt], va, bh0, bh1);
+        mma16816(o[mt], va, bl0, bl1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == nst) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // ---- finalize: full row sums, then direct output or partial
+#pragma unroll
+    for (int sh = 4; sh < 32; sh <<= 1) {
+      l[0] += __shfl_xor_sync(0xffffffffu, l[0], sh);
+      l[1] += __shfl_xor_sync(0xffffffffu, l[1], sh);
+    }
+    const bool direct = pc.flags & 1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int hq = 2 * tq + j;
+      if (hq >= G) continue;
+      const int qh = hk * G + hq;
+      if (direct) {
+        float* orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * kHD;
+        const float inv = 1.0f / l[j];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          orow[16 * mt + gq] = o[mt][j] * inv;
+          orow[16 * mt + gq + 8] = o[mt][2 + j] * inv;
+        }
+      } else {
+        float* pa = a.part_acc + (static_cast<int64_t>(w) * Hq + qh) * kHD;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          pa[16 * mt + gq] = o[mt][j];
+          pa[16 * mt + gq + 8] = o[mt][2 + j];
+        }
+        if (gq == 0) {
+          float* pm = a.part_ml + (static_cast<int64_t>(w) * Hq + qh) * 2;
+          pm[0] = m[j];
+          pm[1] = l[j];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+bool attention_mma_supported(const KvGeom& g, int G) {
+  return g.fmt == SD_KV_HALF && g.hd == kHD && g.hc == kWarps && (G == 2 || G == 4 || G == 8) &&
+         g.P % kT == 0;
+}
+
+size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* nstages) {
+  const int pitch = g.pos_bytes + 16;
+  *stage_region = ((kT * pitch + 127) / 128) * 128;
+  *nstages = 3;
+  while (*nstages > 2 && 128 + static_cast<size_t>(*nstages) * 2 * *stage_region > 215 * 1024) --*nstages;
+  return 128 + static_cast<size_t>(*nstages) * 2 * *stage_region;
+}
+
+void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
+  void (*fn)(const AttnArgs) = nullptr;
+  switch (a.G) {
+    case 2: fn = attn_mma_kernel<2>; break;
+    case 4: fn = attn_mma_kernel<4>; break;
+    case 8: fn = attn_mma_kernel<8>; break;
+    default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
+  }
+  SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  fn<<<grid, kThreads, smem, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace sd

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -102,6 +103,12 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
     --nstages_;
   }
   attn_smem_ = attention_smem_bytes(g, T_, nstages_, G_, &stage_region_, &sc_region_);
+  use_mma_ = attention_mma_supported(g, G_) && std::getenv("SD_ATTN_NO_MMA") == nullptr;
+  if (use_mma_) {
+    T_ = 16;
+    sc_region_ = 0;
+    attn_smem_ = attention_mma_smem(g, &stage_region_, &nstages_);
+  }
 
   ring_.resize(8);
   for (Blob& b : ring_) SD_CUDA(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming));
@@ -428,7 +435,11 @@ void KvStore::launch_attention_plan(int layer, const float* q, int64_t qs, float
     e1 = take();
     SD_CUDA(cudaEventRecord(e0, s));
   }
-  if (!launch_attention(a, plan_grid_, attn_smem_, s)) launch_attention_generic(a, plan_npieces_, s);
+  if (use_mma_) {
+    launch_attention_mma(a, plan_grid_, attn_smem_, s);
+  } else if (!launch_attention(a, plan_grid_, attn_smem_, s)) {
+    launch_attention_generic(a, plan_npieces_, s);
+  }
   if (timing_) {
     SD_CUDA(cudaEventRecord(e1, s));
     ev_pending_.emplace_back(e0, e1);

@@ -80,6 +80,7 @@ class KvStore {
   KvGeom geom_{};
   int T_ = 1, nstages_ = 2, stage_region_ = 0, sc_region_ = 0;
   size_t attn_smem_ = 0;
+  bool use_mma_ = false;  // tensor-core GQA kernel (kv_mma.cu)
   int max_seqs_ = 0, max_len_ = 0, pool_groups_ = 0;
 
   // host mirror

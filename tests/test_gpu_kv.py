@@ -180,6 +180,33 @@ def test_many_sequences_split_and_combine(sd, oracle):
     assert err < 2e-5, err
 
 
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_gqa_tensor_core_path_parity(sd, oracle, G):
+    """fp16 KV, hd 128, 8 kv heads: the mma.sync attention path (kv_mma.cu),
+    with ragged lengths (tails of 16-position stages) and split pieces."""
+    H = 8 * G
+    D = H * 128
+    s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
+    B, Lmax = 40, 700
+    gpu = sd.KvShard(s, 0, 8, B * Lmax, "half")
+    cpu = oracle.KvShard(os_, 0, 8, B * Lmax, "half")
+    rng = _rng(G)
+    lens = rng.integers(1, Lmax, B)
+    lens[0], lens[1] = 1, 17
+    seqs = list(range(1, B + 1))
+    for pos in range(int(lens.max())):
+        act = [i for i in range(B) if lens[i] > pos]
+        k = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        v = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        ids = [seqs[i] for i in act]
+        gpu.append_request(0, ids, [pos] * len(act), k, v)
+        cpu.append_request(0, ids, [pos] * len(act), k, v)
+    q = rng.uniform(-3, 3, (B, D)).astype(np.float32)
+    og, oc = gpu.attend(0, seqs, q), cpu.attend(0, seqs, q)
+    err = float(np.abs(og - oc).max())
+    assert err < 2e-5, err
+
+
 def test_capacity_positions_atomicity_drop(sd):
     # proj/tests/test_attention.cpp:205-284, reference error types
     vec = rnd_stream(17)
