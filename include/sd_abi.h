@@ -174,6 +174,15 @@ int sd_s_logits_argmax(sd_weights* w, int32_t B, const float* x, float* logits,
  * sd_weights_upload, 1..6 per layer, 7 = head). */
 int sd_s_apply_linear(sd_weights* w, int layer, int which, int32_t B, const float* x, float* y);
 
+/* The tcgen05 GEMM behind the S-Part on device pointers:
+ * C[M][N] = A[M][K] . B[N][K]^T, row-major, both operands K-major;
+ * kind SD_DENSE_BF16 (bf16 operands) or SD_DENSE_TF32 (fp32 operands); fused
+ * epilogue epi: 0 none, 1 + res (dense.cpp:60), 2 SiLU (dense.cpp:47-49).
+ * Writes fp32 C and/or bf16 Cb (either may be NULL). */
+int sd_gemm_dev(int kind, int M, int N, int K, const void* A, int64_t lda, const void* B,
+                int64_t ldb, float* C, int64_t ldc, void* Cb, int64_t ldcb, int epi,
+                const float* res, int64_t ldr, void* stream);
+
 /* -------------------------------------------------------------- runtime
  * The GPU StepComputation (workers.hpp:151-158): decode_step_monolithic
  * (dense.cpp:90-129) with the KV store, S-Part and head on one device. */

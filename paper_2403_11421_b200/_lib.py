@@ -89,6 +89,8 @@ SIGNATURES = {
     "sd_s_finish_block": (C.c_int, [P, C.c_int, C.c_int32, FP, FP, FP]),
     "sd_s_logits_argmax": (C.c_int, [P, C.c_int32, FP, FP, I32P]),
     "sd_s_apply_linear": (C.c_int, [P, C.c_int, C.c_int, C.c_int32, FP, FP]),
+    "sd_gemm_dev": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, P, C.c_int64, P, C.c_int64, P,
+                              C.c_int64, P, C.c_int64, C.c_int, P, C.c_int64, P]),
     "sd_engine_create": (C.c_int, [P, P, PP]),
     "sd_engine_destroy": (C.c_int, [P]),
     "sd_engine_step": (C.c_int, [P, C.c_int32, U64P, I32P, I32P, FP]),

@@ -350,6 +350,14 @@ def apply_linear(w: DeviceWeights, layer: int, which: int, x):
     return y
 
 
+def gemm_dev(kind: str, M: int, N: int, K: int, A, lda, B, ldb, C=None, ldc=0, Cb=None, ldcb=0,
+             epi: int = 0, res=None, ldr=0, stream=0):
+    """tcgen05 GEMM on device pointers (ints, e.g. torch .data_ptr()):
+    C = A . B^T (+ epilogue). kind: "bf16" | "tf32"."""
+    _check(lib.sd_gemm_dev(DENSE_MODES[kind], M, N, K, A, lda, B, ldb, C, ldc, Cb, ldcb, epi, res,
+                           ldr, stream))
+
+
 # ----------------------------------------------------------------- runtime
 class Engine:
     """The GPU StepComputation (workers.hpp:151-158)."""

@@ -401,6 +401,32 @@ int sd_s_apply_linear(sd_weights* w, int layer, int which, int32_t B, const floa
   });
 }
 
+int sd_gemm_dev(int kind, int M, int N, int K, const void* A, int64_t lda, const void* B,
+                int64_t ldb, float* C, int64_t ldc, void* Cb, int64_t ldcb, int epi,
+                const float* res, int64_t ldr, void* stream) {
+  return guard([&] {
+    sd::GemmArgs g{};
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.B = B;
+    g.ldb = ldb;
+    g.C = C;
+    g.ldc = ldc;
+    g.Cb = static_cast<__nv_bfloat16*>(Cb);
+    g.ldcb = ldcb;
+    g.epi = epi;
+    g.res = res;
+    g.ldr = ldr;
+    g.kind = kind;
+    if (!sd::gemm_sm100_supported(g)) sd::fail(SD_ERR_CONFIG, "sd_gemm_dev: unsupported shape/alignment");
+    if (epi == sd::kEpiResidual && !res) sd::fail(SD_ERR_CONFIG, "sd_gemm_dev: residual epilogue needs res");
+    sd::launch_gemm_sm100(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
 // --------------------------------------------------------------- engine ---
 int sd_engine_create(sd_weights* w, sd_kv* kv, sd_engine** out) {
   return guard([&] {
