@@ -233,6 +233,37 @@ const float* sd_drive_activations(const sd_drive_result* r);
 double sd_drive_wall_seconds(const sd_drive_result* r);
 int sd_drive_destroy(sd_drive_result* r);
 
+/* ---------------------------------------------------------- multi-GPU
+ * DistributedComputation (workers.cpp:264-501) on NVLink: every rank is an
+ * R-shard holding the sequences ShardMap by-sequence assigns it
+ * (mix64(seq) % world, transport.cpp:352-353); S-ranks (rank 0 when
+ * s_ranks == 1, the paper's topology; every rank when s_ranks == world)
+ * run the S-Part for their home rows (seq % s_ranks). Per layer Q/K/V rows
+ * go to the owning shard and O rows come back (send_layer / receive_layer,
+ * workers.cpp:324-391) as NCCL grouped send/recv. Every rank passes the
+ * full step batch; tokens are read and written for its home rows only. */
+typedef struct sd_dist sd_dist;
+/* ncclGetUniqueId into `out` (NCCL_UNIQUE_ID_BYTES = 128 bytes) on one rank. */
+int sd_nccl_unique_id(void* out, size_t bytes);
+int sd_dist_create(sd_weights* weights_or_null, sd_kv* kv, int rank, int world,
+                   const void* nccl_id, int s_ranks, sd_dist** out);
+int sd_dist_destroy(sd_dist* d);
+int sd_dist_step(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens,
+                 int32_t* next_tokens, float* final_x);
+int sd_dist_retire(sd_dist* d, int32_t n, const uint64_t* seqs);
+int sd_dist_bench(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens,
+                  int32_t steps, double* device_ms);
+/* drive_schedule over the distributed computation; the result holds the
+ * transcript rows this rank produced (its home rows). */
+int sd_dist_drive(sd_dist* d, const sd_drive_config* cfg, sd_drive_result** out);
+int sd_dist_timing(sd_dist* d, int enable);
+int sd_dist_timing_read(sd_dist* d, double* exchange_ms, double* exchange_bytes, int reset);
+/* Host-only row plan of a step (CPU-testable): home rows grouped by shard,
+ * shard rows grouped by source, per-peer counts. Arrays sized B / world. */
+int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs,
+                 int32_t* home_rows, int32_t* n_home, int32_t* shard_rows, int32_t* n_shard,
+                 int32_t* send_counts, int32_t* recv_counts);
+
 /* ------------------------------------------------------- ShardMap, load
  * ShardMap (transport.cpp:319-380). */
 int sd_shardmap_worker_for(int mode, int num_heads, int workers, uint64_t seq, int head,

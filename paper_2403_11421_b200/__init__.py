@@ -6,7 +6,7 @@ fp32 CUDA-core path). Host: the reference's KvShard / StepComputation /
 drive_schedule / ShardMap interfaces over the C-ABI in include/sd_abi.h.
 """
 from .api import (AdmissionError, AttentionItem, AttentionRequest, CapacityError, ConfigError,
-                  CudaError, DeviceWeights, Engine, KvShard, LogicError, ProtocolError, ShardMap,
+                  CudaError, DeviceWeights, DistEngine, Engine, dist_plan, nccl_unique_id, KvShard, LogicError, ProtocolError, ShardMap,
                   SplitDecodeError, UnknownSequenceError, apply_linear, cold_start_schedule,
                   finish_block, gemm_dev, launch_count, make_model_spec, micro_batch_size, mix64, output_logits_argmax,
                   project_qkv, prompt_token, run_generation, transcript_csv)

@@ -107,6 +107,17 @@ SIGNATURES = {
     "sd_drive_activations": (FP, [P]),
     "sd_drive_wall_seconds": (C.c_double, [P]),
     "sd_drive_destroy": (C.c_int, [P]),
+    "sd_nccl_unique_id": (C.c_int, [P, C.c_size_t]),
+    "sd_dist_create": (C.c_int, [P, P, C.c_int, C.c_int, P, C.c_int, PP]),
+    "sd_dist_destroy": (C.c_int, [P]),
+    "sd_dist_step": (C.c_int, [P, C.c_int32, U64P, I32P, I32P, FP]),
+    "sd_dist_retire": (C.c_int, [P, C.c_int32, U64P]),
+    "sd_dist_bench": (C.c_int, [P, C.c_int32, U64P, I32P, C.c_int32, DP]),
+    "sd_dist_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
+    "sd_dist_timing": (C.c_int, [P, C.c_int]),
+    "sd_dist_timing_read": (C.c_int, [P, DP, DP, C.c_int]),
+    "sd_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int32, U64P, I32P, I32P, I32P, I32P,
+                               I32P, I32P]),
     "sd_shardmap_worker_for": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, I32P]),
     "sd_shardmap_head_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, I32P, I32P]),
     "sd_micro_batch_size": (C.c_int, [C.c_int, C.c_int, C.c_int, I32P]),

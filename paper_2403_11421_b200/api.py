@@ -416,16 +416,93 @@ class Engine:
         return ms.value, nxt
 
 
-def run_generation(engine: Engine, batch: int, target_len: int, interval: int, steps: int,
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes), to be broadcast to every rank."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib.sd_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def dist_plan(world: int, rank: int, s_ranks: int, seqs):
+    """Host row plan of one distributed step (sd_dist_plan)."""
+    s, sp = _u64(seqs)
+    B = len(s)
+    home = np.zeros(max(B, 1), np.int32)
+    shard = np.zeros(max(B, 1), np.int32)
+    nh, ns = C.c_int32(), C.c_int32()
+    sc, rc = np.zeros(world, np.int32), np.zeros(world, np.int32)
+    _check(lib.sd_dist_plan(world, rank, s_ranks, B, sp, home.ctypes.data_as(I32P), C.byref(nh),
+                            shard.ctypes.data_as(I32P), C.byref(ns), sc.ctypes.data_as(I32P),
+                            rc.ctypes.data_as(I32P)))
+    return {"home_rows": home[:nh.value].tolist(), "shard_rows": shard[:ns.value].tolist(),
+            "send_counts": sc.tolist(), "recv_counts": rc.tolist()}
+
+
+class DistEngine:
+    """DistributedComputation (workers.cpp:264-501) over NCCL: this rank's
+    R-shard (`kv`, sequences with mix64(seq) % world == rank) and, on
+    S-ranks, the weights. s_ranks = 1: rank 0 is the only S-worker (the
+    paper's topology); s_ranks = world: data-parallel S-workers."""
+
+    def __init__(self, weights, kv: KvShard, rank: int, world: int, nccl_id: bytes | None,
+                 s_ranks: int = 1):
+        self.weights, self.kv, self.rank, self.world = weights, kv, rank, world
+        self.spec = kv.spec
+        self.h = C.c_void_p()
+        idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
+        _check(lib.sd_dist_create(weights.h if weights is not None else None, kv.h, rank, world,
+                                  idbuf, s_ranks, C.byref(self.h)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sd_dist_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def compute(self, seqs, tokens, want_final=False):
+        """One step over the full batch; next tokens (and final activations)
+        are valid for this rank's home rows."""
+        s, sp = _u64(seqs)
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        nxt = np.full(len(s), -1, np.int32)
+        fx = np.zeros((len(s), self.spec.model_dim), np.float32) if want_final else None
+        _check(lib.sd_dist_step(self.h, len(s), sp, t.ctypes.data_as(I32P), nxt.ctypes.data_as(I32P),
+                                _fp(fx) if fx is not None else None))
+        return nxt, fx
+
+    def retire(self, seqs):
+        s, sp = _u64(seqs)
+        _check(lib.sd_dist_retire(self.h, len(s), sp))
+
+    def bench(self, seqs, tokens, steps: int) -> float:
+        s, sp = _u64(seqs)
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        ms = C.c_double()
+        _check(lib.sd_dist_bench(self.h, len(s), sp, t.ctypes.data_as(I32P), steps, C.byref(ms)))
+        return ms.value
+
+    def timing(self, enable: bool):
+        _check(lib.sd_dist_timing(self.h, int(enable)))
+
+    def timing_read(self, reset=True):
+        ms, b = C.c_double(), C.c_double()
+        _check(lib.sd_dist_timing_read(self.h, C.byref(ms), C.byref(b), int(reset)))
+        return ms.value, b.value
+
+
+def run_generation(engine, batch: int, target_len: int, interval: int, steps: int,
                    seed: int = 0, cold_start: str = "fixed-interval", load_limit: int = 0,
                    record_activations: bool = False):
-    """drive_schedule (workers.cpp:547-684) over the GPU engine ->
-    (transcript [(step, seq, token)], activations, wall_seconds)."""
+    """drive_schedule (workers.cpp:547-684) over the GPU engine (Engine or
+    DistEngine) -> (transcript [(step, seq, token)], activations, wall_seconds).
+    A DistEngine returns the rows its rank produced."""
     cfg = DriveConfig(batch, target_len, interval,
                       {"fixed-interval": 0, "ramped-limit": 1}[cold_start], steps, load_limit,
                       seed, int(record_activations))
     h = C.c_void_p()
-    _check(lib.sd_drive(engine.h, C.byref(cfg), C.byref(h)))
+    fn = lib.sd_dist_drive if isinstance(engine, DistEngine) else lib.sd_drive
+    _check(fn(engine.h, C.byref(cfg), C.byref(h)))
     try:
         n = lib.sd_drive_count(h)
         st, sq, tk = C.c_int64(), C.c_uint64(), C.c_int32()
@@ -436,7 +513,8 @@ def run_generation(engine: Engine, batch: int, target_len: int, interval: int, s
         acts = None
         if record_activations and n:
             p = lib.sd_drive_activations(h)
-            acts = np.ctypeslib.as_array(p, shape=(n * engine.weights.spec.model_dim,)).reshape(n, -1).copy()
+            D = engine.spec.model_dim if isinstance(engine, DistEngine) else engine.weights.spec.model_dim
+            acts = np.ctypeslib.as_array(p, shape=(n * D,)).reshape(n, -1).copy()
         return recs, acts, lib.sd_drive_wall_seconds(h)
     finally:
         lib.sd_drive_destroy(h)

@@ -1,0 +1,327 @@
+// DistEngine: sequence-sharded R-Part over NCCL (see dist.h).
+#include "dist.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+namespace sd {
+
+namespace {
+
+// NCCL is resolved at run time: inside a torch process this binds the NCCL
+// torch already loaded (one NCCL per process), else the system libnccl.so.2.
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static Nccl& get() {
+    static Nccl n;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) {
+        err = dlerror() ? dlerror() : "dlopen failed";
+        return;
+      }
+#define SD_SYM(f) n.f = reinterpret_cast<decltype(n.f)>(dlsym(h, "nccl" #f))
+      SD_SYM(GetUniqueId);
+      SD_SYM(CommInitRank);
+      SD_SYM(CommDestroy);
+      SD_SYM(GroupStart);
+      SD_SYM(GroupEnd);
+      SD_SYM(Send);
+      SD_SYM(Recv);
+      SD_SYM(GetErrorString);
+#undef SD_SYM
+    });
+    if (!n.Send || !n.Recv || !n.CommInitRank) fail(SD_ERR_NCCL, "libnccl.so.2 unavailable: " + err);
+    return n;
+  }
+};
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    fail(SD_ERR_NCCL, std::string(what) + ": " + Nccl::get().GetErrorString(r));
+  }
+}
+
+}  // namespace
+
+void nccl_unique_id(ncclUniqueId* id) { nccl_check(Nccl::get().GetUniqueId(id), "ncclGetUniqueId"); }
+
+void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p) {
+  p.home_rows.clear();
+  p.shard_rows.clear();
+  p.shard_seqs.clear();
+  p.send_cnt.assign(static_cast<size_t>(world), 0);
+  p.send_off.assign(static_cast<size_t>(world), 0);
+  p.recv_cnt.assign(static_cast<size_t>(world), 0);
+  p.recv_off.assign(static_cast<size_t>(world), 0);
+  // home rows grouped by destination shard (batch order inside a group):
+  // send_layer's per-worker record filter (workers.cpp:336-351)
+  for (int d = 0; d < world; ++d) {
+    p.send_off[static_cast<size_t>(d)] = static_cast<int32_t>(p.home_rows.size());
+    for (int i = 0; i < B; ++i) {
+      if (home_of(seqs[i], s_ranks) == rank && shard_of(seqs[i], world) == d) p.home_rows.push_back(i);
+    }
+    p.send_cnt[static_cast<size_t>(d)] = static_cast<int32_t>(p.home_rows.size()) - p.send_off[static_cast<size_t>(d)];
+  }
+  // shard rows grouped by source S-rank, each group in that source's send order
+  for (int src = 0; src < world; ++src) {
+    p.recv_off[static_cast<size_t>(src)] = static_cast<int32_t>(p.shard_rows.size());
+    for (int i = 0; i < B; ++i) {
+      if (home_of(seqs[i], s_ranks) == src && shard_of(seqs[i], world) == rank) {
+        p.shard_rows.push_back(i);
+        p.shard_seqs.push_back(seqs[i]);
+      }
+    }
+    p.recv_cnt[static_cast<size_t>(src)] = static_cast<int32_t>(p.shard_rows.size()) - p.recv_off[static_cast<size_t>(src)];
+  }
+}
+
+DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks)
+    : spec_(kv->spec()), w_(w), kv_(kv), rank_(rank), world_(world), s_ranks_(s_ranks),
+      device_(kv->device()) {
+  if (world < 1 || rank < 0 || rank >= world) fail(SD_ERR_CONFIG, "bad rank / world");
+  if (s_ranks != 1 && s_ranks != world) fail(SD_ERR_CONFIG, "s_ranks must be 1 or world");
+  const bool s_rank = s_ranks == world || rank == 0;
+  if (s_rank && !w) fail(SD_ERR_CONFIG, "an S-rank needs weights");
+  if (w && w->device() != device_) fail(SD_ERR_CONFIG, "weights and KV store on different devices");
+  if (kv->width() != spec_.kv_width()) fail(SD_ERR_CONFIG, "R-shard must hold all kv heads (by-sequence)");
+  DeviceGuard dg(device_);
+  SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    nccl_check(Nccl::get().CommInitRank(&comm_, world, id, rank), "ncclCommInitRank");
+  }
+}
+
+DistEngine::~DistEngine() {
+  DeviceGuard dg(device_);
+  cudaStreamSynchronize(stream_);
+  if (comm_) Nccl::get().CommDestroy(comm_);
+  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_h_), static_cast<void*>(qkv_s_),
+                  static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
+                  static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
+                  static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
+                  static_cast<void*>(tok_)}) {
+    if (p) cudaFree(p);
+  }
+  for (auto& e : ev_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  cudaStreamDestroy(stream_);
+}
+
+void DistEngine::ensure(int B) {
+  if (B <= cap_) return;
+  DeviceGuard dg(device_);
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_h_), static_cast<void*>(qkv_s_),
+                  static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
+                  static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
+                  static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
+                  static_cast<void*>(tok_)}) {
+    if (p) cudaFree(p);
+  }
+  const size_t bp = (static_cast<size_t>(B) + 127) / 128 * 128;
+  const Spec& s = spec_;
+  auto zalloc = [&](void** p, size_t bytes) {
+    SD_CUDA(cudaMalloc(p, bytes));
+    SD_CUDA(cudaMemset(*p, 0, bytes));
+  };
+  zalloc(reinterpret_cast<void**>(&x_), bp * s.D * 4);
+  zalloc(reinterpret_cast<void**>(&qkv_h_), bp * s.qkv_width() * 4);
+  zalloc(reinterpret_cast<void**>(&qkv_s_), bp * s.qkv_width() * 4);
+  zalloc(reinterpret_cast<void**>(&o_s_), bp * s.D * 4);
+  zalloc(reinterpret_cast<void**>(&o_h_), bp * s.D * 4);
+  zalloc(reinterpret_cast<void**>(&y_), bp * s.D * 4);
+  zalloc(reinterpret_cast<void**>(&h_), bp * s.F * 4);
+  zalloc(reinterpret_cast<void**>(&logits_), bp * s.V * 4);
+  zalloc(reinterpret_cast<void**>(&xb_), bp * s.D * 2);
+  zalloc(reinterpret_cast<void**>(&ob_), bp * s.D * 2);
+  zalloc(reinterpret_cast<void**>(&yb_), bp * s.D * 2);
+  zalloc(reinterpret_cast<void**>(&hb_), bp * s.F * 2);
+  zalloc(reinterpret_cast<void**>(&tok_), bp * 4);
+  cap_ = B;
+}
+
+void DistEngine::plan_for(int B, const uint64_t* seqs) {
+  if (plan_key_.size() == static_cast<size_t>(B) && std::equal(plan_key_.begin(), plan_key_.end(), seqs)) return;
+  make_plan(world_, rank_, s_ranks_, B, seqs, plan_);
+  plan_key_.assign(seqs, seqs + B);
+}
+
+// per-destination grouped send/recv (the scatter of send_layer and the
+// gather of receive_layer); the rank's own rows are a device copy
+void DistEngine::exchange(const float* send, const std::vector<int32_t>& sc, const std::vector<int32_t>& so,
+                          float* recv, const std::vector<int32_t>& rc, const std::vector<int32_t>& ro,
+                          int width) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double bytes = 0;
+  if (timing_) {
+    SD_CUDA(cudaEventCreate(&e0));
+    SD_CUDA(cudaEventCreate(&e1));
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  const size_t w = static_cast<size_t>(width);
+  const int self = rank_;
+  if (sc[static_cast<size_t>(self)]) {
+    SD_CUDA(cudaMemcpyAsync(recv + ro[static_cast<size_t>(self)] * w, send + so[static_cast<size_t>(self)] * w,
+                            static_cast<size_t>(sc[static_cast<size_t>(self)]) * w * 4, cudaMemcpyDeviceToDevice,
+                            stream_));
+  }
+  if (world_ > 1) {
+    Nccl& n = Nccl::get();
+    nccl_check(n.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < world_; ++p) {
+      if (p == self) continue;
+      const size_t c_s = static_cast<size_t>(sc[static_cast<size_t>(p)]);
+      const size_t c_r = static_cast<size_t>(rc[static_cast<size_t>(p)]);
+      if (c_s) {
+        nccl_check(n.Send(send + so[static_cast<size_t>(p)] * w, c_s * w, ncclFloat32, p, comm_, stream_), "ncclSend");
+        bytes += static_cast<double>(c_s * w * 4);
+      }
+      if (c_r) {
+        nccl_check(n.Recv(recv + ro[static_cast<size_t>(p)] * w, c_r * w, ncclFloat32, p, comm_, stream_), "ncclRecv");
+      }
+    }
+    nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  }
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    ev_bytes_.push_back(bytes);
+  }
+}
+
+void DistEngine::read_timing(double* ms, double* bytes, bool reset) {
+  for (size_t i = 0; i < ev_.size(); ++i) {
+    SD_CUDA(cudaEventSynchronize(ev_[i].second));
+    float t = 0;
+    SD_CUDA(cudaEventElapsedTime(&t, ev_[i].first, ev_[i].second));
+    x_ms_ += t;
+    x_bytes_ += ev_bytes_[i];
+    cudaEventDestroy(ev_[i].first);
+    cudaEventDestroy(ev_[i].second);
+  }
+  ev_.clear();
+  ev_bytes_.clear();
+  if (ms) *ms = x_ms_;
+  if (bytes) *bytes = x_bytes_;
+  if (reset) x_ms_ = x_bytes_ = 0;
+}
+
+// one decode step with the home tokens already in tok_ (home order)
+void DistEngine::run_step() {
+  const Spec& s = spec_;
+  const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
+  const int nh = static_cast<int>(plan_.home_rows.size());
+  const int ns = static_cast<int>(plan_.shard_rows.size());
+  const bool bf = w_ && w_->mode() == SD_DENSE_BF16;
+  if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, stream_);
+  for (int l = 0; l < s.L; ++l) {
+    if (nh) w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s_, plan_.recv_cnt, plan_.recv_off, qkvw);
+    if (ns) {
+      for (int i = 0; i < ns; ++i) {
+        pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
+      }
+      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s_ + D, qkvw, qkv_s_ + D + kvw, qkvw, stream_);
+      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s_, qkvw, o_s_, D, stream_);
+    }
+    exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h_, plan_.send_cnt, plan_.send_off, D);
+    if (nh) {
+      if (bf) launch_to_bf16(nh, D, o_h_, D, ob_, D, stream_);
+      w_->linear(l, 4, nh, o_h_, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
+      w_->linear(l, 5, nh, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0, stream_);
+      w_->linear(l, 6, nh, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D, stream_);
+    }
+  }
+  if (nh) {
+    w_->linear(0, 7, nh, x_, D, xb_, D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    launch_argmax(nh, s.V, logits_, s.V, tok_, stream_);
+  }
+}
+
+void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next, float* final_x) {
+  if (B == 0) fail(SD_ERR_CONFIG, "project_qkv: empty batch");
+  DeviceGuard dg(device_);
+  ensure(B);
+  plan_for(B, seqs);
+  pos_.resize(static_cast<size_t>(B));
+  const int nh = static_cast<int>(plan_.home_rows.size());
+  host_tok_.resize(static_cast<size_t>(nh));
+  for (int i = 0; i < nh; ++i) {
+    const int32_t t = tokens[plan_.home_rows[static_cast<size_t>(i)]];
+    if (t < 0 || t >= spec_.V) fail(SD_ERR_CONFIG, "token out of the vocabulary");
+    host_tok_[static_cast<size_t>(i)] = t;
+  }
+  if (nh) SD_CUDA(cudaMemcpyAsync(tok_, host_tok_.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
+  run_step();
+  std::vector<float> fx;
+  if (nh) {
+    SD_CUDA(cudaMemcpyAsync(host_tok_.data(), tok_, static_cast<size_t>(nh) * 4, cudaMemcpyDeviceToHost, stream_));
+    if (final_x) {
+      fx.resize(static_cast<size_t>(nh) * spec_.D);
+      SD_CUDA(cudaMemcpyAsync(fx.data(), x_, fx.size() * 4, cudaMemcpyDeviceToHost, stream_));
+    }
+  }
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  for (int i = 0; i < nh; ++i) {
+    const int row = plan_.home_rows[static_cast<size_t>(i)];
+    next[row] = host_tok_[static_cast<size_t>(i)];
+    if (final_x) {
+      std::memcpy(final_x + static_cast<size_t>(row) * spec_.D, fx.data() + static_cast<size_t>(i) * spec_.D,
+                  static_cast<size_t>(spec_.D) * 4);
+    }
+  }
+}
+
+double DistEngine::bench(int B, const uint64_t* seqs, const int32_t* tokens, int steps) {
+  DeviceGuard dg(device_);
+  ensure(B);
+  plan_for(B, seqs);
+  pos_.resize(static_cast<size_t>(B));
+  const int nh = static_cast<int>(plan_.home_rows.size());
+  host_tok_.resize(static_cast<size_t>(nh));
+  for (int i = 0; i < nh; ++i) host_tok_[static_cast<size_t>(i)] = tokens[plan_.home_rows[static_cast<size_t>(i)]];
+  if (nh) SD_CUDA(cudaMemcpyAsync(tok_, host_tok_.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
+  cudaEvent_t e0, e1;
+  SD_CUDA(cudaEventCreate(&e0));
+  SD_CUDA(cudaEventCreate(&e1));
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  SD_CUDA(cudaEventRecord(e0, stream_));
+  for (int i = 0; i < steps; ++i) run_step();
+  SD_CUDA(cudaEventRecord(e1, stream_));
+  SD_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  SD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ms;
+}
+
+// DROP_SEQ routed to worker_for(seq, 0) under by-sequence sharding
+// (workers.cpp:482-501): each rank drops the retiring sequences it stores.
+void DistEngine::retire(int n, const uint64_t* seqs) {
+  for (int i = 0; i < n; ++i) {
+    if (shard_of(seqs[i], world_) == rank_) kv_->drop(seqs[i]);
+  }
+}
+
+}  // namespace sd

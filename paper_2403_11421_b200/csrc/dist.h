@@ -1,0 +1,81 @@
+// Multi-GPU decode: the reference's DistributedComputation (workers.cpp:264-501)
+// on NVLink. Every rank is an R-shard holding the KV of the sequences the
+// ShardMap assigns it (mix64(seq) % world, transport.cpp:352-353); S-ranks
+// hold the weights and run the S-Part for their home rows. Per layer the
+// Q/K/V rows of each home row go to the owning shard and the attention
+// outputs come back (send_layer / receive_layer, workers.cpp:324-391), as
+// NCCL grouped send/recv on the compute stream.
+#pragma once
+
+#include <nccl.h>
+
+#include <vector>
+
+#include "engine.h"
+
+namespace sd {
+
+// S-rank of a sequence: rank 0 when s_ranks == 1 (the paper's single
+// S-worker), else seq % s_ranks (data-parallel S-workers).
+inline int home_of(uint64_t seq, int s_ranks) {
+  return s_ranks <= 1 ? 0 : static_cast<int>(seq % static_cast<uint64_t>(s_ranks));
+}
+inline int shard_of(uint64_t seq, int world) {
+  return static_cast<int>(mix64(seq) % static_cast<uint64_t>(world));
+}
+
+// Row plan of one step, identical on every rank (computed from the batch).
+struct DistPlan {
+  std::vector<int32_t> home_rows;   // batch rows this rank runs the S-Part for, grouped by shard
+  std::vector<int32_t> send_cnt, send_off;
+  std::vector<int32_t> shard_rows;  // batch rows whose KV lives here, grouped by source S-rank
+  std::vector<int32_t> recv_cnt, recv_off;
+  std::vector<uint64_t> shard_seqs;
+};
+void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p);
+void nccl_unique_id(ncclUniqueId* id);
+
+class DistEngine : public StepComputation {
+ public:
+  DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks);
+  ~DistEngine() override;
+  void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
+               float* final_x) override;
+  void retire(int n, const uint64_t* seqs) override;
+  bool owns(uint64_t seq) const override { return home_of(seq, s_ranks_) == rank_; }
+  int model_dim() const override { return spec_.D; }
+  int vocab() const override { return spec_.V; }
+  // device-timed loop of `steps` steps over a fixed batch; tokens fed back on device
+  double bench(int B, const uint64_t* seqs, const int32_t* tokens, int steps);
+  void set_timing(bool on) { timing_ = on; }
+  void read_timing(double* exch_ms, double* exch_bytes, bool reset);
+
+ private:
+  void ensure(int B);
+  void plan_for(int B, const uint64_t* seqs);
+  void run_step();
+  void exchange(const float* send, const std::vector<int32_t>& sc, const std::vector<int32_t>& so,
+                float* recv, const std::vector<int32_t>& rc, const std::vector<int32_t>& ro, int width);
+
+  Spec spec_;
+  Weights* w_;
+  KvStore* kv_;
+  int rank_, world_, s_ranks_, device_;
+  ncclComm_t comm_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  DistPlan plan_;
+  std::vector<uint64_t> plan_key_;
+  int cap_ = 0;
+  float *x_ = nullptr, *qkv_h_ = nullptr, *qkv_s_ = nullptr, *o_s_ = nullptr, *o_h_ = nullptr,
+        *y_ = nullptr, *h_ = nullptr, *logits_ = nullptr;
+  __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
+  int32_t* tok_ = nullptr;
+  std::vector<uint32_t> pos_;
+  std::vector<int32_t> host_tok_;
+  bool timing_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
+  std::vector<double> ev_bytes_;
+  double x_ms_ = 0, x_bytes_ = 0;
+};
+
+}  // namespace sd

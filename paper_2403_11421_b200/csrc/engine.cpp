@@ -601,12 +601,14 @@ std::pair<int, int> shard_head_range(int mode, int heads, int workers, int w) {
 }
 
 // ================================================================= drive ===
-DriveResult drive(Engine& e, const Weights& w, const sd_drive_config& c) {
+DriveResult drive(StepComputation& e, const sd_drive_config& c) {
   if (c.batch < 1 || c.target_len < 1 || c.interval < 1) {
     fail(SD_ERR_CONFIG, "generation config: batch, target_len, interval must be >= 1");
   }
   const auto t0 = std::chrono::steady_clock::now();
-  const Spec& s = w.spec();
+  struct {
+    int D, V;
+  } s{e.model_dim(), e.vocab()};
   const bool to_completion = c.steps <= 0;
   int64_t adm_h;
   if (to_completion) {
@@ -670,19 +672,22 @@ DriveResult drive(Engine& e, const Weights& w, const sd_drive_config& c) {
       next.resize(static_cast<size_t>(B));
       for (int i = 0; i < B; ++i) toks[static_cast<size_t>(i)] = last.at(ids[static_cast<size_t>(i)]);
       if (c.record_activations) fx.resize(static_cast<size_t>(B) * s.D);
-      e.step(B, ids.data(), toks.data(), nullptr, next.data(), c.record_activations ? fx.data() : nullptr,
-             nullptr);
+      e.compute(B, ids.data(), toks.data(), next.data(), c.record_activations ? fx.data() : nullptr);
       for (int i = 0; i < B; ++i) {
         const uint64_t q = ids[static_cast<size_t>(i)];
-        res.steps.push_back(u);
-        res.seqs.push_back(q);
-        res.tokens.push_back(next[static_cast<size_t>(i)]);
         last[q] = next[static_cast<size_t>(i)];
         auto& st = states.at(q);
         st.first += 1;
         if (st.first > st.second) fail(SD_ERR_LOGIC, "sequence ran past its target length");
+        if (!e.owns(q)) continue;  // another rank produced this row's token
+        res.steps.push_back(u);
+        res.seqs.push_back(q);
+        res.tokens.push_back(next[static_cast<size_t>(i)]);
+        if (c.record_activations) {
+          res.activations.insert(res.activations.end(), fx.begin() + static_cast<int64_t>(i) * s.D,
+                                 fx.begin() + static_cast<int64_t>(i + 1) * s.D);
+        }
       }
-      if (c.record_activations) res.activations.insert(res.activations.end(), fx.begin(), fx.end());
     }
     if (!plan.ending.empty()) {
       std::vector<uint64_t> retiring;

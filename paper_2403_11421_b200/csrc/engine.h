@@ -54,17 +54,38 @@ class Weights {
   size_t head_off_ = 0;
 };
 
-// The GPU StepComputation (workers.hpp:151-158): decode_step_monolithic
-// (dense.cpp:90-129) with the S-Part on tensor cores / CUDA cores and the
-// R-Part on the KvStore, all on one device stream.
-class Engine {
+// StepComputation (workers.hpp:151-158): the per-step hook drive_schedule
+// runs against. `owns` tells the driver which rows' tokens this process
+// produced (all of them single-GPU; the home rows of a rank when
+// distributed).
+class StepComputation {
+ public:
+  virtual ~StepComputation() = default;
+  virtual void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
+                       float* final_x) = 0;
+  virtual void retire(int n, const uint64_t* seqs) = 0;
+  virtual bool owns(uint64_t /*seq*/) const { return true; }
+  virtual int model_dim() const = 0;
+  virtual int vocab() const = 0;
+};
+
+// The GPU StepComputation: decode_step_monolithic (dense.cpp:90-129) with the
+// S-Part on tensor cores / CUDA cores and the R-Part on the KvStore, all on
+// one device stream.
+class Engine : public StepComputation {
  public:
   Engine(Weights* w, KvStore* kv);
-  ~Engine();
+  ~Engine() override;
+  void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
+               float* final_x) override {
+    step(B, seqs, tokens, nullptr, next, final_x, nullptr);
+  }
+  int model_dim() const override { return w_->spec().D; }
+  int vocab() const override { return w_->spec().V; }
   // features from token ids (workers.cpp:629-638) or explicit [B][D]
   void step(int B, const uint64_t* seqs, const int32_t* tokens_host, const float* x_host,
             int32_t* next_host, float* final_host, float* logits_host);
-  void retire(int n, const uint64_t* seqs);
+  void retire(int n, const uint64_t* seqs) override;
   double bench(int B, const uint64_t* seqs, const int32_t* tokens_host, int steps,
                int32_t* next_host);
   cudaStream_t stream() const { return stream_; }
@@ -146,6 +167,6 @@ struct DriveResult {
   std::vector<float> activations;
   double wall_seconds = 0;
 };
-DriveResult drive(Engine& e, const Weights& w, const sd_drive_config& c);
+DriveResult drive(StepComputation& e, const sd_drive_config& c);
 
 }  // namespace sd

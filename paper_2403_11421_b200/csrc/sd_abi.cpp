@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "dist.h"
 #include "engine.h"
 #include "kv_store.h"
 #include "sd_common.h"
@@ -25,6 +26,9 @@ struct sd_engine {
 };
 struct sd_drive_result {
   sd::DriveResult r;
+};
+struct sd_dist {
+  std::unique_ptr<sd::DistEngine> d;
 };
 
 namespace {
@@ -512,7 +516,7 @@ int sd_drive(sd_engine* e, const sd_drive_config* cfg, sd_drive_result** out) {
     need(cfg, "config");
     need(out, "out");
     auto r = std::make_unique<sd_drive_result>();
-    r->r = sd::drive(*e->e, *e->w->w, *cfg);
+    r->r = sd::drive(*e->e, *cfg);
     *out = r.release();
   });
 }
@@ -540,6 +544,102 @@ double sd_drive_wall_seconds(const sd_drive_result* r) { return r ? r->r.wall_se
 
 int sd_drive_destroy(sd_drive_result* r) {
   return guard([&] { delete r; });
+}
+
+// ------------------------------------------------------------ multi-GPU ---
+int sd_nccl_unique_id(void* out, size_t bytes) {
+  return guard([&] {
+    need(out, "out");
+    if (bytes < sizeof(ncclUniqueId)) sd::fail(SD_ERR_CONFIG, "nccl id buffer too small");
+    ncclUniqueId id;
+    sd::nccl_unique_id(&id);
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int sd_dist_create(sd_weights* w, sd_kv* kv, int rank, int world, const void* nccl_id, int s_ranks,
+                   sd_dist** out) {
+  return guard([&] {
+    need(kv, "kv");
+    need(out, "out");
+    if (world > 1) need(nccl_id, "nccl_id");
+    auto h = std::make_unique<sd_dist>();
+    h->d = std::make_unique<sd::DistEngine>(w ? w->w.get() : nullptr, kv->s.get(), rank, world, nccl_id,
+                                            s_ranks);
+    *out = h.release();
+  });
+}
+
+int sd_dist_destroy(sd_dist* d) {
+  return guard([&] { delete d; });
+}
+
+int sd_dist_step(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
+                 float* final_x) {
+  return guard([&] {
+    need(d, "dist");
+    need(seqs, "seqs");
+    need(tokens, "tokens");
+    need(next, "next_tokens");
+    d->d->compute(B, seqs, tokens, next, final_x);
+  });
+}
+
+int sd_dist_retire(sd_dist* d, int32_t n, const uint64_t* seqs) {
+  return guard([&] {
+    need(d, "dist");
+    d->d->retire(n, seqs);
+  });
+}
+
+int sd_dist_bench(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens, int32_t steps,
+                  double* ms) {
+  return guard([&] {
+    need(d, "dist");
+    need(ms, "ms");
+    *ms = d->d->bench(B, seqs, tokens, steps);
+  });
+}
+
+int sd_dist_drive(sd_dist* d, const sd_drive_config* cfg, sd_drive_result** out) {
+  return guard([&] {
+    need(d, "dist");
+    need(cfg, "config");
+    need(out, "out");
+    auto r = std::make_unique<sd_drive_result>();
+    r->r = sd::drive(*d->d, *cfg);
+    *out = r.release();
+  });
+}
+
+int sd_dist_timing(sd_dist* d, int enable) {
+  return guard([&] {
+    need(d, "dist");
+    d->d->set_timing(enable != 0);
+  });
+}
+
+int sd_dist_timing_read(sd_dist* d, double* ms, double* bytes, int reset) {
+  return guard([&] {
+    need(d, "dist");
+    d->d->read_timing(ms, bytes, reset != 0);
+  });
+}
+
+int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs, int32_t* home_rows,
+                 int32_t* n_home, int32_t* shard_rows, int32_t* n_shard, int32_t* send_counts,
+                 int32_t* recv_counts) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) sd::fail(SD_ERR_CONFIG, "bad rank / world");
+    sd::DistPlan p;
+    sd::make_plan(world, rank, s_ranks, B, seqs, p);
+    if (n_home) *n_home = static_cast<int32_t>(p.home_rows.size());
+    if (n_shard) *n_shard = static_cast<int32_t>(p.shard_rows.size());
+    if (home_rows) std::copy(p.home_rows.begin(), p.home_rows.end(), home_rows);
+    if (shard_rows) std::copy(p.shard_rows.begin(), p.shard_rows.end(), shard_rows);
+    if (send_counts) std::copy(p.send_cnt.begin(), p.send_cnt.end(), send_counts);
+    if (recv_counts) std::copy(p.recv_cnt.begin(), p.recv_cnt.end(), recv_counts);
+  });
 }
 
 // ------------------------------------------------------ shardmap / load ---

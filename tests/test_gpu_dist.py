@@ -1,0 +1,78 @@
+"""Distributed ≡ monolithic on >= 2 GPUs (proj/tests/test_workers.cpp:280-332,
+acceptance.cpp:259-301): the DistEngine's NCCL Q/K/V / O exchange over
+sequence-sharded KV with one S-rank (the paper's topology) or data-parallel
+S-ranks; identical tokens, activations <= 1e-5 against the oracle."""
+import os
+import pickle
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, s_ranks, cfg, out_path):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
+    import torch
+    import torch.distributed as dist
+    import oracle as o
+    import paper_2403_11421_b200 as sd
+    from conftest import upload_oracle_weights
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    obj = [sd.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    W = o.Weights(o.make_spec(2, 64, 4, 256, 128), 0)
+    is_s = s_ranks == world or rank == 0
+    dw = upload_oracle_weights(W, "exact", device=rank) if is_s else None
+    spec = sd.make_model_spec(2, 64, 4, 256, 128)
+    kv = sd.KvShard(spec, 0, 4, 1 << 16, "single", rank)
+    eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks)
+    recs, acts, _ = sd.run_generation(eng, *cfg, seed=0, record_activations=True)
+    rows = [(r, acts[i].tolist()) for i, r in enumerate(recs)]
+    allr = [None] * world
+    dist.all_gather_object(allr, rows)
+    if rank == 0:
+        with open(out_path, "wb") as f:
+            pickle.dump([x for part in allr for x in part], f)
+    eng.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("s_ranks", [1, 2])
+@pytest.mark.parametrize("cfg", [(8, 32, 32, 32), (8, 16, 4, 48)], ids=["batch", "stabilized"])
+def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg):
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rows.pkl")
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out), nprocs=2, join=True)
+    rows = pickle.load(open(out, "rb"))
+    W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 128), 0)
+    orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
+    ref = {(s, q): (t, oacts[i]) for i, (s, q, t) in enumerate(orecs)}
+    assert len(rows) == len(ref)
+    worst = 0.0
+    for (s, q, t), x in rows:
+        rt, rx = ref[(s, q)]
+        assert t == rt
+        worst = max(worst, float(np.abs(np.asarray(x, np.float32) - rx).max()))
+    assert worst <= 1e-5
