@@ -127,8 +127,111 @@ def host_threads():
         return os.cpu_count() or 1
 
 
+# ------------------------------------------------------- ours, N GPUs
+def run_dist(args, wl, rank, world, dev, dist):
+    """DistributedComputation over NCCL (workers.cpp:264-501): every rank an
+    R-shard of the sequences ShardMap by-sequence gives it, every rank an
+    S-worker for its home rows (seq % N); per layer Q/K/V rows go to the
+    owning shard and O rows come back over NVLink. Weak scaling: B rows and
+    ~B KV sequences per GPU."""
+    import numpy as np
+    import torch
+    import paper_2403_11421_b200 as sd
+
+    L, D, H, Hkv, F, V, B, ctx, fmt, dense = wl
+    pk = peaks()
+    spec = sd.make_model_spec(L, D, H, F, V, Hkv)
+    steps_total = args.warmup + args.steps + args.e2e_steps + 8
+    s_ranks = world if args.s_ranks == 0 else args.s_ranks
+    seqs = list(range(1, B * world + 1))
+    plan = sd.dist_plan(world, rank, s_ranks, seqs)
+    mine = [seqs[i] for i in plan["shard_rows"]]
+    nmax = torch.tensor([len(mine)], device=f"cuda:{dev}")
+    dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
+    cap_seqs = int(nmax.item())
+    is_s = s_ranks == world or rank == 0
+    weights = sd.DeviceWeights(spec, None, dense, dev, seed=0) if is_s else None
+    kv = sd.KvShard(spec, 0, spec.num_kv_heads, cap_seqs * (ctx + steps_total), fmt, dev,
+                    max_sequences=cap_seqs, max_seq_len=ctx + steps_total + 16)
+    kv.prefill_synthetic(mine, ctx, salt=rank)
+    obj = [sd.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks)
+    tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
+
+    eng.bench(seqs, tokens, args.warmup)
+    torch.cuda.synchronize(dev)
+    kv.timing(True)
+    eng.timing(True)
+    kv.timing_read(reset=True)
+    eng.timing_read(reset=True)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = Clocks(dev)
+    l0 = sd.launch_count()
+    ms = eng.bench(seqs, tokens, args.steps)
+    l1 = sd.launch_count()
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    a_ms, a_n, a_bytes = kv.timing_read()
+    x_ms, x_bytes = eng.timing_read()
+    kv.timing(False)
+    eng.timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = B * world * args.steps / (ms / 1e3)
+
+    pin_in = torch.empty(len(seqs), dtype=torch.int32).pin_memory().numpy()
+    pin_in[:] = tokens
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        nxt, _ = eng.compute(seqs, pin_in)
+        home = np.asarray(plan["home_rows"], dtype=np.int64)
+        pin_in[home] = nxt[home]
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    eng.close()
+    kv.close()
+    if weights is not None:
+        weights.close()
+    achieved = a_bytes / (a_ms / 1e3) / 1e9 if a_ms > 0 else 0.0
+    return {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (counter-hash weights and KV prefill; no checkpoint)",
+        "config": {"workload": args.workload, "model": "Llama-3-8B GQA shape (reference 2-matrix SiLU MLP)",
+                   "layers": L, "model_dim": D, "heads": H, "kv_heads": Hkv, "mlp_dim": F, "vocab": V,
+                   "batch_per_gpu": B, "global_batch": B * world, "context": ctx, "kv_format": fmt,
+                   "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
+                   "parallelism": f"kv sharded by mix64(seq)%{world} (ShardMap by-sequence); "
+                                  f"{s_ranks} S-rank(s); per-layer NCCL Q/K/V->shard, O->S",
+                   "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
+        "roofline": {"bound": "hbm", "kernel": "attention (rank 0)", "achieved": achieved,
+                     "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                     "traffic": None, "launches": a_n, "ms_per_launch": a_ms / max(a_n, 1),
+                     "share_of_step": a_ms / ms if ms else None},
+        "exchange": {"ms_per_step": x_ms / args.steps, "bytes_per_step_rank0": x_bytes / args.steps,
+                     "gbs": x_bytes / (x_ms / 1e3) / 1e9 if x_ms else None, "shard_rows_rank0": len(mine),
+                     "max_shard_rows": cap_seqs},
+        "e2e": {"value": B * world * args.e2e_steps / e2e_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": int(len(plan["home_rows"]) * 4),
+                "d2h_bytes_per_step": int(len(plan["home_rows"]) * 4),
+                "steps": args.e2e_steps, "api": "sd_dist_step (include/sd_abi.h)"},
+        "gpu_launches": int(l1 - l0),
+        "clocks": clocks,
+    }
+
+
 # ------------------------------------------------------------------ ours
 def run_ours(args, wl, rank, world, dev, dist):
+    if world > 1:
+        return run_dist(args, wl, rank, world, dev, dist)
     import numpy as np
     import torch
     import paper_2403_11421_b200 as sd
@@ -281,6 +384,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT, choices=sorted(WORKLOADS))
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--s-ranks", type=int, default=0,
+                    help="N>1: S-workers (1 = the paper's single S-rank; 0 = every rank)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
