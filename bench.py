@@ -244,6 +244,8 @@ def run_ours(args, wl, rank, world, dev, dist):
     kv = sd.KvShard(spec, 0, spec.num_kv_heads, B * (ctx + steps_total), fmt, dev,
                     max_sequences=B, max_seq_len=ctx + steps_total + 16)
     eng = sd.Engine(weights, kv)
+    if args.r_sms > 0:  # two-mini-batch S/R pipeline (workers.cpp:405-452)
+        eng.pipeline(True, args.r_sms)
     # sequence ids of this rank's shard: ids whose mix64 hash lands here
     # (ShardMap by-sequence, transport.cpp:352-353), B per GPU
     seqs, q = [], 1
@@ -384,6 +386,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT, choices=sorted(WORKLOADS))
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--r-sms", type=int, default=0,
+                    help="two-mini-batch S/R pipeline: SMs for the R-Part (0 = off)")
     ap.add_argument("--s-ranks", type=int, default=0,
                     help="N>1: S-workers (1 = the paper's single S-rank; 0 = every rank)")
     args = ap.parse_args()

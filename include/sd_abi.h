@@ -207,6 +207,11 @@ int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t
  * milliseconds and algorithmic flops since the last reset). */
 int sd_engine_timing(sd_engine* e, int enable);
 int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* launches, int reset);
+/* Two-mini-batch pipeline (workers.cpp:405-452): rows split by seq % 2; the
+ * R-Part of one mini-batch runs on r_sms SMs (its own stream) beside the
+ * S-Part of the other on the remaining SMs. enable = 0: one batch, one
+ * stream (default). */
+int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
 /* Kernel launches issued by this library in this process (all devices). */
 int64_t sd_launch_count(void);
 /* Synthetic device-generated weights (uniform +-1/sqrt(fan_in), counter

@@ -100,6 +100,7 @@ SIGNATURES = {
     "sd_engine_timing": (C.c_int, [P, C.c_int]),
     "sd_engine_timing_read": (C.c_int, [P, DP, DP, I64P, C.c_int]),
     "sd_launch_count": (C.c_int64, []),
+    "sd_engine_pipeline": (C.c_int, [P, C.c_int, C.c_int]),
     "sd_weights_synthetic": (C.c_int, [SPEC_P, C.c_int, C.c_uint64, C.c_int, PP]),
     "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_drive_count": (C.c_int64, [P]),

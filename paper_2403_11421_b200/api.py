@@ -396,6 +396,11 @@ class Engine:
         s, sp = _u64(seqs)
         _check(lib.sd_engine_retire(self.h, len(s), sp))
 
+    def pipeline(self, enable: bool, r_sms: int = 96):
+        """Two-mini-batch S/R pipeline (workers.cpp:405-452): attention of one
+        mini-batch on r_sms SMs beside the GEMMs of the other."""
+        _check(lib.sd_engine_pipeline(self.h, int(enable), r_sms))
+
     def timing(self, enable: bool):
         """CUDA-event timing of the S-Part GEMMs."""
         _check(lib.sd_engine_timing(self.h, int(enable)))

@@ -46,7 +46,8 @@ struct GemmArgs {
   int epi;
   const float* res;
   int64_t ldr;
-  int kind;  // 1 = bf16 (kind::f16), 2 = tf32
+  int kind;      // 1 = bf16 (kind::f16), 2 = tf32
+  int max_ctas;  // SM budget of the persistent grid (0 = every SM)
 };
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);

@@ -157,6 +157,7 @@ void DistEngine::ensure(int B) {
   zalloc(reinterpret_cast<void**>(&yb_), bp * s.D * 2);
   zalloc(reinterpret_cast<void**>(&hb_), bp * s.F * 2);
   zalloc(reinterpret_cast<void**>(&tok_), bp * 4);
+  SD_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets before non-blocking-stream use
   cap_ = B;
 }
 

@@ -203,7 +203,7 @@ Weights::~Weights() {
 void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
                      const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy,
                      __nv_bfloat16* yb, int64_t ldyb, int epi, const float* res, int64_t ldr,
-                     cudaStream_t s) const {
+                     cudaStream_t s, int max_ctas) const {
   if (which != 7 && (layer < 0 || layer >= spec_.L)) fail(SD_ERR_CONFIG, "layer out of range");
   const int in = in_dim(which), out = out_dim(which);
   const void* W = tensor(layer, which);
@@ -236,207 +236,9 @@ void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
   g.epi = epi;
   g.res = res;
   g.ldr = ldr;
+  g.max_ctas = max_ctas;
   if (!gemm_sm100_supported(g)) fail(SD_ERR_CONFIG, "shape not supported by the tcgen05 GEMM");
   launch_gemm_sm100(g, s);
-}
-
-// ================================================================ engine ===
-Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
-  if (w->device() != kv->device()) fail(SD_ERR_CONFIG, "weights and KV store on different devices");
-  const Spec& a = w->spec();
-  const Spec& b = kv->spec();
-  if (a.L != b.L || a.D != b.D || a.H != b.H || a.Hkv != b.Hkv || a.hd != b.hd) {
-    fail(SD_ERR_CONFIG, "weights and KV store specs differ");
-  }
-  if (kv->width() != a.kv_width()) fail(SD_ERR_CONFIG, "engine needs a KV store over all kv heads");
-  DeviceGuard dg(w->device());
-  SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-}
-
-Engine::~Engine() {
-  DeviceGuard dg(w_->device());
-  cudaStreamSynchronize(stream_);
-  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_), static_cast<void*>(o_),
-                  static_cast<void*>(y_), static_cast<void*>(h_), static_cast<void*>(logits_),
-                  static_cast<void*>(xb_), static_cast<void*>(ob_), static_cast<void*>(yb_),
-                  static_cast<void*>(hb_), static_cast<void*>(tok_)}) {
-    if (p) cudaFree(p);
-  }
-  cudaStreamDestroy(stream_);
-}
-
-void Engine::ensure(int B) {
-  if (B <= cap_B_) return;
-  DeviceGuard dg(w_->device());
-  SD_CUDA(cudaStreamSynchronize(stream_));
-  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_), static_cast<void*>(o_),
-                  static_cast<void*>(y_), static_cast<void*>(h_), static_cast<void*>(logits_),
-                  static_cast<void*>(xb_), static_cast<void*>(ob_), static_cast<void*>(yb_),
-                  static_cast<void*>(hb_), static_cast<void*>(tok_)}) {
-    if (p) cudaFree(p);
-  }
-  const Spec& s = w_->spec();
-  const size_t b = static_cast<size_t>(B);
-  // rows padded to 128 so tensor-core tiles never read past the buffers
-  const size_t bp = (b + 127) / 128 * 128;
-  SD_CUDA(cudaMalloc(&x_, bp * s.D * 4));
-  SD_CUDA(cudaMalloc(&qkv_, bp * s.qkv_width() * 4));
-  SD_CUDA(cudaMalloc(&o_, bp * s.D * 4));
-  SD_CUDA(cudaMalloc(&y_, bp * s.D * 4));
-  SD_CUDA(cudaMalloc(&h_, bp * s.F * 4));
-  SD_CUDA(cudaMalloc(&logits_, bp * s.V * 4));
-  SD_CUDA(cudaMalloc(&xb_, bp * s.D * 2));
-  SD_CUDA(cudaMalloc(&ob_, bp * s.D * 2));
-  SD_CUDA(cudaMalloc(&yb_, bp * s.D * 2));
-  SD_CUDA(cudaMalloc(&hb_, bp * s.F * 2));
-  SD_CUDA(cudaMalloc(&tok_, bp * 4));
-  SD_CUDA(cudaMemset(xb_, 0, bp * s.D * 2));
-  SD_CUDA(cudaMemset(ob_, 0, bp * s.D * 2));
-  SD_CUDA(cudaMemset(yb_, 0, bp * s.D * 2));
-  SD_CUDA(cudaMemset(hb_, 0, bp * s.F * 2));
-  SD_CUDA(cudaMemset(x_, 0, bp * s.D * 4));
-  SD_CUDA(cudaMemset(o_, 0, bp * s.D * 4));
-  SD_CUDA(cudaMemset(y_, 0, bp * s.D * 4));
-  SD_CUDA(cudaMemset(h_, 0, bp * s.F * 4));
-  cap_B_ = static_cast<int>(B);
-  pos_.resize(b);
-}
-
-void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
-                  const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
-                  int64_t ldyb, int epi, const float* res, int64_t ldr) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing_) {
-    for (cudaEvent_t* e : {&e0, &e1}) {
-      if (ev_pool_.empty()) {
-        SD_CUDA(cudaEventCreate(e));
-      } else {
-        *e = ev_pool_.back();
-        ev_pool_.pop_back();
-      }
-    }
-    SD_CUDA(cudaEventRecord(e0, stream_));
-  }
-  w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_);
-  if (timing_) {
-    SD_CUDA(cudaEventRecord(e1, stream_));
-    ev_.emplace_back(e0, e1);
-    ev_flops_.push_back(2.0 * B * w_->out_dim(which) * w_->in_dim(which));
-  }
-}
-
-void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool reset) {
-  for (size_t i = 0; i < ev_.size(); ++i) {
-    SD_CUDA(cudaEventSynchronize(ev_[i].second));
-    float t = 0;
-    SD_CUDA(cudaEventElapsedTime(&t, ev_[i].first, ev_[i].second));
-    t_ms_ += t;
-    t_flops_ += ev_flops_[i];
-    t_n_ += 1;
-    ev_pool_.push_back(ev_[i].first);
-    ev_pool_.push_back(ev_[i].second);
-  }
-  ev_.clear();
-  ev_flops_.clear();
-  if (ms) *ms = t_ms_;
-  if (flops) *flops = t_flops_;
-  if (launches) *launches = t_n_;
-  if (reset) {
-    t_ms_ = t_flops_ = 0;
-    t_n_ = 0;
-  }
-}
-
-// decode_step_monolithic body after the features are in x_ (dense.cpp:95-122)
-void Engine::run_layers(int B, const uint64_t* seqs) {
-  const Spec& s = w_->spec();
-  const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
-  const bool bf = w_->mode() == SD_DENSE_BF16;
-  for (int l = 0; l < s.L; ++l) {
-    gemm(l, 0, B, x_, D, xb_, D, qkv_, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
-    for (int i = 0; i < B; ++i) pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(seqs[i], l));
-    kv_->append(l, B, seqs, pos_.data(), qkv_ + D, qkvw, qkv_ + D + kvw, qkvw, stream_);
-    kv_->attend(l, B, seqs, qkv_, qkvw, o_, D, stream_);
-    if (bf) launch_to_bf16(B, D, o_, D, ob_, D, stream_);
-    gemm(l, 4, B, o_, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D);
-    gemm(l, 5, B, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0);
-    gemm(l, 6, B, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D);
-  }
-}
-
-void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const float* x_host,
-                  int32_t* next_host, float* final_host, float* logits_host) {
-  const Spec& s = w_->spec();
-  if (B == 0) fail(SD_ERR_CONFIG, "project_qkv: empty batch");
-  {
-    std::unordered_set<uint64_t> seen;  // validate_batch (core.cpp:37-54)
-    for (int i = 0; i < B; ++i) {
-      if (!seen.insert(seqs[i]).second) {
-        fail(SD_ERR_CONFIG, "token batch: duplicate sequence id " + std::to_string(seqs[i]));
-      }
-    }
-  }
-  ensure(B);
-  DeviceGuard dg(w_->device());
-  const bool bf = w_->mode() == SD_DENSE_BF16;
-  if (tokens_host) {
-    for (int i = 0; i < B; ++i) {
-      if (tokens_host[i] < 0 || tokens_host[i] >= s.V) fail(SD_ERR_CONFIG, "token out of the vocabulary");
-    }
-    SD_CUDA(cudaMemcpyAsync(tok_, tokens_host, static_cast<size_t>(B) * 4, cudaMemcpyHostToDevice, stream_));
-    launch_embed(B, s.D, tok_, w_->embedding(), x_, s.D, bf ? xb_ : nullptr, stream_);
-  } else {
-    SD_CUDA(cudaMemcpyAsync(x_, x_host, static_cast<size_t>(B) * s.D * 4, cudaMemcpyHostToDevice, stream_));
-    if (bf) launch_to_bf16(B, s.D, x_, s.D, xb_, s.D, stream_);
-  }
-  run_layers(B, seqs);
-  gemm(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0);
-  launch_argmax(B, s.V, logits_, s.V, tok_, stream_);
-  if (next_host) {
-    SD_CUDA(cudaMemcpyAsync(next_host, tok_, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
-  }
-  if (final_host) {
-    SD_CUDA(cudaMemcpyAsync(final_host, x_, static_cast<size_t>(B) * s.D * 4, cudaMemcpyDeviceToHost, stream_));
-  }
-  if (logits_host) {
-    SD_CUDA(cudaMemcpyAsync(logits_host, logits_, static_cast<size_t>(B) * s.V * 4, cudaMemcpyDeviceToHost, stream_));
-  }
-  SD_CUDA(cudaStreamSynchronize(stream_));
-}
-
-void Engine::step_device(int B, const uint64_t* seqs, const int32_t* tokens_dev, int32_t* next_dev) {
-  const Spec& s = w_->spec();
-  ensure(B);
-  const bool bf = w_->mode() == SD_DENSE_BF16;
-  launch_embed(B, s.D, tokens_dev, w_->embedding(), x_, s.D, bf ? xb_ : nullptr, stream_);
-  run_layers(B, seqs);
-  gemm(0, 7, B, x_, s.D, xb_, s.D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0);
-  launch_argmax(B, s.V, logits_, s.V, next_dev, stream_);
-}
-
-double Engine::bench(int B, const uint64_t* seqs, const int32_t* tokens_host, int steps,
-                     int32_t* next_host) {
-  ensure(B);
-  DeviceGuard dg(w_->device());
-  SD_CUDA(cudaMemcpyAsync(tok_, tokens_host, static_cast<size_t>(B) * 4, cudaMemcpyHostToDevice, stream_));
-  cudaEvent_t e0, e1;
-  SD_CUDA(cudaEventCreate(&e0));
-  SD_CUDA(cudaEventCreate(&e1));
-  SD_CUDA(cudaStreamSynchronize(stream_));
-  SD_CUDA(cudaEventRecord(e0, stream_));
-  for (int i = 0; i < steps; ++i) step_device(B, seqs, tok_, tok_);
-  SD_CUDA(cudaEventRecord(e1, stream_));
-  SD_CUDA(cudaEventSynchronize(e1));
-  float ms = 0;
-  SD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (next_host) SD_CUDA(cudaMemcpy(next_host, tok_, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost));
-  return ms;
-}
-
-void Engine::retire(int n, const uint64_t* seqs) {
-  for (int i = 0; i < n; ++i) kv_->drop(seqs[i]);
 }
 
 // ============================================================= scheduler ===

@@ -37,7 +37,8 @@ class Weights {
   // x_bf16 is required in BF16 mode (A operand), ignored otherwise.
   void linear(int layer, int which, int B, const float* x, int64_t ldx,
               const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
-              int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s) const;
+              int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s,
+              int max_ctas = 0) const;
   const float* embedding() const { return emb_; }
   int out_dim(int which) const;
   int in_dim(int which) const;
@@ -89,15 +90,31 @@ class Engine : public StepComputation {
   double bench(int B, const uint64_t* seqs, const int32_t* tokens_host, int steps,
                int32_t* next_host);
   cudaStream_t stream() const { return stream_; }
-  // device-resident step: tokens_dev -> next_dev (no host sync)
-  void step_device(int B, const uint64_t* seqs, const int32_t* tokens_dev, int32_t* next_dev);
-  // CUDA-event timing of the S-Part GEMMs (on the engine stream)
+  // CUDA-event timing of the S-Part GEMMs (on the S stream)
   void set_timing(bool on) { timing_ = on; }
   void read_timing(double* ms, double* flops, int64_t* launches, bool reset);
+  // Two-mini-batch pipeline (workers.cpp:405-452): rows split by seq % 2;
+  // the R-Part of one mini-batch (r_sms SMs, R stream) runs beside the
+  // S-Part of the other (the remaining SMs, S stream). Off: one batch, one
+  // stream, every kernel on every SM.
+  void set_pipeline(bool on, int r_sms);
 
  private:
-  void ensure(int B);
-  void run_layers(int B, const uint64_t* seqs);
+  struct Group {  // one mini-batch in flight (DistributedComputation::GroupState)
+    std::vector<int> rows;
+    std::vector<uint64_t> seqs;
+    int cap = 0;
+    float *x = nullptr, *qkv = nullptr, *o = nullptr, *y = nullptr, *h = nullptr, *logits = nullptr;
+    __nv_bfloat16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
+    int32_t* tok = nullptr;
+    cudaEvent_t ev_s = nullptr, ev_r = nullptr;
+    std::vector<uint32_t> pos;
+    std::vector<int32_t> host_tok;
+  };
+  int split(int B, const uint64_t* seqs);  // fills groups_, returns the group count
+  void ensure(Group& g, int n);
+  void free_group(Group& g);
+  void run(int ng, bool embed);
   void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
             int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
             const float* res, int64_t ldr);
@@ -111,13 +128,11 @@ class Engine : public StepComputation {
 
   Weights* w_;
   KvStore* kv_;
-  cudaStream_t stream_ = nullptr;
-  int cap_B_ = 0;
-  float *x_ = nullptr, *qkv_ = nullptr, *o_ = nullptr, *y_ = nullptr, *h_ = nullptr,
-        *logits_ = nullptr;
-  __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
-  int32_t* tok_ = nullptr;
-  std::vector<uint32_t> pos_;
+  cudaStream_t stream_ = nullptr;    // S stream (the only stream without the pipeline)
+  cudaStream_t stream_r_ = nullptr;  // R stream
+  bool pipeline_ = false;
+  int r_sms_ = 0, s_sms_ = 0;
+  Group groups_[2];
 };
 
 // ---- scheduler (scheduler.cpp:10-236), kept in host C++

@@ -1,0 +1,328 @@
+// The GPU StepComputation: decode_step_monolithic (dense.cpp:90-129), run
+// either as one batch on one stream or as the reference's two interleaved
+// mini-batches (DistributedComputation::compute, workers.cpp:399-480) on an
+// S stream and an R stream, so that the R-Part of one mini-batch (HBM-bound
+// attention) overlaps the S-Part of the other (tensor-core GEMMs) on
+// disjoint SM partitions — FastDecode's S/R split inside one B200.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+
+#include "engine.h"
+
+namespace sd {
+
+Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
+  if (w->device() != kv->device()) fail(SD_ERR_CONFIG, "weights and KV store on different devices");
+  const Spec& a = w->spec();
+  const Spec& b = kv->spec();
+  if (a.L != b.L || a.D != b.D || a.H != b.H || a.Hkv != b.Hkv || a.hd != b.hd) {
+    fail(SD_ERR_CONFIG, "weights and KV store specs differ");
+  }
+  if (kv->width() != a.kv_width()) fail(SD_ERR_CONFIG, "engine needs a KV store over all kv heads");
+  DeviceGuard dg(w->device());
+  SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  SD_CUDA(cudaStreamCreateWithFlags(&stream_r_, cudaStreamNonBlocking));
+  for (Group& g : groups_) {
+    SD_CUDA(cudaEventCreateWithFlags(&g.ev_s, cudaEventDisableTiming));
+    SD_CUDA(cudaEventCreateWithFlags(&g.ev_r, cudaEventDisableTiming));
+  }
+}
+
+void Engine::free_group(Group& g) {
+  for (void* p : {static_cast<void*>(g.x), static_cast<void*>(g.qkv), static_cast<void*>(g.o),
+                  static_cast<void*>(g.y), static_cast<void*>(g.h), static_cast<void*>(g.logits),
+                  static_cast<void*>(g.xb), static_cast<void*>(g.ob), static_cast<void*>(g.yb),
+                  static_cast<void*>(g.hb), static_cast<void*>(g.tok)}) {
+    if (p) cudaFree(p);
+  }
+  g.x = g.qkv = g.o = g.y = g.h = g.logits = nullptr;
+  g.xb = g.ob = g.yb = g.hb = nullptr;
+  g.tok = nullptr;
+  g.cap = 0;
+}
+
+Engine::~Engine() {
+  DeviceGuard dg(w_->device());
+  cudaStreamSynchronize(stream_);
+  cudaStreamSynchronize(stream_r_);
+  for (Group& g : groups_) {
+    free_group(g);
+    cudaEventDestroy(g.ev_s);
+    cudaEventDestroy(g.ev_r);
+  }
+  for (auto& e : ev_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  cudaStreamDestroy(stream_);
+  cudaStreamDestroy(stream_r_);
+}
+
+void Engine::set_pipeline(bool on, int r_sms) {
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, w_->device());
+  pipeline_ = on;
+  r_sms_ = on ? std::max(1, std::min(r_sms, nsm - 1)) : 0;
+  s_sms_ = on ? nsm - r_sms_ : 0;
+  kv_->set_grid_limit(r_sms_);
+}
+
+void Engine::ensure(Group& g, int n) {
+  if (n <= g.cap) return;
+  DeviceGuard dg(w_->device());
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  SD_CUDA(cudaStreamSynchronize(stream_r_));
+  free_group(g);
+  const Spec& s = w_->spec();
+  // rows padded to 128 so tensor-core tiles never read past the buffers
+  const size_t bp = (static_cast<size_t>(n) + 127) / 128 * 128;
+  auto zalloc = [&](auto** p, size_t bytes) {
+    SD_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    SD_CUDA(cudaMemset(*p, 0, bytes));
+  };
+  zalloc(&g.x, bp * s.D * 4);
+  zalloc(&g.qkv, bp * s.qkv_width() * 4);
+  zalloc(&g.o, bp * s.D * 4);
+  zalloc(&g.y, bp * s.D * 4);
+  zalloc(&g.h, bp * s.F * 4);
+  zalloc(&g.logits, bp * s.V * 4);
+  zalloc(&g.xb, bp * s.D * 2);
+  zalloc(&g.ob, bp * s.D * 2);
+  zalloc(&g.yb, bp * s.D * 2);
+  zalloc(&g.hb, bp * s.F * 2);
+  zalloc(&g.tok, bp * 4);
+  // cudaMemset runs on the legacy stream, which does not order with the
+  // engine's non-blocking streams: finish it before any kernel touches g
+  SD_CUDA(cudaDeviceSynchronize());
+  g.cap = n;
+}
+
+// Mini-batches by sequence id parity, merged when one is empty
+// (workers.cpp:405-420); without the pipeline, one batch in row order.
+int Engine::split(int B, const uint64_t* seqs) {
+  for (Group& g : groups_) {
+    g.rows.clear();
+    g.seqs.clear();
+  }
+  if (pipeline_) {
+    for (int b = 0; b < B; ++b) groups_[seqs[b] % 2].rows.push_back(b);
+    if (groups_[0].rows.empty() || groups_[1].rows.empty()) {
+      std::vector<int> all;
+      for (Group& g : groups_) all.insert(all.end(), g.rows.begin(), g.rows.end());
+      std::sort(all.begin(), all.end());
+      groups_[0].rows = all;
+      groups_[1].rows.clear();
+    }
+  } else {
+    for (int b = 0; b < B; ++b) groups_[0].rows.push_back(b);
+  }
+  int ng = 0;
+  for (Group& g : groups_) {
+    if (g.rows.empty()) continue;
+    for (int r : g.rows) g.seqs.push_back(seqs[r]);
+    ensure(g, static_cast<int>(g.rows.size()));
+    g.pos.resize(g.rows.size());
+    ++ng;
+  }
+  return ng;
+}
+
+void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
+                  const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
+                  int64_t ldyb, int epi, const float* res, int64_t ldr) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing_) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (ev_pool_.empty()) {
+        SD_CUDA(cudaEventCreate(e));
+      } else {
+        *e = ev_pool_.back();
+        ev_pool_.pop_back();
+      }
+    }
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_, s_sms_);
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    ev_flops_.push_back(2.0 * B * w_->out_dim(which) * w_->in_dim(which));
+  }
+}
+
+void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool reset) {
+  for (size_t i = 0; i < ev_.size(); ++i) {
+    SD_CUDA(cudaEventSynchronize(ev_[i].second));
+    float t = 0;
+    SD_CUDA(cudaEventElapsedTime(&t, ev_[i].first, ev_[i].second));
+    t_ms_ += t;
+    t_flops_ += ev_flops_[i];
+    t_n_ += 1;
+    ev_pool_.push_back(ev_[i].first);
+    ev_pool_.push_back(ev_[i].second);
+  }
+  ev_.clear();
+  ev_flops_.clear();
+  if (ms) *ms = t_ms_;
+  if (flops) *flops = t_flops_;
+  if (launches) *launches = t_n_;
+  if (reset) {
+    t_ms_ = t_flops_ = 0;
+    t_n_ = 0;
+  }
+}
+
+// One decode step over the `ng` groups; embed = features from g.tok (else
+// g.x/g.xb already hold them). Per group and layer: S_pre (finish_block of
+// the previous layer + project_qkv) on the S stream, then the R-Part
+// (append + attend) on the R stream; the S stream of a group waits for its
+// own R-Part only, so group A's attention overlaps group B's GEMMs.
+void Engine::run(int ng, bool embed) {
+  const Spec& s = w_->spec();
+  const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
+  const bool bf = w_->mode() == SD_DENSE_BF16;
+  cudaStream_t rs = pipeline_ ? stream_r_ : stream_;
+  for (int gi = 0; gi < ng; ++gi) {
+    Group& g = groups_[gi];
+    const int n = static_cast<int>(g.rows.size());
+    if (embed) launch_embed(n, D, g.tok, w_->embedding(), g.x, D, bf ? g.xb : nullptr, stream_);
+    gemm(0, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+    if (pipeline_) SD_CUDA(cudaEventRecord(g.ev_s, stream_));
+  }
+  for (int l = 0; l < s.L; ++l) {
+    for (int gi = 0; gi < ng; ++gi) {
+      Group& g = groups_[gi];
+      const int n = static_cast<int>(g.rows.size());
+      if (pipeline_) SD_CUDA(cudaStreamWaitEvent(rs, g.ev_s, 0));
+      for (int i = 0; i < n; ++i) g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], l));
+      kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
+      kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi);
+      if (pipeline_) {
+        SD_CUDA(cudaEventRecord(g.ev_r, rs));
+        SD_CUDA(cudaStreamWaitEvent(stream_, g.ev_r, 0));
+      }
+      // finish_block (dense.cpp:51-70), then the next layer's project_qkv
+      if (bf) launch_to_bf16(n, D, g.o, D, g.ob, D, stream_);
+      gemm(l, 4, n, g.o, D, g.ob, D, g.y, D, bf ? g.yb : nullptr, D, kEpiResidual, g.x, D);
+      gemm(l, 5, n, g.y, D, g.yb, D, bf ? nullptr : g.h, F, bf ? g.hb : nullptr, F, kEpiSilu, nullptr, 0);
+      gemm(l, 6, n, g.h, F, g.hb, F, g.x, D, bf ? g.xb : nullptr, D, kEpiResidual, g.y, D);
+      if (l + 1 < s.L) {
+        gemm(l + 1, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+        if (pipeline_) SD_CUDA(cudaEventRecord(g.ev_s, stream_));
+      }
+    }
+  }
+  for (int gi = 0; gi < ng; ++gi) {  // output_logits + argmax_token (dense.cpp:72-88)
+    Group& g = groups_[gi];
+    const int n = static_cast<int>(g.rows.size());
+    gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+    launch_argmax(n, s.V, g.logits, s.V, g.tok, stream_);
+  }
+}
+
+void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const float* x_host,
+                  int32_t* next_host, float* final_host, float* logits_host) {
+  const Spec& s = w_->spec();
+  if (B == 0) fail(SD_ERR_CONFIG, "project_qkv: empty batch");
+  {
+    std::unordered_set<uint64_t> seen;  // validate_batch (core.cpp:37-54)
+    for (int i = 0; i < B; ++i) {
+      if (!seen.insert(seqs[i]).second) {
+        fail(SD_ERR_CONFIG, "token batch: duplicate sequence id " + std::to_string(seqs[i]));
+      }
+    }
+  }
+  if (tokens_host) {
+    for (int i = 0; i < B; ++i) {
+      if (tokens_host[i] < 0 || tokens_host[i] >= s.V) fail(SD_ERR_CONFIG, "token out of the vocabulary");
+    }
+  }
+  DeviceGuard dg(w_->device());
+  const int ng = split(B, seqs);
+  const bool bf = w_->mode() == SD_DENSE_BF16;
+  std::vector<float> xrows;
+  for (int gi = 0; gi < ng; ++gi) {
+    Group& g = groups_[gi];
+    const int n = static_cast<int>(g.rows.size());
+    if (tokens_host) {
+      g.host_tok.resize(static_cast<size_t>(n));
+      for (int i = 0; i < n; ++i) g.host_tok[static_cast<size_t>(i)] = tokens_host[g.rows[static_cast<size_t>(i)]];
+      SD_CUDA(cudaMemcpyAsync(g.tok, g.host_tok.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, stream_));
+    } else {
+      xrows.resize(static_cast<size_t>(n) * s.D);
+      for (int i = 0; i < n; ++i) {
+        std::memcpy(xrows.data() + static_cast<size_t>(i) * s.D, x_host + static_cast<size_t>(g.rows[static_cast<size_t>(i)]) * s.D,
+                    static_cast<size_t>(s.D) * 4);
+      }
+      SD_CUDA(cudaMemcpyAsync(g.x, xrows.data(), xrows.size() * 4, cudaMemcpyHostToDevice, stream_));
+      SD_CUDA(cudaStreamSynchronize(stream_));  // xrows is reused by the next group
+      if (bf) launch_to_bf16(n, s.D, g.x, s.D, g.xb, s.D, stream_);
+    }
+  }
+  run(ng, tokens_host != nullptr);
+  std::vector<int32_t> nt;
+  std::vector<float> buf;
+  for (int gi = 0; gi < ng; ++gi) {
+    Group& g = groups_[gi];
+    const int n = static_cast<int>(g.rows.size());
+    nt.resize(static_cast<size_t>(n));
+    SD_CUDA(cudaMemcpyAsync(nt.data(), g.tok, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, stream_));
+    SD_CUDA(cudaStreamSynchronize(stream_));
+    for (int i = 0; i < n; ++i) {
+      if (next_host) next_host[g.rows[static_cast<size_t>(i)]] = nt[static_cast<size_t>(i)];
+    }
+    auto scatter = [&](const float* dev, int width, float* dst) {
+      buf.resize(static_cast<size_t>(n) * width);
+      SD_CUDA(cudaMemcpy(buf.data(), dev, buf.size() * 4, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) {
+        std::memcpy(dst + static_cast<size_t>(g.rows[static_cast<size_t>(i)]) * width,
+                    buf.data() + static_cast<size_t>(i) * width, static_cast<size_t>(width) * 4);
+      }
+    };
+    if (final_host) scatter(g.x, s.D, final_host);
+    if (logits_host) scatter(g.logits, s.V, logits_host);
+  }
+}
+
+double Engine::bench(int B, const uint64_t* seqs, const int32_t* tokens_host, int steps,
+                     int32_t* next_host) {
+  DeviceGuard dg(w_->device());
+  const int ng = split(B, seqs);
+  for (int gi = 0; gi < ng; ++gi) {
+    Group& g = groups_[gi];
+    const int n = static_cast<int>(g.rows.size());
+    g.host_tok.resize(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) g.host_tok[static_cast<size_t>(i)] = tokens_host[g.rows[static_cast<size_t>(i)]];
+    SD_CUDA(cudaMemcpyAsync(g.tok, g.host_tok.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, stream_));
+  }
+  cudaEvent_t e0, e1;
+  SD_CUDA(cudaEventCreate(&e0));
+  SD_CUDA(cudaEventCreate(&e1));
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  SD_CUDA(cudaEventRecord(e0, stream_));
+  for (int i = 0; i < steps; ++i) run(ng, true);  // tokens fed back on device
+  SD_CUDA(cudaEventRecord(e1, stream_));
+  SD_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  SD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (next_host) {
+    for (int gi = 0; gi < ng; ++gi) {
+      Group& g = groups_[gi];
+      const int n = static_cast<int>(g.rows.size());
+      SD_CUDA(cudaMemcpy(g.host_tok.data(), g.tok, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) next_host[g.rows[static_cast<size_t>(i)]] = g.host_tok[static_cast<size_t>(i)];
+    }
+  }
+  return ms;
+}
+
+void Engine::retire(int n, const uint64_t* seqs) {
+  for (int i = 0; i < n; ++i) kv_->drop(seqs[i]);
+}
+
+}  // namespace sd

@@ -20,7 +20,9 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <functional>
 #include <mutex>
+#include <unordered_map>
 
 #include "dense_kernels.cuh"
 #include "sd_common.h"
@@ -351,7 +353,43 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows);
+
+// Tensor maps only encode (address, extents, strides, box), so they are
+// cached: the weights' maps never change and the activations' maps repeat
+// every layer and step.
 CUtensorMap make_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows) {
+  struct Key {
+    const void* b;
+    int r, c, k, box;
+    int64_t ld;
+    bool operator==(const Key& o) const {
+      return b == o.b && r == o.r && c == o.c && k == o.k && box == o.box && ld == o.ld;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      size_t h = std::hash<const void*>()(k.b);
+      for (int64_t v : {static_cast<int64_t>(k.r), static_cast<int64_t>(k.c), static_cast<int64_t>(k.k),
+                        static_cast<int64_t>(k.box), k.ld}) {
+        h = h * 1000003u ^ std::hash<int64_t>()(v);
+      }
+      return h;
+    }
+  };
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  static std::mutex mu;
+  const Key key{base, rows, cols, kind, box_rows, ld};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 4096) cache.clear();
+  const CUtensorMap m = encode_map(base, rows, cols, ld, kind, box_rows);
+  cache.emplace(key, m);
+  return m;
+}
+
+CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows) {
   CUtensorMap m;
   const int es = kind == 2 ? 4 : 2;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -408,7 +446,8 @@ void launch(const GemmArgs& g, int cs, cudaStream_t s) {
   p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
             (static_cast<uint32_t>(BM >> 4) << 24);
   const int items = (p.mb / cs) * p.nb;
-  const int max_clusters = num_sms() / cs;
+  const int budget = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
+  const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * cs));
@@ -447,7 +486,8 @@ void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s) {
   static const int force_cs = getenv("SD_GEMM_CS") ? atoi(getenv("SD_GEMM_CS")) : 0;
   static const int force_bn = getenv("SD_GEMM_BN") ? atoi(getenv("SD_GEMM_BN")) : 0;
   const int tiles256 = mb * ((g.N + 255) / 256);
-  int bn = tiles256 * 2 <= num_sms() ? 128 : 256;
+  const int sms = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
+  int bn = tiles256 * 2 <= sms ? 128 : 256;
   int cs = (bn == 256 && mb % 2 == 0) ? 2 : 1;
   if (force_cs > 0 && mb % force_cs == 0) cs = force_cs;
   if (force_bn == 128 || force_bn == 256) bn = force_bn;

@@ -45,8 +45,13 @@ class KvStore {
               const float* k_dev, int64_t k_stride, const float* v_dev, int64_t v_stride,
               cudaStream_t s);
   // KvShard::attend semantics (attention.cpp:204-282).
+  // `slot` selects one of the cached split plans (one per interleaved
+  // mini-batch, so alternating batches do not rebuild each other's plan).
   void attend(int layer, int n, const uint64_t* seqs, const float* q_dev, int64_t q_stride,
-              float* o_dev, int64_t o_stride, cudaStream_t s);
+              float* o_dev, int64_t o_stride, cudaStream_t s, int slot = 0);
+  // SM budget of the attention grid (0 = every SM): the R-Part's share when
+  // it runs beside the S-Part of the other mini-batch
+  void set_grid_limit(int sms) { grid_limit_ = sms; }
   // KvShard::drop_sequence (attention.cpp:284-294)
   void drop(uint64_t seq);
   int64_t export_lane(uint64_t seq, int layer, int which, void* host, size_t host_bytes,
@@ -69,7 +74,16 @@ class KvStore {
   void release_slot(int slot);
   int alloc_group();
   void upload(Blob& b, size_t bytes, cudaStream_t s);
-  void launch_attention_plan(int layer, const float* q, int64_t qs, float* o, int64_t os,
+  struct Plan {
+    std::vector<int32_t> slots, lens;
+    int npieces = 0, grid = 0, ncombine = 0, sms = 0;
+    int64_t positions = 0;
+    Blob blob;
+    size_t off_slot = 0, off_pieces = 0, off_cta = 0, off_comb = 0;
+    DevBuf part_acc, part_ml;
+  };
+  static constexpr int kPlanSlots = 2;
+  void launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o, int64_t os,
                              cudaStream_t s);
 
   Spec spec_;
@@ -97,12 +111,22 @@ class KvStore {
   size_t ring_next_ = 0;
   // cached attention plan (reused while (slots, lengths) repeat, e.g. across
   // the layers of one lockstep decode step)
-  std::vector<int32_t> plan_slots_, plan_lens_;
-  int plan_npieces_ = 0, plan_grid_ = 0, plan_ncombine_ = 0;
-  int64_t plan_positions_ = 0;
-  Blob plan_blob_;
-  size_t off_slot_ = 0, off_pieces_ = 0, off_cta_ = 0, off_comb_ = 0;
-  DevBuf part_acc_, part_ml_;
+  Plan plans_[kPlanSlots];
+  int grid_limit_ = 0;
+  // recent appends (lockstep fast path across the layers of a decode step;
+  // two entries for the two interleaved mini-batches)
+  struct Fast {
+    bool valid = false;
+    int n = 0, layer = -1;
+    uint64_t used = 0;
+    std::vector<uint64_t> seqs;
+    std::vector<uint32_t> pos;
+    std::vector<int32_t> slots;
+    Blob* blob = nullptr;
+  };
+  Fast fast_[2];
+  uint64_t fast_clock_ = 0;
+  const Fast* fast_match(int n, const uint64_t* seqs) const;
 
   // timing
   bool timing_ = false;

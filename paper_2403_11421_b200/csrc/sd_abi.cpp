@@ -499,6 +499,13 @@ int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* laun
 
 int64_t sd_launch_count(void) { return sd::g_launches.load(); }
 
+int sd_engine_pipeline(sd_engine* e, int enable, int r_sms) {
+  return guard([&] {
+    need(e, "engine");
+    e->e->set_pipeline(enable != 0, r_sms);
+  });
+}
+
 int sd_weights_synthetic(const sd_model_spec* spec, int mode, uint64_t seed, int device,
                          sd_weights** out) {
   return guard([&] {

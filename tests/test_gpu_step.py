@@ -72,6 +72,25 @@ def test_stabilized_schedule_with_retirement(sd, oracle):
     assert set(c.values()) == {16}
 
 
+@pytest.mark.parametrize("mode", ["exact", "bf16"])
+def test_two_minibatch_pipeline_matches_oracle(sd, oracle, mode):
+    """The S/R-overlapped two-mini-batch step (seq % 2 groups on two streams,
+    workers.cpp:405-452) computes the same decode as the monolithic oracle."""
+    W, dw, kv, eng = _engine(sd, oracle, (2, 64, 4, 256, 128), mode=mode)
+    eng.pipeline(True, 100)
+    recs, acts, _ = sd.run_generation(eng, 8, 16, 4, 48, seed=0, record_activations=True)
+    orecs, oacts = oracle.run_monolithic(W, 8, 16, 4, 48, seed=0, record=True)
+    assert recs == orecs
+    if mode == "exact":
+        assert np.abs(acts - oacts).max() <= 1e-5
+    with open(os.path.join(GOLDEN, "golden_transcript_2x64_3seq_20.csv")) as f:
+        golden = f.read()
+    W2, dw2, kv2, eng2 = _engine(sd, oracle, (2, 64, 4, 256, 128), mode=mode)
+    eng2.pipeline(True, 64)
+    recs2, _, _ = sd.run_generation(eng2, 3, 20, 20, 20, seed=0)
+    assert sd.transcript_csv(recs2) == golden
+
+
 def test_c1_tiny_config_matches_oracle(sd, oracle):
     """BASELINE config 1: 2 layers, d=256 (hd 128), batch 16, context 128, fp32."""
     W, dw, kv, eng = _engine(sd, oracle, (2, 256, 2, 1024, 256))
