@@ -48,43 +48,85 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock / throttle-reason sampling during the timed region
+    (B200_PROFILING.md clocks line), in-process through NVML on a background
+    thread. SD_BENCH_CLOCKS=smi uses an nvidia-smi subprocess instead;
+    SD_BENCH_CLOCKS=off disables sampling (reported as such)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, dev):
+    def __init__(self, dev, interval=0.25):
+        import threading
+        self.mode = os.environ.get("SD_BENCH_CLOCKS", "nvml")
+        self.samples, self.reasons, self.mx = [], set(), None
+        self._stop = threading.Event()
+        self.t = None
         self.p = None
+        if self.mode == "off":
+            return
+        if self.mode == "smi":
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "250"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self.p = None
+            return
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(dev), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[dev]) if vis else dev
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            self.mode = "unavailable"
+            return
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for n, bit in self.REASONS.items():
+                        if r & bit:
+                            self.reasons.add(n)
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(interval)
+
+        self.t = threading.Thread(target=loop, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if not self.p:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        out, _ = self.p.communicate(timeout=10)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        loaded = [s for s in sm if s > 0.5 * (mx or 1)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        if self.mode == "smi" and self.p:
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in out.strip().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 6:
+                    continue
+                try:
+                    self.samples.append(float(f[0]))
+                    self.mx = float(f[1])
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(n)
+        if self.t:
+            self._stop.set()
+            self.t.join(timeout=5)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "samples": 0,
+                    "reasons": [f"clock sampling {self.mode}"]}
+        loaded = [x for x in self.samples if x > 0.5 * (self.mx or 1)] or self.samples
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.mx, "samples": len(self.samples),
+                "source": self.mode, "reasons": sorted(self.reasons)}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -159,6 +201,9 @@ def run_dist(args, wl, rank, world, dev, dist):
     eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks)
     tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
 
+    # the clock sampler starts before warm-up: nvidia-smi's NVML start-up can
+    # stall the driver for ~100 ms, which must not land in the timed region
+    clk = Clocks(dev)
     eng.bench(seqs, tokens, args.warmup)
     torch.cuda.synchronize(dev)
     kv.timing(True)
@@ -167,7 +212,6 @@ def run_dist(args, wl, rank, world, dev, dist):
     eng.timing_read(reset=True)
     dist.barrier()
     torch.cuda.synchronize(dev)
-    clk = Clocks(dev)
     l0 = sd.launch_count()
     ms = eng.bench(seqs, tokens, args.steps)
     l1 = sd.launch_count()
@@ -256,7 +300,8 @@ def run_ours(args, wl, rank, world, dev, dist):
     kv.prefill_synthetic(seqs, ctx, salt=rank)
     tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
 
-    # warm-up (untimed)
+    # warm-up (untimed); the clock sampler starts first (see run_dist)
+    clk = Clocks(dev)
     _, tok = eng.bench(seqs, tokens, args.warmup)
     torch.cuda.synchronize(dev)
 
@@ -268,7 +313,6 @@ def run_ours(args, wl, rank, world, dev, dist):
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    clk = Clocks(dev)
     l0 = sd.launch_count()
     ms, tok = eng.bench(seqs, tok, args.steps)
     l1 = sd.launch_count()

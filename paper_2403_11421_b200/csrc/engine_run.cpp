@@ -11,6 +11,10 @@
 
 #include "engine.h"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace sd {
 
 Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
@@ -302,12 +306,36 @@ double Engine::bench(int B, const uint64_t* seqs, const int32_t* tokens_host, in
   SD_CUDA(cudaEventCreate(&e0));
   SD_CUDA(cudaEventCreate(&e1));
   SD_CUDA(cudaStreamSynchronize(stream_));
+  // SD_STEP_LOG=1: per-step device times (stderr) for diagnosing host stalls
+  static const bool step_log = getenv("SD_STEP_LOG") != nullptr;
+  std::vector<cudaEvent_t> marks;
+  std::vector<double> host_ms;
   SD_CUDA(cudaEventRecord(e0, stream_));
-  for (int i = 0; i < steps; ++i) run(ng, true);  // tokens fed back on device
+  const auto h0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < steps; ++i) {
+    run(ng, true);  // tokens fed back on device
+    if (step_log) {
+      cudaEvent_t ev;
+      SD_CUDA(cudaEventCreate(&ev));
+      SD_CUDA(cudaEventRecord(ev, stream_));
+      marks.push_back(ev);
+      host_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    }
+  }
   SD_CUDA(cudaEventRecord(e1, stream_));
   SD_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
   SD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  if (step_log) {
+    cudaEvent_t prev = e0;
+    for (size_t i = 0; i < marks.size(); ++i) {
+      float d = 0;
+      SD_CUDA(cudaEventElapsedTime(&d, prev, marks[i]));
+      fprintf(stderr, "[step %zu] device %.2f ms, host enqueue done at %.2f ms\n", i, d, host_ms[i]);
+      prev = marks[i];
+    }
+    for (cudaEvent_t ev : marks) cudaEventDestroy(ev);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (next_host) {

@@ -37,14 +37,6 @@ constexpr int A_STAGE = BM * BK_BYTES;     // 16 KB
 constexpr int kThreads = 192;
 constexpr int EPI_TILE = 32 * 33;          // floats per epilogue warp transpose tile
 
-template <int BN>
-struct Cfg {
-  static constexpr int B_STAGE = BN * BK_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 256 + 4 * EPI_TILE * 4;
-};
-
 struct Params {
   int M, N, K;
   int mb, nb, kb;  // blocks along M, N, K
@@ -58,6 +50,8 @@ struct Params {
   int64_t ldr;
   uint32_t idesc;
   int kind;
+  int bn;    // tile width along N (<= BN; a multiple of 16 in PAIR mode)
+  int diag;  // 1: reuse resident smem after the first ring fill (MMA-rate probe)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -113,6 +107,46 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) forms
+// shared::cluster address of the same variable in CTA `rank`
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// TMA load into this CTA's smem whose completion bytes count on the pair
+// leader's mbarrier (`bar_cluster` from mapa)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_pair(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive on the same-offset mbarrier of both pair CTAs once the issued MMAs complete
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -159,16 +193,50 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
+// Stage geometry. A stage holds ATOMS 128-B swizzle atoms along K per
+// operand (ATOMS x 4 MMAs per barrier handshake: the MMA thread's
+// wait/fence/issue costs ~430 cycles per handshake, more than four 256 x 128
+// MMAs take; tools/mma_rate.cu). PAIR: a CTA pair computes a 256 x bn tile
+// with cta_group::2 MMAs, each CTA staging its own 128 A rows and half of
+// the B tile.
+template <int BN, bool PAIR, int ATOMS>
+struct Cfg {
+  static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA (max)
+  static constexpr int A_ATOM = BM * BK_BYTES;
+  static constexpr int B_ATOM = B_ROWS * BK_BYTES;
+  static constexpr int A_ST = ATOMS * A_ATOM;
+  static constexpr int B_ST = ATOMS * B_ATOM;
+  static constexpr int STAGES = (200 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (200 * 1024 / (A_ST + B_ST));
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr size_t SMEM = 1024 + STAGES * (A_ST + B_ST) + 256 + 4 * EPI_TILE * 4;
+};
+
+template <int KIND, bool PAIR>
+__device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (PAIR) {
+    if (KIND == 2) {
+      mma_tf32_pair(d, a, b, idesc, acc);
+    } else {
+      mma_f16_pair(d, a, b, idesc, acc);
+    }
+  } else if (KIND == 2) {
+    mma_tf32(d, a, b, idesc, acc);
+  } else {
+    mma_f16(d, a, b, idesc, acc);
+  }
+}
+
+template <int BN, bool PAIR, int ATOMS, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
-  using C_ = Cfg<BN>;
+  using C_ = Cfg<BN, PAIR, ATOMS>;
   constexpr int STAGES = C_::STAGES;
+  constexpr int KELEMS = BK_BYTES / (KIND == 2 ? 4 : 2);  // elements per atom row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_STAGE;
-  uint8_t* tail = sB + STAGES * C_::B_STAGE;
+  uint8_t* sB = smem + STAGES * C_::A_ST;
+  uint8_t* tail = sB + STAGES * C_::B_ST;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -178,11 +246,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int cs = p.cs;
+  const int cs = PAIR ? 2 : p.cs;
   const int rank = cs > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const bool leader = rank == 0;
   const uint16_t mask = static_cast<uint16_t>((1u << cs) - 1u);
   const int cluster = blockIdx.x / cs, nclusters = gridDim.x / cs;
-  const int mgroups = p.mb / cs;
+  // PAIR: a cluster item is a 256-row M block (rank r owns rows r*128..);
+  // otherwise cs consecutive 128-row M blocks sharing one B tile (multicast)
+  const int mgroups = PAIR ? (p.mb + 1) / 2 : p.mb / cs;
   const int items = mgroups * p.nb;
 
   if (warp == 0 && lane == 0) {
@@ -190,18 +261,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], cs);  // one release per cluster CTA
+      mbar_init(&empty[s], PAIR ? 1 : cs);  // PAIR: one multicast commit from the leader
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], PAIR ? 8 : 4);  // PAIR: both CTAs' epilogue warps release the leader
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C_::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C_::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(C_::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -209,24 +286,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  auto m_origin = [&](int it) { return ((it % mgroups) * cs + rank) * BM; };
+
   if (warp == 0) {
     // ------------------------------------------------------- TMA producer
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      const int kelems = p.kind == 2 ? 32 : 64;
-      const int slice = BN / cs;
+      const int slice = PAIR ? p.bn / 2 : BN / cs;
+      const uint32_t bytes = static_cast<uint32_t>(ATOMS * (C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
+                             (PAIR ? 2u : 1u);  // PAIR: both CTAs' bytes land on the leader's barrier
+      const uint32_t full0 = PAIR ? mapa(&full[0], 0) : 0;
       for (int it = cluster; it < items; it += nclusters) {
-        const int m0 = ((it % mgroups) * cs + rank) * BM, n0 = (it / mgroups) * BN;
+        const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         for (int kb = 0; kb < p.kb; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);  // every cluster CTA released slot s
-          mbar_expect_tx(&full[s], A_STAGE + C_::B_STAGE);
-          tma_load_2d(sA + s * A_STAGE, &tma_a, &full[s], kb * kelems, m0);
-          if (cs > 1) {
-            tma_load_2d_mc(sB + s * C_::B_STAGE + rank * slice * BK_BYTES, &tma_b, &full[s], kb * kelems,
-                           n0 + rank * slice, mask);
+          mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
+          if (p.diag && (kb >= STAGES || it != cluster)) {
+            if (!PAIR || leader) mbar_arrive(&full[s]);
           } else {
-            tma_load_2d(sB + s * C_::B_STAGE, &tma_b, &full[s], kb * kelems, n0);
+            if (!PAIR || leader) mbar_expect_tx(&full[s], bytes);
+#pragma unroll
+            for (int a = 0; a < ATOMS; ++a) {
+              const int kc = (kb * ATOMS + a) * KELEMS;
+              uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
+              uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
+              if (PAIR) {
+                const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
+                tma_load_2d_pair(dA, &tma_a, fb, kc, m0);
+                tma_load_2d_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
+              } else {
+                tma_load_2d(dA, &tma_a, &full[s], kc, m0);
+                if (cs > 1) {
+                  tma_load_2d_mc(dB + rank * slice * BK_BYTES, &tma_b, &full[s], kc, n0 + rank * slice, mask);
+                } else {
+                  tma_load_2d(dB, &tma_b, &full[s], kc, n0);
+                }
+              }
+            }
           }
           if (++s == STAGES) {
             s = 0;
@@ -234,8 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      // tail: wait until every in-flight slot has been released by all
-      // cluster CTAs, so no remote arrive targets an exited CTA
+      // tail: wait until every in-flight slot has been released, so no
+      // remote arrive targets an exited CTA
       for (int i = 0; i < STAGES; ++i) {
         mbar_wait(&empty[s], ph ^ 1);
         if (++s == STAGES) {
@@ -246,10 +342,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && (!PAIR || leader)) {
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
+      const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
       for (int it = cluster; it < items; it += nclusters, ++local) {
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -259,18 +356,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t da = make_desc(smem_u32(sA + s * A_STAGE));
-          const uint64_t db = make_desc(smem_u32(sB + s * C_::B_STAGE));
+          // descriptor start addresses advance in 16-B units
+          const uint64_t da = da0 + static_cast<uint64_t>(s * (C_::A_ST >> 4));
+          const uint64_t db = db0 + static_cast<uint64_t>(s * (C_::B_ST >> 4));
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 x 32 B along the 128-B swizzle row
-            const uint32_t accum = (kb | k) != 0;
-            if (p.kind == 2) {
-              mma_tf32(dcol, da + 2 * k, db + 2 * k, p.idesc, accum);
-            } else {
-              mma_f16(dcol, da + 2 * k, db + 2 * k, p.idesc, accum);
+          for (int a = 0; a < ATOMS; ++a) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {  // 4 x 32 B along the 128-B swizzle row
+              mma_issue<KIND, PAIR>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k,
+                                    p.idesc, (kb | a | k) != 0);
             }
           }
-          if (cs > 1) {
+          if (PAIR) {
+            tc_commit_pair(&empty[s]);  // release slot s in both CTAs
+          } else if (cs > 1) {
             tc_commit_mc(&empty[s], mask);  // release slot s in every cluster CTA
           } else {
             tc_commit(&empty[s]);
@@ -280,52 +379,66 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph ^= 1;
           }
         }
-        tc_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (PAIR) {
+          tc_commit_pair(&tfull[acc]);  // both CTAs' accumulator halves ready
+        } else {
+          tc_commit(&tfull[acc]);
+        }
       }
     }
   } else {
     // ----------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     float* tile = epi_smem + (warp - 2) * EPI_TILE;
+    const uint32_t tempty_leader0 = PAIR ? mapa(&tempty[0], 0) : 0;
     int local = 0;
     for (int it = cluster; it < items; it += nclusters, ++local) {
       const int acc = local & 1;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int m0 = ((it % mgroups) * cs + rank) * BM, n0 = (it / mgroups) * BN;
+      const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
+      const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
       mbar_wait(&tfull[acc], use & 1);
       __syncwarp();  // lanes leave the try_wait spin independently; .sync.aligned needs convergence
       tc_fence_after();
       const int row0 = m0 + q * 32;
+      const int nrows = p.M - row0 < 32 ? p.M - row0 : 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < (p.bn + 31) / 32; ++c) {
         const int col0 = n0 + c * 32;
-        if (col0 >= p.N) break;  // warp-uniform
+        if (col0 >= nend) break;  // warp-uniform
         float v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+        if (nrows <= 0) continue;  // rows past M (warp-uniform; the load above keeps the warp aligned)
         // lane = row (q*32 + lane) of the tile; transpose through smem
 #pragma unroll
         for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = v[i];
         __syncwarp();
         const int col = col0 + lane;
-        if (col < p.N) {
-          for (int r = 0; r < 32; ++r) {
-            const int row = row0 + r;
-            if (row >= p.M) break;
+        if (col < nend) {
+#pragma unroll 4
+          for (int r = 0; r < nrows; ++r) {
+            const int64_t row = row0 + r;
             float x = tile[r * 33 + lane];
             if (p.epi == kEpiResidual) {
-              x = x + p.res[static_cast<int64_t>(row) * p.ldr + col];
+              x = x + p.res[row * p.ldr + col];
             } else if (p.epi == kEpiSilu) {
               x = x / (1.0f + expf(-x));
             }
-            if (p.C) p.C[static_cast<int64_t>(row) * p.ldc + col] = x;
-            if (p.Cb) p.Cb[static_cast<int64_t>(row) * p.ldcb + col] = __float2bfloat16_rn(x);
+            if (p.C) p.C[row * p.ldc + col] = x;
+            if (p.Cb) p.Cb[row * p.ldcb + col] = __float2bfloat16_rn(x);
           }
         }
         __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) {
+          mbar_arrive_cluster(tempty_leader0 + acc * static_cast<uint32_t>(sizeof(uint64_t)));
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
+      }
     }
   }
 
@@ -334,7 +447,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (cs > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
+    if (PAIR) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
+    }
   }
 }
 
@@ -353,25 +470,25 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows);
+CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows, int swb);
 
 // Tensor maps only encode (address, extents, strides, box), so they are
 // cached: the weights' maps never change and the activations' maps repeat
 // every layer and step.
-CUtensorMap make_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows) {
+CUtensorMap make_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows, int swb = 128) {
   struct Key {
     const void* b;
-    int r, c, k, box;
+    int r, c, k, box, sw;
     int64_t ld;
     bool operator==(const Key& o) const {
-      return b == o.b && r == o.r && c == o.c && k == o.k && box == o.box && ld == o.ld;
+      return b == o.b && r == o.r && c == o.c && k == o.k && box == o.box && sw == o.sw && ld == o.ld;
     }
   };
   struct Hash {
     size_t operator()(const Key& k) const {
       size_t h = std::hash<const void*>()(k.b);
       for (int64_t v : {static_cast<int64_t>(k.r), static_cast<int64_t>(k.c), static_cast<int64_t>(k.k),
-                        static_cast<int64_t>(k.box), k.ld}) {
+                        static_cast<int64_t>(k.box), static_cast<int64_t>(k.sw), k.ld}) {
         h = h * 1000003u ^ std::hash<int64_t>()(v);
       }
       return h;
@@ -379,29 +496,36 @@ CUtensorMap make_map(const void* base, int rows, int cols, int64_t ld, int kind,
   };
   static std::unordered_map<Key, CUtensorMap, Hash> cache;
   static std::mutex mu;
-  const Key key{base, rows, cols, kind, box_rows, ld};
+  const Key key{base, rows, cols, kind, box_rows, swb, ld};
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   if (cache.size() > 4096) cache.clear();
-  const CUtensorMap m = encode_map(base, rows, cols, ld, kind, box_rows);
+  const CUtensorMap m = encode_map(base, rows, cols, ld, kind, box_rows, swb);
   cache.emplace(key, m);
   return m;
 }
 
-CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows) {
+CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kind, int box_rows, int swb) {
   CUtensorMap m;
   const int es = kind == 2 ? 4 : 2;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * es};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK_BYTES / es), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(swb / es), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw =
+      swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (swb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
   const CUresult r = get_encode()(&m, kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fail(SD_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
   return m;
+}
+
+int env_int(const char* name) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : 0;
 }
 
 int num_sms() {
@@ -414,25 +538,53 @@ int num_sms() {
   return n;
 }
 
-template <int BN>
-void launch(const GemmArgs& g, int cs, cudaStream_t s) {
-  using C_ = Cfg<BN>;
+
+// Tile choice (measured at decode batches, tools/tune_gemm.py, tools/gemm_diag.py):
+// the S-Part GEMMs at M = 512 are neither L2- nor HBM-bound (keeping the
+// operands resident in smem changes their time by < 3%); their cost is
+// tensor-pipe time quantized into waves of CTA pairs. So when M spans at
+// least two 128-row blocks, a CTA pair (cta_group::2, 256 x bn tiles) is used
+// with the tile width bn (a multiple of 16, 64..256) that minimizes
+// waves x (bn + fixed per-tile cost); e.g. N = 14336 -> bn 208 (138 tiles on
+// 74 pairs) instead of 256 (112 tiles = 1.5 waves).
+int pick_pair_bn(int mgroups, int N, int pairs) {
+  int best = 256;
+  long best_cost = -1;
+  for (int bn = 256; bn >= 64; bn -= 16) {
+    const long items = static_cast<long>(mgroups) * ((N + bn - 1) / bn);
+    const long waves = (items + pairs - 1) / pairs;
+    const long cost = waves * (bn + 32);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+template <int BN, bool PAIR, int ATOMS, int KIND>
+void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
+  using C_ = Cfg<BN, PAIR, ATOMS>;
+  auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND>;
   static bool attr_set = false;
   if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(C_::SMEM)));
-    SD_CUDA(cudaFuncSetAttribute(gemm_kernel<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr_set = true;
   }
+  if (PAIR) cs = 2;
+  if (!PAIR) bn = BN;
+  if (bn < 16 || bn > BN || (PAIR && bn % 16)) fail(SD_ERR_CONFIG, "gemm: bad tile width");
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, g.kind, BM);
-  const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, g.kind, BN / cs);
+  const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, g.kind, PAIR ? bn / 2 : BN / cs);
   Params p{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
   p.mb = (g.M + BM - 1) / BM;
-  p.nb = (g.N + BN - 1) / BN;
-  p.kb = g.K / (BK_BYTES / (g.kind == 2 ? 4 : 2));
+  p.nb = (g.N + bn - 1) / bn;
+  const int kstage = ATOMS * (BK_BYTES / (KIND == 2 ? 4 : 2));
+  p.kb = (g.K + kstage - 1) / kstage;  // a partial last stage reads zero-filled columns
   p.cs = cs;
   p.C = g.C;
   p.ldc = g.ldc;
@@ -441,11 +593,13 @@ void launch(const GemmArgs& g, int cs, cudaStream_t s) {
   p.epi = g.epi;
   p.res = g.res;
   p.ldr = g.ldr;
-  p.kind = g.kind;
-  const uint32_t fmt = g.kind == 2 ? 2u : 1u;  // TF32 : BF16
-  p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-            (static_cast<uint32_t>(BM >> 4) << 24);
-  const int items = (p.mb / cs) * p.nb;
+  p.kind = KIND;
+  p.bn = bn;
+  p.diag = env_int("SD_GEMM_DIAG");
+  const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16
+  p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
+            (static_cast<uint32_t>((PAIR ? 2 * BM : BM) >> 4) << 24);
+  const int items = (PAIR ? (p.mb + 1) / 2 : p.mb / cs) * p.nb;
   const int budget = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
   const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
@@ -461,8 +615,34 @@ void launch(const GemmArgs& g, int cs, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, gemm_kernel<BN>, ta, tb, p));
+  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   count_launch();
+}
+
+template <int KIND>
+void dispatch(const GemmArgs& g, cudaStream_t s) {
+  const int mb = (g.M + BM - 1) / BM;
+  const int force_cs = env_int("SD_GEMM_CS");
+  const int force_bn = env_int("SD_GEMM_BN");
+  const char* pair_env = getenv("SD_GEMM_PAIR");
+  const int sms = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
+  const bool pair = pair_env ? atoi(pair_env) > 0 : (mb >= 2 && sms >= 2);
+  if (pair) {
+    int bn = pick_pair_bn((mb + 1) / 2, g.N, sms / 2);
+    if (force_bn >= 16 && force_bn <= 256 && force_bn % 16 == 0) bn = force_bn;
+    launch<256, true, 2, KIND>(g, 2, bn, s);
+    return;
+  }
+  const int tiles256 = mb * ((g.N + 255) / 256);
+  int bn = tiles256 * 2 <= sms ? 128 : 256;
+  int cs = (bn == 256 && mb % 2 == 0) ? 2 : 1;
+  if (force_cs > 0 && mb % force_cs == 0) cs = force_cs;
+  if (force_bn == 128 || force_bn == 256) bn = force_bn;
+  if (bn == 128) {
+    launch<128, false, 2, KIND>(g, cs, 128, s);
+  } else {
+    launch<256, false, 1, KIND>(g, cs, 256, s);
+  }
 }
 
 }  // namespace
@@ -473,28 +653,15 @@ bool gemm_sm100_supported(const GemmArgs& g) {
   if (g.M < 1 || g.N < 1 || g.K < 1) return false;
   if ((g.lda * es) % 16 || (g.ldb * es) % 16) return false;
   if (reinterpret_cast<uintptr_t>(g.A) % 16 || reinterpret_cast<uintptr_t>(g.B) % 16) return false;
-  if (g.K % (BK_BYTES / es) != 0) return false;  // whole k-blocks
+  if (g.K % (BK_BYTES / es) != 0) return false;  // whole 128-B atoms
   return true;
 }
 
-// Tile shape and cluster size (measured at decode batches, tools/bench_gemm.py):
-// 256-wide tiles with a 2-CTA cluster sharing each weight tile by multicast;
-// 128-wide tiles without a cluster when 256-wide tiles would leave more than
-// half of the SMs idle (the N = D GEMMs at M = 512).
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s) {
-  const int mb = (g.M + BM - 1) / BM;
-  static const int force_cs = getenv("SD_GEMM_CS") ? atoi(getenv("SD_GEMM_CS")) : 0;
-  static const int force_bn = getenv("SD_GEMM_BN") ? atoi(getenv("SD_GEMM_BN")) : 0;
-  const int tiles256 = mb * ((g.N + 255) / 256);
-  const int sms = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
-  int bn = tiles256 * 2 <= sms ? 128 : 256;
-  int cs = (bn == 256 && mb % 2 == 0) ? 2 : 1;
-  if (force_cs > 0 && mb % force_cs == 0) cs = force_cs;
-  if (force_bn == 128 || force_bn == 256) bn = force_bn;
-  if (bn == 128) {
-    launch<128>(g, cs, s);
+  if (g.kind == 2) {
+    dispatch<2>(g, s);
   } else {
-    launch<256>(g, cs, s);
+    dispatch<1>(g, s);
   }
 }
 

@@ -270,6 +270,7 @@ void KvStore::append(int layer, int n, const uint64_t* seqs, const uint32_t* pos
   }
   const size_t need = static_cast<size_t>(n) * 3 * 4 + static_cast<size_t>(n) * 2 * 4 + 64;
   int32_t* h = static_cast<int32_t*>(b.host.get(need));
+  b.dev.get(need);  // upper bound (nupd <= n): no reallocation when a step opens pages
   int32_t* h_slot = h;
   int32_t* h_pos = h + n;
   int32_t* h_grp = h + 2 * n;
@@ -442,6 +443,18 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
       }
       i = j;
     }
+    // descriptor and partial buffers sized for the worst case of this batch,
+    // so context growth never reallocates them: every item ends one piece and
+    // every CTA boundary adds at most two (the T-aligned cut inside an item
+    // plus the sub-T remainder up to the boundary)
+    const size_t max_pieces = static_cast<size_t>(n) + 2 * static_cast<size_t>(grid) + 1;
+    if (pieces.size() > max_pieces) fail(SD_ERR_INTERNAL, "attend: split plan exceeds its piece bound");
+    const size_t bound = static_cast<size_t>(round_up(static_cast<int64_t>(n) * 4, 16)) +
+                         static_cast<size_t>(round_up(static_cast<int64_t>(max_pieces * sizeof(Piece)), 16)) +
+                         static_cast<size_t>(round_up(static_cast<int64_t>(grid + 2) * 4, 16)) +
+                         static_cast<size_t>(n) * sizeof(int4) + 16;
+    P.blob.host.get(bound);
+    P.blob.dev.get(bound);
     P.off_slot = 0;
     P.off_pieces = round_up(static_cast<int64_t>(n) * 4, 16);
     P.off_cta = P.off_pieces + round_up(static_cast<int64_t>(pieces.size()) * sizeof(Piece), 16);
@@ -461,9 +474,8 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
     P.positions = total;
     P.slots = slots;
     P.lens = lens;
-    const size_t pa = static_cast<size_t>(P.npieces) * q_width() * sizeof(float);
-    const size_t pm = static_cast<size_t>(P.npieces) * spec_.H / spec_.Hkv * head_count_ * 2 *
-                      sizeof(float);
+    const size_t pa = max_pieces * q_width() * sizeof(float);
+    const size_t pm = max_pieces * spec_.H / spec_.Hkv * head_count_ * 2 * sizeof(float);
     if (pa > P.part_acc.bytes || pm > P.part_ml.bytes) {
       SD_CUDA(cudaStreamSynchronize(s));
       P.part_acc.get(pa);

@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -76,16 +77,25 @@ __host__ __device__ inline float synth_value(uint64_t idx) {
 }
 
 // Device scratch buffer that only grows.
+// Growth is geometric: a reallocation's cudaFree synchronizes the device, so
+// a buffer that grows by a few bytes per decode step must not reallocate per
+// step (callers on hot paths also pre-size to their upper bound).
+inline size_t grow_bytes(size_t need, size_t have) {
+  size_t n = have * 2 > need ? have * 2 : need;
+  return (n + 4095) / 4096 * 4096;
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   void* get(size_t need) {
     if (need > bytes) {
+      const size_t n = grow_bytes(need, bytes);
       if (p) cudaFree(p);
       p = nullptr;
       bytes = 0;
-      SD_CUDA(cudaMalloc(&p, need));
-      bytes = need;
+      SD_CUDA(cudaMalloc(&p, n));
+      bytes = n;
     }
     return p;
   }
@@ -99,11 +109,12 @@ struct HostBuf {  // pinned
   size_t bytes = 0;
   void* get(size_t need) {
     if (need > bytes) {
+      const size_t n = grow_bytes(need, bytes);
       if (p) cudaFreeHost(p);
       p = nullptr;
       bytes = 0;
-      SD_CUDA(cudaMallocHost(&p, need));
-      bytes = need;
+      SD_CUDA(cudaMallocHost(&p, n));
+      bytes = n;
     }
     return p;
   }
