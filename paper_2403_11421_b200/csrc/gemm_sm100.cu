@@ -35,7 +35,6 @@ constexpr int BM = 128;
 constexpr int BK_BYTES = 128;              // one 128-B swizzle row per operand row
 constexpr int A_STAGE = BM * BK_BYTES;     // 16 KB
 constexpr int kThreads = 192;
-constexpr int EPI_TILE = 32 * 33;          // floats per epilogue warp transpose tile
 
 struct Params {
   int M, N, K;
@@ -51,6 +50,8 @@ struct Params {
   uint32_t idesc;
   int kind;
   int bn;    // tile width along N (<= BN; a multiple of 16 in PAIR mode)
+  int vec;   // outputs / residual 16-B aligned: vector epilogue
+  int tma_out;  // outputs written by TMA tensor stores
   int diag;  // 1: reuse resident smem after the first ring fill (MMA-rate probe)
 };
 
@@ -177,6 +178,35 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void sts128(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(
@@ -206,9 +236,13 @@ struct Cfg {
   static constexpr int B_ATOM = B_ROWS * BK_BYTES;
   static constexpr int A_ST = ATOMS * A_ATOM;
   static constexpr int B_ST = ATOMS * B_ATOM;
-  static constexpr int STAGES = (200 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (200 * 1024 / (A_ST + B_ST));
+  static constexpr int STAGES = (196 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (196 * 1024 / (A_ST + B_ST));
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-  static constexpr size_t SMEM = 1024 + STAGES * (A_ST + B_ST) + 256 + 4 * EPI_TILE * 4;
+  // epilogue staging for TMA stores: per epilogue warp, two buffers of
+  // 32 rows x 16 columns in fp32 (2 KB, 64-B swizzle) and bf16 (1 KB, 32-B swizzle)
+  static constexpr int OUT_F32 = 32 * 16 * 4, OUT_BF16 = 32 * 16 * 2;
+  static constexpr int OUT_WARP = 2 * (OUT_F32 + OUT_BF16);
+  static constexpr size_t SMEM = 1024 + STAGES * (A_ST + B_ST) + 4 * OUT_WARP + 256;
 };
 
 template <int KIND, bool PAIR>
@@ -228,7 +262,8 @@ __device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, ui
 
 template <int BN, bool PAIR, int ATOMS, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_cb, const Params p) {
   using C_ = Cfg<BN, PAIR, ATOMS>;
   constexpr int STAGES = C_::STAGES;
   constexpr int KELEMS = BK_BYTES / (KIND == 2 ? 4 : 2);  // elements per atom row
@@ -236,13 +271,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * C_::A_ST;
-  uint8_t* tail = sB + STAGES * C_::B_ST;
+  uint8_t* sOut = sB + STAGES * C_::B_ST;  // 1024-aligned: stage sizes are multiples of 1 KB
+  uint8_t* tail = sOut + 4 * C_::OUT_WARP;
   uint64_t* full = reinterpret_cast<uint64_t*>(tail);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* epi_smem = reinterpret_cast<float*>(tail + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -301,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
-          if (p.diag && (kb >= STAGES || it != cluster)) {
+          if ((p.diag & 1) && (kb >= STAGES || it != cluster)) {
             if (!PAIR || leader) mbar_arrive(&full[s]);
           } else {
             if (!PAIR || leader) mbar_expect_tx(&full[s], bytes);
@@ -388,10 +423,101 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ----------------------------------------------------------- epilogue
+    // tcgen05.ld 32x32b gives each lane one row and 32 consecutive columns:
+    // with aligned outputs the lane writes them straight from registers as
+    // 16-B vectors (8 per fp32 chunk, 4 per bf16 chunk), no smem transpose.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    float* tile = epi_smem + (warp - 2) * EPI_TILE;
     const uint32_t tempty_leader0 = PAIR ? mapa(&tempty[0], 0) : 0;
     int local = 0;
+    if (p.tma_out) {
+      // TMA-store epilogue: 16-column chunks staged in swizzled smem (two
+      // buffers per warp) and written by one bulk tensor store per output;
+      // the tensor maps clip rows >= M and columns >= N
+      uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
+      int nchunk = 0;
+      for (int it = cluster; it < items; it += nclusters, ++local) {
+        const int acc = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
+        const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
+        mbar_wait(&tfull[acc], use & 1);
+        __syncwarp();
+        tc_fence_after();
+        const int rowb = m0 + q * 32;
+        const int64_t row = rowb + lane;
+        const bool rin = row < p.M;
+#pragma unroll 1
+        for (int c = 0; c < (p.bn + 15) / 16; ++c) {
+          const int col0 = n0 + c * 16;
+          if (col0 >= nend) break;  // warp-uniform
+          float v[16];
+          tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 16, v);
+          if (p.epi == kEpiResidual) {
+            if (rin && p.vec && col0 + 16 <= p.N) {
+              const float4* r4 = reinterpret_cast<const float4*>(p.res + row * p.ldr + col0);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float4 t = r4[k];
+                v[4 * k] = v[4 * k] + t.x;
+                v[4 * k + 1] = v[4 * k + 1] + t.y;
+                v[4 * k + 2] = v[4 * k + 2] + t.z;
+                v[4 * k + 3] = v[4 * k + 3] + t.w;
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                if (rin && col0 + k < p.N) v[k] = v[k] + p.res[row * p.ldr + col0 + k];
+              }
+            }
+          } else if (p.epi == kEpiSilu) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = v[k] / (1.0f + expf(-v[k]));
+          }
+          uint8_t* bf = myout + (nchunk & 1) * (C_::OUT_F32 + C_::OUT_BF16);
+          uint8_t* bb = bf + C_::OUT_F32;
+          ++nchunk;
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's store (two chunks ago) has read it
+          __syncwarp();
+          if (p.C) {  // row = lane, 64 B = four 16-B chunks, 64-B swizzle
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              sts128(bf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), __float_as_uint(v[4 * j]),
+                     __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            }
+          }
+          if (p.Cb) {  // 32 B = two 16-B chunks, 32-B swizzle
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+              w[e] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              sts128(bb + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                     w[4 * j + 3]);
+            }
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (p.C) tma_store_2d(&tma_c, bf, col0, rowb);
+            if (p.Cb) tma_store_2d(&tma_cb, bb, col0, rowb);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR) {
+            mbar_arrive_cluster(tempty_leader0 + acc * static_cast<uint32_t>(sizeof(uint64_t)));
+          } else {
+            mbar_arrive(&tempty[acc]);
+          }
+        }
+      }
+      if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
+    } else
     for (int it = cluster; it < items; it += nclusters, ++local) {
       const int acc = local & 1;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -400,25 +526,56 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull[acc], use & 1);
       __syncwarp();  // lanes leave the try_wait spin independently; .sync.aligned needs convergence
       tc_fence_after();
-      const int row0 = m0 + q * 32;
-      const int nrows = p.M - row0 < 32 ? p.M - row0 : 32;
+      const int64_t row = m0 + q * 32 + lane;
+      const bool rowok = row < p.M && !(p.diag & 4);
 #pragma unroll 1
       for (int c = 0; c < (p.bn + 31) / 32; ++c) {
         const int col0 = n0 + c * 32;
         if (col0 >= nend) break;  // warp-uniform
         float v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
-        if (nrows <= 0) continue;  // rows past M (warp-uniform; the load above keeps the warp aligned)
-        // lane = row (q*32 + lane) of the tile; transpose through smem
+        if (!rowok) continue;
+        const int ncols = nend - col0 < 32 ? nend - col0 : 32;
+        if (p.vec && ncols == 32) {
+          if (p.epi == kEpiResidual) {
+            const float4* r4 = reinterpret_cast<const float4*>(p.res + row * p.ldr + col0);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) tile[lane * 33 + i] = v[i];
-        __syncwarp();
-        const int col = col0 + lane;
-        if (col < nend) {
-#pragma unroll 4
-          for (int r = 0; r < nrows; ++r) {
-            const int64_t row = row0 + r;
-            float x = tile[r * 33 + lane];
+            for (int k = 0; k < 8; ++k) {
+              const float4 t = r4[k];
+              v[4 * k] = v[4 * k] + t.x;
+              v[4 * k + 1] = v[4 * k + 1] + t.y;
+              v[4 * k + 2] = v[4 * k + 2] + t.z;
+              v[4 * k + 3] = v[4 * k + 3] + t.w;
+            }
+          } else if (p.epi == kEpiSilu) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = v[k] / (1.0f + expf(-v[k]));
+          }
+          if (p.C) {
+            float4* c4 = reinterpret_cast<float4*>(p.C + row * p.ldc + col0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) c4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          }
+          if (p.Cb) {
+            uint4* b4 = reinterpret_cast<uint4*>(p.Cb + row * p.ldcb + col0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * k + 2 * e], v[8 * k + 2 * e + 1]);
+                w[e] = *reinterpret_cast<const uint32_t*>(&h);
+              }
+              b4[k] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int k = 0; k < ncols; ++k) {
+            const int col = col0 + k;
+            float x = v[0];
+#pragma unroll
+            for (int e = 1; e < 32; ++e) x = k == e ? v[e] : x;  // v[k] without local-memory indexing
             if (p.epi == kEpiResidual) {
               x = x + p.res[row * p.ldr + col];
             } else if (p.epi == kEpiSilu) {
@@ -428,7 +585,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (p.Cb) p.Cb[row * p.ldcb + col] = __float2bfloat16_rn(x);
           }
         }
-        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -576,6 +732,12 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   if (!PAIR) bn = BN;
   if (bn < 16 || bn > BN || (PAIR && bn % 16)) fail(SD_ERR_CONFIG, "gemm: bad tile width");
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, g.kind, BM);
+  // output tensor maps (16-column boxes: fp32 rows 64 B, bf16 rows 32 B)
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool tma_out = env_int("SD_GEMM_NO_TMA_OUT") == 0 && (g.C || g.Cb) &&
+                       (!g.C || (al16(g.C) && g.ldc % 4 == 0)) && (!g.Cb || (al16(g.Cb) && g.ldcb % 8 == 0));
+  const CUtensorMap tc = tma_out && g.C ? make_map(g.C, g.M, g.N, g.ldc, 2, 32, 64) : ta;
+  const CUtensorMap tcb = tma_out && g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, 1, 32, 32) : ta;
   const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, g.kind, PAIR ? bn / 2 : BN / cs);
   Params p{};
   p.M = g.M;
@@ -596,6 +758,9 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   p.kind = KIND;
   p.bn = bn;
   p.diag = env_int("SD_GEMM_DIAG");
+  p.tma_out = tma_out ? 1 : 0;
+  p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
+          (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));
   const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16
   p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
             (static_cast<uint32_t>((PAIR ? 2 * BM : BM) >> 4) << 24);
@@ -615,7 +780,7 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tcb, p));
   count_launch();
 }
 
