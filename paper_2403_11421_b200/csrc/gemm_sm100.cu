@@ -108,6 +108,90 @@ __device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
       "h"(mask)
       : "memory");
 }
+// ---- elected forms: the producer and MMA warps run their loops warp-wide
+// (uniform control flow keeps descriptors and coordinates in uniform
+// registers) and let one elected lane issue each instruction
+#define SD_ELECT "elect.sync _|e, 0xffffffff;\n"
+__device__ __forceinline__ void e_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\n" SD_ELECT "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void e_arrive(uint64_t* bar) {
+  asm volatile("{\n.reg .pred e;\n" SD_ELECT "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void e_tma_load(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "{\n.reg .pred e;\n" SD_ELECT
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void e_tma_load_mc(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                              uint16_t mask) {
+  asm volatile(
+      "{\n.reg .pred e;\n" SD_ELECT
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void e_tma_load_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "{\n.reg .pred e;\n" SD_ELECT
+      "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int KIND, bool PAIR>
+__device__ __forceinline__ void e_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (PAIR) {
+    if (KIND == 2) {
+      asm volatile("{\n.reg .pred e, p;\n" SD_ELECT
+                   "setp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                   "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    } else {
+      asm volatile("{\n.reg .pred e, p;\n" SD_ELECT
+                   "setp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                   "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    }
+  } else if (KIND == 2) {
+    asm volatile("{\n.reg .pred e, p;\n" SD_ELECT
+                 "setp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile("{\n.reg .pred e, p;\n" SD_ELECT
+                 "setp.ne.b32 p, %4, 0;\n@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                 "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+}
+// commit: arrive (once) on `bar` in every CTA of `mask` when the issued MMAs complete
+template <bool PAIR>
+__device__ __forceinline__ void e_commit(uint64_t* bar, uint16_t mask) {
+  if (PAIR) {
+    asm volatile("{\n.reg .pred e;\n" SD_ELECT
+                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                 "%1;\n}\n" ::"r"(smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+  } else if (mask != 1) {
+    asm volatile("{\n.reg .pred e;\n" SD_ELECT
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                 "%1;\n}\n" ::"r"(smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+  } else {
+    asm volatile("{\n.reg .pred e;\n" SD_ELECT
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  }
+}
+
 // ---- CTA-pair (cta_group::2) forms
 // shared::cluster address of the same variable in CTA `rank`
 __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
@@ -325,36 +409,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------- TMA producer
-    if (lane == 0) {
+    {
       int s = 0;
       uint32_t ph = 0;
       const int slice = PAIR ? p.bn / 2 : BN / cs;
       const uint32_t bytes = static_cast<uint32_t>(ATOMS * (C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
                              (PAIR ? 2u : 1u);  // PAIR: both CTAs' bytes land on the leader's barrier
-      const uint32_t full0 = PAIR ? mapa(&full[0], 0) : 0;
+      const uint32_t full0 = PAIR ? mapa(&full[0], 0) : smem_u32(&full[0]);
       for (int it = cluster; it < items; it += nclusters) {
         const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
           if ((p.diag & 1) && (kb >= STAGES || it != cluster)) {
-            if (!PAIR || leader) mbar_arrive(&full[s]);
+            if (!PAIR || leader) e_arrive(&full[s]);
           } else {
-            if (!PAIR || leader) mbar_expect_tx(&full[s], bytes);
+            if (!PAIR || leader) e_expect_tx(&full[s], bytes);
+            const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
 #pragma unroll
             for (int a = 0; a < ATOMS; ++a) {
               const int kc = (kb * ATOMS + a) * KELEMS;
               uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
               uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
               if (PAIR) {
-                const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
-                tma_load_2d_pair(dA, &tma_a, fb, kc, m0);
-                tma_load_2d_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
+                e_tma_load_pair(dA, &tma_a, fb, kc, m0);
+                e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
               } else {
-                tma_load_2d(dA, &tma_a, &full[s], kc, m0);
+                e_tma_load(dA, &tma_a, fb, kc, m0);
                 if (cs > 1) {
-                  tma_load_2d_mc(dB + rank * slice * BK_BYTES, &tma_b, &full[s], kc, n0 + rank * slice, mask);
+                  e_tma_load_mc(dB + rank * slice * BK_BYTES, &tma_b, fb, kc, n0 + rank * slice, mask);
                 } else {
-                  tma_load_2d(dB, &tma_b, &full[s], kc, n0);
+                  e_tma_load(dB, &tma_b, fb, kc, n0);
                 }
               }
             }
@@ -377,11 +461,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer
-    if (lane == 0 && (!PAIR || leader)) {
+    if (!PAIR || leader) {
       int s = 0;
       uint32_t ph = 0;
       int local = 0;
       const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
+      const uint16_t cmask = PAIR ? static_cast<uint16_t>(3) : mask;
       for (int it = cluster; it < items; it += nclusters, ++local) {
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -398,27 +483,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < ATOMS; ++a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32 B along the 128-B swizzle row
-              mma_issue<KIND, PAIR>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k,
-                                    p.idesc, (kb | a | k) != 0);
+              e_mma<KIND, PAIR>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k,
+                                p.idesc, (kb | a | k) != 0);
             }
           }
-          if (PAIR) {
-            tc_commit_pair(&empty[s]);  // release slot s in both CTAs
-          } else if (cs > 1) {
-            tc_commit_mc(&empty[s], mask);  // release slot s in every cluster CTA
-          } else {
-            tc_commit(&empty[s]);
-          }
+          e_commit<PAIR>(&empty[s], cmask);  // release slot s (both pair CTAs / every cluster CTA)
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        if (PAIR) {
-          tc_commit_pair(&tfull[acc]);  // both CTAs' accumulator halves ready
-        } else {
-          tc_commit(&tfull[acc]);
-        }
+        e_commit<PAIR>(&tfull[acc], PAIR ? static_cast<uint16_t>(3) : static_cast<uint16_t>(1));
       }
     }
   } else {
