@@ -203,13 +203,13 @@ void Engine::run(int ng, bool embed) {
       if (pipeline_) SD_CUDA(cudaStreamWaitEvent(rs, g.ev_s, 0));
       for (int i = 0; i < n; ++i) g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], l));
       kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
-      kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi);
+      // the attention also writes the bf16 copy of o that W_o consumes
+      kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi, bf ? g.ob : nullptr, D);
       if (pipeline_) {
         SD_CUDA(cudaEventRecord(g.ev_r, rs));
         SD_CUDA(cudaStreamWaitEvent(stream_, g.ev_r, 0));
       }
       // finish_block (dense.cpp:51-70), then the next layer's project_qkv
-      if (bf) launch_to_bf16(n, D, g.o, D, g.ob, D, stream_);
       gemm(l, 4, n, g.o, D, g.ob, D, g.y, D, bf ? g.yb : nullptr, D, kEpiResidual, g.x, D);
       gemm(l, 5, n, g.y, D, g.yb, D, bf ? nullptr : g.h, F, bf ? g.hb : nullptr, F, kEpiSilu, nullptr, 0);
       gemm(l, 6, n, g.h, F, g.hb, F, g.x, D, bf ? g.xb : nullptr, D, kEpiResidual, g.y, D);

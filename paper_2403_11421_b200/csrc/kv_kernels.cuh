@@ -2,6 +2,7 @@
 // split combine (K3). See DESIGN.md "R-Part kernels".
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,7 +47,9 @@ struct AppendArgs {
 
 // One contiguous piece of one item's positions, processed by one CTA.
 struct Piece {
-  int32_t item, p0, p1, flags;  // flags & 1: item has a single piece (write o directly)
+  // flags & 1: the item has a single piece (write o directly); otherwise
+  // flags >> 1 is the item's index in the combine list
+  int32_t item, p0, p1, flags;
 };
 
 struct AttnArgs {
@@ -66,6 +69,13 @@ struct AttnArgs {
   int32_t nstages;
   int32_t stage_region;       // bytes of one K (or V) stage region (128-B aligned)
   int32_t sc_region;          // bytes of one int8 scale region per stage (0: scales read from L2)
+  // fused combine (kv_mma.cu): the last piece of a split item to finish, per
+  // kv head, merges the item's partials in piece order (the combine_kernel
+  // arithmetic) and resets its counter
+  const int4* comb;           // [ncombine] (item, first piece, piece count, -)
+  int32_t* comb_cnt;          // [ncombine][hc] arrival counters, zero between launches
+  __nv_bfloat16* ob;          // optional bf16 copy of o (the W_o GEMM operand)
+  int64_t ob_stride;
 };
 
 // Static shape of the fast attention kernel for a geometry (kv_kernels.cu).

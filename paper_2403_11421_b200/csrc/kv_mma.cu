@@ -17,6 +17,7 @@
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
 // positions and each position row is copied to a 16-B padded pitch so the
 // eight ldmatrix row addresses of a warp fall in distinct bank groups.
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include "kv_kernels.cuh"
@@ -278,11 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const int qh = hk * G + hq;
       if (direct) {
         float* orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * kHD;
+        __nv_bfloat16* brow = a.ob ? a.ob + static_cast<int64_t>(pc.item) * a.ob_stride + qh * kHD : nullptr;
         const float inv = 1.0f / l[j];
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
-          orow[16 * mt + gq] = o[mt][j] * inv;
-          orow[16 * mt + gq + 8] = o[mt][2 + j] * inv;
+          const float x0 = o[mt][j] * inv, x1 = o[mt][2 + j] * inv;
+          orow[16 * mt + gq] = x0;
+          orow[16 * mt + gq + 8] = x1;
+          if (brow) {
+            brow[16 * mt + gq] = __float2bfloat16_rn(x0);
+            brow[16 * mt + gq + 8] = __float2bfloat16_rn(x1);
+          }
         }
       } else {
         float* pa = a.part_acc + (static_cast<int64_t>(w) * Hq + qh) * kHD;
@@ -296,6 +303,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           pm[0] = m[j];
           pm[1] = l[j];
         }
+      }
+    }
+    if (!direct && a.comb_cnt) {
+      // last arriver of this (item, kv head) merges the item's partials
+      const int ci = pc.flags >> 1;
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      const int4 it = a.comb[ci];
+      if (lane == 0) last = atomicAdd(&a.comb_cnt[ci * g.hc + hk], 1) == it.z - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        // lane -> (head hq, DPL contiguous head dims); independent 16-B loads
+        // per piece, same operation order as combine_kernel
+        constexpr int LPH = 32 / G, DPL = kHD / LPH;
+        const int hq = lane / LPH, d0 = (lane % LPH) * DPL;
+        const int qh = hk * G + hq;
+        const float* mlb = a.part_ml + static_cast<int64_t>(it.y) * Hq * 2 + qh * 2;
+        const float* accb = a.part_acc + static_cast<int64_t>(it.y) * Hq * kHD + qh * kHD + d0;
+        float M = -INFINITY;
+        for (int p = 0; p < it.z; ++p) M = fmaxf(M, __ldcg(mlb + static_cast<int64_t>(p) * Hq * 2));
+        float L = 0.0f, acc[DPL];
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) acc[e] = 0.0f;
+#pragma unroll 2
+        for (int p = 0; p < it.z; ++p) {
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(mlb + static_cast<int64_t>(p) * Hq * 2));
+          const float4* src = reinterpret_cast<const float4*>(accb + static_cast<int64_t>(p) * Hq * kHD);
+          float4 t[DPL / 4];
+#pragma unroll
+          for (int k = 0; k < DPL / 4; ++k) t[k] = __ldcg(src + k);
+          const float wgt = fast_exp2(ml.x - M);
+          L = fmaf(wgt, ml.y, L);
+#pragma unroll
+          for (int k = 0; k < DPL / 4; ++k) {
+            acc[4 * k] = fmaf(wgt, t[k].x, acc[4 * k]);
+            acc[4 * k + 1] = fmaf(wgt, t[k].y, acc[4 * k + 1]);
+            acc[4 * k + 2] = fmaf(wgt, t[k].z, acc[4 * k + 2]);
+            acc[4 * k + 3] = fmaf(wgt, t[k].w, acc[4 * k + 3]);
+          }
+        }
+        float* orow = a.o + static_cast<int64_t>(it.x) * a.o_stride + qh * kHD + d0;
+#pragma unroll
+        for (int k = 0; k < DPL / 4; ++k) {
+          const float4 x = make_float4(acc[4 * k] / L, acc[4 * k + 1] / L, acc[4 * k + 2] / L, acc[4 * k + 3] / L);
+          *reinterpret_cast<float4*>(orow + 4 * k) = x;
+          if (a.ob) {
+            __nv_bfloat16* brow = a.ob + static_cast<int64_t>(it.x) * a.ob_stride + qh * kHD + d0 + 4 * k;
+            *reinterpret_cast<__nv_bfloat162*>(brow) = __floats2bfloat162_rn(x.x, x.y);
+            *reinterpret_cast<__nv_bfloat162*>(brow + 2) = __floats2bfloat162_rn(x.z, x.w);
+          }
+        }
+        if (lane == 0) a.comb_cnt[ci * g.hc + hk] = 0;  // ready for the next launch
       }
     }
   }

@@ -2,6 +2,8 @@
 // slot / page-group allocation, balanced split planning and kernel launch.
 #include "kv_store.h"
 
+#include "dense_kernels.cuh"
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -371,7 +373,8 @@ const KvStore::Fast* KvStore::fast_match(int n, const uint64_t* seqs) const {
 
 // --------------------------------------------------------------- attend ---
 void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
-                     int64_t q_stride, float* o_dev, int64_t o_stride, cudaStream_t s, int slot) {
+                     int64_t q_stride, float* o_dev, int64_t o_stride, cudaStream_t s, int slot,
+                     __nv_bfloat16* ob, int64_t ob_stride) {
   DeviceGuard dg(device_);
   const int L = spec_.L;
   if (layer < 0 || layer >= L) fail(SD_ERR_PROTOCOL, "attend: layer index out of range");
@@ -439,6 +442,7 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
       if (j - i == 1) {
         pieces[i].flags = 1;
       } else {
+        for (size_t k = i; k < j; ++k) pieces[k].flags = static_cast<int32_t>(comb.size()) << 1;
         comb.push_back(make_int4(pieces[i].item, static_cast<int>(i), static_cast<int>(j - i), 0));
       }
       i = j;
@@ -476,17 +480,21 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
     P.lens = lens;
     const size_t pa = max_pieces * q_width() * sizeof(float);
     const size_t pm = max_pieces * spec_.H / spec_.Hkv * head_count_ * 2 * sizeof(float);
-    if (pa > P.part_acc.bytes || pm > P.part_ml.bytes) {
+    const size_t pc = static_cast<size_t>(n) * static_cast<size_t>(geom_.hc) * sizeof(int32_t);
+    if (pa > P.part_acc.bytes || pm > P.part_ml.bytes || pc > P.comb_cnt.bytes) {
       SD_CUDA(cudaStreamSynchronize(s));
       P.part_acc.get(pa);
       P.part_ml.get(pm);
+      P.comb_cnt.get(pc);
+      // arrival counters start at zero; the fused combine leaves them zero
+      SD_CUDA(cudaMemsetAsync(P.comb_cnt.p, 0, P.comb_cnt.bytes, s));
     }
   }
-  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, s);
+  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, ob, ob_stride, s);
 }
 
 void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o,
-                                    int64_t os, cudaStream_t s) {
+                                    int64_t os, __nv_bfloat16* ob, int64_t obs, cudaStream_t s) {
   const uint8_t* base = static_cast<const uint8_t*>(P.blob.dev.p);
   AttnArgs a{};
   a.g = geom_;
@@ -506,6 +514,14 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   a.nstages = nstages_;
   a.stage_region = stage_region_;
   a.sc_region = sc_region_;
+  // the tensor-core kernel fuses the combine and the bf16 copy
+  // (SD_ATTN_SEPARATE_COMBINE=1 keeps the separate combine kernel)
+  static const bool separate = std::getenv("SD_ATTN_SEPARATE_COMBINE") != nullptr;
+  const bool fused = use_mma_ && !separate;
+  a.comb = reinterpret_cast<const int4*>(base + P.off_comb);
+  a.comb_cnt = fused ? static_cast<int32_t*>(P.comb_cnt.p) : nullptr;
+  a.ob = fused ? ob : nullptr;
+  a.ob_stride = obs;
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timing_) {
@@ -537,6 +553,10 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
     bytes += static_cast<double>(P.slots.size()) * q_width() * 4 * 2;  // q in, o out
     ev_bytes_.push_back(bytes);
   }
+  if (fused) {
+    SD_CUDA(cudaEventRecord(P.blob.done, s));
+    return;
+  }
   CombineArgs c{};
   c.items = reinterpret_cast<const int4*>(base + P.off_comb);
   c.m = P.ncombine;
@@ -547,6 +567,7 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   c.Hq = head_count_ * G_;
   c.hd = spec_.hd;
   launch_combine(c, s);
+  if (ob) launch_to_bf16(static_cast<int>(P.slots.size()), q_width(), o, os, ob, obs, s);
   SD_CUDA(cudaEventRecord(P.blob.done, s));
 }
 

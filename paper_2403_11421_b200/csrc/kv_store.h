@@ -47,8 +47,10 @@ class KvStore {
   // KvShard::attend semantics (attention.cpp:204-282).
   // `slot` selects one of the cached split plans (one per interleaved
   // mini-batch, so alternating batches do not rebuild each other's plan).
+  // `ob` (optional): also write o in bf16 (the W_o GEMM operand).
   void attend(int layer, int n, const uint64_t* seqs, const float* q_dev, int64_t q_stride,
-              float* o_dev, int64_t o_stride, cudaStream_t s, int slot = 0);
+              float* o_dev, int64_t o_stride, cudaStream_t s, int slot = 0,
+              __nv_bfloat16* ob = nullptr, int64_t ob_stride = 0);
   // SM budget of the attention grid (0 = every SM): the R-Part's share when
   // it runs beside the S-Part of the other mini-batch
   void set_grid_limit(int sms) { grid_limit_ = sms; }
@@ -80,11 +82,11 @@ class KvStore {
     int64_t positions = 0;
     Blob blob;
     size_t off_slot = 0, off_pieces = 0, off_cta = 0, off_comb = 0;
-    DevBuf part_acc, part_ml;
+    DevBuf part_acc, part_ml, comb_cnt;
   };
   static constexpr int kPlanSlots = 2;
   void launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o, int64_t os,
-                             cudaStream_t s);
+                             __nv_bfloat16* ob, int64_t obs, cudaStream_t s);
 
   Spec spec_;
   int head_start_, head_count_, G_;
