@@ -199,6 +199,8 @@ def run_dist(args, wl, rank, world, dev, dist):
     obj = [sd.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks)
+    if args.exchange == "p2p":  # direct NVLink stores into the peers' receive buffers
+        eng.enable_p2p(len(seqs))
     tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
 
     # the clock sampler starts before warm-up: nvidia-smi's NVML start-up can
@@ -254,7 +256,8 @@ def run_dist(args, wl, rank, world, dev, dist):
                    "batch_per_gpu": B, "global_batch": B * world, "context": ctx, "kv_format": fmt,
                    "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
                    "parallelism": f"kv sharded by mix64(seq)%{world} (ShardMap by-sequence); "
-                                  f"{s_ranks} S-rank(s); per-layer NCCL Q/K/V->shard, O->S",
+                                  f"{s_ranks} S-rank(s); per-layer Q/K/V->shard, O->S over "
+                                  + ("NVLink peer stores (CUDA IPC)" if args.exchange == "p2p" else "NCCL send/recv"),
                    "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": "attention (rank 0)", "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
@@ -434,6 +437,8 @@ def main():
                     help="two-mini-batch S/R pipeline: SMs for the R-Part (0 = off)")
     ap.add_argument("--s-ranks", type=int, default=0,
                     help="N>1: S-workers (1 = the paper's single S-rank; 0 = every rank)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: per-layer activation exchange transport")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -263,6 +263,15 @@ int sd_dist_bench(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* to
 int sd_dist_drive(sd_dist* d, const sd_drive_config* cfg, sd_drive_result** out);
 int sd_dist_timing(sd_dist* d, int enable);
 int sd_dist_timing_read(sd_dist* d, double* exchange_ms, double* exchange_bytes, int reset);
+/* Peer-memory exchange over NVLink in place of NCCL send/recv (same rows,
+ * same order): each rank allocates receive buffers for up to `max_rows`
+ * rows and writes SD_DIST_IPC_BYTES of CUDA IPC handles; after every rank's
+ * handles are gathered (rank order, world * SD_DIST_IPC_BYTES), connect maps
+ * the peers' buffers. Every later step scatters rows with direct NVLink
+ * stores and an epoch flag per (exchange, source). */
+#define SD_DIST_IPC_BYTES 192
+int sd_dist_p2p_setup(sd_dist* d, int32_t max_rows, void* handles_out);
+int sd_dist_p2p_connect(sd_dist* d, const void* all_handles);
 /* Host-only row plan of a step (CPU-testable): home rows grouped by shard,
  * shard rows grouped by source, per-peer counts. Arrays sized B / world. */
 int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs,

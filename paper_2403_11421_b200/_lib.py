@@ -117,6 +117,8 @@ SIGNATURES = {
     "sd_dist_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_dist_timing": (C.c_int, [P, C.c_int]),
     "sd_dist_timing_read": (C.c_int, [P, DP, DP, C.c_int]),
+    "sd_dist_p2p_setup": (C.c_int, [P, C.c_int32, P]),
+    "sd_dist_p2p_connect": (C.c_int, [P, P]),
     "sd_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int32, U64P, I32P, I32P, I32P, I32P,
                                I32P, I32P]),
     "sd_shardmap_worker_for": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, I32P]),

@@ -495,6 +495,32 @@ class DistEngine:
         _check(lib.sd_dist_timing_read(self.h, C.byref(ms), C.byref(b), int(reset)))
         return ms.value, b.value
 
+    IPC_BYTES = 192
+
+    def p2p_handles(self, max_rows: int) -> bytes:
+        """Allocate this rank's peer-exchange receive buffers (up to `max_rows`
+        rows) and return their CUDA IPC handles."""
+        buf = (C.c_uint8 * self.IPC_BYTES)()
+        _check(lib.sd_dist_p2p_setup(self.h, int(max_rows), buf))
+        return bytes(buf)
+
+    def p2p_connect(self, all_handles):
+        """Map every rank's buffers (handles in rank order) and switch the
+        per-layer exchange from NCCL send/recv to direct NVLink stores."""
+        blob = b"".join(all_handles)
+        if len(blob) != self.IPC_BYTES * self.world:
+            raise ConfigError("p2p_connect: need one handle block per rank")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        _check(lib.sd_dist_p2p_connect(self.h, buf))
+
+    def enable_p2p(self, max_rows: int, group=None):
+        """Collective over torch.distributed: exchange handles and connect."""
+        import torch.distributed as dist
+        mine = self.p2p_handles(max_rows)
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self.p2p_connect(allh)
+
 
 def run_generation(engine, batch: int, target_len: int, interval: int, steps: int,
                    seed: int = 0, cold_start: str = "fixed-interval", load_limit: int = 0,

@@ -112,6 +112,11 @@ DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void*
 DistEngine::~DistEngine() {
   DeviceGuard dg(device_);
   cudaStreamSynchronize(stream_);
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
+  for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
+                  static_cast<void*>(done_)}) {
+    if (p) cudaFree(p);
+  }
   if (comm_) Nccl::get().CommDestroy(comm_);
   for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_h_), static_cast<void*>(qkv_s_),
                   static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
@@ -165,6 +170,120 @@ void DistEngine::plan_for(int B, const uint64_t* seqs) {
   if (plan_key_.size() == static_cast<size_t>(B) && std::equal(plan_key_.begin(), plan_key_.end(), seqs)) return;
   make_plan(world_, rank_, s_ranks_, B, seqs, plan_);
   plan_key_.assign(seqs, seqs + B);
+  if (p2p_) {
+    // where this rank's rows land in each peer's receive buffers (every rank
+    // derives every plan from the same batch)
+    peer_qkv_off_.assign(static_cast<size_t>(world_), 0);
+    peer_o_off_.assign(static_cast<size_t>(world_), 0);
+    DistPlan q;
+    for (int d = 0; d < world_; ++d) {
+      make_plan(world_, d, s_ranks_, B, seqs, q);
+      peer_qkv_off_[static_cast<size_t>(d)] = q.recv_off[static_cast<size_t>(rank_)];
+      peer_o_off_[static_cast<size_t>(d)] = q.send_off[static_cast<size_t>(rank_)];
+      if (static_cast<int>(q.home_rows.size()) > p2p_cap_ || static_cast<int>(q.shard_rows.size()) > p2p_cap_) {
+        fail(SD_ERR_CAPACITY, "peer exchange: batch exceeds the p2p_setup row capacity");
+      }
+    }
+  }
+}
+
+void DistEngine::p2p_setup(int max_rows, void* handles_out) {
+  if (world_ > kMaxWorld) fail(SD_ERR_CONFIG, "peer exchange supports at most 8 ranks");
+  if (max_rows < 1) fail(SD_ERR_CONFIG, "p2p_setup: max_rows must be positive");
+  DeviceGuard dg(device_);
+  SD_CUDA(cudaStreamSynchronize(stream_));
+  for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
+                  static_cast<void*>(done_)}) {
+    if (p) cudaFree(p);
+  }
+  const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_qkv_), rows * spec_.qkv_width() * 4));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), rows * spec_.D * 4));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), 2 * kMaxWorld * sizeof(int64_t)));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&done_), sizeof(int32_t)));
+  SD_CUDA(cudaMemset(rx_qkv_, 0, rows * spec_.qkv_width() * 4));
+  SD_CUDA(cudaMemset(rx_o_, 0, rows * spec_.D * 4));
+  SD_CUDA(cudaMemset(flags_, 0, 2 * kMaxWorld * sizeof(int64_t)));
+  SD_CUDA(cudaMemset(done_, 0, sizeof(int32_t)));
+  SD_CUDA(cudaDeviceSynchronize());
+  cudaIpcMemHandle_t h[3];
+  SD_CUDA(cudaIpcGetMemHandle(&h[0], rx_qkv_));
+  SD_CUDA(cudaIpcGetMemHandle(&h[1], rx_o_));
+  SD_CUDA(cudaIpcGetMemHandle(&h[2], flags_));
+  std::memcpy(handles_out, h, sizeof(h));
+  p2p_cap_ = max_rows;
+  epoch_ = 0;
+}
+
+void DistEngine::p2p_connect(const void* all_handles) {
+  if (!rx_qkv_) fail(SD_ERR_CONFIG, "p2p_connect before p2p_setup");
+  DeviceGuard dg(device_);
+  const auto* hb = static_cast<const uint8_t*>(all_handles);
+  for (int p = 0; p < world_; ++p) {
+    if (p == rank_) {
+      peer_qkv_[p] = rx_qkv_;
+      peer_o_[p] = rx_o_;
+      peer_flags_[p] = flags_;
+      continue;
+    }
+    cudaIpcMemHandle_t h[3];
+    std::memcpy(h, hb + static_cast<size_t>(p) * kIpcBytes, sizeof(h));
+    void* ptr[3];
+    for (int i = 0; i < 3; ++i) {
+      SD_CUDA(cudaIpcOpenMemHandle(&ptr[i], h[i], cudaIpcMemLazyEnablePeerAccess));
+      opened_.push_back(ptr[i]);
+    }
+    peer_qkv_[p] = static_cast<float*>(ptr[0]);
+    peer_o_[p] = static_cast<float*>(ptr[1]);
+    peer_flags_[p] = static_cast<int64_t*>(ptr[2]);
+  }
+  p2p_ = true;
+  plan_key_.clear();  // recompute the peer offsets
+}
+
+void DistEngine::exchange_p2p(int kind) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing_) {
+    SD_CUDA(cudaEventCreate(&e0));
+    SD_CUDA(cudaEventCreate(&e1));
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  const int width = kind == 0 ? spec_.qkv_width() : spec_.D;
+  P2PScatter a{};
+  a.src = kind == 0 ? qkv_h_ : o_s_;
+  a.src_stride = width;
+  a.dst_stride = width;
+  a.width = width;
+  a.world = world_;
+  a.self = rank_;
+  a.slot = kind;
+  a.epoch = ++epoch_;
+  a.done = done_;
+  const std::vector<int32_t>& sc = kind == 0 ? plan_.send_cnt : plan_.recv_cnt;
+  const std::vector<int32_t>& so = kind == 0 ? plan_.send_off : plan_.recv_off;
+  const std::vector<int32_t>& rc = kind == 0 ? plan_.recv_cnt : plan_.send_cnt;
+  double bytes = 0;
+  uint32_t expect = 0;
+  for (int d = 0; d < world_; ++d) {
+    const size_t u = static_cast<size_t>(d);
+    a.cnt[d] = sc[u];
+    a.src_off[d] = so[u];
+    a.dst_off[d] = kind == 0 ? peer_qkv_off_[u] : peer_o_off_[u];
+    a.dst[d] = kind == 0 ? peer_qkv_[d] : peer_o_[d];
+    a.flag[d] = peer_flags_[d];
+    if (d != rank_ && sc[u] > 0) {
+      a.notify |= 1u << d;
+      bytes += static_cast<double>(sc[u]) * width * 4;
+    }
+    if (d != rank_ && rc[u] > 0) expect |= 1u << d;
+  }
+  launch_p2p_scatter(a, stream_);
+  launch_p2p_wait(flags_, kind, expect, world_, a.epoch, stream_);
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    ev_bytes_.push_back(bytes);
+  }
 }
 
 // per-destination grouped send/recv (the scatter of send_layer and the
@@ -237,18 +356,28 @@ void DistEngine::run_step() {
   if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, stream_);
   for (int l = 0; l < s.L; ++l) {
     if (nh) w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
-    exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s_, plan_.recv_cnt, plan_.recv_off, qkvw);
+    float* qkv_s = p2p_ ? rx_qkv_ : qkv_s_;
+    float* o_h = p2p_ ? rx_o_ : o_h_;
+    if (p2p_) {
+      exchange_p2p(0);
+    } else {
+      exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s, plan_.recv_cnt, plan_.recv_off, qkvw);
+    }
     if (ns) {
       for (int i = 0; i < ns; ++i) {
         pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
       }
-      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s_ + D, qkvw, qkv_s_ + D + kvw, qkvw, stream_);
-      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s_, qkvw, o_s_, D, stream_);
+      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + D, qkvw, qkv_s + D + kvw, qkvw, stream_);
+      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, qkvw, o_s_, D, stream_);
     }
-    exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h_, plan_.send_cnt, plan_.send_off, D);
+    if (p2p_) {
+      exchange_p2p(1);
+    } else {
+      exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h, plan_.send_cnt, plan_.send_off, D);
+    }
     if (nh) {
-      if (bf) launch_to_bf16(nh, D, o_h_, D, ob_, D, stream_);
-      w_->linear(l, 4, nh, o_h_, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
+      if (bf) launch_to_bf16(nh, D, o_h, D, ob_, D, stream_);
+      w_->linear(l, 4, nh, o_h, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
       w_->linear(l, 5, nh, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0, stream_);
       w_->linear(l, 6, nh, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D, stream_);
     }

@@ -11,6 +11,7 @@
 
 #include <vector>
 
+#include "dist_p2p.cuh"
 #include "engine.h"
 
 namespace sd {
@@ -49,6 +50,13 @@ class DistEngine : public StepComputation {
   double bench(int B, const uint64_t* seqs, const int32_t* tokens, int steps);
   void set_timing(bool on) { timing_ = on; }
   void read_timing(double* exch_ms, double* exch_bytes, bool reset);
+  // Peer-memory exchange (dist_p2p.cu): allocate fixed receive buffers for
+  // up to `max_rows` rows and export their CUDA IPC handles (kIpcBytes);
+  // connect() maps every rank's buffers (world x kIpcBytes, rank order).
+  static constexpr size_t kIpcBytes = 3 * sizeof(cudaIpcMemHandle_t);
+  void p2p_setup(int max_rows, void* handles_out);
+  void p2p_connect(const void* all_handles);
+  bool p2p() const { return p2p_; }
 
  private:
   void ensure(int B);
@@ -56,6 +64,8 @@ class DistEngine : public StepComputation {
   void run_step();
   void exchange(const float* send, const std::vector<int32_t>& sc, const std::vector<int32_t>& so,
                 float* recv, const std::vector<int32_t>& rc, const std::vector<int32_t>& ro, int width);
+  // kind 0: Q/K/V rows home -> shard; kind 1: attention rows shard -> home
+  void exchange_p2p(int kind);
 
   Spec spec_;
   Weights* w_;
@@ -76,6 +86,18 @@ class DistEngine : public StepComputation {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
   std::vector<double> ev_bytes_;
   double x_ms_ = 0, x_bytes_ = 0;
+  // peer-memory exchange state
+  bool p2p_ = false;
+  int p2p_cap_ = 0;
+  float *rx_qkv_ = nullptr, *rx_o_ = nullptr;  // receive buffers (shard rows / home rows)
+  int64_t* flags_ = nullptr;                   // [2][kMaxWorld] epochs published by sources
+  int32_t* done_ = nullptr;
+  float* peer_qkv_[kMaxWorld] = {};
+  float* peer_o_[kMaxWorld] = {};
+  int64_t* peer_flags_[kMaxWorld] = {};
+  std::vector<void*> opened_;
+  int64_t epoch_ = 0;
+  std::vector<int32_t> peer_qkv_off_, peer_o_off_;  // row offset of this rank's rows in each peer's buffer
 };
 
 }  // namespace sd

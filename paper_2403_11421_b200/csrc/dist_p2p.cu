@@ -1,0 +1,90 @@
+// Peer-memory exchange for DistEngine (dist.h): the per-layer scatter of
+// Q/K/V rows to their R-shards and the gather of attention outputs back
+// (send_layer / receive_layer, workers.cpp:324-391) as direct NVLink stores
+// into the destination rank's receive buffer (CUDA IPC mapping), signalled
+// by a per-(exchange, source) epoch flag in the destination's memory.
+#include <cstdint>
+
+#include "dist_p2p.cuh"
+#include "sd_common.h"
+
+namespace sd {
+
+namespace {
+
+__device__ __forceinline__ void st_release_sys(int64_t* p, int64_t v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// grid-stride over (row, 16-B chunk) of every destination's row range
+__global__ void p2p_scatter_kernel(const P2PScatter a) {
+  const int vec = a.width / 4;  // float4 per row
+  int64_t total = 0;
+  for (int d = 0; d < a.world; ++d) total += static_cast<int64_t>(a.cnt[d]) * vec;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int64_t r = i / vec;
+    const int c = static_cast<int>(i - r * vec);
+    int d = 0;
+    while (r >= a.cnt[d]) {
+      r -= a.cnt[d];
+      ++d;
+    }
+    const float4 v = reinterpret_cast<const float4*>(a.src + (a.src_off[d] + r) * a.src_stride)[c];
+    reinterpret_cast<float4*>(a.dst[d] + (a.dst_off[d] + r) * a.dst_stride)[c] = v;
+  }
+  // last block publishes: all of this rank's stores to every peer are
+  // visible system-wide before the epoch flag
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int last;
+  if (threadIdx.x == 0) last = atomicAdd(a.done, 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (last) {
+    __threadfence_system();
+    if (threadIdx.x < a.world && (a.notify >> threadIdx.x & 1)) {
+      st_release_sys(a.flag[threadIdx.x] + a.slot * kMaxWorld + a.self, a.epoch);
+    }
+    if (threadIdx.x == 0) *a.done = 0;
+  }
+}
+
+// spin until every expected source has published this epoch; bounded so a
+// lost peer traps instead of hanging the GPU
+__global__ void p2p_wait_kernel(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch) {
+  const int t = threadIdx.x;
+  if (t >= world || !(expect >> t & 1)) return;
+  const int64_t* f = flags + slot * kMaxWorld + t;
+  const long long t0 = clock64();
+  while (ld_acquire_sys(f) < epoch) {
+    if (clock64() - t0 > 40'000'000'000LL) __trap();  // ~20 s
+    __nanosleep(64);
+  }
+}
+
+}  // namespace
+
+void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s) {
+  int64_t rows = 0;
+  for (int d = 0; d < a.world; ++d) rows += a.cnt[d];
+  const int64_t work = rows * (a.width / 4);
+  int grid = static_cast<int>(std::min<int64_t>(264, (work + 255) / 256));
+  if (grid < 1) grid = 1;
+  p2p_scatter_kernel<<<grid, 256, 0, s>>>(a);
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s) {
+  if (!expect) return;
+  p2p_wait_kernel<<<1, 32, 0, s>>>(flags, slot, expect, world, epoch);
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace sd

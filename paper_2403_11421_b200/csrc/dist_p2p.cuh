@@ -1,0 +1,34 @@
+// Peer-memory exchange kernels (dist_p2p.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+namespace sd {
+
+constexpr int kMaxWorld = 8;
+
+// One exchange: rows [src_off[d], +cnt[d]) of `src` go to rows
+// [dst_off[d], +cnt[d]) of rank d's buffer dst[d] (a peer mapping, or this
+// rank's own buffer for d == self); then flag[d][slot][self] = epoch for
+// every d in `notify`.
+struct P2PScatter {
+  const float* src;
+  int64_t src_stride, dst_stride;  // floats
+  int width;                       // floats per row (multiple of 4)
+  int world, self, slot;
+  int64_t epoch;
+  uint32_t notify;
+  int32_t cnt[kMaxWorld], src_off[kMaxWorld], dst_off[kMaxWorld];
+  float* dst[kMaxWorld];
+  int64_t* flag[kMaxWorld];  // each rank's flag array [2 slots][kMaxWorld sources]
+  int32_t* done;             // block-arrival counter (this rank), zero between launches
+};
+
+void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s);
+// wait until flags[slot][src] >= epoch for every src bit in `expect`
+void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s);
+
+}  // namespace sd

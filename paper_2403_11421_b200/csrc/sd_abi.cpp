@@ -633,6 +633,23 @@ int sd_dist_timing_read(sd_dist* d, double* ms, double* bytes, int reset) {
   });
 }
 
+int sd_dist_p2p_setup(sd_dist* d, int32_t max_rows, void* handles_out) {
+  static_assert(sd::DistEngine::kIpcBytes == SD_DIST_IPC_BYTES, "IPC handle block size");
+  return guard([&] {
+    need(d, "dist");
+    need(handles_out, "handles_out");
+    d->d->p2p_setup(max_rows, handles_out);
+  });
+}
+
+int sd_dist_p2p_connect(sd_dist* d, const void* all_handles) {
+  return guard([&] {
+    need(d, "dist");
+    need(all_handles, "all_handles");
+    d->d->p2p_connect(all_handles);
+  });
+}
+
 int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs, int32_t* home_rows,
                  int32_t* n_home, int32_t* shard_rows, int32_t* n_shard, int32_t* send_counts,
                  int32_t* recv_counts) {

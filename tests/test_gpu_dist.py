@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, s_ranks, cfg, out_path):
+def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -47,6 +47,8 @@ def _worker(rank, world, port, s_ranks, cfg, out_path):
     spec = sd.make_model_spec(2, 64, 4, 256, 128)
     kv = sd.KvShard(spec, 0, 4, 1 << 16, "single", rank)
     eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks)
+    if exchange == "p2p":
+        eng.enable_p2p(64)
     recs, acts, _ = sd.run_generation(eng, *cfg, seed=0, record_activations=True)
     rows = [(r, acts[i].tolist()) for i, r in enumerate(recs)]
     allr = [None] * world
@@ -61,10 +63,13 @@ def _worker(rank, world, port, s_ranks, cfg, out_path):
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("s_ranks", [1, 2])
 @pytest.mark.parametrize("cfg", [(8, 32, 32, 32), (8, 16, 4, 48)], ids=["batch", "stabilized"])
-def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg):
+@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
+def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, exchange):
+    """`exchange`: NCCL grouped send/recv, or direct NVLink stores into the
+    peers' receive buffers with epoch flags (dist_p2p.cu)."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange), nprocs=2, join=True)
     rows = pickle.load(open(out, "rb"))
     W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 128), 0)
     orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
