@@ -51,7 +51,8 @@ enum sd_status {
   SD_ERR_CONFIG = 8,
   SD_ERR_CUDA = 9,
   SD_ERR_NCCL = 10,
-  SD_ERR_ADMISSION = 11
+  SD_ERR_ADMISSION = 11,
+  SD_ERR_INFEASIBLE = 12 /* InfeasiblePlanError (planner.hpp:18-23) */
 };
 
 /* KvFormat (attention.hpp:24) */
@@ -277,6 +278,56 @@ int sd_dist_p2p_connect(sd_dist* d, const void* all_handles);
 int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs,
                  int32_t* home_rows, int32_t* n_home, int32_t* shard_rows, int32_t* n_shard,
                  int32_t* send_counts, int32_t* recv_counts);
+
+/* ------------------------------------------- planner inputs and planner
+ * The planner's measured inputs on the B200, with the reference bench
+ * definitions: T(B) = seconds of one block's S-Part (project_qkv +
+ * finish_block of layer 0) at batch B (bench_dense_block, dense.cpp:145-196);
+ * R = seconds of attend per token-position per layer for a shard holding all
+ * kv heads (bench_attention_per_token, attention.cpp:307-354). Device-timed
+ * medians of >= 2 ms samples. */
+int sd_bench_dense_block(sd_weights* w, const int32_t* batches, int32_t n, int32_t reps, double* seconds_out);
+int sd_bench_attention_per_token(const sd_model_spec* spec, int kv_format, int32_t batch, int32_t seq_len,
+                                 int32_t reps, int device, double* r_out);
+/* C: token positions of full-depth KV (all layers and kv heads) that fit in
+ * the device's free memory minus `reserve_bytes`. */
+int sd_kv_capacity_tokens(const sd_model_spec* spec, int kv_format, int device, double reserve_bytes,
+                          int64_t* tokens_out);
+
+/* The planner (Eq. 7-11; planner.hpp:25-109, planner.cpp:48-222). Host only. */
+typedef struct sd_perf_profile {
+  const int32_t* batch;   /* ascending */
+  const double* seconds;  /* T(batch) per block */
+  int32_t n;
+  double r_per_token;
+  int64_t capacity_c;
+} sd_perf_profile;
+typedef struct sd_plan_request {
+  int32_t num_layers, target_len;
+  int32_t has_latency_budget; /* 0: knee rule; 1: budget (must be > 0) */
+  double latency_budget;      /* seconds per full sequence */
+  const int32_t* candidates;  /* NULL/0: the profile's batches */
+  int32_t n_candidates;
+  double knee_threshold;     /* 0.10 in the reference */
+  double balance_tolerance;  /* 0.15 */
+} sd_plan_request;
+enum sd_plan_binding { SD_BIND_LATENCY = 0, SD_BIND_KNEE = 1, SD_BIND_MEMORY = 2 };
+typedef struct sd_hardware_plan {
+  int32_t batch_size, worker_count;
+  double worker_estimate, predicted_seq_seconds, efficiency, balance_residual;
+  int32_t balanced, binding_constraint;
+  int32_t tightest_batch; /* set with SD_ERR_INFEASIBLE */
+} sd_hardware_plan;
+int sd_plan(const sd_perf_profile* profile, const sd_plan_request* request, sd_hardware_plan* out);
+int sd_plan_batch_size(const sd_perf_profile* profile, const sd_plan_request* request, int32_t* batch_out,
+                       int32_t* tightest_out);
+int sd_plan_block_seconds(const sd_perf_profile* profile, int32_t batch, double* seconds_out);
+int sd_plan_worker_count(const sd_perf_profile* profile, int32_t batch, int32_t target_len, int32_t* workers,
+                         double* estimate);
+int sd_plan_check_memory(int64_t batch, int64_t target_len, int64_t capacity, int64_t workers,
+                         int32_t* feasible, int32_t* min_workers);
+int sd_plan_check_balance(const sd_perf_profile* profile, int32_t batch, int32_t target_len, int32_t workers,
+                          double tolerance, double* stage_seconds, double* residual, int32_t* accepted);
 
 /* ------------------------------------------------------- ShardMap, load
  * ShardMap (transport.cpp:319-380). */

@@ -55,6 +55,25 @@ I64P = C.POINTER(C.c_int64)
 DP = C.POINTER(C.c_double)
 SPEC_P = C.POINTER(ModelSpec)
 
+class PerfProfileC(C.Structure):
+    _fields_ = [("batch", C.POINTER(C.c_int32)), ("seconds", C.POINTER(C.c_double)), ("n", C.c_int32),
+                ("r_per_token", C.c_double), ("capacity_c", C.c_int64)]
+
+
+class PlanRequestC(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("target_len", C.c_int32), ("has_latency_budget", C.c_int32),
+                ("latency_budget", C.c_double),
+                ("candidates", C.POINTER(C.c_int32)), ("n_candidates", C.c_int32),
+                ("knee_threshold", C.c_double), ("balance_tolerance", C.c_double)]
+
+
+class HardwarePlanC(C.Structure):
+    _fields_ = [("batch_size", C.c_int32), ("worker_count", C.c_int32), ("worker_estimate", C.c_double),
+                ("predicted_seq_seconds", C.c_double), ("efficiency", C.c_double),
+                ("balance_residual", C.c_double), ("balanced", C.c_int32), ("binding_constraint", C.c_int32),
+                ("tightest_batch", C.c_int32)]
+
+
 SIGNATURES = {
     "sd_last_error": (C.c_char_p, []),
     "sd_abi_version": (C.c_int, []),
@@ -118,6 +137,16 @@ SIGNATURES = {
     "sd_dist_timing": (C.c_int, [P, C.c_int]),
     "sd_dist_timing_read": (C.c_int, [P, DP, DP, C.c_int]),
     "sd_dist_p2p_setup": (C.c_int, [P, C.c_int32, P]),
+    "sd_bench_dense_block": (C.c_int, [P, I32P, C.c_int32, C.c_int32, DP]),
+    "sd_bench_attention_per_token": (C.c_int, [SPEC_P, C.c_int, C.c_int32, C.c_int32, C.c_int32, C.c_int, DP]),
+    "sd_kv_capacity_tokens": (C.c_int, [SPEC_P, C.c_int, C.c_int, C.c_double, I64P]),
+    "sd_plan": (C.c_int, [C.POINTER(PerfProfileC), C.POINTER(PlanRequestC), C.POINTER(HardwarePlanC)]),
+    "sd_plan_batch_size": (C.c_int, [C.POINTER(PerfProfileC), C.POINTER(PlanRequestC), I32P, I32P]),
+    "sd_plan_block_seconds": (C.c_int, [C.POINTER(PerfProfileC), C.c_int32, DP]),
+    "sd_plan_worker_count": (C.c_int, [C.POINTER(PerfProfileC), C.c_int32, C.c_int32, I32P, DP]),
+    "sd_plan_check_memory": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, I32P, I32P]),
+    "sd_plan_check_balance": (C.c_int, [C.POINTER(PerfProfileC), C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                        DP, DP, I32P]),
     "sd_dist_p2p_connect": (C.c_int, [P, P]),
     "sd_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int32, U64P, I32P, I32P, I32P, I32P,
                                I32P, I32P]),

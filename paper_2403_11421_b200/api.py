@@ -51,8 +51,13 @@ class CudaError(SplitDecodeError):
     code = 9
 
 
+class InfeasiblePlanError(SplitDecodeError):  # planner.hpp:18-23
+    code = 12
+    tightest_batch = 0
+
+
 _BY_CODE = {c.code: c for c in (ConfigError, ProtocolError, UnknownSequenceError, CapacityError,
-                                LogicError, AdmissionError, CudaError)}
+                                LogicError, AdmissionError, CudaError, InfeasiblePlanError)}
 
 
 def _check(rc: int):

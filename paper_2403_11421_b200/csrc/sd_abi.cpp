@@ -8,6 +8,8 @@
 #include <vector>
 
 #include "dist.h"
+#include "perf_bench.h"
+#include "planner.h"
 #include "engine.h"
 #include "kv_store.h"
 #include "sd_common.h"
@@ -706,3 +708,157 @@ int sd_cold_start_schedule(int batch, int target_len, int interval, int mode, in
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- planner and inputs
+namespace {
+sd::PerfProfile to_profile(const sd_perf_profile* p) {
+  need(p, "profile");
+  sd::PerfProfile r;
+  if (p->n > 0) {
+    need(p->batch, "profile.batch");
+    need(p->seconds, "profile.seconds");
+  }
+  for (int i = 0; i < p->n; ++i) r.t_table.emplace_back(p->batch[i], p->seconds[i]);
+  r.r_per_token = p->r_per_token;
+  r.capacity_c = p->capacity_c;
+  return r;
+}
+sd::PlanRequest to_request(const sd_plan_request* q) {
+  need(q, "request");
+  sd::PlanRequest r;
+  r.num_layers = q->num_layers;
+  r.target_len = q->target_len;
+  if (q->has_latency_budget && !(q->latency_budget > 0)) {
+    sd::fail(SD_ERR_CONFIG, "plan request: latency budget must be positive");
+  }
+  r.latency_budget = q->has_latency_budget ? q->latency_budget : sd::kNoBudget;
+  if (q->candidates && q->n_candidates > 0) r.candidates.assign(q->candidates, q->candidates + q->n_candidates);
+  r.knee_threshold = q->knee_threshold;
+  r.balance_tolerance = q->balance_tolerance;
+  return r;
+}
+}  // namespace
+
+int sd_bench_dense_block(sd_weights* w, const int32_t* batches, int32_t n, int32_t reps, double* seconds_out) {
+  return guard([&] {
+    need(w, "weights");
+    need(batches, "batches");
+    need(seconds_out, "seconds_out");
+    sd::bench_dense_block(*w->w, batches, n, reps, seconds_out);
+  });
+}
+
+int sd_bench_attention_per_token(const sd_model_spec* spec, int kv_format, int32_t batch, int32_t seq_len,
+                                 int32_t reps, int device, double* r_out) {
+  return guard([&] {
+    need(spec, "spec");
+    need(r_out, "r_out");
+    *r_out = sd::bench_attention_per_token(sd::from_abi(spec), kv_format, batch, seq_len, reps, device);
+  });
+}
+
+int sd_kv_capacity_tokens(const sd_model_spec* spec, int kv_format, int device, double reserve_bytes,
+                          int64_t* tokens_out) {
+  return guard([&] {
+    need(spec, "spec");
+    need(tokens_out, "tokens_out");
+    *tokens_out = sd::kv_capacity_tokens(sd::from_abi(spec), kv_format, device, reserve_bytes);
+  });
+}
+
+int sd_plan(const sd_perf_profile* profile, const sd_plan_request* request, sd_hardware_plan* out) {
+  return guard([&] {
+    need(out, "out");
+    const sd::PerfProfile p = to_profile(profile);
+    const sd::PlanRequest q = to_request(request);
+    *out = sd_hardware_plan{};
+    try {
+      const sd::HardwarePlan h = sd::plan(p, q);
+      out->batch_size = h.batch_size;
+      out->worker_count = h.worker_count;
+      out->worker_estimate = h.worker_estimate;
+      out->predicted_seq_seconds = h.predicted_seq_seconds;
+      out->efficiency = h.efficiency;
+      out->balance_residual = h.balance_residual;
+      out->balanced = h.balanced ? 1 : 0;
+      out->binding_constraint = h.binding;
+      out->tightest_batch = h.tightest_batch;
+    } catch (const sd::Error& e) {
+      if (e.code == SD_ERR_INFEASIBLE) {
+        int t = 0;
+        try {
+          sd::plan_batch_size(p, q, &t);
+        } catch (const sd::Error&) {
+        }
+        out->tightest_batch = t;
+      }
+      throw;
+    }
+  });
+}
+
+int sd_plan_batch_size(const sd_perf_profile* profile, const sd_plan_request* request, int32_t* batch_out,
+                       int32_t* tightest_out) {
+  return guard([&] {
+    need(batch_out, "batch_out");
+    int t = 0;
+    const sd::PerfProfile p = to_profile(profile);
+    sd::validate_profile(p);
+    try {
+      *batch_out = sd::plan_batch_size(p, to_request(request), &t);
+    } catch (const sd::Error&) {
+      if (tightest_out) *tightest_out = t;
+      throw;
+    }
+    if (tightest_out) *tightest_out = t;
+  });
+}
+
+int sd_plan_block_seconds(const sd_perf_profile* profile, int32_t batch, double* seconds_out) {
+  return guard([&] {
+    need(seconds_out, "seconds_out");
+    const sd::PerfProfile p = to_profile(profile);
+    if (p.t_table.empty()) sd::fail(SD_ERR_CONFIG, "profile: empty T(B) table");
+    *seconds_out = sd::block_seconds(p, batch);
+  });
+}
+
+int sd_plan_worker_count(const sd_perf_profile* profile, int32_t batch, int32_t target_len, int32_t* workers,
+                         double* estimate) {
+  return guard([&] {
+    need(workers, "workers");
+    need(estimate, "estimate");
+    const sd::PerfProfile p = to_profile(profile);
+    if (p.t_table.empty()) sd::fail(SD_ERR_CONFIG, "profile: empty T(B) table");
+    int w = 0;
+    sd::plan_worker_count(p, batch, target_len, &w, estimate);
+    *workers = w;
+  });
+}
+
+int sd_plan_check_memory(int64_t batch, int64_t target_len, int64_t capacity, int64_t workers, int32_t* feasible,
+                         int32_t* min_workers) {
+  return guard([&] {
+    need(feasible, "feasible");
+    need(min_workers, "min_workers");
+    bool f = false;
+    int m = 0;
+    sd::check_memory(batch, target_len, capacity, workers, &f, &m);
+    *feasible = f ? 1 : 0;
+    *min_workers = m;
+  });
+}
+
+int sd_plan_check_balance(const sd_perf_profile* profile, int32_t batch, int32_t target_len, int32_t workers,
+                          double tolerance, double* stage_seconds, double* residual, int32_t* accepted) {
+  return guard([&] {
+    need(stage_seconds, "stage_seconds");
+    need(residual, "residual");
+    need(accepted, "accepted");
+    const sd::PerfProfile p = to_profile(profile);
+    if (p.t_table.empty()) sd::fail(SD_ERR_CONFIG, "profile: empty T(B) table");
+    bool ok = false;
+    sd::check_balance(p, batch, target_len, workers, tolerance, stage_seconds, residual, &ok);
+    *accepted = ok ? 1 : 0;
+  });
+}
