@@ -109,12 +109,19 @@ struct Fmt<SD_KV_HALF> {
 template <>
 struct Fmt<SD_KV_INT8> {
   static constexpr int kBytes = 1;
+  // int8 -> fp32 without I2F: byte b becomes the float 2^23 + (b + 128)
+  // (one PRMT into 0x4B0000xx), minus 2^23 + 128: exact, equal to (float)b
+  __device__ static __forceinline__ void cvt4(uint32_t w, float* x) {
+    const uint32_t u = w ^ 0x80808080u;
+    x[0] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7650)) - 8388736.0f;
+    x[1] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7651)) - 8388736.0f;
+    x[2] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7652)) - 8388736.0f;
+    x[3] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7653)) - 8388736.0f;
+  }
   __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
     const uint2 r = *reinterpret_cast<const uint2*>(p);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = static_cast<float>(static_cast<int8_t>(r.x >> (8 * i)));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x[4 + i] = static_cast<float>(static_cast<int8_t>(r.y >> (8 * i)));
+    cvt4(r.x, x);
+    cvt4(r.y, x + 4);
   }
 };
 
