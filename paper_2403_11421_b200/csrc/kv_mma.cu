@@ -106,15 +106,27 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_h2(x0 - hf.x, x1 - hf.y);
 }
 
-template <int G>
+// four int8 (one 32-bit word) -> two fp16 pairs holding the exact integers:
+// byte b becomes fp16 1024 + (b + 128) (0x64xx), minus 1152
+__device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
+  const uint32_t biased = __byte_perm(u, 0x64646464u, sel);
+  __half2 h = *reinterpret_cast<const __half2*>(&biased);
+  h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+constexpr int kVPitch = kHD * 2 + 16;  // bytes per row of a warp's dequantized V tile
+
+template <int G, int FMT>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
+  constexpr bool I8 = FMT == SD_KV_INT8;
   extern __shared__ __align__(128) uint8_t smem[];
   const int nst = a.nstages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + nst;
   uint8_t* ring = smem + 128 * ((16 * nst + 127) / 128);
   const int pitch = a.stage_region / kT;  // padded bytes per position row
-  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region;
+  // int8: [K rows][V rows][K scales kT x hc][V scales kT x hc]
+  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + (I8 ? 2 * a.sc_region : 0);
   const KvGeom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -149,14 +161,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         const int cnt = min(kT, pc.p1 - pos);
         const uint8_t* base = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes +
                               static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
+        const uint32_t scb = I8 ? static_cast<uint32_t>(cnt * g.hc * 4) : 0u;
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes);
+          mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes + 2u * scb);
         }
         __syncwarp();
         if (t < cnt) {
           uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + t * pitch;
           bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + t * g.pos_bytes, g.pos_bytes, &full[stage], pol);
+        }
+        if (I8 && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
+          const uint8_t* lb = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes;
+          const int off = pos & (g.P - 1);
+          uint8_t* dst = ring + stage * stage_bytes + 2 * a.stage_region + (lane ? a.sc_region : 0);
+          bulk_g2s(dst, lb + (lane ? g.vs_off : g.ks_off) + off * g.hc * 4, scb, &full[stage], pol);
         }
         if (++stage == nst) {
           stage = 0;
@@ -189,7 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float2 x = make_float2(0.0f, 0.0f);
-          if (gq < G) x = *reinterpret_cast<const float2*>(qrow + gq * kHD + 16 * kk + 8 * h + 2 * tq);
+          // int8 K fragments take 4 contiguous d per lane (a permutation of
+          // the dot's k index); Q^T uses the same permutation
+          const int d = I8 ? 16 * kk + 4 * tq + 2 * h : 16 * kk + 8 * h + 2 * tq;
+          if (gq < G) x = *reinterpret_cast<const float2*>(qrow + gq * kHD + d);
           split2(x.x * a.qscale, x.y * a.qscale, qb[kk][h][0], qb[kk][h][1]);
         }
       }
@@ -205,17 +227,51 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const int cnt = min(kT, pc.p1 - pos);
       mbar_wait(&full[stage], phase);
       __syncwarp();
-      const uint32_t Ks = smem_u32(ring + stage * stage_bytes) + hk * kHD * 2;
-      const uint32_t Vs = Ks + a.stage_region;
+      const uint8_t* st8 = ring + stage * stage_bytes;
+      const uint32_t Ks = smem_u32(st8) + hk * kHD * (I8 ? 1 : 2);
+      uint32_t Vs = Ks + a.stage_region;
+      int vpitch = pitch;
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (I8) {
+        const uint8_t* kb = st8 + hk * kHD + 4 * tq;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        uint32_t ka[4];
-        // matrices: (pos 0-7, d 0-7), (pos 8-15, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 8-15)
-        ldsm_x4(Ks + (lr + 8 * (lm & 1)) * pitch + (16 * kk + 8 * (lm >> 1)) * 2, ka);
-        mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
-        mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + gq * pitch + 16 * kk) ^ 0x80808080u;
+          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + (gq + 8) * pitch + 16 * kk) ^ 0x80808080u;
+          const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
+                                  i8x2_to_h2(w1, 0x5342)};
+          mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
+          mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+        }
+        // per-(position, head) K scales: S = scale * (q . k_int)
+        const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
+        const float k0 = ksc[gq * g.hc + hk], k1 = ksc[(gq + 8) * g.hc + hk];
+        s[0] *= k0;
+        s[1] *= k0;
+        s[2] *= k1;
+        s[3] *= k1;
+        // V tile of this head -> exact fp16 integers in the warp's scratch
+        uint8_t* vscr = ring + nst * stage_bytes + warp * (kT * kVPitch);
+        const uint8_t* vb = st8 + a.stage_region + hk * kHD + (lane >> 1) * pitch + (lane & 1) * 64;
+        uint8_t* vd = vscr + (lane >> 1) * kVPitch + (lane & 1) * 128;
+#pragma unroll
+        for (int wv = 0; wv < 16; ++wv) {
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + 4 * wv) ^ 0x80808080u;
+          *reinterpret_cast<uint2*>(vd + 8 * wv) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
+        }
+        __syncwarp();
+        Vs = smem_u32(vscr);
+        vpitch = kVPitch;
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t ka[4];
+          // matrices: (pos 0-7, d 0-7), (pos 8-15, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 8-15)
+          ldsm_x4(Ks + (lr + 8 * (lm & 1)) * pitch + (16 * kk + 8 * (lm >> 1)) * 2, ka);
+          mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
+          mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+        }
       }
       // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
       const bool v0 = gq < cnt, v1 = gq + 8 < cnt;
@@ -243,9 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         o[mt][3] *= c1;
       }
       // ---- P^T B-fragments via transposes of the S^T accumulator layout
+      // (int8: the V scale of each position is folded into p)
+      float vs0 = 1.0f, vs1 = 1.0f;
+      if (I8) {
+        const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
+        vs0 = vsc[gq * g.hc + hk];
+        vs1 = vsc[(gq + 8) * g.hc + hk];
+      }
       uint32_t h01, l01, h23, l23;
-      split2(p0, p1, h01, l01);  // (pos gq, heads 2tq..): rows = pos
-      split2(p2, p3, h23, l23);  // (pos gq+8, ...)
+      split2(p0 * vs0, p1 * vs0, h01, l01);  // (pos gq, heads 2tq..): rows = pos
+      split2(p2 * vs1, p3 * vs1, h23, l23);  // (pos gq+8, ...)
       const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
       const uint32_t bl0 = movm_t(l01), bl1 = movm_t(l23);
       // ---- O^T += V^T . P^T  (8 tiles of 16 head-dims)
@@ -253,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       for (int mt = 0; mt < 8; ++mt) {
         uint32_t va[4];
         // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
-        ldsm_x4_t(Vs + (lr + 8 * (lm >> 1)) * pitch + (16 * mt + 8 * (lm & 1)) * 2, va);
+        ldsm_x4_t(Vs + (lr + 8 * (lm >> 1)) * vpitch + (16 * mt + 8 * (lm & 1)) * 2, va);
         mma16816(o[mt], va, bh0, bh1);
         mma16816(o[mt], va, bl0, bl1);
       }
@@ -365,24 +428,28 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 }  // namespace
 
 bool attention_mma_supported(const KvGeom& g, int G) {
-  return g.fmt == SD_KV_HALF && g.hd == kHD && g.hc == kWarps && (G == 2 || G == 4 || G == 8) &&
-         g.P % kT == 0;
+  return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD && g.hc == kWarps &&
+         (G == 2 || G == 4 || G == 8) && g.P % kT == 0;
 }
 
-size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* nstages) {
+size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages) {
   const int pitch = g.pos_bytes + 16;
-  *stage_region = ((kT * pitch + 127) / 128) * 128;
-  *nstages = 3;
-  while (*nstages > 2 && 128 + static_cast<size_t>(*nstages) * 2 * *stage_region > 215 * 1024) --*nstages;
-  return 128 + static_cast<size_t>(*nstages) * 2 * *stage_region;
+  *stage_region = kT * pitch;  // a multiple of 16 (bulk-copy alignment)
+  *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
+  const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
+  const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0;
+  *nstages = 5;
+  while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
+  return 128 + *nstages * stage + scratch;
 }
 
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
+  const bool i8 = a.g.fmt == SD_KV_INT8;
   switch (a.G) {
-    case 2: fn = attn_mma_kernel<2>; break;
-    case 4: fn = attn_mma_kernel<4>; break;
-    case 8: fn = attn_mma_kernel<8>; break;
+    case 2: fn = i8 ? attn_mma_kernel<2, SD_KV_INT8> : attn_mma_kernel<2, SD_KV_HALF>; break;
+    case 4: fn = i8 ? attn_mma_kernel<4, SD_KV_INT8> : attn_mma_kernel<4, SD_KV_HALF>; break;
+    case 8: fn = i8 ? attn_mma_kernel<8, SD_KV_INT8> : attn_mma_kernel<8, SD_KV_HALF>; break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

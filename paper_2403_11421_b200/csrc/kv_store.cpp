@@ -109,8 +109,7 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   use_mma_ = attention_mma_supported(g, G_) && std::getenv("SD_ATTN_NO_MMA") == nullptr;
   if (use_mma_) {
     T_ = 16;
-    sc_region_ = 0;
-    attn_smem_ = attention_mma_smem(g, &stage_region_, &nstages_);
+    attn_smem_ = attention_mma_smem(g, &stage_region_, &sc_region_, &nstages_);
   }
 
   ring_.resize(8);

@@ -180,16 +180,19 @@ def test_many_sequences_split_and_combine(sd, oracle):
     assert err < 2e-5, err
 
 
+@pytest.mark.parametrize("fmt", ["half", "int8"])
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_gqa_tensor_core_path_parity(sd, oracle, G):
-    """fp16 KV, hd 128, 8 kv heads: the mma.sync attention path (kv_mma.cu),
-    with ragged lengths (tails of 16-position stages) and split pieces."""
+def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt):
+    """fp16 / int8 KV, hd 128, 8 kv heads: the mma.sync attention path
+    (kv_mma.cu), with ragged lengths (tails of 16-position stages) and split
+    pieces. int8 keys enter the MMA as exact fp16 integers with the K scale
+    applied to the scores and the V scale folded into p; same bar as fp16."""
     H = 8 * G
     D = H * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
     B, Lmax = 40, 700
-    gpu = sd.KvShard(s, 0, 8, B * Lmax, "half")
-    cpu = oracle.KvShard(os_, 0, 8, B * Lmax, "half")
+    gpu = sd.KvShard(s, 0, 8, B * Lmax, fmt)
+    cpu = oracle.KvShard(os_, 0, 8, B * Lmax, fmt)
     rng = _rng(G)
     lens = rng.integers(1, Lmax, B)
     lens[0], lens[1] = 1, 17
