@@ -61,6 +61,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// bulk copy issued by one elected lane of a converged warp (uniform operands)
+__device__ __forceinline__ void e_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                           uint64_t policy) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;\n}\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void e_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+               "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -149,7 +165,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   if (warp == kWarps) {
     // producer warp: lane 0 arms the stage barrier, then lanes 0-15 copy the
-    // K rows and lanes 16-31 the V rows of the stage in parallel
+    // K rows and lanes 16-31 the V rows of the stage in parallel (per-lane
+    // issue measured faster than one elected lane issuing all 32 copies)
     const uint64_t pol = evict_first_policy();
     int stage = 0;
     uint32_t phase = 0;
@@ -167,7 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes + 2u * scb);
         }
         __syncwarp();
-        if (t < cnt) {
+        if (I8) {
+          // int8: two consecutive positions per copy (copy issue rate, not
+          // bytes, limits small rows); pair slots carry the 16-B pad
+          const int pr = lane & 15;
+          if (pr < 8 && 2 * pr < cnt) {
+            uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + pr * (2 * g.pos_bytes + 16);
+            const uint32_t nb = (2 * pr + 1 < cnt ? 2u : 1u) * g.pos_bytes;
+            bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + 2 * pr * g.pos_bytes, nb, &full[stage], pol);
+          }
+        } else if (t < cnt) {
           uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + t * pitch;
           bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + t * g.pos_bytes, g.pos_bytes, &full[stage], pol);
         }
@@ -234,11 +260,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (I8) {
-        const uint8_t* kb = st8 + hk * kHD + 4 * tq;
+        // MMA row m holds position 2m (m < 8) or 2(m-8)+1: rows gq and gq+8 of
+        // this lane are the pair slot gq (conflict-free: slot pitch = 4 mod 32 words)
+        const int ppitch = 2 * g.pos_bytes + 16;
+        const uint8_t* kb = st8 + hk * kHD + 4 * tq + gq * ppitch;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + gq * pitch + 16 * kk) ^ 0x80808080u;
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + (gq + 8) * pitch + 16 * kk) ^ 0x80808080u;
+          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
+          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + g.pos_bytes + 16 * kk) ^ 0x80808080u;
           const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
                                   i8x2_to_h2(w1, 0x5342)};
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
@@ -246,19 +275,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         }
         // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
-        const float k0 = ksc[gq * g.hc + hk], k1 = ksc[(gq + 8) * g.hc + hk];
+        const float k0 = ksc[(2 * gq) * g.hc + hk], k1 = ksc[(2 * gq + 1) * g.hc + hk];
         s[0] *= k0;
         s[1] *= k0;
         s[2] *= k1;
         s[3] *= k1;
         // V tile of this head -> exact fp16 integers in the warp's scratch
+        // lane l converts word l (4 head dims) of every row: conflict-free
+        // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
         uint8_t* vscr = ring + nst * stage_bytes + warp * (kT * kVPitch);
-        const uint8_t* vb = st8 + a.stage_region + hk * kHD + (lane >> 1) * pitch + (lane & 1) * 64;
-        uint8_t* vd = vscr + (lane >> 1) * kVPitch + (lane & 1) * 128;
+        const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
+        uint8_t* vd = vscr + 8 * lane;
 #pragma unroll
-        for (int wv = 0; wv < 16; ++wv) {
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + 4 * wv) ^ 0x80808080u;
-          *reinterpret_cast<uint2*>(vd + 8 * wv) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
+        for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
+          const int slot = m & 7, odd = m >> 3;
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + odd * g.pos_bytes) ^ 0x80808080u;
+          *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
         }
         __syncwarp();
         Vs = smem_u32(vscr);
@@ -274,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         }
       }
       // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
-      const bool v0 = gq < cnt, v1 = gq + 8 < cnt;
+      const bool v0 = (I8 ? 2 * gq : gq) < cnt, v1 = (I8 ? 2 * gq + 1 : gq + 8) < cnt;
       if (!v0) s[0] = s[1] = -INFINITY;
       if (!v1) s[2] = s[3] = -INFINITY;
       float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
@@ -303,8 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       float vs0 = 1.0f, vs1 = 1.0f;
       if (I8) {
         const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
-        vs0 = vsc[gq * g.hc + hk];
-        vs1 = vsc[(gq + 8) * g.hc + hk];
+        vs0 = vsc[(2 * gq) * g.hc + hk];
+        vs1 = vsc[(2 * gq + 1) * g.hc + hk];
       }
       uint32_t h01, l01, h23, l23;
       split2(p0 * vs0, p1 * vs0, h01, l01);  // (pos gq, heads 2tq..): rows = pos
@@ -434,7 +466,8 @@ bool attention_mma_supported(const KvGeom& g, int G) {
 
 size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages) {
   const int pitch = g.pos_bytes + 16;
-  *stage_region = kT * pitch;  // a multiple of 16 (bulk-copy alignment)
+  // fp16: kT rows at a 16-B padded pitch; int8: kT/2 pair slots (2 rows + 16 B)
+  *stage_region = g.fmt == SD_KV_INT8 ? (kT / 2) * (2 * g.pos_bytes + 16) : kT * pitch;
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
   const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0;
