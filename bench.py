@@ -309,8 +309,11 @@ def run_ours(args, wl, rank, world, dev, dist):
     torch.cuda.synchronize(dev)
 
     # ---- device-timed region: K steps, CUDA events on the engine stream
-    kv.timing(True)
-    eng.timing(True)
+    # (SD_BENCH_NO_KTIMING=1: no per-kernel events, for A/B experiments only;
+    # the roofline fields are then empty)
+    ktiming = os.environ.get("SD_BENCH_NO_KTIMING") is None
+    kv.timing(ktiming)
+    eng.timing(ktiming)
     kv.timing_read(reset=True)
     eng.timing_read(reset=True)
     if dist:

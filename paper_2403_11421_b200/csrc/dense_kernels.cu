@@ -5,6 +5,7 @@
 #include <cfloat>
 
 #include "dense_kernels.cuh"
+#include "pdl.cuh"
 #include "sd_common.h"
 
 namespace sd {
@@ -26,6 +27,8 @@ __global__ void __launch_bounds__(kCols) linear_exact_kernel(int B, int in, int 
                                                              const float* __restrict__ w, int64_t ldw,
                                                              float* __restrict__ y, int64_t ldy, int epi,
                                                              const float* __restrict__ res, int64_t ldr) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float xs[kRows][kKTile];
   const int j = blockIdx.x * kCols + threadIdx.x;
   const int b0 = blockIdx.y * kRows;
@@ -66,6 +69,8 @@ __global__ void __launch_bounds__(kCols) linear_exact_kernel(int B, int in, int 
 __global__ void embed_kernel(int B, int D, const int32_t* __restrict__ tokens,
                              const float* __restrict__ emb, float* __restrict__ x, int64_t ldx,
                              __nv_bfloat16* __restrict__ xb) {
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x;
   const float* col = emb + static_cast<int64_t>(tokens[b]) * D;  // column-major D x V
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
@@ -79,6 +84,8 @@ __global__ void embed_kernel(int B, int D, const int32_t* __restrict__ tokens,
 // then the smaller index. NaN logits never win (the reference's `>` test).
 __global__ void argmax_kernel(int V, const float* __restrict__ logits, int64_t ld,
                               int32_t* __restrict__ tokens) {
+  pdl_trigger();
+  pdl_wait();
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * ld;
   float bv = -INFINITY;
   int bi = 0x7fffffff;
@@ -125,6 +132,8 @@ __global__ void argmax_kernel(int V, const float* __restrict__ logits, int64_t l
 
 __global__ void to_bf16_kernel(int rows, int cols, const float* __restrict__ x, int64_t ldx,
                                __nv_bfloat16* __restrict__ y, int64_t ldy) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
     y[static_cast<int64_t>(r) * ldy + c] = __float2bfloat16_rn(x[static_cast<int64_t>(r) * ldx + c]);
@@ -138,7 +147,7 @@ void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, co
                          int64_t ldr, cudaStream_t s) {
   if (B == 0 || out == 0) return;
   dim3 grid((out + kCols - 1) / kCols, (B + kRows - 1) / kRows);
-  linear_exact_kernel<<<grid, kCols, 0, s>>>(B, in, out, x, ldx, w, ldw, y, ldy, epi, res, ldr);
+  SD_CUDA(launch_pdl(linear_exact_kernel, grid, dim3(kCols), 0, s, 1, B, in, out, x, ldx, w, ldw, y, ldy, epi, res, ldr));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -146,7 +155,7 @@ void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, co
 void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
                   __nv_bfloat16* xb, cudaStream_t s) {
   if (B == 0) return;
-  embed_kernel<<<B, 256, 0, s>>>(B, D, tokens, emb, x, ldx, xb);
+  SD_CUDA(launch_pdl(embed_kernel, dim3(B), dim3(256), 0, s, 1, B, D, tokens, emb, x, ldx, xb));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -154,7 +163,7 @@ void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* 
 void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
                    cudaStream_t s) {
   if (B == 0) return;
-  argmax_kernel<<<B, 512, 0, s>>>(V, logits, ld, tokens);
+  SD_CUDA(launch_pdl(argmax_kernel, dim3(B), dim3(512), 0, s, 1, V, logits, ld, tokens));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -163,7 +172,7 @@ void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat
                     int64_t ldy, cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
   dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, rows);
-  to_bf16_kernel<<<grid, 256, 0, s>>>(rows, cols, x, ldx, y, ldy);
+  SD_CUDA(launch_pdl(to_bf16_kernel, grid, dim3(256), 0, s, 1, rows, cols, x, ldx, y, ldy));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "dist_p2p.cuh"
+#include "pdl.cuh"
 #include "sd_common.h"
 
 namespace sd {
@@ -23,6 +24,8 @@ __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
 
 // grid-stride over (row, 16-B chunk) of every destination's row range
 __global__ void p2p_scatter_kernel(const P2PScatter a) {
+  pdl_trigger();
+  pdl_wait();
   const int vec = a.width / 4;  // float4 per row
   int64_t total = 0;
   for (int d = 0; d < a.world; ++d) total += static_cast<int64_t>(a.cnt[d]) * vec;
@@ -57,6 +60,8 @@ __global__ void p2p_scatter_kernel(const P2PScatter a) {
 // spin until every expected source has published this epoch; bounded so a
 // lost peer traps instead of hanging the GPU
 __global__ void p2p_wait_kernel(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch) {
+  pdl_trigger();
+  pdl_wait();
   const int t = threadIdx.x;
   if (t >= world || !(expect >> t & 1)) return;
   const int64_t* f = flags + slot * kMaxWorld + t;
@@ -75,14 +80,14 @@ void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s) {
   const int64_t work = rows * (a.width / 4);
   int grid = static_cast<int>(std::min<int64_t>(264, (work + 255) / 256));
   if (grid < 1) grid = 1;
-  p2p_scatter_kernel<<<grid, 256, 0, s>>>(a);
+  SD_CUDA(launch_pdl(p2p_scatter_kernel, dim3(grid), dim3(256), 0, s, 1, a));
   SD_CUDA(cudaGetLastError());
   count_launch();
 }
 
 void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s) {
   if (!expect) return;
-  p2p_wait_kernel<<<1, 32, 0, s>>>(flags, slot, expect, world, epoch);
+  SD_CUDA(launch_pdl(p2p_wait_kernel, dim3(1), dim3(32), 0, s, 1, flags, slot, expect, world, epoch));
   SD_CUDA(cudaGetLastError());
   count_launch();
 }

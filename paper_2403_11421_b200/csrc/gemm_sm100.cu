@@ -25,6 +25,7 @@
 #include <unordered_map>
 
 #include "dense_kernels.cuh"
+#include "pdl.cuh"
 #include "sd_common.h"
 
 namespace sd {
@@ -400,10 +401,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
+  pdl_trigger();
   __syncthreads();
   if (cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // A operand / residual of the previous kernel from here on
 
   auto m_origin = [&](int it) { return ((it % mgroups) * cs + rank) * BM; };
 
@@ -843,19 +846,8 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   const int budget = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
   const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(clusters * cs));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C_::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  SD_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tcb, p));
+  SD_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(clusters * cs)), dim3(kThreads), C_::SMEM, s,
+                     static_cast<unsigned>(cs), ta, tb, tc, tcb, p));
   count_launch();
 }
 

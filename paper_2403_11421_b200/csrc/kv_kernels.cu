@@ -13,6 +13,7 @@
 #include <cmath>
 
 #include "kv_kernels.cuh"
+#include "pdl.cuh"
 #include "sd_common.h"
 
 namespace sd {
@@ -166,7 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();  // inputs of the previous kernel (q, plan, pool) from here on
 
   const int cb = a.cta_begin[blockIdx.x];
   const int ce = a.cta_begin[blockIdx.x + 1];
@@ -500,6 +503,8 @@ __device__ __forceinline__ float load_elem(const KvGeom& g, const uint8_t* lb, i
 constexpr int kGenericMaxPerLane = 8;  // hd <= 256
 
 __global__ void attn_generic_kernel(const AttnArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const KvGeom& g = a.g;
   const int w = blockIdx.x;
   const int qh = blockIdx.y;
@@ -570,6 +575,8 @@ __global__ void attn_generic_kernel(const AttnArgs a) {
 // --------------------------------------------------------------- K3 ------
 // Deterministic combine of an item's pieces in piece order.
 __global__ void combine_kernel(const CombineArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int4 it = a.items[blockIdx.x];
   const int width = a.Hq * a.hd;
   float* orow = a.o + static_cast<int64_t>(it.x) * a.o_stride;
@@ -594,6 +601,8 @@ __global__ void combine_kernel(const CombineArgs a) {
 // (attention.cpp:28-46) bit for bit: scale = max|x| / 127.0f (IEEE fp32
 // division), q = clamp(rint((double)x * (1.0 / (double)scale)), +-127).
 __global__ void append_kernel(const AppendArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const KvGeom& g = a.g;
   // page-table updates for pages opened by this call
   if (blockIdx.x == 0 && blockIdx.y == 0) {
@@ -645,6 +654,8 @@ __global__ void append_kernel(const AppendArgs a) {
 // Synthetic prefill: element (slot, layer, pos, kv, i) = synth_value(idx).
 __global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* slots, int n,
                                int length, uint64_t salt) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t rows = static_cast<int64_t>(n) * num_layers * length * 2;
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     int64_t t = r;
@@ -795,7 +806,7 @@ bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) 
     SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   }
-  fn<<<grid, kThreads, smem, s>>>(a);
+  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(kThreads), smem, s, 1, a));
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};
@@ -812,14 +823,14 @@ bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) 
 void launch_attention_generic(const AttnArgs& a, int npieces, cudaStream_t s) {
   if (a.g.hd > 32 * kGenericMaxPerLane) fail(SD_ERR_CONFIG, "head_dim > 256 is not supported");
   dim3 grid(npieces, a.g.hc * a.G);
-  attn_generic_kernel<<<grid, 32, 0, s>>>(a);
+  SD_CUDA(launch_pdl(attn_generic_kernel, dim3(grid), dim3(32), 0, s, 1, a));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
 
 void launch_combine(const CombineArgs& a, cudaStream_t s) {
   if (a.m == 0) return;
-  combine_kernel<<<a.m, 256, 0, s>>>(a);
+  SD_CUDA(launch_pdl(combine_kernel, dim3(a.m), dim3(256), 0, s, 1, a));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -827,7 +838,7 @@ void launch_combine(const CombineArgs& a, cudaStream_t s) {
 void launch_append(const AppendArgs& a, cudaStream_t s) {
   if (a.n == 0 && a.nupd == 0) return;
   dim3 grid(a.n > 0 ? a.n : 1, 2);
-  append_kernel<<<grid, 256, 0, s>>>(a);
+  SD_CUDA(launch_pdl(append_kernel, grid, dim3(256), 0, s, 1, a));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -835,7 +846,7 @@ void launch_append(const AppendArgs& a, cudaStream_t s) {
 void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, int n,
                               int length, uint64_t salt, cudaStream_t s) {
   if (n == 0 || length == 0) return;
-  prefill_kernel<<<148 * 16, 256, 0, s>>>(g, num_layers, slots, n, length, salt);
+  SD_CUDA(launch_pdl(prefill_kernel, dim3(148 * 16), dim3(256), 0, s, 1, g, num_layers, slots, n, length, salt));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }

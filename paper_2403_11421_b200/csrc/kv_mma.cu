@@ -21,6 +21,7 @@
 #include <cuda_fp16.h>
 
 #include "kv_kernels.cuh"
+#include "pdl.cuh"
 #include "sd_common.h"
 
 namespace sd {
@@ -158,7 +159,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     *reinterpret_cast<uint4*>(ring + i) = make_uint4(0, 0, 0, 0);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  pdl_trigger();
   __syncthreads();
+  pdl_wait();  // inputs of the previous kernel (q, plan, pool) from here on
 
   const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
   const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
@@ -486,7 +489,7 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  fn<<<grid, kThreads, smem, s>>>(a);
+  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(kThreads), smem, s, 1, a));
   SD_CUDA(cudaGetLastError());
   count_launch();
 }
