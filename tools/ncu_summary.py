@@ -41,21 +41,38 @@ def launches(path, out):
     rows = list(csv.reader(l for l in open(path) if not l.startswith("==")))
     h = rows[0]
     iK, iV = h.index("Kernel Name"), h.index("Metric Value")
+    iM = h.index("Metric Name") if "Metric Name" in h else None
     iG = h.index("Grid Size") if "Grid Size" in h else None
-    t = collections.defaultdict(list)
+    iID = h.index("ID") if "ID" in h else None
+    per = collections.defaultdict(dict)  # launch id -> {metric: value}
+    key_of = {}
     for r in rows[1:]:
         try:
             v = float(r[iV].replace(",", ""))
         except ValueError:
             continue
+        lid = r[iID] if iID is not None else len(per)
         name = r[iK].split("(")[0].replace("void ", "").replace("sd::", "").replace("<unnamed>::", "")
-        t[(name, r[iG] if iG is not None else "")].append(v)
-    tot = sum(sum(v) for v in t.values())
+        key_of[lid] = (name, r[iG] if iG is not None else "")
+        per[lid][r[iM] if iM is not None else "gpu__time_duration.sum"] = v
+    t = collections.defaultdict(list)
+    for lid, m in per.items():
+        if "gpu__time_duration.sum" in m:
+            t[key_of[lid]].append(m)
+    tot = sum(m["gpu__time_duration.sum"] for v in t.values() for m in v)
+    has_dram = any("dram__bytes_read.sum" in m for v in t.values() for m in v)
     lines = [f"# ncu launch list ({path}): gpu__time_duration.sum per launch, cold-cache & serialised",
              f"# {sum(len(v) for v in t.values())} launches, {tot/1e6:.3f} ms total",
-             f"{'kernel':48s} {'grid':14s} {'n':>5s} {'avg_us':>10s} {'share':>7s}"]
-    for k, v in sorted(t.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"{k[0][:48]:48s} {k[1]:14s} {len(v):5d} {sum(v)/len(v)/1e3:10.2f} {sum(v)/tot*100:6.1f}%")
+             f"{'kernel':48s} {'grid':14s} {'n':>5s} {'avg_us':>10s} {'share':>7s}"
+             + (f" {'dram_rd_MB':>11s} {'dram_wr_MB':>11s}" if has_dram else "")]
+    for k, v in sorted(t.items(), key=lambda kv: -sum(m["gpu__time_duration.sum"] for m in kv[1])):
+        d = [m["gpu__time_duration.sum"] for m in v]
+        line = f"{k[0][:48]:48s} {k[1]:14s} {len(v):5d} {sum(d)/len(d)/1e3:10.2f} {sum(d)/tot*100:6.1f}%"
+        if has_dram:
+            rd = sum(m.get("dram__bytes_read.sum", 0) for m in v) / len(v)
+            wr = sum(m.get("dram__bytes_write.sum", 0) for m in v) / len(v)
+            line += f" {rd/1e6:11.1f} {wr/1e6:11.1f}"
+        lines.append(line)
     open(out, "w").write("\n".join(lines) + "\n")
 
 
