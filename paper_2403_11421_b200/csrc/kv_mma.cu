@@ -15,8 +15,10 @@
 //
 // Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
-// positions and each position row is copied to a 16-B padded pitch so the
-// eight ldmatrix row addresses of a warp fall in distinct bank groups.
+// positions copied two per bulk copy (the per-SM copy issue rate, not bytes,
+// limits row-sized copies) into pair slots with a 16-B pad; MMA row m holds
+// position 2m (m < 8) or 2(m-8)+1, so the eight ldmatrix row addresses of a
+// matrix fall in distinct bank groups.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -141,7 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + nst;
   uint8_t* ring = smem + 128 * ((16 * nst + 127) / 128);
-  const int pitch = a.stage_region / kT;  // padded bytes per position row
+  // stage region: kT/2 pair slots of two position rows + a 16-B pad; MMA row m
+  // holds position 2m (m < 8) or 2(m-8)+1, i.e. slot m & 7, row m >> 3
+  const int ppitch = 2 * a.g.pos_bytes + 16;
   // int8: [K rows][V rows][K scales kT x hc][V scales kT x hc]
   const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + (I8 ? 2 * a.sc_region : 0);
   const KvGeom& g = a.g;
@@ -173,7 +177,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const uint64_t pol = evict_first_policy();
     int stage = 0;
     uint32_t phase = 0;
-    const int t = lane & 15;
     for (int w = cb; w < ce; ++w) {
       const Piece pc = a.pieces[w];
       const int32_t* pt = g.page_table + static_cast<int64_t>(a.item_slot[pc.item]) * g.max_pages;
@@ -187,18 +190,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes + 2u * scb);
         }
         __syncwarp();
-        if (I8) {
-          // int8: two consecutive positions per copy (copy issue rate, not
-          // bytes, limits small rows); pair slots carry the 16-B pad
+        {
+          // two consecutive positions per copy (the per-SM bulk-copy issue
+          // rate, not bytes, limits row-sized copies); each pair slot carries
+          // a 16-B pad so the ldmatrix / 32-bit fragment rows are conflict-free
           const int pr = lane & 15;
           if (pr < 8 && 2 * pr < cnt) {
-            uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + pr * (2 * g.pos_bytes + 16);
+            uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + pr * ppitch;
             const uint32_t nb = (2 * pr + 1 < cnt ? 2u : 1u) * g.pos_bytes;
             bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + 2 * pr * g.pos_bytes, nb, &full[stage], pol);
           }
-        } else if (t < cnt) {
-          uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + t * pitch;
-          bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + t * g.pos_bytes, g.pos_bytes, &full[stage], pol);
         }
         if (I8 && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
           const uint8_t* lb = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes;
@@ -259,13 +260,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const uint8_t* st8 = ring + stage * stage_bytes;
       const uint32_t Ks = smem_u32(st8) + hk * kHD * (I8 ? 1 : 2);
       uint32_t Vs = Ks + a.stage_region;
-      int vpitch = pitch;
+      int vpitch = 0;  // 0: fp16 rows in the ring's pair slots; else the int8 scratch pitch
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (I8) {
         // MMA row m holds position 2m (m < 8) or 2(m-8)+1: rows gq and gq+8 of
         // this lane are the pair slot gq (conflict-free: slot pitch = 4 mod 32 words)
-        const int ppitch = 2 * g.pos_bytes + 16;
         const uint8_t* kb = st8 + hk * kHD + 4 * tq + gq * ppitch;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -303,13 +303,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         for (int kk = 0; kk < 8; ++kk) {
           uint32_t ka[4];
           // matrices: (pos 0-7, d 0-7), (pos 8-15, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 8-15)
-          ldsm_x4(Ks + (lr + 8 * (lm & 1)) * pitch + (16 * kk + 8 * (lm >> 1)) * 2, ka);
+          // matrix rows are MMA rows lr (+8): positions 2lr / 2lr+1 -> slot lr
+          ldsm_x4(Ks + lr * ppitch + (lm & 1) * g.pos_bytes + (16 * kk + 8 * (lm >> 1)) * 2, ka);
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
           mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
       }
       // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
-      const bool v0 = (I8 ? 2 * gq : gq) < cnt, v1 = (I8 ? 2 * gq + 1 : gq + 8) < cnt;
+      const bool v0 = 2 * gq < cnt, v1 = 2 * gq + 1 < cnt;
       if (!v0) s[0] = s[1] = -INFINITY;
       if (!v1) s[2] = s[3] = -INFINITY;
       float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
@@ -351,7 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       for (int mt = 0; mt < 8; ++mt) {
         uint32_t va[4];
         // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
-        ldsm_x4_t(Vs + (lr + 8 * (lm >> 1)) * vpitch + (16 * mt + 8 * (lm & 1)) * 2, va);
+        const int vrow = lr + 8 * (lm >> 1);  // MMA k row (position mapping as for K)
+        const uint32_t vaddr = vpitch ? Vs + vrow * vpitch : Vs + (vrow & 7) * ppitch + (vrow >> 3) * g.pos_bytes;
+        ldsm_x4_t(vaddr + (16 * mt + 8 * (lm & 1)) * 2, va);
         mma16816(o[mt], va, bh0, bh1);
         mma16816(o[mt], va, bl0, bl1);
       }
@@ -468,9 +471,8 @@ bool attention_mma_supported(const KvGeom& g, int G) {
 }
 
 size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages) {
-  const int pitch = g.pos_bytes + 16;
-  // fp16: kT rows at a 16-B padded pitch; int8: kT/2 pair slots (2 rows + 16 B)
-  *stage_region = g.fmt == SD_KV_INT8 ? (kT / 2) * (2 * g.pos_bytes + 16) : kT * pitch;
+  // kT/2 pair slots of two rows + a 16-B pad
+  *stage_region = (kT / 2) * (2 * g.pos_bytes + 16);
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
   const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0;
