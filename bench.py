@@ -186,19 +186,23 @@ def run_dist(args, wl, rank, world, dev, dist):
     steps_total = args.warmup + args.steps + args.e2e_steps + 8
     s_ranks = world if args.s_ranks == 0 else args.s_ranks
     seqs = list(range(1, B * world + 1))
-    plan = sd.dist_plan(world, rank, s_ranks, seqs)
+    mode = args.shard_mode
+    if mode != "sequence" and args.exchange != "p2p":
+        raise SystemExit("--shard-mode head/hybrid needs --exchange p2p")
+    plan = sd.dist_plan(world, rank, s_ranks, seqs, mode, Hkv)
+    h0, hc = (0, Hkv) if mode == "sequence" else sd.ShardMap(mode, Hkv, world).head_range(rank)
     mine = [seqs[i] for i in plan["shard_rows"]]
     nmax = torch.tensor([len(mine)], device=f"cuda:{dev}")
     dist.all_reduce(nmax, op=dist.ReduceOp.MAX)
     cap_seqs = int(nmax.item())
     is_s = s_ranks == world or rank == 0
     weights = sd.DeviceWeights(spec, None, dense, dev, seed=0) if is_s else None
-    kv = sd.KvShard(spec, 0, spec.num_kv_heads, cap_seqs * (ctx + steps_total), fmt, dev,
+    kv = sd.KvShard(spec, h0, hc, cap_seqs * (ctx + steps_total), fmt, dev,
                     max_sequences=cap_seqs, max_seq_len=ctx + steps_total + 16)
     kv.prefill_synthetic(mine, ctx, salt=rank)
     obj = [sd.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks)
+    eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks, shard_mode=mode)
     if args.exchange == "p2p":  # direct NVLink stores into the peers' receive buffers
         eng.enable_p2p(len(seqs))
     tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
@@ -255,8 +259,9 @@ def run_dist(args, wl, rank, world, dev, dist):
                    "layers": L, "model_dim": D, "heads": H, "kv_heads": Hkv, "mlp_dim": F, "vocab": V,
                    "batch_per_gpu": B, "global_batch": B * world, "context": ctx, "kv_format": fmt,
                    "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
-                   "parallelism": f"kv sharded by mix64(seq)%{world} (ShardMap by-sequence); "
-                                  f"{s_ranks} S-rank(s); per-layer Q/K/V->shard, O->S over "
+                   "parallelism": (f"kv sharded by mix64(seq)%{world} (ShardMap by-sequence); " if mode == "sequence"
+                                   else f"kv sharded {mode} over {Hkv} kv heads (ShardMap {mode}); ")
+                                  + f"{s_ranks} S-rank(s); per-layer Q/K/V->shard, O->S over "
                                   + ("NVLink peer stores (CUDA IPC)" if args.exchange == "p2p" else "NCCL send/recv"),
                    "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": "attention (rank 0)", "achieved": achieved,
@@ -442,6 +447,8 @@ def main():
                     help="N>1: S-workers (1 = the paper's single S-rank; 0 = every rank)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: per-layer activation exchange transport")
+    ap.add_argument("--shard-mode", default="sequence", choices=["sequence", "head", "hybrid"],
+                    help="N>1: ShardMap mode of the KV shards (head/hybrid need --exchange p2p)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

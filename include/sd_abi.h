@@ -251,8 +251,11 @@ int sd_drive_destroy(sd_drive_result* r);
 typedef struct sd_dist sd_dist;
 /* ncclGetUniqueId into `out` (NCCL_UNIQUE_ID_BYTES = 128 bytes) on one rank. */
 int sd_nccl_unique_id(void* out, size_t bytes);
+/* shard_mode (enum sd_shard_mode, over kv heads): BY_SEQUENCE (default,
+ * NCCL or peer exchange), BY_HEAD or HYBRID (peer exchange only); `kv` must
+ * hold this rank's head range (sd_shardmap_head_range). */
 int sd_dist_create(sd_weights* weights_or_null, sd_kv* kv, int rank, int world,
-                   const void* nccl_id, int s_ranks, sd_dist** out);
+                   const void* nccl_id, int s_ranks, int shard_mode, sd_dist** out);
 int sd_dist_destroy(sd_dist* d);
 int sd_dist_step(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens,
                  int32_t* next_tokens, float* final_x);
@@ -275,7 +278,7 @@ int sd_dist_p2p_setup(sd_dist* d, int32_t max_rows, void* handles_out);
 int sd_dist_p2p_connect(sd_dist* d, const void* all_handles);
 /* Host-only row plan of a step (CPU-testable): home rows grouped by shard,
  * shard rows grouped by source, per-peer counts. Arrays sized B / world. */
-int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs,
+int sd_dist_plan(int world, int rank, int s_ranks, int shard_mode, int heads, int32_t B, const uint64_t* seqs,
                  int32_t* home_rows, int32_t* n_home, int32_t* shard_rows, int32_t* n_shard,
                  int32_t* send_counts, int32_t* recv_counts);
 

@@ -128,7 +128,7 @@ SIGNATURES = {
     "sd_drive_wall_seconds": (C.c_double, [P]),
     "sd_drive_destroy": (C.c_int, [P]),
     "sd_nccl_unique_id": (C.c_int, [P, C.c_size_t]),
-    "sd_dist_create": (C.c_int, [P, P, C.c_int, C.c_int, P, C.c_int, PP]),
+    "sd_dist_create": (C.c_int, [P, P, C.c_int, C.c_int, P, C.c_int, C.c_int, PP]),
     "sd_dist_destroy": (C.c_int, [P]),
     "sd_dist_step": (C.c_int, [P, C.c_int32, U64P, I32P, I32P, FP]),
     "sd_dist_retire": (C.c_int, [P, C.c_int32, U64P]),
@@ -148,7 +148,7 @@ SIGNATURES = {
     "sd_plan_check_balance": (C.c_int, [C.POINTER(PerfProfileC), C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                         DP, DP, I32P]),
     "sd_dist_p2p_connect": (C.c_int, [P, P]),
-    "sd_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int32, U64P, I32P, I32P, I32P, I32P,
+    "sd_dist_plan": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int32, U64P, I32P, I32P, I32P, I32P,
                                I32P, I32P]),
     "sd_shardmap_worker_for": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, I32P]),
     "sd_shardmap_head_range": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, I32P, I32P]),

@@ -68,7 +68,7 @@ def _check(rc: int):
 
 FORMATS = {"single": 0, "half": 1, "int8": 2}
 DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2}
-SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2}
+SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2, "sequence": 0, "head": 1}
 
 
 def _f32(a) -> np.ndarray:
@@ -433,15 +433,17 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def dist_plan(world: int, rank: int, s_ranks: int, seqs):
-    """Host row plan of one distributed step (sd_dist_plan)."""
+def dist_plan(world: int, rank: int, s_ranks: int, seqs, shard_mode: str = "sequence", heads: int = 1):
+    """Host row plan of one distributed step (sd_dist_plan); `heads` are the
+    kv heads the ShardMap splits under by-head / hybrid sharding."""
     s, sp = _u64(seqs)
     B = len(s)
     home = np.zeros(max(B, 1), np.int32)
     shard = np.zeros(max(B, 1), np.int32)
     nh, ns = C.c_int32(), C.c_int32()
     sc, rc = np.zeros(world, np.int32), np.zeros(world, np.int32)
-    _check(lib.sd_dist_plan(world, rank, s_ranks, B, sp, home.ctypes.data_as(I32P), C.byref(nh),
+    _check(lib.sd_dist_plan(world, rank, s_ranks, SHARD_MODES[shard_mode], heads, B, sp,
+                            home.ctypes.data_as(I32P), C.byref(nh),
                             shard.ctypes.data_as(I32P), C.byref(ns), sc.ctypes.data_as(I32P),
                             rc.ctypes.data_as(I32P)))
     return {"home_rows": home[:nh.value].tolist(), "shard_rows": shard[:ns.value].tolist(),
@@ -455,13 +457,16 @@ class DistEngine:
     paper's topology); s_ranks = world: data-parallel S-workers."""
 
     def __init__(self, weights, kv: KvShard, rank: int, world: int, nccl_id: bytes | None,
-                 s_ranks: int = 1):
+                 s_ranks: int = 1, shard_mode: str = "sequence"):
+        """shard_mode: "sequence" (ShardMap by-sequence, the default), "head" or
+        "hybrid" (over kv heads; `kv` holds this rank's head range, see
+        ShardMap.head_range; needs enable_p2p before the first step)."""
         self.weights, self.kv, self.rank, self.world = weights, kv, rank, world
         self.spec = kv.spec
         self.h = C.c_void_p()
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
         _check(lib.sd_dist_create(weights.h if weights is not None else None, kv.h, rank, world,
-                                  idbuf, s_ranks, C.byref(self.h)))
+                                  idbuf, s_ranks, SHARD_MODES[shard_mode], C.byref(self.h)))
 
     def close(self):
         if getattr(self, "h", None):

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <string>
 
 namespace sd {
@@ -61,28 +62,61 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 void nccl_unique_id(ncclUniqueId* id) { nccl_check(Nccl::get().GetUniqueId(id), "ncclGetUniqueId"); }
 
-void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p) {
+void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p, int mode, int heads) {
+  if (mode == SD_SHARD_BY_SEQUENCE) {
+    p.hg = 1;
+    p.sg = world;
+  } else if (mode == SD_SHARD_BY_HEAD) {
+    if (world > heads) fail(SD_ERR_CONFIG, "by-head sharding cannot use more workers than heads");
+    p.hg = world;
+    p.sg = 1;
+  } else if (mode == SD_SHARD_HYBRID) {
+    p.hg = std::gcd(world, heads);
+    p.sg = world / p.hg;
+  } else {
+    fail(SD_ERR_CONFIG, "invalid shard mode");
+  }
+  p.mode = mode;
+  const size_t W = static_cast<size_t>(world);
+  p.head_start.assign(W, 0);
+  p.head_count.assign(W, heads);
+  for (int w = 0; w < world; ++w) {
+    if (mode == SD_SHARD_BY_SEQUENCE) continue;
+    const auto r = shard_head_range(mode, heads, world, w);
+    p.head_start[static_cast<size_t>(w)] = r.first;
+    p.head_count[static_cast<size_t>(w)] = r.second;
+  }
+  auto sg_of = [&](uint64_t seq) {
+    return p.sg == 1 ? 0 : static_cast<int>(mix64(seq) % static_cast<uint64_t>(p.sg));
+  };
   p.home_rows.clear();
   p.shard_rows.clear();
   p.shard_seqs.clear();
-  p.send_cnt.assign(static_cast<size_t>(world), 0);
-  p.send_off.assign(static_cast<size_t>(world), 0);
-  p.recv_cnt.assign(static_cast<size_t>(world), 0);
-  p.recv_off.assign(static_cast<size_t>(world), 0);
-  // home rows grouped by destination shard (batch order inside a group):
-  // send_layer's per-worker record filter (workers.cpp:336-351)
-  for (int d = 0; d < world; ++d) {
-    p.send_off[static_cast<size_t>(d)] = static_cast<int32_t>(p.home_rows.size());
+  p.send_cnt.assign(W, 0);
+  p.send_off.assign(W, 0);
+  p.recv_cnt.assign(W, 0);
+  p.recv_off.assign(W, 0);
+  // home rows grouped by sequence group (batch order inside a group); each
+  // worker of group sg receives the group's block with its head slice
+  std::vector<int32_t> blk_off(static_cast<size_t>(p.sg), 0), blk_cnt(static_cast<size_t>(p.sg), 0);
+  for (int g = 0; g < p.sg; ++g) {
+    blk_off[static_cast<size_t>(g)] = static_cast<int32_t>(p.home_rows.size());
     for (int i = 0; i < B; ++i) {
-      if (home_of(seqs[i], s_ranks) == rank && shard_of(seqs[i], world) == d) p.home_rows.push_back(i);
+      if (home_of(seqs[i], s_ranks) == rank && sg_of(seqs[i]) == g) p.home_rows.push_back(i);
     }
-    p.send_cnt[static_cast<size_t>(d)] = static_cast<int32_t>(p.home_rows.size()) - p.send_off[static_cast<size_t>(d)];
+    blk_cnt[static_cast<size_t>(g)] = static_cast<int32_t>(p.home_rows.size()) - blk_off[static_cast<size_t>(g)];
   }
-  // shard rows grouped by source S-rank, each group in that source's send order
+  for (int w = 0; w < world; ++w) {
+    p.send_off[static_cast<size_t>(w)] = blk_off[static_cast<size_t>(w % p.sg)];
+    p.send_cnt[static_cast<size_t>(w)] = blk_cnt[static_cast<size_t>(w % p.sg)];
+  }
+  // shard rows: this worker's sequence group from every source S-rank, each
+  // in that source's send order
+  const int my_sg = rank % p.sg;
   for (int src = 0; src < world; ++src) {
     p.recv_off[static_cast<size_t>(src)] = static_cast<int32_t>(p.shard_rows.size());
     for (int i = 0; i < B; ++i) {
-      if (home_of(seqs[i], s_ranks) == src && shard_of(seqs[i], world) == rank) {
+      if (home_of(seqs[i], s_ranks) == src && sg_of(seqs[i]) == my_sg) {
         p.shard_rows.push_back(i);
         p.shard_seqs.push_back(seqs[i]);
       }
@@ -91,15 +125,26 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
   }
 }
 
-DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks)
+DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks,
+                       int shard_mode)
     : spec_(kv->spec()), w_(w), kv_(kv), rank_(rank), world_(world), s_ranks_(s_ranks),
-      device_(kv->device()) {
+      device_(kv->device()), mode_(shard_mode) {
   if (world < 1 || rank < 0 || rank >= world) fail(SD_ERR_CONFIG, "bad rank / world");
   if (s_ranks != 1 && s_ranks != world) fail(SD_ERR_CONFIG, "s_ranks must be 1 or world");
   const bool s_rank = s_ranks == world || rank == 0;
   if (s_rank && !w) fail(SD_ERR_CONFIG, "an S-rank needs weights");
   if (w && w->device() != device_) fail(SD_ERR_CONFIG, "weights and KV store on different devices");
-  if (kv->width() != spec_.kv_width()) fail(SD_ERR_CONFIG, "R-shard must hold all kv heads (by-sequence)");
+  {
+    // the shard's kv-head range must be this worker's (ShardMap head_range)
+    DistPlan probe;
+    const uint64_t one = 1;
+    make_plan(world, rank, s_ranks, 1, &one, probe, shard_mode, spec_.Hkv);
+    const int h0 = probe.head_start[static_cast<size_t>(rank)], hc = probe.head_count[static_cast<size_t>(rank)];
+    if (kv->head_start() != h0 || kv->width() != hc * spec_.hd) {
+      fail(SD_ERR_CONFIG, "R-shard must hold kv heads [" + std::to_string(h0) + ", " + std::to_string(h0 + hc) +
+                              ") for this shard mode and rank");
+    }
+  }
   DeviceGuard dg(device_);
   SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   if (world > 1) {
@@ -168,8 +213,11 @@ void DistEngine::ensure(int B) {
 
 void DistEngine::plan_for(int B, const uint64_t* seqs) {
   if (plan_key_.size() == static_cast<size_t>(B) && std::equal(plan_key_.begin(), plan_key_.end(), seqs)) return;
-  make_plan(world_, rank_, s_ranks_, B, seqs, plan_);
+  make_plan(world_, rank_, s_ranks_, B, seqs, plan_, mode_, spec_.Hkv);
   plan_key_.assign(seqs, seqs + B);
+  if (mode_ != SD_SHARD_BY_SEQUENCE && !p2p_) {
+    fail(SD_ERR_CONFIG, "by-head / hybrid sharding needs the peer exchange (sd_dist_p2p_connect)");
+  }
   if (p2p_) {
     // where this rank's rows land in each peer's receive buffers (every rank
     // derives every plan from the same batch)
@@ -177,7 +225,7 @@ void DistEngine::plan_for(int B, const uint64_t* seqs) {
     peer_o_off_.assign(static_cast<size_t>(world_), 0);
     DistPlan q;
     for (int d = 0; d < world_; ++d) {
-      make_plan(world_, d, s_ranks_, B, seqs, q);
+      make_plan(world_, d, s_ranks_, B, seqs, q, mode_, spec_.Hkv);
       peer_qkv_off_[static_cast<size_t>(d)] = q.recv_off[static_cast<size_t>(rank_)];
       peer_o_off_[static_cast<size_t>(d)] = q.send_off[static_cast<size_t>(rank_)];
       if (static_cast<int>(q.home_rows.size()) > p2p_cap_ || static_cast<int>(q.shard_rows.size()) > p2p_cap_) {
@@ -248,12 +296,9 @@ void DistEngine::exchange_p2p(int kind) {
     SD_CUDA(cudaEventCreate(&e1));
     SD_CUDA(cudaEventRecord(e0, stream_));
   }
-  const int width = kind == 0 ? spec_.qkv_width() : spec_.D;
+  const int hd = spec_.hd, G = spec_.H / spec_.Hkv, D = spec_.D, kvw = spec_.kv_width();
+  const int my_hc = plan_.head_count[static_cast<size_t>(rank_)], my_h0 = plan_.head_start[static_cast<size_t>(rank_)];
   P2PScatter a{};
-  a.src = kind == 0 ? qkv_h_ : o_s_;
-  a.src_stride = width;
-  a.dst_stride = width;
-  a.width = width;
   a.world = world_;
   a.self = rank_;
   a.slot = kind;
@@ -262,18 +307,38 @@ void DistEngine::exchange_p2p(int kind) {
   const std::vector<int32_t>& sc = kind == 0 ? plan_.send_cnt : plan_.recv_cnt;
   const std::vector<int32_t>& so = kind == 0 ? plan_.send_off : plan_.recv_off;
   const std::vector<int32_t>& rc = kind == 0 ? plan_.recv_cnt : plan_.send_cnt;
+  // kind 0: home rows (full q|k|v width) -> each worker's head slice packed
+  //         as [q slice | k slice | v slice];
+  // kind 1: shard rows (this worker's o slice) -> the home rows' o columns
+  a.src = kind == 0 ? qkv_h_ : o_s_;
+  a.src_stride = kind == 0 ? spec_.qkv_width() : static_cast<int64_t>(my_hc) * G * hd;
   double bytes = 0;
   uint32_t expect = 0;
   for (int d = 0; d < world_; ++d) {
     const size_t u = static_cast<size_t>(d);
+    const int h0 = plan_.head_start[u], hc = plan_.head_count[u];
     a.cnt[d] = sc[u];
     a.src_off[d] = so[u];
     a.dst_off[d] = kind == 0 ? peer_qkv_off_[u] : peer_o_off_[u];
     a.dst[d] = kind == 0 ? peer_qkv_[d] : peer_o_[d];
     a.flag[d] = peer_flags_[d];
+    if (kind == 0) {
+      const int qw = hc * G * hd, kw = hc * hd;
+      a.dst_stride[d] = qw + 2 * kw;
+      a.nseg[d] = 3;
+      a.seg_src[d][0] = h0 * G * hd, a.seg_dst[d][0] = 0, a.seg_n[d][0] = qw;
+      a.seg_src[d][1] = D + h0 * hd, a.seg_dst[d][1] = qw, a.seg_n[d][1] = kw;
+      a.seg_src[d][2] = D + kvw + h0 * hd, a.seg_dst[d][2] = qw + kw, a.seg_n[d][2] = kw;
+    } else {
+      a.dst_stride[d] = D;
+      a.nseg[d] = 1;
+      a.seg_src[d][0] = 0, a.seg_dst[d][0] = my_h0 * G * hd, a.seg_n[d][0] = my_hc * G * hd;
+    }
     if (d != rank_ && sc[u] > 0) {
       a.notify |= 1u << d;
-      bytes += static_cast<double>(sc[u]) * width * 4;
+      int w = 0;
+      for (int q = 0; q < a.nseg[d]; ++q) w += a.seg_n[d][q];
+      bytes += static_cast<double>(sc[u]) * w * 4;
     }
     if (d != rank_ && rc[u] > 0) expect |= 1u << d;
   }
@@ -358,6 +423,10 @@ void DistEngine::run_step() {
     if (nh) w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
     float* qkv_s = p2p_ ? rx_qkv_ : qkv_s_;
     float* o_h = p2p_ ? rx_o_ : o_h_;
+    // this worker's head slice of a shard row: [q | k | v] (full width when by-sequence)
+    const int G = s.H / s.Hkv;
+    const int hc = plan_.head_count[static_cast<size_t>(rank_)];
+    const int sq = hc * G * s.hd, sk = hc * s.hd, srow = p2p_ ? sq + 2 * sk : qkvw;
     if (p2p_) {
       exchange_p2p(0);
     } else {
@@ -367,8 +436,8 @@ void DistEngine::run_step() {
       for (int i = 0; i < ns; ++i) {
         pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
       }
-      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + D, qkvw, qkv_s + D + kvw, qkvw, stream_);
-      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, qkvw, o_s_, D, stream_);
+      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + sq, srow, qkv_s + sq + sk, srow, stream_);
+      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, srow, o_s_, p2p_ ? sq : D, stream_);
     }
     if (p2p_) {
       exchange_p2p(1);

@@ -26,24 +26,38 @@ inline int shard_of(uint64_t seq, int world) {
 }
 
 // Row plan of one step, identical on every rank (computed from the batch).
+// ShardMap modes (transport.cpp:319-380): worker w = hg * SG + sg holds the
+// kv heads of head group hg for the sequences of sequence group
+// sg = mix64(seq) % SG. By-sequence: HG = 1, SG = world (the default); by
+// head: HG = world, SG = 1; hybrid: HG = gcd(world, heads), SG = world / HG.
+// Home rows are ordered by sg, so the rows a worker receives from an S-rank
+// are one contiguous block (send_layer's per-worker filter, workers.cpp:336-351).
 struct DistPlan {
-  std::vector<int32_t> home_rows;   // batch rows this rank runs the S-Part for, grouped by shard
-  std::vector<int32_t> send_cnt, send_off;
+  int mode = 0, hg = 1, sg = 1;     // shard mode, head groups, sequence groups
+  std::vector<int32_t> home_rows;   // batch rows this rank runs the S-Part for, grouped by seq group
+  std::vector<int32_t> send_cnt, send_off;  // per destination worker: block of home rows
   std::vector<int32_t> shard_rows;  // batch rows whose KV lives here, grouped by source S-rank
   std::vector<int32_t> recv_cnt, recv_off;
   std::vector<uint64_t> shard_seqs;
+  std::vector<int32_t> head_start, head_count;  // per worker, in (kv) heads
 };
-void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p);
+void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p, int mode = 0,
+               int heads = 1);
 void nccl_unique_id(ncclUniqueId* id);
 
 class DistEngine : public StepComputation {
  public:
-  DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks);
+  // shard_mode: SD_SHARD_BY_SEQUENCE (default), _BY_HEAD or _HYBRID over kv
+  // heads; the KV store must hold this rank's head range (by-head / hybrid
+  // need the peer exchange)
+  DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks,
+             int shard_mode = 0);
   ~DistEngine() override;
   void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
                float* final_x) override;
   void retire(int n, const uint64_t* seqs) override;
   bool owns(uint64_t seq) const override { return home_of(seq, s_ranks_) == rank_; }
+  int shard_mode() const { return mode_; }
   int model_dim() const override { return spec_.D; }
   int vocab() const override { return spec_.V; }
   // device-timed loop of `steps` steps over a fixed batch; tokens fed back on device
@@ -70,7 +84,7 @@ class DistEngine : public StepComputation {
   Spec spec_;
   Weights* w_;
   KvStore* kv_;
-  int rank_, world_, s_ranks_, device_;
+  int rank_, world_, s_ranks_, device_, mode_ = 0;
   ncclComm_t comm_ = nullptr;
   cudaStream_t stream_ = nullptr;
   DistPlan plan_;

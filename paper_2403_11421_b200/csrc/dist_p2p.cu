@@ -22,24 +22,35 @@ __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t* p) {
   return v;
 }
 
-// grid-stride over (row, 16-B chunk) of every destination's row range
+// grid-stride over (destination, row, 16-B chunk of the row's segments)
 __global__ void p2p_scatter_kernel(const P2PScatter a) {
   pdl_trigger();
   pdl_wait();
-  const int vec = a.width / 4;  // float4 per row
   int64_t total = 0;
-  for (int d = 0; d < a.world; ++d) total += static_cast<int64_t>(a.cnt[d]) * vec;
+  int vrow[kMaxWorld];
+  for (int d = 0; d < a.world; ++d) {
+    vrow[d] = 0;
+    for (int q = 0; q < a.nseg[d]; ++q) vrow[d] += a.seg_n[d][q] / 4;
+    total += static_cast<int64_t>(a.cnt[d]) * vrow[d];
+  }
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    int64_t r = i / vec;
-    const int c = static_cast<int>(i - r * vec);
+    int64_t rem = i;
     int d = 0;
-    while (r >= a.cnt[d]) {
-      r -= a.cnt[d];
+    while (rem >= static_cast<int64_t>(a.cnt[d]) * vrow[d]) {
+      rem -= static_cast<int64_t>(a.cnt[d]) * vrow[d];
       ++d;
     }
-    const float4 v = reinterpret_cast<const float4*>(a.src + (a.src_off[d] + r) * a.src_stride)[c];
-    reinterpret_cast<float4*>(a.dst[d] + (a.dst_off[d] + r) * a.dst_stride)[c] = v;
+    const int64_t r = rem / vrow[d];
+    int c = static_cast<int>(rem - r * vrow[d]);
+    int q = 0;
+    while (c >= a.seg_n[d][q] / 4) {
+      c -= a.seg_n[d][q] / 4;
+      ++q;
+    }
+    const float4 v =
+        reinterpret_cast<const float4*>(a.src + (a.src_off[d] + r) * a.src_stride + a.seg_src[d][q])[c];
+    reinterpret_cast<float4*>(a.dst[d] + (a.dst_off[d] + r) * a.dst_stride[d] + a.seg_dst[d][q])[c] = v;
   }
   // last block publishes: all of this rank's stores to every peer are
   // visible system-wide before the epoch flag
@@ -75,9 +86,17 @@ __global__ void p2p_wait_kernel(const int64_t* flags, int slot, uint32_t expect,
 }  // namespace
 
 void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s) {
-  int64_t rows = 0;
-  for (int d = 0; d < a.world; ++d) rows += a.cnt[d];
-  const int64_t work = rows * (a.width / 4);
+  int64_t work = 0;
+  for (int d = 0; d < a.world; ++d) {
+    int w = 0;
+    for (int q = 0; q < a.nseg[d]; ++q) {
+      if (a.seg_n[d][q] % 4 || a.seg_src[d][q] % 4 || a.seg_dst[d][q] % 4) {
+        fail(SD_ERR_CONFIG, "peer exchange: row segments must be multiples of 4 floats");
+      }
+      w += a.seg_n[d][q] / 4;
+    }
+    work += static_cast<int64_t>(a.cnt[d]) * w;
+  }
   int grid = static_cast<int>(std::min<int64_t>(264, (work + 255) / 256));
   if (grid < 1) grid = 1;
   SD_CUDA(launch_pdl(p2p_scatter_kernel, dim3(grid), dim3(256), 0, s, 1, a));

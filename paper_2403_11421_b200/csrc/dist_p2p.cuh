@@ -10,18 +10,23 @@ namespace sd {
 
 constexpr int kMaxWorld = 8;
 
-// One exchange: rows [src_off[d], +cnt[d]) of `src` go to rows
-// [dst_off[d], +cnt[d]) of rank d's buffer dst[d] (a peer mapping, or this
-// rank's own buffer for d == self); then flag[d][slot][self] = epoch for
-// every d in `notify`.
+// One exchange: for every destination rank d, rows [src_off[d], +cnt[d]) of
+// `src` go to rows [dst_off[d], +cnt[d]) of rank d's buffer dst[d] (a peer
+// mapping, or this rank's own buffer for d == self). A row's payload is up
+// to three column segments (src column, dst column, width; multiples of 4
+// floats): the full Q/K/V row under by-sequence sharding, a worker's head
+// slices [q | k | v] under by-head / hybrid, an o slice on the way back.
+// Then flag[d][slot][self] = epoch for every d in `notify`.
 struct P2PScatter {
   const float* src;
-  int64_t src_stride, dst_stride;  // floats
-  int width;                       // floats per row (multiple of 4)
+  int64_t src_stride;  // floats
   int world, self, slot;
   int64_t epoch;
   uint32_t notify;
   int32_t cnt[kMaxWorld], src_off[kMaxWorld], dst_off[kMaxWorld];
+  int64_t dst_stride[kMaxWorld];
+  int32_t nseg[kMaxWorld];
+  int32_t seg_src[kMaxWorld][3], seg_dst[kMaxWorld][3], seg_n[kMaxWorld][3];
   float* dst[kMaxWorld];
   int64_t* flag[kMaxWorld];  // each rank's flag array [2 slots][kMaxWorld sources]
   int32_t* done;             // block-arrival counter (this rank), zero between launches

@@ -25,6 +25,7 @@ class KvStore {
 
   // ---- reference queries (attention.hpp:73-111)
   int width() const { return geom_.width; }
+  int head_start() const { return head_start_; }
   int q_width() const { return geom_.width * G_; }
   int group_size() const { return G_; }
   int64_t capacity() const { return cap_; }

@@ -567,14 +567,14 @@ int sd_nccl_unique_id(void* out, size_t bytes) {
 }
 
 int sd_dist_create(sd_weights* w, sd_kv* kv, int rank, int world, const void* nccl_id, int s_ranks,
-                   sd_dist** out) {
+                   int shard_mode, sd_dist** out) {
   return guard([&] {
     need(kv, "kv");
     need(out, "out");
     if (world > 1) need(nccl_id, "nccl_id");
     auto h = std::make_unique<sd_dist>();
     h->d = std::make_unique<sd::DistEngine>(w ? w->w.get() : nullptr, kv->s.get(), rank, world, nccl_id,
-                                            s_ranks);
+                                            s_ranks, shard_mode);
     *out = h.release();
   });
 }
@@ -652,13 +652,13 @@ int sd_dist_p2p_connect(sd_dist* d, const void* all_handles) {
   });
 }
 
-int sd_dist_plan(int world, int rank, int s_ranks, int32_t B, const uint64_t* seqs, int32_t* home_rows,
-                 int32_t* n_home, int32_t* shard_rows, int32_t* n_shard, int32_t* send_counts,
+int sd_dist_plan(int world, int rank, int s_ranks, int shard_mode, int heads, int32_t B, const uint64_t* seqs,
+                 int32_t* home_rows, int32_t* n_home, int32_t* shard_rows, int32_t* n_shard, int32_t* send_counts,
                  int32_t* recv_counts) {
   return guard([&] {
     if (world < 1 || rank < 0 || rank >= world) sd::fail(SD_ERR_CONFIG, "bad rank / world");
     sd::DistPlan p;
-    sd::make_plan(world, rank, s_ranks, B, seqs, p);
+    sd::make_plan(world, rank, s_ranks, B, seqs, p, shard_mode, heads);
     if (n_home) *n_home = static_cast<int32_t>(p.home_rows.size());
     if (n_shard) *n_shard = static_cast<int32_t>(p.shard_rows.size());
     if (home_rows) std::copy(p.home_rows.begin(), p.home_rows.end(), home_rows);

@@ -46,6 +46,51 @@ def test_plan_partitions_rows_and_follows_shardmap(oracle, world, s_mode):
             assert sent == got
 
 
+@pytest.mark.parametrize("mode,world,heads", [("head", 2, 8), ("head", 4, 8), ("head", 8, 8), ("head", 3, 8),
+                                              ("hybrid", 4, 2), ("hybrid", 8, 4), ("hybrid", 6, 4),
+                                              ("hybrid", 2, 3)])
+@pytest.mark.parametrize("s_mode", ["single", "all"])
+def test_plan_head_and_hybrid_sharding(oracle, mode, world, heads, s_mode):
+    """By-head / hybrid ShardMap on the data path: worker w holds the kv heads
+    of its head group for the sequences of its sequence group; every (row,
+    head group) is attended exactly once, by the worker the reference's
+    ShardMap names (transport.cpp:345-380), and each worker receives an
+    S-rank's rows in that S-rank's send order."""
+    import paper_2403_11421_b200 as sd
+    s_ranks = 1 if s_mode == "single" else world
+    rng = np.random.default_rng(world * 10 + heads)
+    seqs = [int(x) for x in rng.choice(10**6, size=61, replace=False) + 1]
+    plans = [sd.dist_plan(world, r, s_ranks, seqs, mode, heads) for r in range(world)]
+    name = "by-head" if mode == "head" else "hybrid"
+    sm = sd.ShardMap(name, heads, world)
+    ranges = [sm.head_range(w) for w in range(world)]
+    assert sorted(i for p in plans for i in p["home_rows"]) == list(range(len(seqs)))
+    # per head group, the shard rows partition the batch
+    groups = {}
+    for w, (h0, hc) in enumerate(ranges):
+        groups.setdefault((h0, hc), []).append(w)
+    for (h0, hc), ws in groups.items():
+        rows = sorted(i for w in ws for i in plans[w]["shard_rows"])
+        assert rows == list(range(len(seqs)))
+        for w in ws:
+            for i in plans[w]["shard_rows"]:
+                assert oracle.shardmap_worker_for(name, heads, world, seqs[i], h0) == w
+    for r in range(world):
+        for d in range(world):
+            assert plans[r]["send_counts"][d] == plans[d]["recv_counts"][r]
+            off_r = np.cumsum([0] + plans[d]["recv_counts"])
+            got = plans[d]["shard_rows"][off_r[r]:off_r[r + 1]]
+            sent = [i for i in plans[r]["home_rows"]
+                    if oracle.shardmap_worker_for(name, heads, world, seqs[i], ranges[d][0]) == d]
+            assert got == sent
+
+
+def test_plan_head_mode_rejects_more_workers_than_heads():
+    import paper_2403_11421_b200 as sd
+    with pytest.raises(sd.ConfigError):
+        sd.dist_plan(4, 0, 4, [1, 2, 3], "head", 2)
+
+
 def _gloo_worker(rank, world, port, s_ranks, out_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl"):
+def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -45,8 +45,12 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl"):
     is_s = s_ranks == world or rank == 0
     dw = upload_oracle_weights(W, "exact", device=rank) if is_s else None
     spec = sd.make_model_spec(2, 64, 4, 256, 128)
-    kv = sd.KvShard(spec, 0, 4, 1 << 16, "single", rank)
-    eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks)
+    if shard_mode == "sequence":
+        h0, hc = 0, 4
+    else:
+        h0, hc = sd.ShardMap(shard_mode, 4, world).head_range(rank)
+    kv = sd.KvShard(spec, h0, hc, 1 << 16, "single", rank)
+    eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks, shard_mode=shard_mode)
     if exchange == "p2p":
         eng.enable_p2p(64)
     recs, acts, _ = sd.run_generation(eng, *cfg, seed=0, record_activations=True)
@@ -63,13 +67,16 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl"):
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("s_ranks", [1, 2])
 @pytest.mark.parametrize("cfg", [(8, 32, 32, 32), (8, 16, 4, 48)], ids=["batch", "stabilized"])
-@pytest.mark.parametrize("exchange", ["nccl", "p2p"])
-def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, exchange):
+@pytest.mark.parametrize("exchange,shard_mode", [("nccl", "sequence"), ("p2p", "sequence"), ("p2p", "head")])
+def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, exchange, shard_mode):
     """`exchange`: NCCL grouped send/recv, or direct NVLink stores into the
-    peers' receive buffers with epoch flags (dist_p2p.cu)."""
+    peers' receive buffers with epoch flags (dist_p2p.cu). `shard_mode`
+    "head": each rank attends every sequence for its half of the heads
+    (ShardMap by-head, transport.cpp:345-380) and the o slices are gathered
+    back into the S-rank's rows."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode), nprocs=2, join=True)
     rows = pickle.load(open(out, "rb"))
     W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 128), 0)
     orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
