@@ -133,7 +133,10 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
-constexpr int kVPitch = kHD * 2 + 16;  // bytes per row of a warp's dequantized V tile
+constexpr int kVPitch = kHD * 2 + 16;
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}  // bytes per row of a warp's dequantized V tile
 
 template <int G, int FMT>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
+      mbar_init(&empty[s], g.hc);  // the hc warps of the stage's position class
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -169,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
   const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
+  // softmax-state merge slots (hc < 8): after the ring and the int8 V scratch
+  float* mrg = reinterpret_cast<float*>(ring + nst * stage_bytes + (I8 ? kWarps * kT * kVPitch : 0));
 
   if (warp == kWarps) {
     // producer warp: lane 0 arms the stage barrier, then lanes 0-15 copy the
@@ -184,7 +189,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         const int cnt = min(kT, pc.p1 - pos);
         const uint8_t* base = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes +
                               static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
-        const uint32_t scb = I8 ? static_cast<uint32_t>(cnt * g.hc * 4) : 0u;
+        // scale block rounded up to the bulk-copy granule (16 B): stages start
+        // 16-aligned in a page group, so the extra scales stay inside its region
+        const uint32_t scb = I8 ? (static_cast<uint32_t>(cnt * g.hc * 4) + 15u) & ~15u : 0u;
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes + 2u * scb);
@@ -217,8 +224,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   }
 
   // ---------------------------------------------------------------- consumer
-  // warp = kv head; fragment coordinates: gq = lane/4 (row group), tq = lane%4
-  const int hk = warp;
+  // warp = (kv head, position class): with hc < 8 kv heads per shard the
+  // P = 8/hc warps of a head take every P-th stage and merge their softmax
+  // states at the end of a piece. fragment coordinates: gq = lane/4, tq = lane%4
+  const int P = kWarps / g.hc;
+  const int hk = warp % g.hc, cls = warp / g.hc;
+  int jst = 0;  // stage sequence number (same order as the producer)
   const int gq = lane >> 2, tq = lane & 3;
   const int Hq = g.hc * G;
   float o[8][4];      // O^T fragments: hd rows 16*mt + {gq, gq+8}, heads {2tq, 2tq+1}
@@ -253,7 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     m[0] = m[1] = -INFINITY;
     l[0] = l[1] = 0.0f;
 
-    for (int pos = pc.p0; pos < pc.p1; pos += kT) {
+    for (int pos = pc.p0; pos < pc.p1; pos += kT, ++jst) {
+      if (P > 1 && jst % P != cls) {  // another class's stage (warp-uniform)
+        if (++stage == nst) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
       const int cnt = min(kT, pc.p1 - pos);
       mbar_wait(&full[stage], phase);
       __syncwarp();
@@ -372,6 +390,42 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], sh);
       l[1] += __shfl_xor_sync(0xffffffffu, l[1], sh);
     }
+    if (P > 1) {
+      // merge the P position classes of this head into class 0 (same
+      // fragment layout in every warp: elementwise per lane)
+      float* mine = mrg + (warp * 32 + lane) * 36;
+      if (cls > 0) {
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) mine[4 * mt + i] = o[mt][i];
+        mine[32] = m[0];
+        mine[33] = m[1];
+        mine[34] = l[0];
+        mine[35] = l[1];
+      }
+      named_bar(1 + hk, P * 32);
+      if (cls == 0) {
+        for (int c = 1; c < P; ++c) {
+          const float* th = mrg + ((hk + c * g.hc) * 32 + lane) * 36;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float mn = fmaxf(m[j], th[32 + j]);
+            const float a0 = m[j] == -INFINITY ? 0.0f : fast_exp2(m[j] - mn);
+            const float a1 = th[32 + j] == -INFINITY ? 0.0f : fast_exp2(th[32 + j] - mn);
+            l[j] = l[j] * a0 + th[34 + j] * a1;
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+              o[mt][j] = o[mt][j] * a0 + th[4 * mt + j] * a1;
+              o[mt][2 + j] = o[mt][2 + j] * a0 + th[4 * mt + 2 + j] * a1;
+            }
+            m[j] = mn;
+          }
+        }
+      }
+      named_bar(1 + hk, P * 32);  // class slots free for the next piece
+      if (cls != 0) continue;
+    }
     const bool direct = pc.flags & 1;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -466,8 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 }  // namespace
 
 bool attention_mma_supported(const KvGeom& g, int G) {
-  return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD && g.hc == kWarps &&
-         (G == 2 || G == 4 || G == 8) && g.P % kT == 0;
+  return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD &&
+         (g.hc == 8 || g.hc == 4 || g.hc == 2 || g.hc == 1) && (G == 2 || G == 4 || G == 8) && g.P % kT == 0;
 }
 
 size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages) {
@@ -475,7 +529,8 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   *stage_region = (kT / 2) * (2 * g.pos_bytes + 16);
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
-  const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0;
+  const size_t scratch = (g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0) +
+                         (g.hc < kWarps ? static_cast<size_t>(kWarps) * 32 * 36 * 4 : 0);  // merge slots
   *nstages = 5;
   while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
   return 128 + *nstages * stage + scratch;

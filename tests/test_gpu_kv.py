@@ -181,6 +181,35 @@ def test_many_sequences_split_and_combine(sd, oracle):
 
 
 @pytest.mark.parametrize("fmt", ["half", "int8"])
+@pytest.mark.parametrize("h0,hc", [(4, 4), (2, 2), (7, 1)])
+def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc):
+    """Shards holding 4 / 2 / 1 of 8 kv heads (by-head / hybrid ShardMap):
+    the tensor-core kernel splits each head's stages over 8/hc warps and
+    merges their softmax states per piece."""
+    G = 4
+    H, D = 8 * G, 8 * G * 128
+    s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
+    B, Lmax = 24, 500
+    gpu = sd.KvShard(s, h0, hc, B * Lmax, fmt)
+    cpu = oracle.KvShard(os_, h0, hc, B * Lmax, fmt)
+    rng = _rng(100 + hc)
+    lens = rng.integers(1, Lmax, B)
+    lens[0], lens[1], lens[2] = 1, 17, 33
+    seqs = list(range(1, B + 1))
+    w = hc * 128
+    for pos in range(int(lens.max())):
+        act = [i for i in range(B) if lens[i] > pos]
+        k = rng.uniform(-1, 1, (len(act), w)).astype(np.float32)
+        v = rng.uniform(-1, 1, (len(act), w)).astype(np.float32)
+        ids = [seqs[i] for i in act]
+        gpu.append_request(0, ids, [pos] * len(act), k, v)
+        cpu.append_request(0, ids, [pos] * len(act), k, v)
+    q = rng.uniform(-3, 3, (B, w * G)).astype(np.float32)
+    err = float(np.abs(gpu.attend(0, seqs, q) - cpu.attend(0, seqs, q)).max())
+    assert err < 2e-5, err
+
+
+@pytest.mark.parametrize("fmt", ["half", "int8"])
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt):
     """fp16 / int8 KV, hd 128, 8 kv heads: the mma.sync attention path
