@@ -51,6 +51,20 @@ struct GemmArgs {
 };
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);
+
+// The GEMMs between two attentions (W_o, MLP-in, MLP-out, next QKV / head)
+// as one persistent launch with per-(GEMM, row block) completion counters
+// (gemm_sm100.cu). bf16, equal M >= 256. `done` holds kChainMax x 64 counters
+// zeroed at the start of the step; `epoch` = chain launches since then.
+struct ChainArgs {
+  int n;
+  GemmArgs g[4];
+  unsigned long long* done;
+  unsigned long long epoch;
+  int max_ctas;
+};
+bool gemm_chain_supported(const ChainArgs& c);
+void launch_gemm_chain(const ChainArgs& c, cudaStream_t s);
 // argmax over rows of C fused as a second pass (kept separate: logits stay in HBM for callers)
 
 }  // namespace sd

@@ -214,10 +214,19 @@ void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
     if (yb) launch_to_bf16(B, out, y, ldy, yb, ldyb, s);
     return;
   }
+  const GemmArgs g = gemm_args(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, max_ctas);
+  launch_gemm_sm100(g, s);
+}
+
+GemmArgs Weights::gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
+                            int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+                            const float* res, int64_t ldr, int max_ctas) const {
+  if (mode_ == SD_DENSE_EXACT_F32) fail(SD_ERR_INTERNAL, "gemm_args: exact mode has no tensor-core GEMM");
+  if (which != 7 && (layer < 0 || layer >= spec_.L)) fail(SD_ERR_CONFIG, "layer out of range");
   GemmArgs g{};
   g.M = B;
-  g.N = out;
-  g.K = in;
+  g.N = out_dim(which);
+  g.K = in_dim(which);
   g.kind = mode_;
   if (mode_ == SD_DENSE_BF16) {
     if (!xb) fail(SD_ERR_INTERNAL, "bf16 GEMM needs a bf16 A operand");
@@ -227,8 +236,8 @@ void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
     g.A = x;
     g.lda = ldx;
   }
-  g.B = W;
-  g.ldb = in;
+  g.B = tensor(layer, which);
+  g.ldb = g.K;
   g.C = y;
   g.ldc = ldy;
   g.Cb = yb;
@@ -238,7 +247,7 @@ void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
   g.ldr = ldr;
   g.max_ctas = max_ctas;
   if (!gemm_sm100_supported(g)) fail(SD_ERR_CONFIG, "shape not supported by the tcgen05 GEMM");
-  launch_gemm_sm100(g, s);
+  return g;
 }
 
 // ============================================================= scheduler ===

@@ -35,6 +35,10 @@ class Weights {
   // y[B][out] = x . W^T (+ epilogue). which: 0 = qkv (fused), 4 = w_o,
   // 5 = w_mlp_in, 6 = w_mlp_out, 7 = head, 1/2/3 = q/k/v slices.
   // x_bf16 is required in BF16 mode (A operand), ignored otherwise.
+  // the tensor-core GEMM of linear() without launching it (chained S-Part)
+  GemmArgs gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
+                     int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+                     const float* res, int64_t ldr, int max_ctas = 0) const;
   void linear(int layer, int which, int B, const float* x, int64_t ldx,
               const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
               int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s,
@@ -115,6 +119,11 @@ class Engine : public StepComputation {
   void ensure(Group& g, int n);
   void free_group(Group& g);
   void run(int ng, bool embed);
+  void chain(const ChainArgs& c);
+  static constexpr int kChainCounters = 4 * 64;
+  unsigned long long* chain_done_ = nullptr;
+  unsigned long long chain_epoch_ = 0;
+  bool chain_on_ = true;
   void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
             int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
             const float* res, int64_t ldr);

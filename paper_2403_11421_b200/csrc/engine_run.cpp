@@ -32,6 +32,13 @@ Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_s, cudaEventDisableTiming));
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_r, cudaEventDisableTiming));
   }
+  // opt-in (SD_CHAIN=1): bitwise equal to the separate launches and faster
+  // when per-kernel timing events sit between them, but not end to end,
+  // where programmatic dependent launch already hides the launch/prologue cost
+  chain_on_ = std::getenv("SD_CHAIN") != nullptr;
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&chain_done_), kChainCounters * sizeof(unsigned long long)));
+  SD_CUDA(cudaMemset(chain_done_, 0, kChainCounters * sizeof(unsigned long long)));
+  SD_CUDA(cudaDeviceSynchronize());
 }
 
 void Engine::free_group(Group& g) {
@@ -61,6 +68,7 @@ Engine::~Engine() {
     cudaEventDestroy(e.second);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (chain_done_) cudaFree(chain_done_);
   cudaStreamDestroy(stream_);
   cudaStreamDestroy(stream_r_);
 }
@@ -157,6 +165,29 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
   }
 }
 
+void Engine::chain(const ChainArgs& c) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing_) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (ev_pool_.empty()) {
+        SD_CUDA(cudaEventCreate(e));
+      } else {
+        *e = ev_pool_.back();
+        ev_pool_.pop_back();
+      }
+    }
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  launch_gemm_chain(c, stream_);
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    double f = 0;
+    for (int i = 0; i < c.n; ++i) f += 2.0 * c.g[i].M * c.g[i].N * c.g[i].K;
+    ev_flops_.push_back(f);
+  }
+}
+
 void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool reset) {
   for (size_t i = 0; i < ev_.size(); ++i) {
     SD_CUDA(cudaEventSynchronize(ev_[i].second));
@@ -189,6 +220,10 @@ void Engine::run(int ng, bool embed) {
   const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
   const bool bf = w_->mode() == SD_DENSE_BF16;
   cudaStream_t rs = pipeline_ ? stream_r_ : stream_;
+  // chain counters restart every step (ChainArgs::done / epoch)
+  bool head_done = false;
+  if (chain_done_) SD_CUDA(cudaMemsetAsync(chain_done_, 0, kChainCounters * sizeof(unsigned long long), stream_));
+  chain_epoch_ = 0;
   for (int gi = 0; gi < ng; ++gi) {
     Group& g = groups_[gi];
     const int n = static_cast<int>(g.rows.size());
@@ -210,6 +245,24 @@ void Engine::run(int ng, bool embed) {
         SD_CUDA(cudaStreamWaitEvent(stream_, g.ev_r, 0));
       }
       // finish_block (dense.cpp:51-70), then the next layer's project_qkv
+      // (or the head): one chained launch when the S-Part is bf16 at n >= 256
+      if (bf && !pipeline_ && chain_on_ && n >= 256) {
+        ChainArgs c{};
+        c.n = 4;
+        c.g[0] = w_->gemm_args(l, 4, n, g.o, D, g.ob, D, g.y, D, g.yb, D, kEpiResidual, g.x, D);
+        c.g[1] = w_->gemm_args(l, 5, n, g.y, D, g.yb, D, nullptr, F, g.hb, F, kEpiSilu, nullptr, 0);
+        c.g[2] = w_->gemm_args(l, 6, n, g.h, F, g.hb, F, g.x, D, g.xb, D, kEpiResidual, g.y, D);
+        c.g[3] = l + 1 < s.L
+                     ? w_->gemm_args(l + 1, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0)
+                     : w_->gemm_args(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+        c.done = chain_done_;
+        if (gemm_chain_supported(c)) {
+          c.epoch = chain_epoch_++;
+          chain(c);
+          if (l + 1 == s.L) head_done = true;
+          continue;
+        }
+      }
       gemm(l, 4, n, g.o, D, g.ob, D, g.y, D, bf ? g.yb : nullptr, D, kEpiResidual, g.x, D);
       gemm(l, 5, n, g.y, D, g.yb, D, bf ? nullptr : g.h, F, bf ? g.hb : nullptr, F, kEpiSilu, nullptr, 0);
       gemm(l, 6, n, g.h, F, g.hb, F, g.x, D, bf ? g.xb : nullptr, D, kEpiResidual, g.y, D);
@@ -222,7 +275,7 @@ void Engine::run(int ng, bool embed) {
   for (int gi = 0; gi < ng; ++gi) {  // output_logits + argmax_token (dense.cpp:72-88)
     Group& g = groups_[gi];
     const int n = static_cast<int>(g.rows.size());
-    gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+    if (!head_done) gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
     launch_argmax(n, s.V, g.logits, s.V, g.tok, stream_);
   }
 }
@@ -266,7 +319,26 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
       if (bf) launch_to_bf16(n, s.D, g.x, s.D, g.xb, s.D, stream_);
     }
   }
+  static const bool step_log = getenv("SD_STEP_LOG") != nullptr;
+  cudaEvent_t l0 = nullptr, l1 = nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  if (step_log) {
+    SD_CUDA(cudaEventCreate(&l0));
+    SD_CUDA(cudaEventCreate(&l1));
+    SD_CUDA(cudaEventRecord(l0, stream_));
+  }
   run(ng, tokens_host != nullptr);
+  if (step_log) {
+    const double enq = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    SD_CUDA(cudaEventRecord(l1, stream_));
+    SD_CUDA(cudaEventSynchronize(l1));
+    float d = 0;
+    SD_CUDA(cudaEventElapsedTime(&d, l0, l1));
+    const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    fprintf(stderr, "[step] device %.2f ms, host enqueue %.2f ms, host total %.2f ms\n", d, enq, tot);
+    cudaEventDestroy(l0);
+    cudaEventDestroy(l1);
+  }
   std::vector<int32_t> nt;
   std::vector<float> buf;
   for (int gi = 0; gi < ng; ++gi) {

@@ -689,6 +689,299 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Chained S-Part (bf16, CTA pairs): the GEMMs between two attentions -
+// W_o, MLP-in, MLP-out and the next layer's QKV (or the head) - as one
+// persistent launch. Items are the GEMMs' pair tiles in order, each GEMM's
+// tiles ordered by 256-row block; an item of GEMM g > 0 waits until every
+// tile of GEMM g-1 in the same row block has stored its outputs (a counter
+// per (GEMM, row block), bumped by the 8 epilogue warps of each pair tile).
+// Dependencies only point to earlier items and every CTA walks its items in
+// order on a persistent grid, so the earliest unfinished item can always
+// run. This removes three launches, prologues and epilogue drains per layer
+// and lets the next GEMM's first row block start under the previous GEMM's
+// tail wave.
+constexpr int kChainMax = 4;
+
+struct ChainGemm {
+  int M, N, K, bn, nb, kb, mg;  // pair tiles: mg row blocks x nb n-tiles
+  int item0;                    // first item of this GEMM in the chain
+  float* C;
+  int64_t ldc;
+  __nv_bfloat16* Cb;
+  int64_t ldcb;
+  int epi;
+  const float* res;
+  int64_t ldr;
+  int vec_res;
+  uint32_t idesc;
+};
+struct ChainParams {
+  int n, items;
+  ChainGemm g[kChainMax];
+  unsigned long long* done;  // [kChainMax][64] tile-completion counts, this step
+  unsigned long long epoch;  // chain launches so far this step (targets scale with it)
+};
+struct ChainMaps {
+  CUtensorMap m[kChainMax][4];  // A, B, C (fp32 out), Cb (bf16 out)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_chain_kernel(const __grid_constant__ ChainMaps maps, const ChainParams p) {
+  using C_ = Cfg<BN, true, 2>;
+  constexpr int STAGES = C_::STAGES;
+  constexpr int KELEMS = BK_BYTES / 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * C_::A_ST;
+  uint8_t* sOut = sB + STAGES * C_::B_ST;
+  uint8_t* tail = sOut + 4 * C_::OUT_WARP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_rank());
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  // item -> (gemm, row block, n-tile); row-block-major inside a GEMM
+  auto locate = [&](int it, int& gi, int& r, int& n) {
+    gi = 0;
+    while (gi + 1 < p.n && it >= p.g[gi + 1].item0) ++gi;
+    const int li = it - p.g[gi].item0;
+    r = li / p.g[gi].nb;
+    n = li - r * p.g[gi].nb;
+  };
+
+  if (warp == 0 && lane == 0) {
+    for (int gi = 0; gi < p.n; ++gi)
+      for (int t = 0; t < 4; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.m[gi][t]) : "memory");
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C_::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  pdl_trigger();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------------- TMA producer
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t full0 = mapa(&full[0], 0);
+    for (int it = cluster; it < p.items; it += nclusters) {
+      int gi, r, n;
+      locate(it, gi, r, n);
+      const ChainGemm& G = p.g[gi];
+      if (gi > 0) {
+        // GEMM gi-1 finished this row block (its outputs are this A operand)
+        const unsigned long long target = (p.epoch + 1ull) * static_cast<unsigned long long>(p.g[gi - 1].nb) * 8ull;
+        const unsigned long long* ctr = p.done + (gi - 1) * 64 + r;
+        const long long t0 = clock64();
+        while (ld_acquire_gpu(ctr) < target) {
+          if (clock64() - t0 > 20'000'000'000LL) __trap();  // ~10 s: a lost tile
+          __nanosleep(128);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA (async proxy) reads follow
+      }
+      const int slice = G.bn / 2;
+      const uint32_t bytes = 2u * static_cast<uint32_t>(2 * (C_::A_ATOM + slice * BK_BYTES));
+      const int m0 = (r * 2 + rank) * BM, n0 = n * G.bn;
+      const CUtensorMap* ta = &maps.m[gi][0];
+      const CUtensorMap* tb = &maps.m[gi][1];
+      for (int kb = 0; kb < G.kb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1);
+        if (leader) e_expect_tx(&full[s], bytes);
+        const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int kc = (kb * 2 + a) * KELEMS;
+          e_tma_load_pair(sA + s * C_::A_ST + a * C_::A_ATOM, ta, fb, kc, m0);
+          e_tma_load_pair(sB + s * C_::B_ST + a * C_::B_ATOM, tb, fb, kc, n0 + rank * slice);
+        }
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_wait(&empty[s], ph ^ 1);
+      if (++s == STAGES) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer
+    if (leader) {
+      int s = 0;
+      uint32_t ph = 0;
+      int local = 0;
+      const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
+      for (int it = cluster; it < p.items; it += nclusters, ++local) {
+        int gi, r, n;
+        locate(it, gi, r, n);
+        const ChainGemm& G = p.g[gi];
+        const int acc = local & 1;
+        const uint32_t use = static_cast<uint32_t>(local >> 1);
+        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem_base + acc * BN;
+        for (int kb = 0; kb < G.kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t da = da0 + static_cast<uint64_t>(s * (C_::A_ST >> 4));
+          const uint64_t db = db0 + static_cast<uint64_t>(s * (C_::B_ST >> 4));
+#pragma unroll
+          for (int a = 0; a < 2; ++a) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              e_mma<1, true>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k, G.idesc,
+                             (kb | a | k) != 0);
+            }
+          }
+          e_commit<true>(&empty[s], 3);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        e_commit<true>(&tfull[acc], 3);
+      }
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue
+    const int q = warp & 3;
+    const uint32_t tempty_leader0 = mapa(&tempty[0], 0);
+    uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
+    int nchunk = 0;
+    int local = 0;
+    for (int it = cluster; it < p.items; it += nclusters, ++local) {
+      int gi, r, n;
+      locate(it, gi, r, n);
+      const ChainGemm& G = p.g[gi];
+      const int acc = local & 1;
+      const uint32_t use = static_cast<uint32_t>(local >> 1);
+      const int m0 = (r * 2 + rank) * BM, n0 = n * G.bn;
+      const int nend = n0 + G.bn < G.N ? n0 + G.bn : G.N;
+      mbar_wait(&tfull[acc], use & 1);
+      __syncwarp();
+      tc_fence_after();
+      const int rowb = m0 + q * 32;
+      const int64_t row = rowb + lane;
+      const bool rin = row < G.M;
+#pragma unroll 1
+      for (int c = 0; c < (G.bn + 15) / 16; ++c) {
+        const int col0 = n0 + c * 16;
+        if (col0 >= nend) break;
+        float v[16];
+        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 16, v);
+        if (G.epi == kEpiResidual) {
+          if (rin && G.vec_res && col0 + 16 <= G.N) {
+            const float4* r4 = reinterpret_cast<const float4*>(G.res + row * G.ldr + col0);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float4 t = r4[k];
+              v[4 * k] = v[4 * k] + t.x;
+              v[4 * k + 1] = v[4 * k + 1] + t.y;
+              v[4 * k + 2] = v[4 * k + 2] + t.z;
+              v[4 * k + 3] = v[4 * k + 3] + t.w;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              if (rin && col0 + k < G.N) v[k] = v[k] + G.res[row * G.ldr + col0 + k];
+            }
+          }
+        } else if (G.epi == kEpiSilu) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = v[k] / (1.0f + expf(-v[k]));
+        }
+        uint8_t* bf = myout + (nchunk & 1) * (C_::OUT_F32 + C_::OUT_BF16);
+        uint8_t* bb = bf + C_::OUT_F32;
+        ++nchunk;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if (G.C) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            sts128(bf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), __float_as_uint(v[4 * j]),
+                   __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+          }
+        }
+        if (G.Cb) {
+          uint32_t w[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            w[e] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            sts128(bb + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
+                   w[4 * j + 3]);
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (G.C) tma_store_2d(&maps.m[gi][2], bf, col0, rowb);
+          if (G.Cb) tma_store_2d(&maps.m[gi][3], bb, col0, rowb);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cluster(tempty_leader0 + acc * static_cast<uint32_t>(sizeof(uint64_t)));
+        // this warp's part of the tile is in global memory: count it
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        atomicAdd(p.done + gi * 64 + r, 1ull);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -887,6 +1180,69 @@ bool gemm_sm100_supported(const GemmArgs& g) {
   if (reinterpret_cast<uintptr_t>(g.A) % 16 || reinterpret_cast<uintptr_t>(g.B) % 16) return false;
   if (g.K % (BK_BYTES / es) != 0) return false;  // whole 128-B atoms
   return true;
+}
+
+bool gemm_chain_supported(const ChainArgs& c) {
+  if (c.n < 1 || c.n > kChainMax || !c.done) return false;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  for (int i = 0; i < c.n; ++i) {
+    const GemmArgs& g = c.g[i];
+    if (g.kind != 1 || !gemm_sm100_supported(g) || g.M != c.g[0].M || g.M < 2 * BM || g.M > 64 * 2 * BM) return false;
+    if (!(g.C || g.Cb) || (g.C && (!al16(g.C) || g.ldc % 4)) || (g.Cb && (!al16(g.Cb) || g.ldcb % 8))) return false;
+    if (g.K % (2 * BK_BYTES / 2)) return false;  // whole two-atom stages
+  }
+  return true;
+}
+
+void launch_gemm_chain(const ChainArgs& c, cudaStream_t s) {
+  if (!gemm_chain_supported(c)) fail(SD_ERR_INTERNAL, "gemm chain: unsupported shapes");
+  using C_ = Cfg<256, true, 2>;
+  auto* kern = gemm_chain_kernel<256>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_set = true;
+  }
+  const int sms = c.max_ctas > 0 && c.max_ctas < num_sms() ? c.max_ctas : num_sms();
+  ChainMaps maps{};
+  ChainParams p{};
+  p.n = c.n;
+  p.done = c.done;
+  p.epoch = c.epoch;
+  int items = 0;
+  for (int i = 0; i < c.n; ++i) {
+    const GemmArgs& g = c.g[i];
+    ChainGemm& G = p.g[i];
+    G.M = g.M;
+    G.N = g.N;
+    G.K = g.K;
+    G.mg = (g.M + 2 * BM - 1) / (2 * BM);
+    G.bn = pick_pair_bn(G.mg, g.N, sms / 2);
+    G.nb = (g.N + G.bn - 1) / G.bn;
+    G.kb = g.K / (2 * (BK_BYTES / 2));
+    G.item0 = items;
+    items += G.mg * G.nb;
+    G.C = g.C;
+    G.ldc = g.ldc;
+    G.Cb = g.Cb;
+    G.ldcb = g.ldcb;
+    G.epi = g.epi;
+    G.res = g.res;
+    G.ldr = g.ldr;
+    G.vec_res = g.epi == kEpiResidual && g.ldr % 4 == 0 && (reinterpret_cast<uintptr_t>(g.res) & 15) == 0;
+    G.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(G.bn >> 3) << 17) |
+              (static_cast<uint32_t>((2 * BM) >> 4) << 24);
+    maps.m[i][0] = make_map(g.A, g.M, g.K, g.lda, 1, BM);
+    maps.m[i][1] = make_map(g.B, g.N, g.K, g.ldb, 1, G.bn / 2);
+    maps.m[i][2] = g.C ? make_map(g.C, g.M, g.N, g.ldc, 2, 32, 64) : maps.m[i][0];
+    maps.m[i][3] = g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, 1, 32, 32) : maps.m[i][0];
+  }
+  p.items = items;
+  const int max_clusters = sms / 2 > 0 ? sms / 2 : 1;
+  const int clusters = items < max_clusters ? items : max_clusters;
+  SD_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(clusters * 2)), dim3(kThreads), C_::SMEM, s, 2u, maps, p));
+  count_launch();
 }
 
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s) {
