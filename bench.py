@@ -33,6 +33,7 @@ WORKLOADS = {
     "c1-tiny-b16-ctx128": (2, 256, 2, 2, 1024, 256, 16, 128, "single", "exact"),
 }
 DEFAULT = "c5-llama3-8b-gqa-b512-ctx2048"
+TIMING_EVERY = 8  # bench.py samples per-kernel CUDA events on every 8th layer
 METRIC = "decode tokens/sec at 1/2/4/8 B200; R-Part HBM GB/s as % of peak"
 
 
@@ -212,7 +213,7 @@ def run_dist(args, wl, rank, world, dev, dist):
     clk = Clocks(dev)
     eng.bench(seqs, tokens, args.warmup)
     torch.cuda.synchronize(dev)
-    kv.timing(True)
+    kv.timing(TIMING_EVERY)
     eng.timing(True)
     kv.timing_read(reset=True)
     eng.timing_read(reset=True)
@@ -267,7 +268,8 @@ def run_dist(args, wl, rank, world, dev, dist):
         "roofline": {"bound": "hbm", "kernel": "attention (rank 0)", "achieved": achieved,
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "traffic": None, "launches": a_n, "ms_per_launch": a_ms / max(a_n, 1),
-                     "share_of_step": a_ms / ms if ms else None},
+                     "launches_timed_of": args.steps * L,
+                     "share_of_step": (a_ms / max(a_n, 1)) * args.steps * L / ms if ms else None},
         "exchange": {"ms_per_step": x_ms / args.steps, "bytes_per_step_rank0": x_bytes / args.steps,
                      "gbs": x_bytes / (x_ms / 1e3) / 1e9 if x_ms else None, "shard_rows_rank0": len(mine),
                      "max_shard_rows": cap_seqs},
@@ -316,9 +318,11 @@ def run_ours(args, wl, rank, world, dev, dist):
     # ---- device-timed region: K steps, CUDA events on the engine stream
     # (SD_BENCH_NO_KTIMING=1: no per-kernel events, for A/B experiments only;
     # the roofline fields are then empty)
-    ktiming = os.environ.get("SD_BENCH_NO_KTIMING") is None
-    kv.timing(ktiming)
-    eng.timing(ktiming)
+    # per-kernel CUDA events on every 8th layer only (layers are identical;
+    # an event pair around every launch costs ~1 ms of a ~28 ms step)
+    every = 0 if os.environ.get("SD_BENCH_NO_KTIMING") else TIMING_EVERY
+    kv.timing(every)
+    eng.timing(every)
     kv.timing_read(reset=True)
     eng.timing_read(reset=True)
     if dist:
@@ -369,6 +373,8 @@ def run_ours(args, wl, rank, world, dev, dist):
     if rank == 0 and world == 1 and not args.no_c2:
         extra["r_part_c2"] = rpart_c2(sd, torch, dev, pk)
     achieved = a_bytes / (a_ms / 1e3) / 1e9 if a_ms > 0 else 0.0
+    hd = D // H
+    step_flops = 2.0 * B * (L * (D * (H + 2 * Hkv) * hd + D * D + 2 * D * F) + D * V)  # this rank's GEMMs
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_attention_traffic.json")
     if os.path.exists(tf):
@@ -392,12 +398,15 @@ def run_ours(args, wl, rank, world, dev, dist):
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "launches": a_n, "ms_per_launch": a_ms / max(a_n, 1),
-                     "share_of_step": a_ms / ms if ms else None,
+                     "launches_timed_of": args.steps * L * (2 if args.r_sms > 0 else 1),
+                     "share_of_step": (a_ms / max(a_n, 1)) * args.steps * L * (2 if args.r_sms > 0 else 1) / ms
+                     if ms else None,
                      "peak_src": pk["src"] + " (MEASURED_PEAKS.json hbm_gbs)"},
         "s_part": {"bound": "tensor", "achieved": g_flops / (g_ms / 1e3) / 1e12 if g_ms else 0.0,
                    "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                    "frac": (g_flops / (g_ms / 1e3) / 1e12) / pk["bf16_tflops_sustained"] if g_ms else 0.0,
-                   "share_of_step": g_ms / ms if ms else None, "launches": g_n},
+                   "share_of_step": (g_ms * step_flops * args.steps / g_flops) / ms if ms and g_flops else None,
+                   "launches": g_n, "timing": f"CUDA events on the GEMMs of every {TIMING_EVERY}th layer + head"},
         "e2e": e2e,
         "gpu_launches": int(l1 - l0),
         "clocks": clocks,

@@ -150,6 +150,7 @@ int sd_kv_prefill_synthetic(sd_kv* kv, int32_t n, const uint64_t* seqs, int32_t 
 /* Per-launch timing of the attention kernel (CUDA events on the launching
  * stream). enable != 0 starts recording; read returns the summed kernel
  * milliseconds, launches and algorithmic bytes since the last reset. */
+/* enable: 0 off, 1 every attention launch, k > 1 the launches of every k-th layer */
 int sd_kv_timing(sd_kv* kv, int enable);
 int sd_kv_timing_read(sd_kv* kv, double* ms, int64_t* launches, double* bytes, int reset);
 
@@ -206,6 +207,7 @@ int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t
                     int32_t steps, int32_t* next_tokens, double* device_ms);
 /* CUDA-event timing of the engine's S-Part GEMM launches (sum of kernel
  * milliseconds and algorithmic flops since the last reset). */
+/* enable: 0 off, 1 every GEMM, k > 1 the GEMMs of every k-th layer (and the head) */
 int sd_engine_timing(sd_engine* e, int enable);
 int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* launches, int reset);
 /* Two-mini-batch pipeline (workers.cpp:405-452): rows split by seq % 2; the

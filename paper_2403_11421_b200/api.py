@@ -265,7 +265,9 @@ class KvShard:
         s, sp = _u64(seqs)
         _check(lib.sd_kv_prefill_synthetic(self.h, len(s), sp, length, salt))
 
-    def timing(self, enable: bool):
+    def timing(self, enable):
+        """CUDA-event timing of the attention launches: False/0 off, True/1
+        every launch, k > 1 the launches of every k-th layer."""
         _check(lib.sd_kv_timing(self.h, int(enable)))
 
     def timing_read(self, reset=True):
@@ -406,8 +408,9 @@ class Engine:
         mini-batch on r_sms SMs beside the GEMMs of the other."""
         _check(lib.sd_engine_pipeline(self.h, int(enable), r_sms))
 
-    def timing(self, enable: bool):
-        """CUDA-event timing of the S-Part GEMMs."""
+    def timing(self, enable):
+        """CUDA-event timing of the S-Part GEMMs: False/0 off, True/1 every
+        GEMM, k > 1 the GEMMs of every k-th layer (and the head)."""
         _check(lib.sd_engine_timing(self.h, int(enable)))
 
     def timing_read(self, reset=True):

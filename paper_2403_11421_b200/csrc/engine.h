@@ -95,7 +95,11 @@ class Engine : public StepComputation {
                int32_t* next_host);
   cudaStream_t stream() const { return stream_; }
   // CUDA-event timing of the S-Part GEMMs (on the S stream)
-  void set_timing(bool on) { timing_ = on; }
+  // every = 0: off; 1: every GEMM; k > 1: the GEMMs of every k-th layer
+  void set_timing(int every) {
+    timing_ = every > 0;
+    timing_every_ = every > 0 ? every : 1;
+  }
   void read_timing(double* ms, double* flops, int64_t* launches, bool reset);
   // Two-mini-batch pipeline (workers.cpp:405-452): rows split by seq % 2;
   // the R-Part of one mini-batch (r_sms SMs, R stream) runs beside the
@@ -124,6 +128,7 @@ class Engine : public StepComputation {
   unsigned long long* chain_done_ = nullptr;
   unsigned long long chain_epoch_ = 0;
   bool chain_on_ = true;
+  int timing_every_ = 1;
   void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
             int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
             const float* res, int64_t ldr);

@@ -146,7 +146,8 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
                   const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
                   int64_t ldyb, int epi, const float* res, int64_t ldr) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing_) {
+  const bool timed = timing_ && (which == 7 || layer % timing_every_ == 0);
+  if (timed) {
     for (cudaEvent_t* e : {&e0, &e1}) {
       if (ev_pool_.empty()) {
         SD_CUDA(cudaEventCreate(e));
@@ -158,7 +159,7 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
     SD_CUDA(cudaEventRecord(e0, stream_));
   }
   w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_, s_sms_);
-  if (timing_) {
+  if (timed) {
     SD_CUDA(cudaEventRecord(e1, stream_));
     ev_.emplace_back(e0, e1);
     ev_flops_.push_back(2.0 * B * w_->out_dim(which) * w_->in_dim(which));

@@ -523,7 +523,8 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   a.ob_stride = obs;
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing_) {
+  const bool timed = timing_ && layer % timing_every_ == 0;
+  if (timed) {
     auto take = [&]() {
       if (ev_pool_.empty()) {
         cudaEvent_t ev;
@@ -543,7 +544,7 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   } else if (!launch_attention(a, P.grid, attn_smem_, s)) {
     launch_attention_generic(a, P.npieces, s);
   }
-  if (timing_) {
+  if (timed) {
     SD_CUDA(cudaEventRecord(e1, s));
     ev_pending_.emplace_back(e0, e1);
     const double e = geom_.fmt == SD_KV_SINGLE ? 4 : geom_.fmt == SD_KV_HALF ? 2 : 1;
@@ -675,7 +676,10 @@ void KvStore::prefill_synthetic(int n, const uint64_t* seqs, int length, uint64_
 }
 
 // --------------------------------------------------------------- timing ---
-void KvStore::set_timing(bool on) { timing_ = on; }
+void KvStore::set_timing(int every) {
+  timing_ = every > 0;
+  timing_every_ = every > 0 ? every : 1;
+}
 
 void KvStore::read_timing(double* ms, int64_t* launches, double* bytes, bool reset) {
   DeviceGuard dg(device_);

@@ -63,7 +63,9 @@ class KvStore {
                          cudaStream_t s);
 
   // ---- timing of the attention kernel (CUDA events on the launching stream)
-  void set_timing(bool on);
+  // every = 0: off; 1: every attention launch; k > 1: launches of every
+  // k-th layer (layers are identical; fewer events perturb the step less)
+  void set_timing(int every);
   void read_timing(double* ms, int64_t* launches, double* bytes, bool reset);
 
  private:
@@ -133,6 +135,7 @@ class KvStore {
 
   // timing
   bool timing_ = false;
+  int timing_every_ = 1;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending_;
   std::vector<double> ev_bytes_;

@@ -279,7 +279,7 @@ int sd_kv_prefill_synthetic(sd_kv* kv, int32_t n, const uint64_t* seqs, int32_t 
 int sd_kv_timing(sd_kv* kv, int enable) {
   return guard([&] {
     need(kv, "kv");
-    kv->s->set_timing(enable != 0);
+    kv->s->set_timing(enable < 0 ? 0 : enable);
   });
 }
 
@@ -488,7 +488,7 @@ int sd_engine_bench(sd_engine* e, int32_t B, const uint64_t* seqs, const int32_t
 int sd_engine_timing(sd_engine* e, int enable) {
   return guard([&] {
     need(e, "engine");
-    e->e->set_timing(enable != 0);
+    e->e->set_timing(enable < 0 ? 0 : enable);
   });
 }
 
