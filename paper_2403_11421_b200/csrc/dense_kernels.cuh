@@ -33,6 +33,23 @@ void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat
 // tcgen05 GEMM: C[M][N] = A[M][K] . B[N][K]^T with fused epilogue; A, B
 // K-major (bf16 for kind::f16, fp32 bits for kind::tf32). Writes fp32 C and,
 // if cb != nullptr, a bf16 copy for the next GEMM's A operand.
+// Multi-GPU exchange fused into a producer's epilogue (dist.cpp): output row
+// m is stored straight into base[rank[m]] + row[m] * ld (a peer's receive
+// buffer through its CUDA IPC mapping, or this rank's own), and the last CTA
+// to finish publishes flag[d][slot * 8 + self] = epoch (release, system
+// scope) for every rank d in `notify`.
+struct RowRoute {
+  const int32_t* rank;
+  const int32_t* row;
+  float* base[8];
+  int64_t ld;
+  int64_t* flag[8];
+  int32_t* done;  // grid arrival counter, zero between launches
+  int64_t epoch;
+  uint32_t notify;
+  int slot, self;
+};
+
 struct GemmArgs {
   int M, N, K;
   const void* A;
@@ -48,6 +65,7 @@ struct GemmArgs {
   int64_t ldr;
   int kind;      // 1 = bf16 (kind::f16), 2 = tf32
   int max_ctas;  // SM budget of the persistent grid (0 = every SM)
+  const RowRoute* route = nullptr;  // fp32 C rows routed to peers (C unused)
 };
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);

@@ -159,7 +159,8 @@ DistEngine::~DistEngine() {
   cudaStreamSynchronize(stream_);
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
-                  static_cast<void*>(done_)}) {
+                  static_cast<void*>(done_), static_cast<void*>(gemm_done_),
+                  static_cast<void*>(attn_done_)}) {
     if (p) cudaFree(p);
   }
   if (comm_) Nccl::get().CommDestroy(comm_);
@@ -232,7 +233,30 @@ void DistEngine::plan_for(int B, const uint64_t* seqs) {
         fail(SD_ERR_CAPACITY, "peer exchange: batch exceeds the p2p_setup row capacity");
       }
     }
+    if (fused_) build_routes();
   }
+}
+
+// device tables of the fused exchange: home row -> (shard rank, row in its
+// receive buffer) and shard row -> (home rank, row in its receive buffer)
+void DistEngine::build_routes() {
+  const size_t nh = plan_.home_rows.size(), ns = plan_.shard_rows.size();
+  std::vector<int32_t> t(2 * nh + 2 * ns + 1, 0);
+  for (int d = 0; d < world_; ++d) {
+    const size_t u = static_cast<size_t>(d);
+    for (int j = 0; j < plan_.send_cnt[u]; ++j) {
+      const size_t i = static_cast<size_t>(plan_.send_off[u] + j);
+      t[i] = d;
+      t[nh + i] = peer_qkv_off_[u] + j;
+    }
+    for (int j = 0; j < plan_.recv_cnt[u]; ++j) {
+      const size_t i = static_cast<size_t>(plan_.recv_off[u] + j);
+      t[2 * nh + i] = d;
+      t[2 * nh + ns + i] = peer_o_off_[u] + j;
+    }
+  }
+  route_.get(t.size() * 4);
+  SD_CUDA(cudaMemcpy(route_.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
 }
 
 void DistEngine::p2p_setup(int max_rows, void* handles_out) {
@@ -241,7 +265,8 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   DeviceGuard dg(device_);
   SD_CUDA(cudaStreamSynchronize(stream_));
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
-                  static_cast<void*>(done_)}) {
+                  static_cast<void*>(done_), static_cast<void*>(gemm_done_),
+                  static_cast<void*>(attn_done_)}) {
     if (p) cudaFree(p);
   }
   const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;
@@ -249,6 +274,10 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), rows * spec_.D * 4));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), 2 * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&done_), sizeof(int32_t)));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&gemm_done_), sizeof(int32_t)));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&attn_done_), sizeof(int32_t)));
+  SD_CUDA(cudaMemset(gemm_done_, 0, sizeof(int32_t)));
+  SD_CUDA(cudaMemset(attn_done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaMemset(rx_qkv_, 0, rows * spec_.qkv_width() * 4));
   SD_CUDA(cudaMemset(rx_o_, 0, rows * spec_.D * 4));
   SD_CUDA(cudaMemset(flags_, 0, 2 * kMaxWorld * sizeof(int64_t)));
@@ -286,6 +315,8 @@ void DistEngine::p2p_connect(const void* all_handles) {
     peer_flags_[p] = static_cast<int64_t*>(ptr[2]);
   }
   p2p_ = true;
+  // the exchange is fused into the producers when both have a routed form
+  fused_ = std::getenv("SD_DIST_NO_FUSE") == nullptr && mode_ == SD_SHARD_BY_SEQUENCE && kv_->tensor_core_path();
   plan_key_.clear();  // recompute the peer offsets
 }
 
@@ -419,27 +450,85 @@ void DistEngine::run_step() {
   const int ns = static_cast<int>(plan_.shard_rows.size());
   const bool bf = w_ && w_->mode() == SD_DENSE_BF16;
   if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, stream_);
+  const bool fused = p2p_ && fused_;
+  const bool route_qkv = fused && nh && w_->mode() != SD_DENSE_EXACT_F32;  // exact mode: scatter kernel
+  const int32_t* tbl = static_cast<const int32_t*>(route_.p);
+  uint32_t to_shards = 0, from_homes = 0, to_homes = 0, from_shards = 0;
+  for (int d = 0; d < world_; ++d) {
+    if (d == rank_) continue;
+    if (plan_.send_cnt[static_cast<size_t>(d)] > 0) to_shards |= 1u << d, from_shards |= 1u << d;
+    if (plan_.recv_cnt[static_cast<size_t>(d)] > 0) from_homes |= 1u << d, to_homes |= 1u << d;
+  }
   for (int l = 0; l < s.L; ++l) {
-    if (nh) w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    if (route_qkv) {
+      // project_qkv with the exchange in its epilogue: every home row lands in
+      // its shard's receive buffer; the last CTA publishes the epoch
+      RowRoute r{};
+      r.rank = tbl;
+      r.row = tbl + nh;
+      r.ld = qkvw;
+      for (int d = 0; d < world_; ++d) {
+        r.base[d] = peer_qkv_[d];
+        r.flag[d] = peer_flags_[d];
+      }
+      r.done = gemm_done_;
+      r.epoch = ++epoch_;
+      r.notify = to_shards;
+      r.slot = 0;
+      r.self = rank_;
+      GemmArgs ga = w_->gemm_args(l, 0, nh, x_, D, xb_, D, nullptr, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+      ga.route = &r;
+      launch_gemm_sm100(ga, stream_);
+      launch_p2p_wait(flags_, 0, from_homes, world_, r.epoch, stream_);
+    } else if (nh) {
+      w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    }
+    if (fused && !route_qkv) {  // nothing to send (or exact mode): the same flags / epochs
+      if (nh) {
+        exchange_p2p(0);
+      } else {
+        launch_p2p_wait(flags_, 0, from_homes, world_, ++epoch_, stream_);
+      }
+    }
     float* qkv_s = p2p_ ? rx_qkv_ : qkv_s_;
     float* o_h = p2p_ ? rx_o_ : o_h_;
     // this worker's head slice of a shard row: [q | k | v] (full width when by-sequence)
     const int G = s.H / s.Hkv;
     const int hc = plan_.head_count[static_cast<size_t>(rank_)];
     const int sq = hc * G * s.hd, sk = hc * s.hd, srow = p2p_ ? sq + 2 * sk : qkvw;
-    if (p2p_) {
+    if (fused) {
+      // (sent above)
+    } else if (p2p_) {
       exchange_p2p(0);
     } else {
       exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s, plan_.recv_cnt, plan_.recv_off, qkvw);
+    }
+    ORoute orr{};
+    if (fused) {  // attention rows straight into their home rank's buffer
+      orr.rank = tbl + 2 * nh;
+      orr.row = tbl + 2 * nh + ns;
+      orr.ld = D;
+      for (int d = 0; d < world_; ++d) {
+        orr.base[d] = peer_o_[d];
+        orr.flag[d] = peer_flags_[d];
+      }
+      orr.done = attn_done_;
+      orr.epoch = ++epoch_;
+      orr.notify = to_homes;
+      orr.slot = 1;
+      orr.self = rank_;
     }
     if (ns) {
       for (int i = 0; i < ns; ++i) {
         pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
       }
       kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + sq, srow, qkv_s + sq + sk, srow, stream_);
-      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, srow, o_s_, p2p_ ? sq : D, stream_);
+      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, srow, o_s_, p2p_ ? sq : D, stream_, 0, nullptr, 0,
+                  fused ? &orr : nullptr);
     }
-    if (p2p_) {
+    if (fused) {
+      launch_p2p_wait(flags_, 1, from_shards, world_, orr.epoch, stream_);
+    } else if (p2p_) {
       exchange_p2p(1);
     } else {
       exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h, plan_.send_cnt, plan_.send_off, D);

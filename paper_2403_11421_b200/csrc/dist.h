@@ -104,6 +104,15 @@ class DistEngine : public StepComputation {
   bool p2p_ = false;
   int p2p_cap_ = 0;
   float *rx_qkv_ = nullptr, *rx_o_ = nullptr;  // receive buffers (shard rows / home rows)
+  // fused exchange: the QKV GEMM and the attention store rows straight into
+  // the peers' buffers (RowRoute / ORoute) and publish the epoch themselves.
+  // Decided from rank-independent facts (a sender may still use the scatter
+  // kernel, e.g. an exact-mode S-rank: receivers only see buffers and flags)
+  bool fused_ = false;
+  DevBuf route_;                   // [qkv rank | qkv row | o rank | o row] int32 tables
+  int32_t* gemm_done_ = nullptr;   // arrival counters of the routed launches
+  int32_t* attn_done_ = nullptr;
+  void build_routes();
   int64_t* flags_ = nullptr;                   // [2][kMaxWorld] epochs published by sources
   int32_t* done_ = nullptr;
   float* peer_qkv_[kMaxWorld] = {};

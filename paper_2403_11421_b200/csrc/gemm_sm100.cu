@@ -54,6 +54,8 @@ struct Params {
   int vec;   // outputs / residual 16-B aligned: vector epilogue
   int tma_out;  // outputs written by TMA tensor stores
   int diag;  // 1: reuse resident smem after the first ring fill (MMA-rate probe)
+  int routed;      // C rows go to route.base[route.rank[m]] (fused multi-GPU exchange)
+  RowRoute route;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -629,8 +631,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 32; ++k) v[k] = v[k] / (1.0f + expf(-v[k]));
           }
-          if (p.C) {
-            float4* c4 = reinterpret_cast<float4*>(p.C + row * p.ldc + col0);
+          if (p.C || p.routed) {
+            float* crow = p.routed ? p.route.base[p.route.rank[row]] + p.route.row[row] * p.route.ld
+                                   : p.C + row * p.ldc;
+            float4* c4 = reinterpret_cast<float4*>(crow + col0);
 #pragma unroll
             for (int k = 0; k < 8; ++k) c4[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
           }
@@ -659,7 +663,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (p.epi == kEpiSilu) {
               x = x / (1.0f + expf(-x));
             }
-            if (p.C) p.C[row * p.ldc + col] = x;
+            if (p.routed) {
+              p.route.base[p.route.rank[row]][p.route.row[row] * p.route.ld + col] = x;
+            } else if (p.C) {
+              p.C[row * p.ldc + col] = x;
+            }
             if (p.Cb) p.Cb[row * p.ldcb + col] = __float2bfloat16_rn(x);
           }
         }
@@ -677,7 +685,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
+  if (p.routed) __threadfence_system();  // this thread's routed stores before the CTA is counted
   __syncthreads();
+  if (p.routed && threadIdx.x == 0) {
+    // the last CTA publishes this exchange's epoch to every destination
+    if (atomicAdd(p.route.done, 1) == static_cast<int>(gridDim.x) - 1) {
+      __threadfence_system();
+      for (int d = 0; d < 8; ++d) {
+        if (p.route.notify >> d & 1) {
+          asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p.route.flag[d] + p.route.slot * 8 + p.route.self),
+                       "l"(p.route.epoch)
+                       : "memory");
+        }
+      }
+      *p.route.done = 0;
+    }
+  }
   if (cs > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
@@ -1129,7 +1152,12 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   p.kind = KIND;
   p.bn = bn;
   p.diag = env_int("SD_GEMM_DIAG");
-  p.tma_out = tma_out ? 1 : 0;
+  p.tma_out = tma_out && !g.route ? 1 : 0;  // routed rows use the per-row vector epilogue
+  if (g.route) {
+    p.routed = 1;
+    p.route = *g.route;
+    if (g.N % 32 || g.route->ld % 4) fail(SD_ERR_CONFIG, "routed GEMM: N and the row stride must be multiples of 32 / 4");
+  }
   p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
           (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));
   const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16

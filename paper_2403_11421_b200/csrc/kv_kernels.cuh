@@ -52,6 +52,23 @@ struct Piece {
   int32_t item, p0, p1, flags;
 };
 
+// Multi-GPU exchange fused into the attention (tensor-core path): the o row of
+// item i (fp32, and bf16 when bbase is set) goes to base[rank[i]] + row[i] * ld
+// on the sequence's home rank; the last CTA publishes flag[d][slot * 8 + self]
+// = epoch (release, system scope) for every d in `notify`.
+struct ORoute {
+  const int32_t* rank;
+  const int32_t* row;
+  float* base[8];
+  __nv_bfloat16* bbase[8];
+  int64_t ld, bld;
+  int64_t* flag[8];
+  int32_t* done;
+  int64_t epoch;
+  uint32_t notify;
+  int slot, self;
+};
+
 struct AttnArgs {
   KvGeom g;
   int32_t layer;
@@ -76,6 +93,8 @@ struct AttnArgs {
   int32_t* comb_cnt;          // [ncombine][hc] arrival counters, zero between launches
   __nv_bfloat16* ob;          // optional bf16 copy of o (the W_o GEMM operand)
   int64_t ob_stride;
+  int routed;                 // o rows go to the home ranks (oroute), o/ob unused
+  ORoute oroute;
 };
 
 // Static shape of the fast attention kernel for a geometry (kv_kernels.cu).

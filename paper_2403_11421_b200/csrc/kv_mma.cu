@@ -433,14 +433,25 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (hq >= G) continue;
       const int qh = hk * G + hq;
       if (direct) {
-        float* orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * kHD;
-        __nv_bfloat16* brow = a.ob ? a.ob + static_cast<int64_t>(pc.item) * a.ob_stride + qh * kHD : nullptr;
+        float* orow;
+        __nv_bfloat16* brow;
+        if (a.routed) {
+          const int rk = a.oroute.rank[pc.item];
+          const int64_t rr = a.oroute.row[pc.item];
+          orow = a.oroute.base[rk] ? a.oroute.base[rk] + rr * a.oroute.ld + qh * kHD : nullptr;
+          brow = a.oroute.bbase[rk] ? a.oroute.bbase[rk] + rr * a.oroute.bld + qh * kHD : nullptr;
+        } else {
+          orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * kHD;
+          brow = a.ob ? a.ob + static_cast<int64_t>(pc.item) * a.ob_stride + qh * kHD : nullptr;
+        }
         const float inv = 1.0f / l[j];
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
           const float x0 = o[mt][j] * inv, x1 = o[mt][2 + j] * inv;
-          orow[16 * mt + gq] = x0;
-          orow[16 * mt + gq + 8] = x1;
+          if (orow) {
+            orow[16 * mt + gq] = x0;
+            orow[16 * mt + gq + 8] = x1;
+          }
           if (brow) {
             brow[16 * mt + gq] = __float2bfloat16_rn(x0);
             brow[16 * mt + gq + 8] = __float2bfloat16_rn(x1);
@@ -500,19 +511,45 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
             acc[4 * k + 3] = fmaf(wgt, t[k].w, acc[4 * k + 3]);
           }
         }
-        float* orow = a.o + static_cast<int64_t>(it.x) * a.o_stride + qh * kHD + d0;
+        float* orow;
+        __nv_bfloat16* bro;
+        if (a.routed) {
+          const int rk = a.oroute.rank[it.x];
+          const int64_t rr = a.oroute.row[it.x];
+          orow = a.oroute.base[rk] ? a.oroute.base[rk] + rr * a.oroute.ld + qh * kHD + d0 : nullptr;
+          bro = a.oroute.bbase[rk] ? a.oroute.bbase[rk] + rr * a.oroute.bld + qh * kHD + d0 : nullptr;
+        } else {
+          orow = a.o + static_cast<int64_t>(it.x) * a.o_stride + qh * kHD + d0;
+          bro = a.ob ? a.ob + static_cast<int64_t>(it.x) * a.ob_stride + qh * kHD + d0 : nullptr;
+        }
 #pragma unroll
         for (int k = 0; k < DPL / 4; ++k) {
           const float4 x = make_float4(acc[4 * k] / L, acc[4 * k + 1] / L, acc[4 * k + 2] / L, acc[4 * k + 3] / L);
-          *reinterpret_cast<float4*>(orow + 4 * k) = x;
-          if (a.ob) {
-            __nv_bfloat16* brow = a.ob + static_cast<int64_t>(it.x) * a.ob_stride + qh * kHD + d0 + 4 * k;
+          if (orow) *reinterpret_cast<float4*>(orow + 4 * k) = x;
+          if (bro) {
+            __nv_bfloat16* brow = bro + 4 * k;
             *reinterpret_cast<__nv_bfloat162*>(brow) = __floats2bfloat162_rn(x.x, x.y);
             *reinterpret_cast<__nv_bfloat162*>(brow + 2) = __floats2bfloat162_rn(x.z, x.w);
           }
         }
         if (lane == 0) a.comb_cnt[ci * g.hc + hk] = 0;  // ready for the next launch
       }
+    }
+  }
+  if (a.routed) {
+    // every consumer's routed o stores, then the last CTA publishes the epoch
+    __threadfence_system();
+    named_bar(15, kWarps * 32);  // the consumer warps (the producer has returned)
+    if (threadIdx.x == 0 && atomicAdd(a.oroute.done, 1) == static_cast<int>(gridDim.x) - 1) {
+      __threadfence_system();
+      for (int d = 0; d < 8; ++d) {
+        if (a.oroute.notify >> d & 1) {
+          asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(a.oroute.flag[d] + a.oroute.slot * 8 + a.oroute.self),
+                       "l"(a.oroute.epoch)
+                       : "memory");
+        }
+      }
+      *a.oroute.done = 0;
     }
   }
 }

@@ -373,7 +373,8 @@ const KvStore::Fast* KvStore::fast_match(int n, const uint64_t* seqs) const {
 // --------------------------------------------------------------- attend ---
 void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
                      int64_t q_stride, float* o_dev, int64_t o_stride, cudaStream_t s, int slot,
-                     __nv_bfloat16* ob, int64_t ob_stride) {
+                     __nv_bfloat16* ob, int64_t ob_stride, const ORoute* oroute) {
+  if (oroute && !use_mma_) fail(SD_ERR_INTERNAL, "routed attention output needs the tensor-core path");
   DeviceGuard dg(device_);
   const int L = spec_.L;
   if (layer < 0 || layer >= L) fail(SD_ERR_PROTOCOL, "attend: layer index out of range");
@@ -489,11 +490,12 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
       SD_CUDA(cudaMemsetAsync(P.comb_cnt.p, 0, P.comb_cnt.bytes, s));
     }
   }
-  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, ob, ob_stride, s);
+  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, ob, ob_stride, s, oroute);
 }
 
 void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o,
-                                    int64_t os, __nv_bfloat16* ob, int64_t obs, cudaStream_t s) {
+                                    int64_t os, __nv_bfloat16* ob, int64_t obs, cudaStream_t s,
+                                    const ORoute* oroute) {
   const uint8_t* base = static_cast<const uint8_t*>(P.blob.dev.p);
   AttnArgs a{};
   a.g = geom_;
@@ -521,6 +523,11 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   a.comb_cnt = fused ? static_cast<int32_t*>(P.comb_cnt.p) : nullptr;
   a.ob = fused ? ob : nullptr;
   a.ob_stride = obs;
+  if (oroute) {
+    if (!fused) fail(SD_ERR_INTERNAL, "routed attention output needs the fused combine");
+    a.routed = 1;
+    a.oroute = *oroute;
+  }
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = timing_ && layer % timing_every_ == 0;

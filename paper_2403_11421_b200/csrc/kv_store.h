@@ -51,7 +51,8 @@ class KvStore {
   // `ob` (optional): also write o in bf16 (the W_o GEMM operand).
   void attend(int layer, int n, const uint64_t* seqs, const float* q_dev, int64_t q_stride,
               float* o_dev, int64_t o_stride, cudaStream_t s, int slot = 0,
-              __nv_bfloat16* ob = nullptr, int64_t ob_stride = 0);
+              __nv_bfloat16* ob = nullptr, int64_t ob_stride = 0, const ORoute* oroute = nullptr);
+  bool tensor_core_path() const { return use_mma_; }
   // SM budget of the attention grid (0 = every SM): the R-Part's share when
   // it runs beside the S-Part of the other mini-batch
   void set_grid_limit(int sms) { grid_limit_ = sms; }
@@ -89,7 +90,7 @@ class KvStore {
   };
   static constexpr int kPlanSlots = 2;
   void launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o, int64_t os,
-                             __nv_bfloat16* ob, int64_t obs, cudaStream_t s);
+                             __nv_bfloat16* ob, int64_t obs, cudaStream_t s, const ORoute* oroute);
 
   Spec spec_;
   int head_start_, head_count_, G_;
