@@ -425,6 +425,34 @@ void DistEngine::exchange(const float* send, const std::vector<int32_t>& sc, con
   }
 }
 
+// bytes this rank sends to peers in one exchange (kind 0: q|k|v rows, 1: o rows)
+double DistEngine::kind_bytes(int kind) const {
+  const std::vector<int32_t>& sc = kind == 0 ? plan_.send_cnt : plan_.recv_cnt;
+  const int w = kind == 0 ? spec_.qkv_width() : spec_.D;
+  double b = 0;
+  for (int d = 0; d < world_; ++d) {
+    if (d != rank_) b += static_cast<double>(sc[static_cast<size_t>(d)]) * w * 4;
+  }
+  return b;
+}
+
+// the receive side of a producer-fused exchange; under timing, the wait is
+// what remains of the exchange once the stores overlapped the producer
+void DistEngine::fused_wait(int slot, uint32_t expect, int64_t epoch, double bytes) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (timing_) {
+    SD_CUDA(cudaEventCreate(&e0));
+    SD_CUDA(cudaEventCreate(&e1));
+    SD_CUDA(cudaEventRecord(e0, stream_));
+  }
+  launch_p2p_wait(flags_, slot, expect, world_, epoch, stream_);
+  if (timing_) {
+    SD_CUDA(cudaEventRecord(e1, stream_));
+    ev_.emplace_back(e0, e1);
+    ev_bytes_.push_back(bytes);
+  }
+}
+
 void DistEngine::read_timing(double* ms, double* bytes, bool reset) {
   for (size_t i = 0; i < ev_.size(); ++i) {
     SD_CUDA(cudaEventSynchronize(ev_[i].second));
@@ -479,7 +507,7 @@ void DistEngine::run_step() {
       GemmArgs ga = w_->gemm_args(l, 0, nh, x_, D, xb_, D, nullptr, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
       ga.route = &r;
       launch_gemm_sm100(ga, stream_);
-      launch_p2p_wait(flags_, 0, from_homes, world_, r.epoch, stream_);
+      fused_wait(0, from_homes, r.epoch, kind_bytes(0));
     } else if (nh) {
       w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
     }
@@ -527,7 +555,7 @@ void DistEngine::run_step() {
                   fused ? &orr : nullptr);
     }
     if (fused) {
-      launch_p2p_wait(flags_, 1, from_shards, world_, orr.epoch, stream_);
+      fused_wait(1, from_shards, orr.epoch, kind_bytes(1));
     } else if (p2p_) {
       exchange_p2p(1);
     } else {

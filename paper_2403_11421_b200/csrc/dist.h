@@ -79,6 +79,8 @@ class DistEngine : public StepComputation {
   void exchange(const float* send, const std::vector<int32_t>& sc, const std::vector<int32_t>& so,
                 float* recv, const std::vector<int32_t>& rc, const std::vector<int32_t>& ro, int width);
   // kind 0: Q/K/V rows home -> shard; kind 1: attention rows shard -> home
+  double kind_bytes(int kind) const;
+  void fused_wait(int slot, uint32_t expect, int64_t epoch, double bytes);
   void exchange_p2p(int kind);
 
   Spec spec_;
