@@ -190,7 +190,7 @@ def run_dist(args, wl, rank, world, dev, dist):
     mode = args.shard_mode
     if mode != "sequence" and args.exchange != "p2p":
         raise SystemExit("--shard-mode head/hybrid needs --exchange p2p")
-    plan = sd.dist_plan(world, rank, s_ranks, seqs, mode, Hkv)
+    plan = sd.dist_plan(world, rank, s_ranks, seqs, mode, Hkv, home=args.home)
     h0, hc = (0, Hkv) if mode == "sequence" else sd.ShardMap(mode, Hkv, world).head_range(rank)
     mine = [seqs[i] for i in plan["shard_rows"]]
     nmax = torch.tensor([len(mine)], device=f"cuda:{dev}")
@@ -203,7 +203,7 @@ def run_dist(args, wl, rank, world, dev, dist):
     kv.prefill_synthetic(mine, ctx, salt=rank)
     obj = [sd.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks, shard_mode=mode)
+    eng = sd.DistEngine(weights, kv, rank, world, obj[0], s_ranks, shard_mode=mode, home=args.home)
     if args.exchange == "p2p":  # direct NVLink stores into the peers' receive buffers
         eng.enable_p2p(len(seqs))
     tokens = np.array([sd.prompt_token(0, s, V) for s in seqs], dtype=np.int32)
@@ -235,13 +235,13 @@ def run_dist(args, wl, rank, world, dev, dist):
 
     pin_in = torch.empty(len(seqs), dtype=torch.int32).pin_memory().numpy()
     pin_in[:] = tokens
+    eng.compute(seqs, pin_in)  # untimed: NCCL connects the token all-reduce lazily
     dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         nxt, _ = eng.compute(seqs, pin_in)
-        home = np.asarray(plan["home_rows"], dtype=np.int64)
-        pin_in[home] = nxt[home]
+        pin_in[:] = nxt  # the whole batch's next tokens on every rank
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -262,7 +262,9 @@ def run_dist(args, wl, rank, world, dev, dist):
                    "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
                    "parallelism": (f"kv sharded by mix64(seq)%{world} (ShardMap by-sequence); " if mode == "sequence"
                                    else f"kv sharded {mode} over {Hkv} kv heads (ShardMap {mode}); ")
-                                  + f"{s_ranks} S-rank(s); per-layer Q/K/V->shard, O->S over "
+                                  + f"{s_ranks} S-rank(s)"
+                                  + (f" with {args.home} homes" if s_ranks == world and mode == "sequence" else "")
+                                  + "; per-layer Q/K/V->shard, O->S over "
                                   + ("NVLink peer stores (CUDA IPC)" if args.exchange == "p2p" else "NCCL send/recv"),
                    "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": "attention (rank 0)", "achieved": achieved,
@@ -272,10 +274,12 @@ def run_dist(args, wl, rank, world, dev, dist):
                      "share_of_step": (a_ms / max(a_n, 1)) * args.steps * L / ms if ms else None},
         "exchange": {"ms_per_step": x_ms / args.steps, "bytes_per_step_rank0": x_bytes / args.steps,
                      "gbs": x_bytes / (x_ms / 1e3) / 1e9 if x_ms else None, "shard_rows_rank0": len(mine),
+                     "home_rows_rank0": len(plan["home_rows"]),
+                     "remote_rows_rank0": int(sum(c for d, c in enumerate(plan["send_counts"]) if d != rank)),
                      "max_shard_rows": cap_seqs},
         "e2e": {"value": B * world * args.e2e_steps / e2e_s, "unit": "tokens/s",
                 "h2d_bytes_per_step": int(len(plan["home_rows"]) * 4),
-                "d2h_bytes_per_step": int(len(plan["home_rows"]) * 4),
+                "d2h_bytes_per_step": int(len(seqs) * 4),  # every rank reads the batch's next tokens
                 "steps": args.e2e_steps, "api": "sd_dist_step (include/sd_abi.h)"},
         "gpu_launches": int(l1 - l0),
         "clocks": clocks,
@@ -394,7 +398,7 @@ def run_ours(args, wl, rank, world, dev, dist):
                    "s_part": f"{dense} tcgen05, fp32 accumulate", "r_part": "fp32 math over fp16 KV",
                    "parallelism": f"kv-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (KV cache 1000x the 126 MB L2)"},
-        "roofline": {"bound": "hbm", "kernel": "attn_kernel (split-K decode attention)",
+        "roofline": {"bound": "hbm", "kernel": "attn_mma_kernel (split-K decode attention, mma.sync over fp16 KV)",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "launches": a_n, "ms_per_launch": a_ms / max(a_n, 1),
@@ -456,6 +460,9 @@ def main():
                     help="N>1: S-workers (1 = the paper's single S-rank; 0 = every rank)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1: per-layer activation exchange transport")
+    ap.add_argument("--home", default="affinity", choices=["affinity", "modulo"],
+                    help="N>1, data-parallel S-ranks, by-sequence: S-Part placement (affinity: balanced "
+                         "homes on the KV's own rank where possible; modulo: seq %% world)")
     ap.add_argument("--shard-mode", default="sequence", choices=["sequence", "head", "hybrid"],
                     help="N>1: ShardMap mode of the KV shards (head/hybrid need --exchange p2p)")
     args = ap.parse_args()

@@ -67,6 +67,13 @@ enum sd_dense_mode {
 
 /* ShardMode (transport.hpp:150-170) */
 enum sd_shard_mode { SD_SHARD_BY_SEQUENCE = 0, SD_SHARD_BY_HEAD = 1, SD_SHARD_HYBRID = 2 };
+/* Home (S-Part) placement of a sequence when s_ranks == world, ORed into a
+ * shard_mode argument. Default under by-sequence sharding: shard-affine and
+ * balanced, each rank is home to floor/ceil(B / world) rows of the step,
+ * preferring the rows whose KV it holds (mix64(seq) % world), so only the
+ * overflow rows cross NVLink. SD_HOME_MODULO: home = seq % s_ranks, every
+ * row crosses when its shard is elsewhere (other shard modes always use it). */
+#define SD_HOME_MODULO 0x100
 
 /* ModelSpec (core.hpp:43-50); num_kv_heads is a GQA extension (0 = num_heads). */
 typedef struct sd_model_spec {
@@ -246,10 +253,13 @@ int sd_drive_destroy(sd_drive_result* r);
  * R-shard holding the sequences ShardMap by-sequence assigns it
  * (mix64(seq) % world, transport.cpp:352-353); S-ranks (rank 0 when
  * s_ranks == 1, the paper's topology; every rank when s_ranks == world)
- * run the S-Part for their home rows (seq % s_ranks). Per layer Q/K/V rows
- * go to the owning shard and O rows come back (send_layer / receive_layer,
- * workers.cpp:324-391) as NCCL grouped send/recv. Every rank passes the
- * full step batch; tokens are read and written for its home rows only. */
+ * run the S-Part for their home rows (SD_HOME_MODULO above: balanced and
+ * shard-affine by default, else seq % s_ranks). Per layer Q/K/V rows go to
+ * the owning shard and O rows come back (send_layer / receive_layer,
+ * workers.cpp:324-391) as NCCL grouped send/recv or peer stores. Every rank
+ * passes the full step batch and reads the tokens of its home rows; the
+ * next tokens of the whole batch come back on every rank (final activations
+ * for the home rows only). */
 typedef struct sd_dist sd_dist;
 /* ncclGetUniqueId into `out` (NCCL_UNIQUE_ID_BYTES = 128 bytes) on one rank. */
 int sd_nccl_unique_id(void* out, size_t bytes);
@@ -275,7 +285,7 @@ int sd_dist_timing_read(sd_dist* d, double* exchange_ms, double* exchange_bytes,
  * handles are gathered (rank order, world * SD_DIST_IPC_BYTES), connect maps
  * the peers' buffers. Every later step scatters rows with direct NVLink
  * stores and an epoch flag per (exchange, source). */
-#define SD_DIST_IPC_BYTES 192
+#define SD_DIST_IPC_BYTES 320
 int sd_dist_p2p_setup(sd_dist* d, int32_t max_rows, void* handles_out);
 int sd_dist_p2p_connect(sd_dist* d, const void* all_handles);
 /* Host-only row plan of a step (CPU-testable): home rows grouped by shard,

@@ -69,6 +69,8 @@ def _check(rc: int):
 FORMATS = {"single": 0, "half": 1, "int8": 2}
 DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2}
 SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2, "sequence": 0, "head": 1}
+# home (S-Part) placement with data-parallel S-ranks (SD_HOME_MODULO, include/sd_abi.h)
+HOME_POLICIES = {"affinity": 0, "modulo": 0x100}
 
 
 def _f32(a) -> np.ndarray:
@@ -436,16 +438,20 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def dist_plan(world: int, rank: int, s_ranks: int, seqs, shard_mode: str = "sequence", heads: int = 1):
+def dist_plan(world: int, rank: int, s_ranks: int, seqs, shard_mode: str = "sequence", heads: int = 1,
+              home: str = "affinity"):
     """Host row plan of one distributed step (sd_dist_plan); `heads` are the
-    kv heads the ShardMap splits under by-head / hybrid sharding."""
+    kv heads the ShardMap splits under by-head / hybrid sharding. `home`:
+    "affinity" (balanced, shard-affine homes under by-sequence sharding with
+    s_ranks == world) or "modulo" (home = seq % s_ranks)."""
     s, sp = _u64(seqs)
     B = len(s)
+    flags = SHARD_MODES[shard_mode] | HOME_POLICIES[home]
     home = np.zeros(max(B, 1), np.int32)
     shard = np.zeros(max(B, 1), np.int32)
     nh, ns = C.c_int32(), C.c_int32()
     sc, rc = np.zeros(world, np.int32), np.zeros(world, np.int32)
-    _check(lib.sd_dist_plan(world, rank, s_ranks, SHARD_MODES[shard_mode], heads, B, sp,
+    _check(lib.sd_dist_plan(world, rank, s_ranks, flags, heads, B, sp,
                             home.ctypes.data_as(I32P), C.byref(nh),
                             shard.ctypes.data_as(I32P), C.byref(ns), sc.ctypes.data_as(I32P),
                             rc.ctypes.data_as(I32P)))
@@ -460,16 +466,18 @@ class DistEngine:
     paper's topology); s_ranks = world: data-parallel S-workers."""
 
     def __init__(self, weights, kv: KvShard, rank: int, world: int, nccl_id: bytes | None,
-                 s_ranks: int = 1, shard_mode: str = "sequence"):
+                 s_ranks: int = 1, shard_mode: str = "sequence", home: str = "affinity"):
         """shard_mode: "sequence" (ShardMap by-sequence, the default), "head" or
         "hybrid" (over kv heads; `kv` holds this rank's head range, see
-        ShardMap.head_range; needs enable_p2p before the first step)."""
+        ShardMap.head_range; needs enable_p2p before the first step).
+        home: S-Part placement with s_ranks == world (see dist_plan)."""
         self.weights, self.kv, self.rank, self.world = weights, kv, rank, world
         self.spec = kv.spec
         self.h = C.c_void_p()
         idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id) if nccl_id else None
         _check(lib.sd_dist_create(weights.h if weights is not None else None, kv.h, rank, world,
-                                  idbuf, s_ranks, SHARD_MODES[shard_mode], C.byref(self.h)))
+                                  idbuf, s_ranks, SHARD_MODES[shard_mode] | HOME_POLICIES[home],
+                                  C.byref(self.h)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -508,7 +516,7 @@ class DistEngine:
         _check(lib.sd_dist_timing_read(self.h, C.byref(ms), C.byref(b), int(reset)))
         return ms.value, b.value
 
-    IPC_BYTES = 192
+    IPC_BYTES = 320
 
     def p2p_handles(self, max_rows: int) -> bytes:
         """Allocate this rank's peer-exchange receive buffers (up to `max_rows`
@@ -540,7 +548,7 @@ def run_generation(engine, batch: int, target_len: int, interval: int, steps: in
                    record_activations: bool = False):
     """drive_schedule (workers.cpp:547-684) over the GPU engine (Engine or
     DistEngine) -> (transcript [(step, seq, token)], activations, wall_seconds).
-    A DistEngine returns the rows its rank produced."""
+    A DistEngine returns the rows its rank produced (its home rows)."""
     cfg = DriveConfig(batch, target_len, interval,
                       {"fixed-interval": 0, "ramped-limit": 1}[cold_start], steps, load_limit,
                       seed, int(record_activations))

@@ -43,6 +43,7 @@ struct RowRoute {
   const int32_t* row;
   float* base[8];
   int64_t ld;
+  int32_t rows;  // rows of every base buffer (tensor-map extent)
   int64_t* flag[8];
   int32_t* done;  // grid arrival counter, zero between launches
   int64_t epoch;

@@ -23,6 +23,8 @@ struct Nccl {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   static Nccl& get() {
@@ -44,10 +46,11 @@ struct Nccl {
       SD_SYM(GroupEnd);
       SD_SYM(Send);
       SD_SYM(Recv);
+      SD_SYM(AllReduce);
       SD_SYM(GetErrorString);
 #undef SD_SYM
     });
-    if (!n.Send || !n.Recv || !n.CommInitRank) fail(SD_ERR_NCCL, "libnccl.so.2 unavailable: " + err);
+    if (!n.Send || !n.Recv || !n.CommInitRank || !n.AllReduce) fail(SD_ERR_NCCL, "libnccl.so.2 unavailable: " + err);
     return n;
   }
 };
@@ -62,7 +65,44 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 void nccl_unique_id(ncclUniqueId* id) { nccl_check(Nccl::get().GetUniqueId(id), "ncclGetUniqueId"); }
 
+// Home rank of every batch row. s_ranks == 1: rank 0 (the paper's single
+// S-worker). Data-parallel S-ranks under by-sequence sharding: each rank is
+// home to a balanced quota (floor/ceil of B / world), filled first with the
+// rows whose KV it holds, in batch order; the overflow rows of the heavier
+// shards fill the remaining quotas in rank order. Every rank derives the same
+// assignment from the batch. SD_HOME_MODULO (and the other shard modes):
+// seq % s_ranks.
+static void assign_homes(int world, int s_ranks, int B, const uint64_t* seqs, int mode, bool modulo,
+                         std::vector<int32_t>& home) {
+  home.assign(static_cast<size_t>(B), 0);
+  if (s_ranks <= 1) return;
+  if (modulo || mode != SD_SHARD_BY_SEQUENCE || s_ranks != world) {
+    for (int i = 0; i < B; ++i) home[static_cast<size_t>(i)] = home_of(seqs[i], s_ranks);
+    return;
+  }
+  std::vector<int32_t> quota(static_cast<size_t>(world)), cnt(static_cast<size_t>(world), 0);
+  for (int r = 0; r < world; ++r) quota[static_cast<size_t>(r)] = B / world + (r < B % world ? 1 : 0);
+  std::vector<int32_t> overflow;
+  for (int i = 0; i < B; ++i) {
+    const size_t pref = static_cast<size_t>(shard_of(seqs[i], world));
+    if (cnt[pref] < quota[pref]) {
+      home[static_cast<size_t>(i)] = static_cast<int32_t>(pref);
+      ++cnt[pref];
+    } else {
+      overflow.push_back(i);
+    }
+  }
+  size_t r = 0;
+  for (int32_t i : overflow) {
+    while (cnt[r] >= quota[r]) ++r;
+    home[static_cast<size_t>(i)] = static_cast<int32_t>(r);
+    ++cnt[r];
+  }
+}
+
 void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, DistPlan& p, int mode, int heads) {
+  const bool modulo = (mode & SD_HOME_MODULO) != 0;
+  mode &= ~SD_HOME_MODULO;
   if (mode == SD_SHARD_BY_SEQUENCE) {
     p.hg = 1;
     p.sg = world;
@@ -89,6 +129,7 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
   auto sg_of = [&](uint64_t seq) {
     return p.sg == 1 ? 0 : static_cast<int>(mix64(seq) % static_cast<uint64_t>(p.sg));
   };
+  assign_homes(world, s_ranks, B, seqs, mode, modulo, p.home);
   p.home_rows.clear();
   p.shard_rows.clear();
   p.shard_seqs.clear();
@@ -102,7 +143,7 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
   for (int g = 0; g < p.sg; ++g) {
     blk_off[static_cast<size_t>(g)] = static_cast<int32_t>(p.home_rows.size());
     for (int i = 0; i < B; ++i) {
-      if (home_of(seqs[i], s_ranks) == rank && sg_of(seqs[i]) == g) p.home_rows.push_back(i);
+      if (p.home[static_cast<size_t>(i)] == rank && sg_of(seqs[i]) == g) p.home_rows.push_back(i);
     }
     blk_cnt[static_cast<size_t>(g)] = static_cast<int32_t>(p.home_rows.size()) - blk_off[static_cast<size_t>(g)];
   }
@@ -116,7 +157,7 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
   for (int src = 0; src < world; ++src) {
     p.recv_off[static_cast<size_t>(src)] = static_cast<int32_t>(p.shard_rows.size());
     for (int i = 0; i < B; ++i) {
-      if (home_of(seqs[i], s_ranks) == src && sg_of(seqs[i]) == my_sg) {
+      if (p.home[static_cast<size_t>(i)] == src && sg_of(seqs[i]) == my_sg) {
         p.shard_rows.push_back(i);
         p.shard_seqs.push_back(seqs[i]);
       }
@@ -128,7 +169,7 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
 DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks,
                        int shard_mode)
     : spec_(kv->spec()), w_(w), kv_(kv), rank_(rank), world_(world), s_ranks_(s_ranks),
-      device_(kv->device()), mode_(shard_mode) {
+      device_(kv->device()), mode_(shard_mode & ~SD_HOME_MODULO), home_flags_(shard_mode & SD_HOME_MODULO) {
   if (world < 1 || rank < 0 || rank >= world) fail(SD_ERR_CONFIG, "bad rank / world");
   if (s_ranks != 1 && s_ranks != world) fail(SD_ERR_CONFIG, "s_ranks must be 1 or world");
   const bool s_rank = s_ranks == world || rank == 0;
@@ -146,6 +187,7 @@ DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void*
     }
   }
   DeviceGuard dg(device_);
+  phases_ = std::getenv("SD_DIST_PHASES") != nullptr;
   SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   if (world > 1) {
     ncclUniqueId id;
@@ -157,10 +199,28 @@ DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void*
 DistEngine::~DistEngine() {
   DeviceGuard dg(device_);
   cudaStreamSynchronize(stream_);
+  if (phases_ && !ph_.empty()) {
+    try {
+      flush_phases();
+    } catch (...) {
+    }
+  }
+  if (phases_ && ph_layers_) {
+    static const char* names[] = {"", "qkv", "recv_qkv", "append", "attend", "recv_o", "to_bf16", "w_o", "mlp_in", "mlp_out"};
+    std::string line = "[dist phases] rank " + std::to_string(rank_) + ", " + std::to_string(ph_layers_) +
+                       " layers, ms/layer:";
+    for (int i = 1; i < 10; ++i) {
+      char b[48];
+      std::snprintf(b, sizeof(b), " %s=%.4f", names[i], ph_ms_[i] / static_cast<double>(ph_layers_));
+      line += b;
+    }
+    line += "\n";
+    std::fputs(line.c_str(), stderr);  // one write: ranks share the terminal
+  }
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
                   static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_)}) {
+                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_)}) {
     if (p) cudaFree(p);
   }
   if (comm_) Nccl::get().CommDestroy(comm_);
@@ -168,7 +228,7 @@ DistEngine::~DistEngine() {
                   static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
                   static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
                   static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_)}) {
+                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_)}) {
     if (p) cudaFree(p);
   }
   for (auto& e : ev_) {
@@ -186,7 +246,7 @@ void DistEngine::ensure(int B) {
                   static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
                   static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
                   static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_)}) {
+                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_)}) {
     if (p) cudaFree(p);
   }
   const size_t bp = (static_cast<size_t>(B) + 127) / 128 * 128;
@@ -208,13 +268,21 @@ void DistEngine::ensure(int B) {
   zalloc(reinterpret_cast<void**>(&yb_), bp * s.D * 2);
   zalloc(reinterpret_cast<void**>(&hb_), bp * s.F * 2);
   zalloc(reinterpret_cast<void**>(&tok_), bp * 4);
+  zalloc(reinterpret_cast<void**>(&all_tok_), bp * 4);
+  zalloc(reinterpret_cast<void**>(&home_idx_), bp * 4);
   SD_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets before non-blocking-stream use
   cap_ = B;
 }
 
 void DistEngine::plan_for(int B, const uint64_t* seqs) {
   if (plan_key_.size() == static_cast<size_t>(B) && std::equal(plan_key_.begin(), plan_key_.end(), seqs)) return;
-  make_plan(world_, rank_, s_ranks_, B, seqs, plan_, mode_, spec_.Hkv);
+  make_plan(world_, rank_, s_ranks_, B, seqs, plan_, mode_ | home_flags_, spec_.Hkv);
+  home_set_.clear();
+  for (int32_t i : plan_.home_rows) home_set_.insert(seqs[i]);
+  if (!plan_.home_rows.empty()) {
+    SD_CUDA(cudaMemcpyAsync(home_idx_, plan_.home_rows.data(), plan_.home_rows.size() * 4, cudaMemcpyHostToDevice,
+                            stream_));
+  }
   plan_key_.assign(seqs, seqs + B);
   if (mode_ != SD_SHARD_BY_SEQUENCE && !p2p_) {
     fail(SD_ERR_CONFIG, "by-head / hybrid sharding needs the peer exchange (sd_dist_p2p_connect)");
@@ -226,7 +294,7 @@ void DistEngine::plan_for(int B, const uint64_t* seqs) {
     peer_o_off_.assign(static_cast<size_t>(world_), 0);
     DistPlan q;
     for (int d = 0; d < world_; ++d) {
-      make_plan(world_, d, s_ranks_, B, seqs, q, mode_, spec_.Hkv);
+      make_plan(world_, d, s_ranks_, B, seqs, q, mode_ | home_flags_, spec_.Hkv);
       peer_qkv_off_[static_cast<size_t>(d)] = q.recv_off[static_cast<size_t>(rank_)];
       peer_o_off_[static_cast<size_t>(d)] = q.send_off[static_cast<size_t>(rank_)];
       if (static_cast<int>(q.home_rows.size()) > p2p_cap_ || static_cast<int>(q.shard_rows.size()) > p2p_cap_) {
@@ -266,12 +334,13 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaStreamSynchronize(stream_));
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
                   static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_)}) {
+                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_)}) {
     if (p) cudaFree(p);
   }
   const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_qkv_), rows * spec_.qkv_width() * 4));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), rows * spec_.D * 4));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_ob_), rows * spec_.D * 2));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), 2 * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&done_), sizeof(int32_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&gemm_done_), sizeof(int32_t)));
@@ -283,11 +352,16 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaMemset(flags_, 0, 2 * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMemset(done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaDeviceSynchronize());
-  cudaIpcMemHandle_t h[3];
+  SD_CUDA(cudaMemset(rx_ob_, 0, rows * spec_.D * 2));
+  cudaIpcMemHandle_t h[4];
   SD_CUDA(cudaIpcGetMemHandle(&h[0], rx_qkv_));
   SD_CUDA(cudaIpcGetMemHandle(&h[1], rx_o_));
   SD_CUDA(cudaIpcGetMemHandle(&h[2], flags_));
+  SD_CUDA(cudaIpcGetMemHandle(&h[3], rx_ob_));
+  std::memset(handles_out, 0, kIpcBytes);
   std::memcpy(handles_out, h, sizeof(h));
+  const int32_t mode = w_ ? w_->mode() : -1;
+  std::memcpy(static_cast<uint8_t*>(handles_out) + sizeof(h), &mode, sizeof(mode));
   p2p_cap_ = max_rows;
   epoch_ = 0;
 }
@@ -297,22 +371,25 @@ void DistEngine::p2p_connect(const void* all_handles) {
   DeviceGuard dg(device_);
   const auto* hb = static_cast<const uint8_t*>(all_handles);
   for (int p = 0; p < world_; ++p) {
+    cudaIpcMemHandle_t h[4];
+    std::memcpy(h, hb + static_cast<size_t>(p) * kIpcBytes, sizeof(h));
+    std::memcpy(&peer_mode_[p], hb + static_cast<size_t>(p) * kIpcBytes + sizeof(h), sizeof(int32_t));
     if (p == rank_) {
       peer_qkv_[p] = rx_qkv_;
       peer_o_[p] = rx_o_;
       peer_flags_[p] = flags_;
+      peer_ob_[p] = rx_ob_;
       continue;
     }
-    cudaIpcMemHandle_t h[3];
-    std::memcpy(h, hb + static_cast<size_t>(p) * kIpcBytes, sizeof(h));
-    void* ptr[3];
-    for (int i = 0; i < 3; ++i) {
+    void* ptr[4];
+    for (int i = 0; i < 4; ++i) {
       SD_CUDA(cudaIpcOpenMemHandle(&ptr[i], h[i], cudaIpcMemLazyEnablePeerAccess));
       opened_.push_back(ptr[i]);
     }
     peer_qkv_[p] = static_cast<float*>(ptr[0]);
     peer_o_[p] = static_cast<float*>(ptr[1]);
     peer_flags_[p] = static_cast<int64_t*>(ptr[2]);
+    peer_ob_[p] = static_cast<__nv_bfloat16*>(ptr[3]);
   }
   p2p_ = true;
   // the exchange is fused into the producers when both have a routed form
@@ -453,7 +530,31 @@ void DistEngine::fused_wait(int slot, uint32_t expect, int64_t epoch, double byt
   }
 }
 
+void DistEngine::mark(int phase) {
+  if (!ph_on_) return;
+  cudaEvent_t e;
+  SD_CUDA(cudaEventCreate(&e));
+  SD_CUDA(cudaEventRecord(e, stream_));
+  ph_.emplace_back(phase, e);
+}
+
+void DistEngine::flush_phases() {
+  for (size_t i = 0; i < ph_.size(); ++i) {
+    SD_CUDA(cudaEventSynchronize(ph_[i].second));
+    if (ph_[i].first == 0) {
+      ++ph_layers_;
+    } else {
+      float t = 0;
+      SD_CUDA(cudaEventElapsedTime(&t, ph_[i - 1].second, ph_[i].second));
+      ph_ms_[ph_[i].first] += t;
+    }
+  }
+  for (auto& p : ph_) cudaEventDestroy(p.second);
+  ph_.clear();
+}
+
 void DistEngine::read_timing(double* ms, double* bytes, bool reset) {
+  if (phases_) flush_phases();
   for (size_t i = 0; i < ev_.size(); ++i) {
     SD_CUDA(cudaEventSynchronize(ev_[i].second));
     float t = 0;
@@ -488,6 +589,8 @@ void DistEngine::run_step() {
     if (plan_.recv_cnt[static_cast<size_t>(d)] > 0) from_homes |= 1u << d, to_homes |= 1u << d;
   }
   for (int l = 0; l < s.L; ++l) {
+    ph_on_ = phases_ && l % 8 == 0;
+    mark(0);
     if (route_qkv) {
       // project_qkv with the exchange in its epilogue: every home row lands in
       // its shard's receive buffer; the last CTA publishes the epoch
@@ -495,6 +598,7 @@ void DistEngine::run_step() {
       r.rank = tbl;
       r.row = tbl + nh;
       r.ld = qkvw;
+      r.rows = (p2p_cap_ + 127) / 128 * 128;  // every rank's rx_qkv_ (p2p_setup)
       for (int d = 0; d < world_; ++d) {
         r.base[d] = peer_qkv_[d];
         r.flag[d] = peer_flags_[d];
@@ -507,9 +611,12 @@ void DistEngine::run_step() {
       GemmArgs ga = w_->gemm_args(l, 0, nh, x_, D, xb_, D, nullptr, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
       ga.route = &r;
       launch_gemm_sm100(ga, stream_);
+      mark(1);
       fused_wait(0, from_homes, r.epoch, kind_bytes(0));
+      mark(2);
     } else if (nh) {
       w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+      mark(1);
     }
     if (fused && !route_qkv) {  // nothing to send (or exact mode): the same flags / epochs
       if (nh) {
@@ -528,6 +635,7 @@ void DistEngine::run_step() {
       // (sent above)
     } else if (p2p_) {
       exchange_p2p(0);
+      mark(2);
     } else {
       exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s, plan_.recv_cnt, plan_.recv_off, qkvw);
     }
@@ -537,9 +645,15 @@ void DistEngine::run_step() {
       orr.row = tbl + 2 * nh + ns;
       orr.ld = D;
       for (int d = 0; d < world_; ++d) {
-        orr.base[d] = peer_o_[d];
+        // a bf16 home takes its W_o operand straight from the attention
+        if (peer_mode_[d] == SD_DENSE_BF16) {
+          orr.bbase[d] = peer_ob_[d];
+        } else {
+          orr.base[d] = peer_o_[d];
+        }
         orr.flag[d] = peer_flags_[d];
       }
+      orr.bld = D;
       orr.done = attn_done_;
       orr.epoch = ++epoch_;
       orr.notify = to_homes;
@@ -551,21 +665,30 @@ void DistEngine::run_step() {
         pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
       }
       kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + sq, srow, qkv_s + sq + sk, srow, stream_);
+      mark(3);
       kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, srow, o_s_, p2p_ ? sq : D, stream_, 0, nullptr, 0,
                   fused ? &orr : nullptr);
+      mark(4);
     }
     if (fused) {
       fused_wait(1, from_shards, orr.epoch, kind_bytes(1));
+      mark(5);
     } else if (p2p_) {
       exchange_p2p(1);
+      mark(5);
     } else {
       exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h, plan_.send_cnt, plan_.send_off, D);
     }
     if (nh) {
-      if (bf) launch_to_bf16(nh, D, o_h, D, ob_, D, stream_);
-      w_->linear(l, 4, nh, o_h, D, ob_, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
+      __nv_bfloat16* ob = fused && bf ? rx_ob_ : ob_;  // fused: the attention wrote it
+      if (bf && !fused) launch_to_bf16(nh, D, o_h, D, ob_, D, stream_);
+      mark(6);
+      w_->linear(l, 4, nh, o_h, D, ob, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
+      mark(7);
       w_->linear(l, 5, nh, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0, stream_);
+      mark(8);
       w_->linear(l, 6, nh, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D, stream_);
+      mark(9);
     }
   }
   if (nh) {
@@ -589,18 +712,28 @@ void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int
   }
   if (nh) SD_CUDA(cudaMemcpyAsync(tok_, host_tok_.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
   run_step();
-  std::vector<float> fx;
-  if (nh) {
+  // every rank returns the whole batch's next tokens: a row's home can move
+  // between steps (balanced homes follow the batch), so each rank's caller
+  // keeps every sequence's last token. Homes write their rows into a zeroed
+  // batch vector, summed across ranks (B int32 per step).
+  if (world_ > 1) {
+    SD_CUDA(cudaMemsetAsync(all_tok_, 0, static_cast<size_t>(B) * 4, stream_));
+    launch_scatter_i32(nh, home_idx_, tok_, all_tok_, stream_);
+    nccl_check(Nccl::get().AllReduce(all_tok_, all_tok_, static_cast<size_t>(B), ncclInt32, ncclSum, comm_, stream_),
+               "ncclAllReduce");
+    SD_CUDA(cudaMemcpyAsync(next, all_tok_, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
+  } else if (nh) {
     SD_CUDA(cudaMemcpyAsync(host_tok_.data(), tok_, static_cast<size_t>(nh) * 4, cudaMemcpyDeviceToHost, stream_));
-    if (final_x) {
-      fx.resize(static_cast<size_t>(nh) * spec_.D);
-      SD_CUDA(cudaMemcpyAsync(fx.data(), x_, fx.size() * 4, cudaMemcpyDeviceToHost, stream_));
-    }
+  }
+  std::vector<float> fx;
+  if (nh && final_x) {
+    fx.resize(static_cast<size_t>(nh) * spec_.D);
+    SD_CUDA(cudaMemcpyAsync(fx.data(), x_, fx.size() * 4, cudaMemcpyDeviceToHost, stream_));
   }
   SD_CUDA(cudaStreamSynchronize(stream_));
   for (int i = 0; i < nh; ++i) {
     const int row = plan_.home_rows[static_cast<size_t>(i)];
-    next[row] = host_tok_[static_cast<size_t>(i)];
+    if (world_ == 1) next[row] = host_tok_[static_cast<size_t>(i)];
     if (final_x) {
       std::memcpy(final_x + static_cast<size_t>(row) * spec_.D, fx.data() + static_cast<size_t>(i) * spec_.D,
                   static_cast<size_t>(spec_.D) * 4);

@@ -9,6 +9,7 @@
 
 #include <nccl.h>
 
+#include <unordered_set>
 #include <vector>
 
 #include "dist_p2p.cuh"
@@ -34,6 +35,7 @@ inline int shard_of(uint64_t seq, int world) {
 // are one contiguous block (send_layer's per-worker filter, workers.cpp:336-351).
 struct DistPlan {
   int mode = 0, hg = 1, sg = 1;     // shard mode, head groups, sequence groups
+  std::vector<int32_t> home;        // home rank of every batch row
   std::vector<int32_t> home_rows;   // batch rows this rank runs the S-Part for, grouped by seq group
   std::vector<int32_t> send_cnt, send_off;  // per destination worker: block of home rows
   std::vector<int32_t> shard_rows;  // batch rows whose KV lives here, grouped by source S-rank
@@ -56,7 +58,9 @@ class DistEngine : public StepComputation {
   void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
                float* final_x) override;
   void retire(int n, const uint64_t* seqs) override;
-  bool owns(uint64_t seq) const override { return home_of(seq, s_ranks_) == rank_; }
+  // whether this rank produced `seq`'s token in the last step (homes are
+  // assigned per step batch)
+  bool owns(uint64_t seq) const override { return home_set_.count(seq) != 0; }
   int shard_mode() const { return mode_; }
   int model_dim() const override { return spec_.D; }
   int vocab() const override { return spec_.V; }
@@ -67,7 +71,8 @@ class DistEngine : public StepComputation {
   // Peer-memory exchange (dist_p2p.cu): allocate fixed receive buffers for
   // up to `max_rows` rows and export their CUDA IPC handles (kIpcBytes);
   // connect() maps every rank's buffers (world x kIpcBytes, rank order).
-  static constexpr size_t kIpcBytes = 3 * sizeof(cudaIpcMemHandle_t);
+  // [rx_qkv | rx_o | flags | rx_ob handles][int32 dense mode of this rank, -1 none][pad]
+  static constexpr size_t kIpcBytes = 4 * sizeof(cudaIpcMemHandle_t) + 64;
   void p2p_setup(int max_rows, void* handles_out);
   void p2p_connect(const void* all_handles);
   bool p2p() const { return p2p_; }
@@ -82,6 +87,14 @@ class DistEngine : public StepComputation {
   double kind_bytes(int kind) const;
   void fused_wait(int slot, uint32_t expect, int64_t epoch, double bytes);
   void exchange_p2p(int kind);
+  // SD_DIST_PHASES=1: per-phase CUDA events on every 8th layer, summed into
+  // ph_ms_ and printed to stderr per rank when the engine is destroyed
+  void mark(int phase);
+  void flush_phases();
+  bool phases_ = false, ph_on_ = false;
+  std::vector<std::pair<int, cudaEvent_t>> ph_;
+  double ph_ms_[12] = {};
+  int64_t ph_layers_ = 0;
 
   Spec spec_;
   Weights* w_;
@@ -90,12 +103,16 @@ class DistEngine : public StepComputation {
   ncclComm_t comm_ = nullptr;
   cudaStream_t stream_ = nullptr;
   DistPlan plan_;
+  int home_flags_ = 0;  // SD_HOME_MODULO or 0
+  std::unordered_set<uint64_t> home_set_;
   std::vector<uint64_t> plan_key_;
   int cap_ = 0;
   float *x_ = nullptr, *qkv_h_ = nullptr, *qkv_s_ = nullptr, *o_s_ = nullptr, *o_h_ = nullptr,
         *y_ = nullptr, *h_ = nullptr, *logits_ = nullptr;
   __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
   int32_t* tok_ = nullptr;
+  int32_t* all_tok_ = nullptr;   // [B] next tokens of the whole batch (compute)
+  int32_t* home_idx_ = nullptr;  // [home rows] batch row of each home row
   std::vector<uint32_t> pos_;
   std::vector<int32_t> host_tok_;
   bool timing_ = false;
@@ -106,6 +123,7 @@ class DistEngine : public StepComputation {
   bool p2p_ = false;
   int p2p_cap_ = 0;
   float *rx_qkv_ = nullptr, *rx_o_ = nullptr;  // receive buffers (shard rows / home rows)
+  __nv_bfloat16* rx_ob_ = nullptr;             // home rows' attention output as the bf16 W_o operand
   // fused exchange: the QKV GEMM and the attention store rows straight into
   // the peers' buffers (RowRoute / ORoute) and publish the epoch themselves.
   // Decided from rank-independent facts (a sender may still use the scatter
@@ -119,6 +137,8 @@ class DistEngine : public StepComputation {
   int32_t* done_ = nullptr;
   float* peer_qkv_[kMaxWorld] = {};
   float* peer_o_[kMaxWorld] = {};
+  __nv_bfloat16* peer_ob_[kMaxWorld] = {};
+  int peer_mode_[kMaxWorld] = {};  // each rank's dense mode (-1: no weights)
   int64_t* peer_flags_[kMaxWorld] = {};
   std::vector<void*> opened_;
   int64_t epoch_ = 0;

@@ -104,6 +104,20 @@ void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s) {
   count_launch();
 }
 
+__global__ void scatter_i32_kernel(int n, const int32_t* idx, const int32_t* src, int32_t* dst) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = src[i];
+  pdl_trigger();
+}
+
+void launch_scatter_i32(int n, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s) {
+  if (n <= 0) return;
+  SD_CUDA(launch_pdl(scatter_i32_kernel, dim3((n + 255) / 256), dim3(256), 0, s, 1, n, idx, src, dst));
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s) {
   if (!expect) return;
   SD_CUDA(launch_pdl(p2p_wait_kernel, dim3(1), dim3(32), 0, s, 1, flags, slot, expect, world, epoch));

@@ -33,6 +33,8 @@ struct P2PScatter {
 };
 
 void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s);
+// dst[idx[i]] = src[i] for i < n (a rank's next tokens into the batch vector)
+void launch_scatter_i32(int n, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s);
 // wait until flags[slot][src] >= epoch for every src bit in `expect`
 void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s);
 

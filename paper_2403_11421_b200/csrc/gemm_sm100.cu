@@ -55,6 +55,8 @@ struct Params {
   int tma_out;  // outputs written by TMA tensor stores
   int diag;  // 1: reuse resident smem after the first ring fill (MMA-rate probe)
   int routed;      // C rows go to route.base[route.rank[m]] (fused multi-GPU exchange)
+  int route_bulk;  // routed rows leave through bulk copies (else smem-transposed st.global)
+  int route_tma;   // contiguous 32-row slabs leave as tensor stores (RouteMaps)
   RowRoute route;
 };
 
@@ -288,6 +290,12 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// contiguous smem -> global bulk copy (any mapped global address, peers included)
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void sts128(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -347,10 +355,17 @@ __device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, ui
   }
 }
 
+// fp32 tensor maps (64-B swizzle, 16-column x 32-row boxes) of a routed
+// GEMM's destination buffers, one per rank
+struct RouteMaps {
+  CUtensorMap m[8];
+};
+
 template <int BN, bool PAIR, int ATOMS, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_cb, const Params p) {
+                const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_cb, const Params p,
+                const __grid_constant__ RouteMaps rmaps) {
   using C_ = Cfg<BN, PAIR, ATOMS>;
   constexpr int STAGES = C_::STAGES;
   constexpr int KELEMS = BK_BYTES / (KIND == 2 ? 4 : 2);  // elements per atom row
@@ -608,12 +623,100 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
       const bool rowok = row < p.M && !(p.diag & 4);
+      // routed rows (peer memory over NVLink): each lane's destination row,
+      // resolved once per tile
+      float* rrow = p.routed && rowok ? p.route.base[p.route.rank[row]] + p.route.row[row] * p.route.ld : nullptr;
+      // a warp slab whose 32 rows land on consecutive rows of one buffer (the
+      // common case: home rows are grouped by destination) leaves as TMA
+      // tensor stores, 16 columns x 32 rows per store
+      bool slab = false;
+      int slab_rank = 0, slab_row = 0;
+      if (p.routed) {
+        const int rk = rowok ? p.route.rank[row] : -1, rw = rowok ? p.route.row[row] : -1;
+        slab_rank = __shfl_sync(0xffffffffu, rk, 0);
+        slab_row = __shfl_sync(0xffffffffu, rw, 0);
+        slab = p.route_tma && __all_sync(0xffffffffu, rk >= 0 && rk == slab_rank && rw == slab_row + lane) != 0;
+        bulk_wait_read<0>();  // no copy of the previous tile still reads this warp's staging
+        __syncwarp();
+      }
+      int nchunk = 0;
 #pragma unroll 1
       for (int c = 0; c < (p.bn + 31) / 32; ++c) {
         const int col0 = n0 + c * 32;
         if (col0 >= nend) break;  // warp-uniform
         float v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+        if (p.routed) {
+          // transpose the 32x32 chunk through smem so that every store
+          // instruction writes 128 contiguous bytes of one row (4 rows per
+          // instruction) instead of 32 rows x 16 B: remote NVLink writes
+          // are packetised per contiguous run. 16-B chunks XOR-swizzled by
+          // row, conflict-free on both sides. (kEpiNone; host-checked)
+          float* st = reinterpret_cast<float*>(sOut + (warp - 2) * C_::OUT_WARP);
+          const int ncols = nend - col0 < 32 ? nend - col0 : 32;  // multiple of 16
+          if (slab) {
+            uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h * 16 >= ncols) break;  // warp-uniform
+              uint8_t* bf = myout + (nchunk & 1) * (C_::OUT_F32 + C_::OUT_BF16);
+              ++nchunk;
+              if (lane == 0) bulk_wait_read<1>();  // this buffer's store (two chunks ago) has read it
+              __syncwarp();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // row = lane, 64 B, 64-B swizzle
+                sts128(bf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), __float_as_uint(v[h * 16 + 4 * j]),
+                       __float_as_uint(v[h * 16 + 4 * j + 1]), __float_as_uint(v[h * 16 + 4 * j + 2]),
+                       __float_as_uint(v[h * 16 + 4 * j + 3]));
+              }
+              fence_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&rmaps.m[slab_rank], bf, col0 + h * 16, slab_row);
+                bulk_commit();
+              }
+            }
+            continue;
+          }
+          if (p.route_bulk) {
+            // each lane stages its own row (144-B stride, conflict-free) and
+            // hands it to the bulk-copy engine: one async smem->peer copy per
+            // row, no LSU slots held while the NVLink writes drain
+            float* mine = st + lane * 36;
+            bulk_wait_read<0>();  // this lane's previous copy has read its row
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              sts128(mine + 4 * k, __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                     __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+            }
+            if (rrow) {
+              fence_async_smem();
+              bulk_s2g(rrow + col0, mine, static_cast<uint32_t>(ncols) * 4u);
+              bulk_commit();
+            }
+            __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
+            continue;
+          }
+          __syncwarp();  // the previous chunk's reads are done
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            sts128(st + lane * 32 + ((k ^ (lane & 7)) << 2), __float_as_uint(v[4 * k]),
+                   __float_as_uint(v[4 * k + 1]), __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+          }
+          __syncwarp();
+          const int c4 = lane & 7;
+#pragma unroll 4
+          for (int r = 0; r < 32; r += 4) {
+            const int rr = r + (lane >> 3);
+            float* dst = reinterpret_cast<float*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rrow), rr));
+            if (dst && c4 * 4 < ncols) {
+              const float4 t = *reinterpret_cast<const float4*>(st + rr * 32 + ((c4 ^ (rr & 7)) << 2));
+              *reinterpret_cast<float4*>(dst + col0 + c4 * 4) = t;
+            }
+          }
+          continue;
+        }
         if (!rowok) continue;
         const int ncols = nend - col0 < 32 ? nend - col0 : 32;
         if (p.vec && ncols == 32) {
@@ -685,10 +788,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  if (p.routed) __threadfence_system();  // this thread's routed stores before the CTA is counted
+  if (p.routed) bulk_wait_all();  // this thread's row copies / tensor stores have landed
   __syncthreads();
   if (p.routed && threadIdx.x == 0) {
-    // the last CTA publishes this exchange's epoch to every destination
+    // one system-scope fence per CTA: cumulative over the CTA's routed
+    // stores, which the barrier ordered before it; then the last CTA
+    // publishes this exchange's epoch to every destination
+    __threadfence_system();
     if (atomicAdd(p.route.done, 1) == static_cast<int>(gridDim.x) - 1) {
       __threadfence_system();
       for (int d = 0; d < 8; ++d) {
@@ -1134,6 +1240,7 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   const CUtensorMap tcb = tma_out && g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, 1, 32, 32) : ta;
   const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, g.kind, PAIR ? bn / 2 : BN / cs);
   Params p{};
+  RouteMaps rmaps{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
@@ -1152,11 +1259,20 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   p.kind = KIND;
   p.bn = bn;
   p.diag = env_int("SD_GEMM_DIAG");
-  p.tma_out = tma_out && !g.route ? 1 : 0;  // routed rows use the per-row vector epilogue
+  p.tma_out = tma_out && !g.route ? 1 : 0;  // routed rows use the smem-transposed row stores
   if (g.route) {
     p.routed = 1;
+    p.route_bulk = env_int("SD_ROUTE_ST") == 0 ? 1 : 0;
+    p.route_tma = env_int("SD_ROUTE_NO_TMA") == 0 && g.route->rows > 0 ? 1 : 0;
     p.route = *g.route;
+    for (int d = 0; d < 8 && p.route_tma; ++d) {
+      if (g.route->base[d]) {
+        if (!al16(g.route->base[d])) fail(SD_ERR_CONFIG, "routed GEMM: destination buffers must be 16-B aligned");
+        rmaps.m[d] = make_map(g.route->base[d], g.route->rows, g.N, g.route->ld, 2, 32, 64);
+      }
+    }
     if (g.N % 32 || g.route->ld % 4) fail(SD_ERR_CONFIG, "routed GEMM: N and the row stride must be multiples of 32 / 4");
+    if (g.C || g.Cb || g.epi != kEpiNone) fail(SD_ERR_CONFIG, "routed GEMM: plain fp32 rows only");
   }
   p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
           (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));
@@ -1168,7 +1284,7 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
   SD_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(clusters * cs)), dim3(kThreads), C_::SMEM, s,
-                     static_cast<unsigned>(cs), ta, tb, tc, tcb, p));
+                     static_cast<unsigned>(cs), ta, tb, tc, tcb, p, rmaps));
   count_launch();
 }
 

@@ -537,9 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
   }
   if (a.routed) {
-    // every consumer's routed o stores, then the last CTA publishes the epoch
-    __threadfence_system();
+    // every consumer's routed o stores, ordered by the barrier before one
+    // cumulative system-scope fence; then the last CTA publishes the epoch
     named_bar(15, kWarps * 32);  // the consumer warps (the producer has returned)
+    if (threadIdx.x == 0) __threadfence_system();
     if (threadIdx.x == 0 && atomicAdd(a.oroute.done, 1) == static_cast<int>(gridDim.x) - 1) {
       __threadfence_system();
       for (int d = 0; d < 8; ++d) {

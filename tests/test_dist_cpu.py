@@ -17,22 +17,58 @@ def _free_port():
     return p
 
 
+def _affinity_homes(world, seqs, oracle):
+    """Restatement of the balanced shard-affine home assignment
+    (dist.cpp assign_homes): quotas floor/ceil(B / world), rows fill their
+    KV rank's quota in batch order, the overflow fills the rest in rank order."""
+    B = len(seqs)
+    quota = [B // world + (1 if r < B % world else 0) for r in range(world)]
+    cnt, home, over = [0] * world, [0] * B, []
+    for i, q in enumerate(seqs):
+        r = oracle.shardmap_worker_for("by-sequence", 8, world, q, 0)
+        if cnt[r] < quota[r]:
+            home[i], cnt[r] = r, cnt[r] + 1
+        else:
+            over.append(i)
+    r = 0
+    for i in over:
+        while cnt[r] >= quota[r]:
+            r += 1
+        home[i], cnt[r] = r, cnt[r] + 1
+    return home
+
+
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("s_mode", ["single", "all"])
-def test_plan_partitions_rows_and_follows_shardmap(oracle, world, s_mode):
+@pytest.mark.parametrize("home", ["affinity", "modulo"])
+def test_plan_partitions_rows_and_follows_shardmap(oracle, world, s_mode, home):
     import paper_2403_11421_b200 as sd
     s_ranks = 1 if s_mode == "single" else world
     rng = np.random.default_rng(world)
     seqs = [int(x) for x in rng.choice(10**6, size=97, replace=False) + 1]
-    plans = [sd.dist_plan(world, r, s_ranks, seqs) for r in range(world)]
+    plans = [sd.dist_plan(world, r, s_ranks, seqs, home=home) for r in range(world)]
     homes = sorted(i for p in plans for i in p["home_rows"])
     shards = sorted(i for p in plans for i in p["shard_rows"])
     assert homes == list(range(len(seqs))) and shards == list(range(len(seqs)))
+    if s_ranks == 1:
+        want = [0] * len(seqs)
+    elif home == "modulo":
+        want = [q % s_ranks for q in seqs]
+    else:
+        want = _affinity_homes(world, seqs, oracle)
     for r, p in enumerate(plans):
         for i in p["shard_rows"]:  # ShardMap by-sequence, bit-exact (transport.cpp:352-353)
             assert oracle.shardmap_worker_for("by-sequence", 8, world, seqs[i], 0) == r
         for i in p["home_rows"]:
-            assert (seqs[i] % s_ranks if s_ranks > 1 else 0) == r
+            assert want[i] == r
+    if s_ranks == world and home == "affinity":
+        # balanced S-Part, and only the unavoidable rows cross between ranks
+        B = len(seqs)
+        assert all(len(p["home_rows"]) in (B // world, -(-B // world)) for p in plans)
+        shard_n = [len(p["shard_rows"]) for p in plans]
+        quota = [B // world + (1 if r < B % world else 0) for r in range(world)]
+        cross = sum(c for r, p in enumerate(plans) for d, c in enumerate(p["send_counts"]) if d != r)
+        assert cross == sum(max(0, n - q) for n, q in zip(shard_n, quota))
     for r in range(world):
         for d in range(world):
             assert plans[r]["send_counts"][d] == plans[d]["recv_counts"][r]

@@ -102,47 +102,66 @@ def _fused_worker(rank, world, port, out_path, s_ranks):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     spec = sd.make_model_spec(2, 1024, 8, 1024, 512, 2)
     seqs = list(range(1, 97))
+    B = len(seqs)
     results = {}
-    for fused in (True, False):
-        if fused:
-            os.environ.pop("SD_DIST_NO_FUSE", None)
-        else:
-            os.environ["SD_DIST_NO_FUSE"] = "1"
-        obj = [sd.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        is_s = s_ranks == world or rank == 0
-        w = sd.DeviceWeights(spec, None, "bf16", rank, seed=5) if is_s else None
-        plan = sd.dist_plan(world, rank, s_ranks, seqs)
-        mine = [seqs[i] for i in plan["shard_rows"]]
-        kv = sd.KvShard(spec, 0, 2, 96 * 64, "half", rank, max_sequences=96, max_seq_len=64)
-        kv.prefill_synthetic(mine, 20, salt=0)
-        eng = sd.DistEngine(w, kv, rank, world, obj[0], s_ranks)
-        eng.enable_p2p(len(seqs))
-        tok = np.array([sd.prompt_token(0, s, spec.vocab_size) for s in seqs], np.int32)
-        outs = []
-        for _ in range(3):
-            nxt, fx = eng.compute(seqs, tok, want_final=True)
-            home = np.asarray(plan["home_rows"], np.int64)
-            outs.append((nxt[home].copy(), fx[home].copy()))
-            tok = tok.copy()
-            tok[home] = nxt[home]
-            allt = [None] * world
-            dist.all_gather_object(allt, (home.tolist(), nxt[home].tolist()))
-            for h, t in allt:
-                tok[np.asarray(h, np.int64)] = np.asarray(t, np.int32)
-        results[fused] = outs
-        eng.close()
-        kv.close()
-        if w is not None:
-            w.close()
-        dist.barrier()
+    homes = ("affinity", "modulo") if s_ranks == world else ("affinity",)
+    for home_policy in homes:
+        for fused in (True, False):
+            if fused:
+                os.environ.pop("SD_DIST_NO_FUSE", None)
+            else:
+                os.environ["SD_DIST_NO_FUSE"] = "1"
+            obj = [sd.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            is_s = s_ranks == world or rank == 0
+            w = sd.DeviceWeights(spec, None, "bf16", rank, seed=5) if is_s else None
+            plan = sd.dist_plan(world, rank, s_ranks, seqs, home=home_policy)
+            # the synthetic prefill is keyed by KV slot: allocate slots in sequence
+            # order so both placements hold the same context per sequence
+            mine = sorted(seqs[i] for i in plan["shard_rows"])
+            kv = sd.KvShard(spec, 0, 2, 96 * 64, "half", rank, max_sequences=96, max_seq_len=64)
+            kv.prefill_synthetic(mine, 20, salt=0)
+            eng = sd.DistEngine(w, kv, rank, world, obj[0], s_ranks, home=home_policy)
+            eng.enable_p2p(len(seqs))
+            tok = np.array([sd.prompt_token(0, s, spec.vocab_size) for s in seqs], np.int32)
+            outs = []
+            for _ in range(3):
+                nxt, fx = eng.compute(seqs, tok, want_final=True)
+                home = np.asarray(plan["home_rows"], np.int64)
+                allt = [None] * world
+                dist.all_gather_object(allt, (home.tolist(), nxt[home].tolist(), fx[home].tolist()))
+                full_t = np.zeros(B, np.int32)
+                full_x = np.zeros((B, spec.model_dim), np.float32)
+                for h, t, x in allt:
+                    full_t[np.asarray(h, np.int64)] = np.asarray(t, np.int32)
+                    full_x[np.asarray(h, np.int64)] = np.asarray(x, np.float32).reshape(-1, spec.model_dim)
+                outs.append((full_t, full_x))
+                tok = full_t.copy()
+            results[(home_policy, fused)] = outs
+            eng.close()
+            kv.close()
+            if w is not None:
+                w.close()
+            dist.barrier()
+    # fused vs scatter: bitwise under each placement
     ok = all(np.array_equal(a[0], b[0]) and np.array_equal(a[1].view(np.uint32), b[1].view(np.uint32))
-             for a, b in zip(results[True], results[False]))
+             for h in homes for a, b in zip(results[(h, True)], results[(h, False)]))
+    # across placements a shard attends the same rows in another order (the
+    # split-K plan follows the order) and a last-bit change of an attention
+    # output can flip a bf16 operand rounding in the next GEMM: same tokens,
+    # activations within the bf16 S-Part's relative precision (2^-8 per
+    # rounding, a few roundings deep)
+    worst = 0.0
+    for h in homes[1:]:
+        for a, b in zip(results[(homes[0], True)], results[(h, True)]):
+            ok = ok and np.array_equal(a[0], b[0])
+            worst = max(worst, float(np.abs(a[1] - b[1]).max() / max(np.abs(a[1]).max(), 1e-30)))
+    ok = ok and worst <= 2e-2
     flags = [None] * world
     dist.all_gather_object(flags, ok)
     if rank == 0:
         with open(out_path, "w") as f:
-            f.write("ok" if all(flags) else "mismatch")
+            f.write("ok" if all(flags) else f"mismatch (relative placement delta {worst:g})")
     dist.destroy_process_group()
 
 
@@ -153,7 +172,10 @@ def test_two_gpu_fused_exchange_is_bitwise_equal(tmp_path, s_ranks):
     home row into its shard's receive buffer over NVLink; the attention stores
     o rows into the home rank's buffer; the last CTA of each publishes the
     epoch) moves exactly the bytes of the separate scatter kernel: tokens and
-    final activations are bitwise equal over three steps."""
+    final activations of the whole batch are bitwise equal over three steps,
+    under either S-Part placement (balanced shard-affine homes, seq % world).
+    Between the placements tokens match and activations agree within the
+    bf16 S-Part's relative precision."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "fused.txt")
     mp.spawn(_fused_worker, args=(2, _free_port(), out, s_ranks), nprocs=2, join=True)
