@@ -487,8 +487,8 @@ class DistEngine:
     __del__ = close
 
     def compute(self, seqs, tokens, want_final=False):
-        """One step over the full batch; next tokens (and final activations)
-        are valid for this rank's home rows."""
+        """One step over the full batch: next tokens of every row (homes can move
+        between steps); final activations for this rank's home rows."""
         s, sp = _u64(seqs)
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         nxt = np.full(len(s), -1, np.int32)

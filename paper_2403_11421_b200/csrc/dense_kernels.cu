@@ -160,6 +160,24 @@ void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* 
   ::sd::count_launch();
 }
 
+__global__ void argmax_keys_kernel(int B, unsigned long long* keys, int32_t* tokens) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) {
+    const unsigned long long k = keys[i];
+    tokens[i] = k ? static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k)) : 0;  // all-NaN row: index 0
+    keys[i] = 0;
+  }
+  pdl_trigger();
+}
+
+void launch_argmax_keys(int B, unsigned long long* keys, int32_t* tokens, cudaStream_t s) {
+  if (B <= 0) return;
+  SD_CUDA(launch_pdl(argmax_keys_kernel, dim3((B + 127) / 128), dim3(128), 0, s, 1, B, keys, tokens));
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
+
 void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
                    cudaStream_t s) {
   if (B == 0) return;

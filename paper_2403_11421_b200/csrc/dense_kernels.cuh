@@ -24,6 +24,9 @@ void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, co
 void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
                   __nv_bfloat16* xb, cudaStream_t s);
 // argmax_token per row (first index wins ties, dense.cpp:78-88)
+// tokens[i] from the fused-argmax keys (first maximum wins, as
+// argmax_token dense.cpp:80-88); resets the keys to zero for the next launch
+void launch_argmax_keys(int B, unsigned long long* keys, int32_t* tokens, cudaStream_t s);
 void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
                    cudaStream_t s);
 // fp32 -> bf16 copy (activation staging for the tensor-core GEMMs)
@@ -67,6 +70,10 @@ struct GemmArgs {
   int kind;      // 1 = bf16 (kind::f16), 2 = tf32
   int max_ctas;  // SM budget of the persistent grid (0 = every SM)
   const RowRoute* route = nullptr;  // fp32 C rows routed to peers (C unused)
+  // argmax_token fused into the epilogue: per row, atomicMax of (ordered
+  // value << 32 | ~column) over every tile (zero before the launch); C and
+  // Cb may be null. launch_argmax_keys turns the keys into tokens.
+  unsigned long long* amax = nullptr;
 };
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);

@@ -228,7 +228,8 @@ DistEngine::~DistEngine() {
                   static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
                   static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
                   static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_)}) {
+                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_),
+                  static_cast<void*>(amax_)}) {
     if (p) cudaFree(p);
   }
   for (auto& e : ev_) {
@@ -246,7 +247,8 @@ void DistEngine::ensure(int B) {
                   static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
                   static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
                   static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_)}) {
+                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_),
+                  static_cast<void*>(amax_)}) {
     if (p) cudaFree(p);
   }
   const size_t bp = (static_cast<size_t>(B) + 127) / 128 * 128;
@@ -270,6 +272,7 @@ void DistEngine::ensure(int B) {
   zalloc(reinterpret_cast<void**>(&tok_), bp * 4);
   zalloc(reinterpret_cast<void**>(&all_tok_), bp * 4);
   zalloc(reinterpret_cast<void**>(&home_idx_), bp * 4);
+  zalloc(reinterpret_cast<void**>(&amax_), bp * 8);
   SD_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets before non-blocking-stream use
   cap_ = B;
 }
@@ -692,8 +695,16 @@ void DistEngine::run_step() {
     }
   }
   if (nh) {
-    w_->linear(0, 7, nh, x_, D, xb_, D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
-    launch_argmax(nh, s.V, logits_, s.V, tok_, stream_);
+    if (w_->mode() != SD_DENSE_EXACT_F32 && getenv("SD_NO_FUSED_ARGMAX") == nullptr) {
+      // argmax_token in the head GEMM's epilogue: no logits round trip
+      GemmArgs ga = w_->gemm_args(0, 7, nh, x_, D, xb_, D, nullptr, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+      ga.amax = amax_;
+      launch_gemm_sm100(ga, stream_);
+      launch_argmax_keys(nh, amax_, tok_, stream_);
+    } else {
+      w_->linear(0, 7, nh, x_, D, xb_, D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+      launch_argmax(nh, s.V, logits_, s.V, tok_, stream_);
+    }
   }
 }
 

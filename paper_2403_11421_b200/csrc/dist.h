@@ -113,6 +113,7 @@ class DistEngine : public StepComputation {
   int32_t* tok_ = nullptr;
   int32_t* all_tok_ = nullptr;   // [B] next tokens of the whole batch (compute)
   int32_t* home_idx_ = nullptr;  // [home rows] batch row of each home row
+  unsigned long long* amax_ = nullptr;  // fused-argmax keys of the head GEMM
   std::vector<uint32_t> pos_;
   std::vector<int32_t> host_tok_;
   bool timing_ = false;

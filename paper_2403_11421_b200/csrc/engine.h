@@ -115,6 +115,7 @@ class Engine : public StepComputation {
     float *x = nullptr, *qkv = nullptr, *o = nullptr, *y = nullptr, *h = nullptr, *logits = nullptr;
     __nv_bfloat16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
     int32_t* tok = nullptr;
+    unsigned long long* amax = nullptr;  // fused-argmax keys of the head GEMM
     cudaEvent_t ev_s = nullptr, ev_r = nullptr;
     std::vector<uint32_t> pos;
     std::vector<int32_t> host_tok;
@@ -131,7 +132,8 @@ class Engine : public StepComputation {
   int timing_every_ = 1;
   void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
             int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
-            const float* res, int64_t ldr);
+            const float* res, int64_t ldr, unsigned long long* amax = nullptr);
+  bool want_logits_ = false;  // this step returns the logits (else the head's argmax is fused)
 
   bool timing_ = false;
   std::vector<cudaEvent_t> ev_pool_;

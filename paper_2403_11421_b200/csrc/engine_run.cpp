@@ -45,12 +45,13 @@ void Engine::free_group(Group& g) {
   for (void* p : {static_cast<void*>(g.x), static_cast<void*>(g.qkv), static_cast<void*>(g.o),
                   static_cast<void*>(g.y), static_cast<void*>(g.h), static_cast<void*>(g.logits),
                   static_cast<void*>(g.xb), static_cast<void*>(g.ob), static_cast<void*>(g.yb),
-                  static_cast<void*>(g.hb), static_cast<void*>(g.tok)}) {
+                  static_cast<void*>(g.hb), static_cast<void*>(g.tok), static_cast<void*>(g.amax)}) {
     if (p) cudaFree(p);
   }
   g.x = g.qkv = g.o = g.y = g.h = g.logits = nullptr;
   g.xb = g.ob = g.yb = g.hb = nullptr;
   g.tok = nullptr;
+  g.amax = nullptr;
   g.cap = 0;
 }
 
@@ -106,6 +107,7 @@ void Engine::ensure(Group& g, int n) {
   zalloc(&g.yb, bp * s.D * 2);
   zalloc(&g.hb, bp * s.F * 2);
   zalloc(&g.tok, bp * 4);
+  zalloc(&g.amax, bp * 8);
   // cudaMemset runs on the legacy stream, which does not order with the
   // engine's non-blocking streams: finish it before any kernel touches g
   SD_CUDA(cudaDeviceSynchronize());
@@ -144,7 +146,7 @@ int Engine::split(int B, const uint64_t* seqs) {
 
 void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
                   const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
-                  int64_t ldyb, int epi, const float* res, int64_t ldr) {
+                  int64_t ldyb, int epi, const float* res, int64_t ldr, unsigned long long* amax) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = timing_ && (which == 7 || layer % timing_every_ == 0);
   if (timed) {
@@ -158,7 +160,13 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
     }
     SD_CUDA(cudaEventRecord(e0, stream_));
   }
-  w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_, s_sms_);
+  if (amax) {
+    GemmArgs ga = w_->gemm_args(layer, which, B, x, ldx, xb, ldxb, nullptr, ldy, nullptr, 0, epi, res, ldr, s_sms_);
+    ga.amax = amax;
+    launch_gemm_sm100(ga, stream_);
+  } else {
+    w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_, s_sms_);
+  }
   if (timed) {
     SD_CUDA(cudaEventRecord(e1, stream_));
     ev_.emplace_back(e0, e1);
@@ -276,6 +284,14 @@ void Engine::run(int ng, bool embed) {
   for (int gi = 0; gi < ng; ++gi) {  // output_logits + argmax_token (dense.cpp:72-88)
     Group& g = groups_[gi];
     const int n = static_cast<int>(g.rows.size());
+    // tensor-core modes: argmax_token folded into the head GEMM's epilogue
+    // (no logits round trip through HBM) unless the caller wants the logits
+    static const bool no_fuse = getenv("SD_NO_FUSED_ARGMAX") != nullptr;
+    if (!head_done && !want_logits_ && !no_fuse && w_->mode() != SD_DENSE_EXACT_F32) {
+      gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0, g.amax);
+      launch_argmax_keys(n, g.amax, g.tok, stream_);
+      continue;
+    }
     if (!head_done) gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
     launch_argmax(n, s.V, g.logits, s.V, g.tok, stream_);
   }
@@ -328,7 +344,9 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
     SD_CUDA(cudaEventCreate(&l1));
     SD_CUDA(cudaEventRecord(l0, stream_));
   }
+  want_logits_ = logits_host != nullptr;
   run(ng, tokens_host != nullptr);
+  want_logits_ = false;
   if (step_log) {
     const double enq = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
     SD_CUDA(cudaEventRecord(l1, stream_));

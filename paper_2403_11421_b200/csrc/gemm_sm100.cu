@@ -58,6 +58,7 @@ struct Params {
   int route_bulk;  // routed rows leave through bulk copies (else smem-transposed st.global)
   int route_tma;   // contiguous 32-row slabs leave as tensor stores (RouteMaps)
   RowRoute route;
+  unsigned long long* amax;  // fused argmax keys per row (GemmArgs::amax)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -640,12 +641,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       int nchunk = 0;
+      unsigned long long best = 0;  // fused argmax: this row's best key in the tile
 #pragma unroll 1
       for (int c = 0; c < (p.bn + 31) / 32; ++c) {
         const int col0 = n0 + c * 32;
         if (col0 >= nend) break;  // warp-uniform
         float v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, v);
+        if (p.amax) {
+          // key = order-preserving bits of the value (NaN never wins, -0 is
+          // +0) above the inverted column, so the largest key is the first
+          // maximum (argmax_token, dense.cpp:80-88)
+          if (rowok) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float x = v[k];
+              if (col0 + k < nend && x == x) {
+                const uint32_t b = x == 0.0f ? 0u : __float_as_uint(x);
+                const uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+                const unsigned long long key =
+                    (static_cast<unsigned long long>(ord) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(col0 + k));
+                best = key > best ? key : best;
+              }
+            }
+          }
+          continue;
+        }
         if (p.routed) {
           // transpose the 32x32 chunk through smem so that every store
           // instruction writes 128 contiguous bytes of one row (4 rows per
@@ -775,6 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (p.amax && best) atomicMax(p.amax + row, best);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1274,6 +1296,8 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
     if (g.N % 32 || g.route->ld % 4) fail(SD_ERR_CONFIG, "routed GEMM: N and the row stride must be multiples of 32 / 4");
     if (g.C || g.Cb || g.epi != kEpiNone) fail(SD_ERR_CONFIG, "routed GEMM: plain fp32 rows only");
   }
+  p.amax = g.amax;
+  if (g.amax && (g.route || g.C || g.Cb)) fail(SD_ERR_CONFIG, "fused-argmax GEMM: no other output");
   p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
           (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));
   const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16

@@ -146,3 +146,31 @@ def test_chained_s_part_is_bitwise_equal_to_separate_gemms(B, monkeypatch):
     for (t1, x1), (t2, x2) in zip(a, b):
         assert np.array_equal(t1, t2)
         assert np.array_equal(x1.view(np.uint32), x2.view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+def test_fused_head_argmax_matches_logits_argmax(sd, oracle, mode):
+    """argmax_token folded into the head GEMM's epilogue (per-tile keys,
+    atomicMax per row) picks exactly the token the separate logits + argmax
+    path picks, including ties across tiles (first maximum wins,
+    dense.cpp:80-88): two identical head rows far apart in the vocabulary."""
+    W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 1024), 3)
+    tensors = [W.raw("embedding")]
+    for l in range(W.spec.num_layers):
+        for n in ("w_q", "w_k", "w_v", "w_o", "w_mlp_in", "w_mlp_out"):
+            tensors.append(W.raw(n, l))
+    head = np.array(W.raw("head"), np.float32, copy=True).reshape(64, 1024)  # (k, j): w(j, k) col-major
+    head[:, 700] *= 40.0
+    head[:, 900] = head[:, 700]
+    tensors.append(head.reshape(-1))
+    spec = sd.make_model_spec(2, 64, 4, 256, 1024)
+    dw = sd.DeviceWeights(spec, tensors, mode, 0)
+    x = np.random.default_rng(1).uniform(-1, 1, (40, 64)).astype(np.float32)
+    seqs = list(range(1, 41))
+    kv1 = sd.KvShard(spec, 0, 4, 1 << 12, "single")
+    t1, _, lg = sd.Engine(dw, kv1).compute(seqs, features=x, want_logits=True)
+    kv2 = sd.KvShard(spec, 0, 4, 1 << 12, "single")
+    t2, _, _ = sd.Engine(dw, kv2).compute(seqs, features=x)
+    assert np.array_equal(t1, np.argmax(lg, axis=1))
+    assert np.array_equal(t2, t1)
+    assert (t1 == 700).any() and not (t1 == 900).any()
