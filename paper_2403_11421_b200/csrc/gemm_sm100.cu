@@ -325,12 +325,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // MMAs take; tools/mma_rate.cu). PAIR: a CTA pair computes a 256 x bn tile
 // with cta_group::2 MMAs, each CTA staging its own 128 A rows and half of
 // the B tile.
-template <int BN, bool PAIR, int ATOMS>
+// MB: 128-row A blocks per CTA (MB = 2, opt-in SD_GEMM_MB=2: a pair computes
+// a 512 x bn tile as two 256 x bn accumulators sharing every B stage, 1.5x
+// the MACs per staged byte; measured no faster at the decode shapes, see
+// pick_pair_bn_mb2).
+template <int BN, bool PAIR, int ATOMS, int MB = 1>
 struct Cfg {
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA (max)
   static constexpr int A_ATOM = BM * BK_BYTES;
   static constexpr int B_ATOM = B_ROWS * BK_BYTES;
-  static constexpr int A_ST = ATOMS * A_ATOM;
+  static constexpr int A_ST = MB * ATOMS * A_ATOM;
   static constexpr int B_ST = ATOMS * B_ATOM;
   static constexpr int STAGES = (196 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (196 * 1024 / (A_ST + B_ST));
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
@@ -362,12 +366,13 @@ struct RouteMaps {
   CUtensorMap m[8];
 };
 
-template <int BN, bool PAIR, int ATOMS, int KIND>
+template <int BN, bool PAIR, int ATOMS, int KIND, int MB>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_cb, const Params p,
                 const __grid_constant__ RouteMaps rmaps) {
-  using C_ = Cfg<BN, PAIR, ATOMS>;
+  static_assert(MB == 1 || PAIR, "two A blocks per CTA only in pair mode");
+  using C_ = Cfg<BN, PAIR, ATOMS, MB>;
   constexpr int STAGES = C_::STAGES;
   constexpr int KELEMS = BK_BYTES / (KIND == 2 ? 4 : 2);  // elements per atom row
   extern __shared__ uint8_t smem_raw[];
@@ -391,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x / cs, nclusters = gridDim.x / cs;
   // PAIR: a cluster item is a 256-row M block (rank r owns rows r*128..);
   // otherwise cs consecutive 128-row M blocks sharing one B tile (multicast)
-  const int mgroups = PAIR ? (p.mb + 1) / 2 : p.mb / cs;
+  const int mgroups = PAIR ? (p.mb + 2 * MB - 1) / (2 * MB) : p.mb / cs;
   const int items = mgroups * p.nb;
 
   if (warp == 0 && lane == 0) {
@@ -426,7 +431,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // A operand / residual of the previous kernel from here on
 
-  auto m_origin = [&](int it) { return ((it % mgroups) * cs + rank) * BM; };
+  // first row of this CTA's block 0 (block b adds b * cs * BM)
+  auto m_origin = [&](int it) { return ((it % mgroups) * cs * MB + rank) * BM; };
 
   if (warp == 0) {
     // ------------------------------------------------------- TMA producer
@@ -434,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const int slice = PAIR ? p.bn / 2 : BN / cs;
-      const uint32_t bytes = static_cast<uint32_t>(ATOMS * (C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
+      const uint32_t bytes = static_cast<uint32_t>(ATOMS * (MB * C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
                              (PAIR ? 2u : 1u);  // PAIR: both CTAs' bytes land on the leader's barrier
       const uint32_t full0 = PAIR ? mapa(&full[0], 0) : smem_u32(&full[0]);
       for (int it = cluster; it < items; it += nclusters) {
@@ -452,7 +458,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
               uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
               if (PAIR) {
-                e_tma_load_pair(dA, &tma_a, fb, kc, m0);
+#pragma unroll
+                for (int b = 0; b < MB; ++b) {
+                  e_tma_load_pair(dA + b * ATOMS * C_::A_ATOM, &tma_a, fb, kc, m0 + b * 2 * BM);
+                }
                 e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
               } else {
                 e_tma_load(dA, &tma_a, fb, kc, m0);
@@ -488,12 +497,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       int local = 0;
       const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
       const uint16_t cmask = PAIR ? static_cast<uint16_t>(3) : mask;
-      for (int it = cluster; it < items; it += nclusters, ++local) {
-        const int acc = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
-        mbar_wait(&tempty[acc], (use & 1) ^ 1);
+      for (int it = cluster; it < items; it += nclusters, local += MB) {
+        // accumulator slots alternate per 256-row block: MB = 1 double-buffers
+        // across items, MB = 2 gives an item's two blocks one slot each
+        for (int b = 0; b < MB; ++b) {
+          const int acc = (local + b) & 1;
+          const uint32_t use = static_cast<uint32_t>((local + b) >> 1);
+          mbar_wait(&tempty[acc], (use & 1) ^ 1);
+        }
         tc_fence_after();
-        const uint32_t dcol = tmem_base + acc * BN;
+        const uint32_t dcol = tmem_base + (local & 1) * BN;  // block b: slot (local + b) & 1
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -504,8 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < ATOMS; ++a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32 B along the 128-B swizzle row
-              e_mma<KIND, PAIR>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k,
-                                p.idesc, (kb | a | k) != 0);
+#pragma unroll
+              for (int b = 0; b < MB; ++b) {
+                e_mma<KIND, PAIR>(MB == 1 ? dcol : tmem_base + ((local + b) & 1) * BN,
+                                  da + (b * ATOMS + a) * (C_::A_ATOM >> 4) + 2 * k,
+                                  db + a * (C_::B_ATOM >> 4) + 2 * k, p.idesc, (kb | a | k) != 0);
+              }
             }
           }
           e_commit<PAIR>(&empty[s], cmask);  // release slot s (both pair CTAs / every cluster CTA)
@@ -514,7 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph ^= 1;
           }
         }
-        e_commit<PAIR>(&tfull[acc], PAIR ? static_cast<uint16_t>(3) : static_cast<uint16_t>(1));
+#pragma unroll
+        for (int b = 0; b < MB; ++b) {
+          e_commit<PAIR>(&tfull[(local + b) & 1], PAIR ? static_cast<uint16_t>(3) : static_cast<uint16_t>(1));
+        }
       }
     }
   } else {
@@ -531,10 +551,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the tensor maps clip rows >= M and columns >= N
       uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
       int nchunk = 0;
-      for (int it = cluster; it < items; it += nclusters, ++local) {
+      for (int itb = cluster * MB; itb < items * MB; itb += itb % MB == MB - 1 ? (nclusters - 1) * MB + 1 : 1, ++local) {
+        const int it = itb / MB, blk = itb % MB;  // item, 256-row block of the item
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
-        const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
+        const int m0 = m_origin(it) + blk * 2 * BM, n0 = (it / mgroups) * p.bn;
         const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
         mbar_wait(&tfull[acc], use & 1);
         __syncwarp();
@@ -614,10 +635,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
     } else
-    for (int it = cluster; it < items; it += nclusters, ++local) {
+    for (int itb = cluster * MB; itb < items * MB; itb += itb % MB == MB - 1 ? (nclusters - 1) * MB + 1 : 1, ++local) {
+      const int it = itb / MB, blk = itb % MB;
       const int acc = local & 1;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
+      const int m0 = m_origin(it) + blk * 2 * BM, n0 = (it / mgroups) * p.bn;
       const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
       mbar_wait(&tfull[acc], use & 1);
       __syncwarp();  // lanes leave the try_wait spin independently; .sync.aligned needs convergence
@@ -1240,10 +1262,19 @@ int pick_pair_bn(int mgroups, int N, int pairs) {
   return best;
 }
 
-template <int BN, bool PAIR, int ATOMS, int KIND>
+// Tile width of the two-block pair tile (MB = 2, opt-in): the same
+// waves x (bn + fixed) rule over half as many tile rows. Measured at M = 512
+// (tools/splitk_probe.py): MLP-in 49.4 vs 50.9 us, the head slower, the other
+// shapes slower — staging 1.5x fewer bytes per MAC did not shorten the tiles,
+// so operand ingress is not what bounds them; kept for experiments.
+int pick_pair_bn_mb2(int mb, int N, int pairs) {
+  return pick_pair_bn((mb + 3) / 4, N, pairs);
+}
+
+template <int BN, bool PAIR, int ATOMS, int KIND, int MB = 1>
 void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
-  using C_ = Cfg<BN, PAIR, ATOMS>;
-  auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND>;
+  using C_ = Cfg<BN, PAIR, ATOMS, MB>;
+  auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND, MB>;
   static bool attr_set = false;
   if (!attr_set) {
     SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
@@ -1303,7 +1334,7 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16
   p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
             (static_cast<uint32_t>((PAIR ? 2 * BM : BM) >> 4) << 24);
-  const int items = (PAIR ? (p.mb + 1) / 2 : p.mb / cs) * p.nb;
+  const int items = (PAIR ? (p.mb + 2 * MB - 1) / (2 * MB) : p.mb / cs) * p.nb;
   const int budget = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
   const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
@@ -1321,9 +1352,17 @@ void dispatch(const GemmArgs& g, cudaStream_t s) {
   const int sms = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
   const bool pair = pair_env ? atoi(pair_env) > 0 : (mb >= 2 && sms >= 2);
   if (pair) {
-    int bn = pick_pair_bn((mb + 1) / 2, g.N, sms / 2);
+    int MB = 1, bn = pick_pair_bn((mb + 1) / 2, g.N, sms / 2);
+    if (env_int("SD_GEMM_MB") == 2 && mb >= 3) {  // 512-row pair tiles (experimental)
+      MB = 2;
+      bn = pick_pair_bn_mb2(mb, g.N, sms / 2);
+    }
     if (force_bn >= 16 && force_bn <= 256 && force_bn % 16 == 0) bn = force_bn;
-    launch<256, true, 2, KIND>(g, 2, bn, s);
+    if (MB == 2) {
+      launch<256, true, 1, KIND, 2>(g, 2, bn, s);
+    } else {
+      launch<256, true, 2, KIND>(g, 2, bn, s);
+    }
     return;
   }
   const int tiles256 = mb * ((g.N + 255) / 256);
