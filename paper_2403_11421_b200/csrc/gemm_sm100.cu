@@ -1239,10 +1239,12 @@ int num_sms() {
 }
 
 
-// Tile choice (measured at decode batches, tools/tune_gemm.py, tools/gemm_diag.py):
-// the S-Part GEMMs at M = 512 are neither L2- nor HBM-bound (keeping the
-// operands resident in smem changes their time by < 3%); their cost is
-// tensor-pipe time quantized into waves of CTA pairs. So when M spans at
+// Tile choice (measured at decode batches, tools/tune_gemm.py, tools/gemm_diag.py,
+// tools/splitk_probe.py): the S-Part GEMMs at M = 512 are neither L2- nor
+// HBM-bandwidth-bound; within a tile the operand loads are latency-bound
+// (bytes in flight per SM / load latency: one more stage of the same smem
+// is -14% on the bn = 112 GEMMs), and across tiles the cost is quantized
+// into waves of CTA pairs. So when M spans at
 // least two 128-row blocks, a CTA pair (cta_group::2, 256 x bn tiles) is used
 // with the tile width bn (a multiple of 16, 64..256) that minimizes
 // waves x (bn + fixed per-tile cost); e.g. N = 14336 -> bn 208 (138 tiles on
@@ -1360,6 +1362,13 @@ void dispatch(const GemmArgs& g, cudaStream_t s) {
     if (force_bn >= 16 && force_bn <= 256 && force_bn % 16 == 0) bn = force_bn;
     if (MB == 2) {
       launch<256, true, 1, KIND, 2>(g, 2, bn, s);
+    } else if (bn <= 128 && getenv("SD_GEMM_NO_NARROW") == nullptr) {
+      // narrow tiles (W_o, MLP-out at M = 512: bn 112): the stage sized for
+      // bn <= 128 fits 4 stages instead of 3 in the same smem. The loads are
+      // latency-bound (bytes in flight / latency), so the extra stage is
+      // -14% on both GEMMs (tools/splitk_probe.py: 20.8 -> 17.8 us,
+      // 58.8 -> 50.5 us)
+      launch<128, true, 2, KIND>(g, 2, bn, s);
     } else {
       launch<256, true, 2, KIND>(g, 2, bn, s);
     }
