@@ -54,6 +54,18 @@ struct RowRoute {
   int slot, self;
 };
 
+// append_lane (attention.cpp:91-112) folded into the QKV GEMM's epilogue:
+// the K and V columns of row r are rounded to fp16 (RNE, as the append
+// kernel) and stored into the row's KV page for this layer instead of C.
+struct KvAppendOut {
+  uint8_t* layer_base;     // pool + layer * layer_bytes
+  int64_t group_bytes, v_off;
+  int32_t pos_bytes, pmask;  // bytes per position row; positions per page - 1
+  const int32_t* group;    // [M] page group holding row r's position
+  const int32_t* pos;      // [M] position of row r
+  int32_t col_k, width;    // K columns [col_k, col_k + width), V the next width
+};
+
 struct GemmArgs {
   int M, N, K;
   const void* A;
@@ -74,6 +86,7 @@ struct GemmArgs {
   // value << 32 | ~column) over every tile (zero before the launch); C and
   // Cb may be null. launch_argmax_keys turns the keys into tokens.
   unsigned long long* amax = nullptr;
+  const KvAppendOut* kvapp = nullptr;  // QKV rows' K/V straight into the KV pages (C keeps q)
 };
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);

@@ -116,6 +116,7 @@ class Engine : public StepComputation {
     __nv_bfloat16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
     int32_t* tok = nullptr;
     unsigned long long* amax = nullptr;  // fused-argmax keys of the head GEMM
+    std::vector<char> appended;          // per layer: K/V already stored by the QKV GEMM
     cudaEvent_t ev_s = nullptr, ev_r = nullptr;
     std::vector<uint32_t> pos;
     std::vector<int32_t> host_tok;
@@ -132,7 +133,11 @@ class Engine : public StepComputation {
   int timing_every_ = 1;
   void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
             int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
-            const float* res, int64_t ldr, unsigned long long* amax = nullptr);
+            const float* res, int64_t ldr, unsigned long long* amax = nullptr,
+            const KvAppendOut* kvapp = nullptr);
+  // the next layer's project_qkv with append_lane folded into its epilogue
+  // when the KV store allows it (returns whether it did)
+  bool qkv_fused_append(int layer, Group& g);
   bool want_logits_ = false;  // this step returns the logits (else the head's argmax is fused)
 
   bool timing_ = false;

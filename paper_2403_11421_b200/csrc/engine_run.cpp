@@ -146,7 +146,8 @@ int Engine::split(int B, const uint64_t* seqs) {
 
 void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
                   const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
-                  int64_t ldyb, int epi, const float* res, int64_t ldr, unsigned long long* amax) {
+                  int64_t ldyb, int epi, const float* res, int64_t ldr, unsigned long long* amax,
+                  const KvAppendOut* kvapp) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   const bool timed = timing_ && (which == 7 || layer % timing_every_ == 0);
   if (timed) {
@@ -163,6 +164,10 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
   if (amax) {
     GemmArgs ga = w_->gemm_args(layer, which, B, x, ldx, xb, ldxb, nullptr, ldy, nullptr, 0, epi, res, ldr, s_sms_);
     ga.amax = amax;
+    launch_gemm_sm100(ga, stream_);
+  } else if (kvapp) {
+    GemmArgs ga = w_->gemm_args(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, s_sms_);
+    ga.kvapp = kvapp;
     launch_gemm_sm100(ga, stream_);
   } else {
     w_->linear(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, stream_, s_sms_);
@@ -219,6 +224,23 @@ void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool rese
   }
 }
 
+bool Engine::qkv_fused_append(int layer, Group& g) {
+  const Spec& s = w_->spec();
+  const int n = static_cast<int>(g.rows.size());
+  const bool off = getenv("SD_NO_FUSED_APPEND") != nullptr;
+  if (off || pipeline_ || w_->mode() == SD_DENSE_EXACT_F32 || n == 0) return false;
+  for (int i = 0; i < n; ++i) {
+    g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], layer));
+  }
+  KvAppendOut ka{};
+  if (!kv_->stage_fused_append(layer, n, g.seqs.data(), g.pos.data(), &ka)) return false;
+  ka.col_k = s.D;
+  ka.width = s.kv_width();
+  gemm(layer, 0, n, g.x, s.D, g.xb, s.D, g.qkv, s.qkv_width(), nullptr, 0, kEpiNone, nullptr, 0, nullptr, &ka);
+  kv_->end_fused_append(stream_);
+  return true;
+}
+
 // One decode step over the `ng` groups; embed = features from g.tok (else
 // g.x/g.xb already hold them). Per group and layer: S_pre (finish_block of
 // the previous layer + project_qkv) on the S stream, then the R-Part
@@ -240,13 +262,18 @@ void Engine::run(int ng, bool embed) {
     gemm(0, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
     if (pipeline_) SD_CUDA(cudaEventRecord(g.ev_s, stream_));
   }
+  for (int gi = 0; gi < ng; ++gi) groups_[gi].appended.assign(static_cast<size_t>(s.L), 0);
   for (int l = 0; l < s.L; ++l) {
     for (int gi = 0; gi < ng; ++gi) {
       Group& g = groups_[gi];
       const int n = static_cast<int>(g.rows.size());
       if (pipeline_) SD_CUDA(cudaStreamWaitEvent(rs, g.ev_s, 0));
-      for (int i = 0; i < n; ++i) g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], l));
-      kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
+      if (!g.appended[static_cast<size_t>(l)]) {
+        for (int i = 0; i < n; ++i) {
+          g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], l));
+        }
+        kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
+      }
       // the attention also writes the bf16 copy of o that W_o consumes
       kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi, bf ? g.ob : nullptr, D);
       if (pipeline_) {
@@ -276,7 +303,11 @@ void Engine::run(int ng, bool embed) {
       gemm(l, 5, n, g.y, D, g.yb, D, bf ? nullptr : g.h, F, bf ? g.hb : nullptr, F, kEpiSilu, nullptr, 0);
       gemm(l, 6, n, g.h, F, g.hb, F, g.x, D, bf ? g.xb : nullptr, D, kEpiResidual, g.y, D);
       if (l + 1 < s.L) {
-        gemm(l + 1, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+        if (qkv_fused_append(l + 1, g)) {
+          g.appended[static_cast<size_t>(l + 1)] = 1;
+        } else {
+          gemm(l + 1, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+        }
         if (pipeline_) SD_CUDA(cudaEventRecord(g.ev_s, stream_));
       }
     }

@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 #include <functional>
@@ -59,6 +60,8 @@ struct Params {
   int route_tma;   // contiguous 32-row slabs leave as tensor stores (RouteMaps)
   RowRoute route;
   unsigned long long* amax;  // fused argmax keys per row (GemmArgs::amax)
+  int kvapp;                 // K/V columns go to the KV pages (kva)
+  KvAppendOut kva;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -563,12 +566,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rowb = m0 + q * 32;
         const int64_t row = rowb + lane;
         const bool rin = row < p.M;
+        // fused append: this row's K row in its KV page (V at + v_off)
+        uint8_t* krow = nullptr;
+        if (p.kvapp && rin) {
+          krow = p.kva.layer_base + static_cast<int64_t>(p.kva.group[row]) * p.kva.group_bytes +
+                 static_cast<int64_t>(p.kva.pos[row] & p.kva.pmask) * p.kva.pos_bytes;
+        }
 #pragma unroll 1
         for (int c = 0; c < (p.bn + 15) / 16; ++c) {
           const int col0 = n0 + c * 16;
           if (col0 >= nend) break;  // warp-uniform
           float v[16];
           tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 16, v);
+          if (p.kvapp && col0 >= p.kva.col_k && col0 < p.kva.col_k + 2 * p.kva.width) {  // warp-uniform
+            if (krow) {
+              const bool isv = col0 >= p.kva.col_k + p.kva.width;
+              const int e0 = col0 - p.kva.col_k - (isv ? p.kva.width : 0);
+              uint32_t w[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const __half2 h = __floats2half2_rn(v[2 * e], v[2 * e + 1]);
+                w[e] = *reinterpret_cast<const uint32_t*>(&h);
+              }
+              uint4* d = reinterpret_cast<uint4*>(krow + (isv ? p.kva.v_off : 0) + static_cast<int64_t>(e0) * 2);
+              d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            continue;
+          }
           if (p.epi == kEpiResidual) {
             if (rin && p.vec && col0 + 16 <= p.N) {
               const float4* r4 = reinterpret_cast<const float4*>(p.res + row * p.ldr + col0);
@@ -1330,6 +1355,13 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
     if (g.C || g.Cb || g.epi != kEpiNone) fail(SD_ERR_CONFIG, "routed GEMM: plain fp32 rows only");
   }
   p.amax = g.amax;
+  if (g.kvapp) {
+    if (!p.tma_out || KIND != 1 && KIND != 2 || g.kvapp->col_k % 16 || g.kvapp->width % 16 || (g.kvapp->pos_bytes % 16)) {
+      fail(SD_ERR_INTERNAL, "fused append: needs the TMA-store epilogue and 16-column-aligned K/V");
+    }
+    p.kvapp = 1;
+    p.kva = *g.kvapp;
+  }
   if (g.amax && (g.route || g.C || g.Cb)) fail(SD_ERR_CONFIG, "fused-argmax GEMM: no other output");
   p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
           (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));

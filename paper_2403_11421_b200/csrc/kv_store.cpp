@@ -361,6 +361,42 @@ void KvStore::append(int layer, int n, const uint64_t* seqs, const uint32_t* pos
   f->blob = &b;
 }
 
+bool KvStore::stage_fused_append(int layer, int n, const uint64_t* seqs, const uint32_t* positions,
+                                 KvAppendOut* out) {
+  const int L = spec_.L;
+  if (geom_.fmt != SD_KV_HALF || layer < 0 || layer >= L || n <= 0 || total_ + n > cap_ * L) return false;
+  Fast* fm = const_cast<Fast*>(fast_match(n, seqs));
+  if (!fm || layer == fm->layer || std::memcmp(positions, fm->pos.data(), static_cast<size_t>(n) * 4) != 0) {
+    return false;
+  }
+  for (int i = 0; i < n; ++i) {  // the reference's per-item checks (attention.cpp:174-195)
+    if (static_cast<uint32_t>(len_[static_cast<size_t>(fm->slots[static_cast<size_t>(i)]) * L + layer]) !=
+        positions[i]) {
+      return false;
+    }
+  }
+  for (int i = 0; i < n; ++i) len_[static_cast<size_t>(fm->slots[static_cast<size_t>(i)]) * L + layer] += 1;
+  total_ += n;
+  const int32_t* d = static_cast<const int32_t*>(fm->blob->dev.p);
+  out->layer_base = geom_.pool + static_cast<int64_t>(layer) * geom_.layer_bytes;
+  out->group_bytes = geom_.group_bytes;
+  out->v_off = geom_.v_off;
+  out->pos_bytes = geom_.pos_bytes;
+  out->pmask = geom_.P - 1;
+  out->pos = d + n;
+  out->group = d + 2 * n;
+  fm->layer = layer;
+  fm->used = ++fast_clock_;
+  fused_pending_ = fm;
+  return true;
+}
+
+void KvStore::end_fused_append(cudaStream_t s) {
+  if (!fused_pending_) return;
+  SD_CUDA(cudaEventRecord(fused_pending_->blob->done, s));
+  fused_pending_ = nullptr;
+}
+
 const KvStore::Fast* KvStore::fast_match(int n, const uint64_t* seqs) const {
   for (const Fast& f : fast_) {
     if (f.valid && f.n == n && n > 0 && std::memcmp(seqs, f.seqs.data(), static_cast<size_t>(n) * 8) == 0) {

@@ -45,6 +45,15 @@ class KvStore {
   void append(int layer, int n, const uint64_t* seqs, const uint32_t* positions,
               const float* k_dev, int64_t k_stride, const float* v_dev, int64_t v_stride,
               cudaStream_t s);
+  // The same append with its stores left to the producer of k and v (the
+  // QKV GEMM's epilogue): only on the lockstep fast path (every target page
+  // open, the previous call at another layer with the same sequences and
+  // positions) with fp16 pages. Returns false, changing nothing, otherwise.
+  // On true the call is committed; `out` locates every row's page and the
+  // producer must run on `s` before end_fused_append(s).
+  bool stage_fused_append(int layer, int n, const uint64_t* seqs, const uint32_t* positions,
+                          struct KvAppendOut* out);
+  void end_fused_append(cudaStream_t s);
   // KvShard::attend semantics (attention.cpp:204-282).
   // `slot` selects one of the cached split plans (one per interleaved
   // mini-batch, so alternating batches do not rebuild each other's plan).
@@ -131,6 +140,7 @@ class KvStore {
     Blob* blob = nullptr;
   };
   Fast fast_[2];
+  Fast* fused_pending_ = nullptr;
   uint64_t fast_clock_ = 0;
   const Fast* fast_match(int n, const uint64_t* seqs) const;
 

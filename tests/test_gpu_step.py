@@ -174,3 +174,39 @@ def test_fused_head_argmax_matches_logits_argmax(sd, oracle, mode):
     assert np.array_equal(t1, np.argmax(lg, axis=1))
     assert np.array_equal(t2, t1)
     assert (t1 == 700).any() and not (t1 == 900).any()
+
+
+@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+def test_fused_append_is_bitwise_equal(monkeypatch, mode):
+    """append_lane folded into the QKV GEMM's epilogue (fp16 pages, lockstep
+    layers) stores exactly the bytes the append kernel stores: KV lanes,
+    tokens and final activations are bitwise equal over several steps,
+    across page boundaries (P = 16 positions; 20 steps from context 9)."""
+    import paper_2403_11421_b200 as sd
+    spec = sd.make_model_spec(3, 512, 8, 1024, 2048, 2)
+    seqs = list(range(1, 301))
+    tok0 = np.array([sd.prompt_token(0, s, spec.vocab_size) for s in seqs], np.int32)
+
+    def run(fused):
+        if fused:
+            monkeypatch.delenv("SD_NO_FUSED_APPEND", raising=False)
+        else:
+            monkeypatch.setenv("SD_NO_FUSED_APPEND", "1")
+        w = sd.DeviceWeights(spec, None, mode, 0, seed=2)
+        kv = sd.KvShard(spec, 0, 2, 300 * 64, "half", 0, max_sequences=300, max_seq_len=64)
+        kv.prefill_synthetic(seqs, 9, salt=1)
+        eng = sd.Engine(w, kv)
+        tok, outs = tok0.copy(), []
+        for _ in range(20):
+            tok, fx = eng.compute(seqs, tokens=tok, want_final=True)
+            outs.append((tok.copy(), fx.copy()))
+        lanes = [kv.export_lane(q, l, which) for q in (1, 150, 300) for l in range(3) for which in (0, 1)]
+        return outs, lanes
+
+    a, la = run(True)
+    b, lb = run(False)
+    for (t1, x1), (t2, x2) in zip(a, b):
+        assert np.array_equal(t1, t2)
+        assert np.array_equal(x1.view(np.uint32), x2.view(np.uint32))
+    for (x, _), (y, _) in zip(la, lb):  # fp16 pages: bytes, no scales
+        assert x.size and np.array_equal(x, y)
