@@ -340,7 +340,8 @@ struct Cfg {
   static constexpr int A_ST = MB * ATOMS * A_ATOM;
   static constexpr int B_ST = ATOMS * B_ATOM;
   static constexpr int STAGES = (196 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (196 * 1024 / (A_ST + B_ST));
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  // two accumulators, allocated in a power-of-two column count
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   // epilogue staging for TMA stores: per epilogue warp, two buffers of
   // 32 rows x 16 columns in fp32 (2 KB, 64-B swizzle) and bf16 (1 KB, 32-B swizzle)
   static constexpr int OUT_F32 = 32 * 16 * 4, OUT_BF16 = 32 * 16 * 2;
@@ -1392,17 +1393,30 @@ void dispatch(const GemmArgs& g, cudaStream_t s) {
       bn = pick_pair_bn_mb2(mb, g.N, sms / 2);
     }
     if (force_bn >= 16 && force_bn <= 256 && force_bn % 16 == 0) bn = force_bn;
+    // The stage ring is sized for the widest tile of the instantiation, so
+    // the tile width picks the instantiation: one swizzle atom per stage and
+    // a B stage no wider than needed gives the most stages in the same smem
+    // (bn <= 128: 8, <= 192: 7, else 6; the loads are latency-bound, so more,
+    // smaller stages keep more of them in flight). Measured at M = 512 with
+    // the weights streamed from HBM (tools/wide_probe.py, splitk_probe.py):
+    // QKV 25.1 -> 22.5 us, MLP-in 50.5 -> 48.2, MLP-out 58.8 -> 50.1, W_o
+    // 20.8 -> 18.2 against the two-atom stages of the 256-wide instantiation
+    // (3 stages). SD_GEMM_ATOMS2=1: two atoms per stage (3-4 stages).
+    const bool two = env_int("SD_GEMM_ATOMS2") == 1;
     if (MB == 2) {
       launch<256, true, 1, KIND, 2>(g, 2, bn, s);
-    } else if (bn <= 128 && getenv("SD_GEMM_NO_NARROW") == nullptr) {
-      // narrow tiles (W_o, MLP-out at M = 512: bn 112): the stage sized for
-      // bn <= 128 fits 4 stages instead of 3 in the same smem. The loads are
-      // latency-bound (bytes in flight / latency), so the extra stage is
-      // -14% on both GEMMs (tools/splitk_probe.py: 20.8 -> 17.8 us,
-      // 58.8 -> 50.5 us)
-      launch<128, true, 2, KIND>(g, 2, bn, s);
-    } else {
+    } else if (bn <= 128) {
+      if (two) {
+        launch<128, true, 2, KIND>(g, 2, bn, s);
+      } else {
+        launch<128, true, 1, KIND>(g, 2, bn, s);
+      }
+    } else if (bn <= 192 && !two) {
+      launch<192, true, 1, KIND>(g, 2, bn, s);
+    } else if (two) {
       launch<256, true, 2, KIND>(g, 2, bn, s);
+    } else {
+      launch<256, true, 1, KIND>(g, 2, bn, s);
     }
     return;
   }

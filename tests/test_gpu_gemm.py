@@ -90,12 +90,14 @@ def test_golden_transcript_tensor_core_modes(sd, oracle, mode):
 
 @pytest.mark.parametrize("kind", ["bf16", "tf32"])
 @pytest.mark.parametrize("M,N,K", [(512, 1024, 512), (300, 640, 256), (1000, 2080, 384), (384, 96, 128)])
-def test_two_block_pair_tiles_are_bitwise_equal(sd, monkeypatch, kind, M, N, K):
-    """The 512-row pair tile (two 256-row accumulators per CTA pair sharing
-    every B stage, SD_GEMM_MB=2) accumulates every output over the same K
-    sequence of MMAs as the 256-row tile: outputs are bitwise equal for every
-    epilogue (plain, residual + bf16 copy, SiLU), ragged M included (the
-    second block partly or wholly past M), and match the rounded reference."""
+def test_pair_tile_variants_are_bitwise_equal(sd, monkeypatch, kind, M, N, K):
+    """Every pair-tile variant accumulates each output over the same K
+    sequence of MMAs: one or two swizzle atoms per stage (the 128 / 192 / 256
+    instantiations picked by tile width), tile widths 112 / 176 / 208, and the
+    512-row tile (two 256-row accumulators per CTA pair sharing every B stage,
+    SD_GEMM_MB=2). Outputs are bitwise equal for every epilogue (plain,
+    residual + bf16 copy, SiLU), ragged M included, and match the rounded
+    reference."""
     import torch
     dev = torch.device("cuda")
     g = torch.Generator(device="cpu").manual_seed(M + N + K)
@@ -103,10 +105,15 @@ def test_two_block_pair_tiles_are_bitwise_equal(sd, monkeypatch, kind, M, N, K):
     A = (torch.rand(M, K, generator=g) * 2 - 1).to(dt).to(dev)
     B = ((torch.rand(N, K, generator=g) * 2 - 1) / K**0.5).to(dt).to(dev)
     res = (torch.rand(M, N, generator=g) * 2 - 1).to(dev)
-    outs = {}
-    for mb in ("1", "2"):
-        monkeypatch.setenv("SD_GEMM_MB", mb)
+    variants = [{}, {"SD_GEMM_ATOMS2": "1"}, {"SD_GEMM_MB": "2"}]
+    variants += [{"SD_GEMM_BN": str(bn), **v} for bn in (112, 176, 208) for v in ({}, {"SD_GEMM_ATOMS2": "1"})]
+    outs = []
+    for env in variants:
+        for k in ("SD_GEMM_ATOMS2", "SD_GEMM_MB", "SD_GEMM_BN"):
+            monkeypatch.delenv(k, raising=False)
         monkeypatch.setenv("SD_GEMM_PAIR", "1")
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         C0 = torch.empty(M, N, device=dev)
         C1 = torch.empty(M, N, device=dev)
         Cb1 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
@@ -116,11 +123,12 @@ def test_two_block_pair_tiles_are_bitwise_equal(sd, monkeypatch, kind, M, N, K):
                     epi=1, res=res.data_ptr(), ldr=N)
         sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C2.data_ptr(), N, epi=2)
         torch.cuda.synchronize()
-        outs[mb] = [t.cpu() for t in (C0, C1, Cb1, C2)]
-    for a, b in zip(outs["1"], outs["2"]):
-        assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32),
-                           b.view(torch.int16) if b.dtype == torch.bfloat16 else b.view(torch.int32))
+        outs.append([t.cpu() for t in (C0, C1, Cb1, C2)])
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32),
+                               b.view(torch.int16) if b.dtype == torch.bfloat16 else b.view(torch.int32))
     ref = A.float().cpu().double() @ B.float().cpu().double().T
     scale = A.float().cpu().double().abs() @ B.float().cpu().double().abs().T
     tol = 2e-5 if kind == "bf16" else 1e-3
-    assert bool(((outs["2"][0].double() - ref).abs() <= tol * scale + 1e-6).all())
+    assert bool(((outs[0][0].double() - ref).abs() <= tol * scale + 1e-6).all())
