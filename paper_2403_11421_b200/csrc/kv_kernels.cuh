@@ -11,7 +11,7 @@ namespace sd {
 
 // Geometry of the paged KV pool.
 // A page group holds P consecutive positions of one sequence for every
-// layer; inside it, layer l's region is
+// layer (one region per layer, the pool layer-major); a region is
 //   [K rows P x pos_bytes][V rows P x pos_bytes][K scales P x hc f32][V scales P x hc f32]
 // where a row is one position's [head][d] vector in the storage format, i.e.
 // the reference's per-(seq, layer) lane order (attention.cpp:117-118).
@@ -26,9 +26,12 @@ struct KvGeom {
   int32_t hd;           // head dim
   int32_t width;        // hc * hd
   int32_t pos_bytes;    // width * elem bytes
-  int64_t layer_bytes;  // bytes per layer region (128-B aligned)
-  int64_t group_bytes;  // layer_bytes * num_layers
-  int64_t v_off, ks_off, vs_off;  // offsets inside a layer region
+  // a (page group, layer) region (128-B aligned) is at
+  // pool + group * group_bytes + layer * layer_bytes; the pool is layer-major
+  // (group_bytes = region, layer_bytes = region * pool groups)
+  int64_t layer_bytes;  // stride between layers
+  int64_t group_bytes;  // stride between page groups
+  int64_t v_off, ks_off, vs_off;  // offsets inside a region
 };
 
 struct AppendArgs {

@@ -70,10 +70,21 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   } else {
     g.ks_off = g.vs_off = 0;
   }
-  g.layer_bytes = round_up(lb, 128);
-  g.group_bytes = g.layer_bytes * spec.L;
+  // Layer-major pool: [layer][page group][region]. A sequence's pages are
+  // allocated in order, so one layer's K/V of a sequence is one contiguous
+  // stream for the attention (bulk copies walking 64-KB regions back to back
+  // read 7.0-7.4 TB/s, at a 2-MB stride 6.5-6.8: tools/bulk_bw.cu).
+  // SD_KV_GROUP_MAJOR=1: [page group][layer][region].
+  const int64_t rbytes = round_up(lb, 128);
+  if (std::getenv("SD_KV_GROUP_MAJOR")) {
+    g.layer_bytes = rbytes;
+    g.group_bytes = rbytes * spec.L;
+  } else {
+    g.group_bytes = rbytes;
+    g.layer_bytes = rbytes * static_cast<int64_t>(pool_groups_);
+  }
 
-  const size_t pool_bytes = static_cast<size_t>(g.group_bytes) * pool_groups_;
+  const size_t pool_bytes = static_cast<size_t>(rbytes) * spec.L * static_cast<size_t>(pool_groups_);
   void* pool = nullptr;
   cudaError_t e = cudaMalloc(&pool, pool_bytes);
   if (e != cudaSuccess) {
