@@ -128,6 +128,7 @@ void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* sl
 int attention_consumer_warps();
 // tensor-core GQA path (kv_mma.cu): fp16 KV, hd 128, 8 kv heads per shard, G in {2, 4, 8}
 bool attention_mma_supported(const KvGeom& g, int G);
+int attention_mma_rows_per_slot(const KvGeom& g);  // positions per bulk copy (2 or 4)
 size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages);
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s);
 size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* stage_region,

@@ -15,12 +15,13 @@
 //
 // Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
-// positions copied two per bulk copy (the per-SM copy issue rate, not bytes,
-// limits row-sized copies) into pair slots with a 16-B pad; MMA row m holds
-// position 2m (m < 8) or 2(m-8)+1, so the eight ldmatrix row addresses of a
-// matrix fall in distinct bank groups.
+// positions copied four (fp16) or two (int8) per bulk copy (the per-SM copy
+// issue rate, not bytes, limits row-sized copies) into slots with a 16-B pad;
+// MMA row r holds position (r % NS) * RPS + r / NS (NS slots of RPS rows).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <cstdlib>
 
 #include "kv_kernels.cuh"
 #include "pdl.cuh"
@@ -138,9 +139,11 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
 
-template <int G, int FMT>
+template <int G, int FMT, int RPS>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
+  static_assert(!I8 || RPS == 2, "int8 fragments assume pair slots");
+  constexpr int NS = kT / RPS;  // slots per K (V) half of a stage
   extern __shared__ __align__(128) uint8_t smem[];
   const int nst = a.nstages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   uint8_t* ring = smem + 128 * ((16 * nst + 127) / 128);
   // stage region: kT/2 pair slots of two position rows + a 16-B pad; MMA row m
   // holds position 2m (m < 8) or 2(m-8)+1, i.e. slot m & 7, row m >> 3
-  const int ppitch = 2 * a.g.pos_bytes + 16;
+  const int ppitch = RPS * a.g.pos_bytes + 16;
   // int8: [K rows][V rows][K scales kT x hc][V scales kT x hc]
   const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + (I8 ? 2 * a.sc_region : 0);
   const KvGeom& g = a.g;
@@ -202,10 +205,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           // rate, not bytes, limits row-sized copies); each pair slot carries
           // a 16-B pad so the ldmatrix / 32-bit fragment rows are conflict-free
           const int pr = lane & 15;
-          if (pr < 8 && 2 * pr < cnt) {
+          if (pr < NS && RPS * pr < cnt) {
             uint8_t* dst = ring + stage * stage_bytes + (lane >= 16 ? a.stage_region : 0) + pr * ppitch;
-            const uint32_t nb = (2 * pr + 1 < cnt ? 2u : 1u) * g.pos_bytes;
-            bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + 2 * pr * g.pos_bytes, nb, &full[stage], pol);
+            const uint32_t nb = static_cast<uint32_t>(min(RPS, cnt - RPS * pr)) * g.pos_bytes;
+            bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + RPS * pr * g.pos_bytes, nb, &full[stage], pol);
           }
         }
         if (I8 && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
@@ -322,13 +325,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           uint32_t ka[4];
           // matrices: (pos 0-7, d 0-7), (pos 8-15, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 8-15)
           // matrix rows are MMA rows lr (+8): positions 2lr / 2lr+1 -> slot lr
-          ldsm_x4(Ks + lr * ppitch + (lm & 1) * g.pos_bytes + (16 * kk + 8 * (lm >> 1)) * 2, ka);
+          const int mr = lr + 8 * (lm & 1);  // MMA row: slot mr % NS, row mr / NS of the slot
+          ldsm_x4(Ks + (mr % NS) * ppitch + (mr / NS) * g.pos_bytes + (16 * kk + 8 * (lm >> 1)) * 2, ka);
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
           mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
       }
       // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
-      const bool v0 = 2 * gq < cnt, v1 = 2 * gq + 1 < cnt;
+      // positions of MMA rows gq and gq + 8 (slot-major: row r is position (r % NS) * RPS + r / NS)
+      const bool v0 = (gq % NS) * RPS + gq / NS < cnt, v1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS < cnt;
       if (!v0) s[0] = s[1] = -INFINITY;
       if (!v1) s[2] = s[3] = -INFINITY;
       float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         uint32_t va[4];
         // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
         const int vrow = lr + 8 * (lm >> 1);  // MMA k row (position mapping as for K)
-        const uint32_t vaddr = vpitch ? Vs + vrow * vpitch : Vs + (vrow & 7) * ppitch + (vrow >> 3) * g.pos_bytes;
+        const uint32_t vaddr = vpitch ? Vs + vrow * vpitch : Vs + (vrow % NS) * ppitch + (vrow / NS) * g.pos_bytes;
         ldsm_x4_t(vaddr + (16 * mt + 8 * (lm & 1)) * 2, va);
         mma16816(o[mt], va, bh0, bh1);
         mma16816(o[mt], va, bl0, bl1);
@@ -557,6 +562,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
 }  // namespace
 
+// fp16 stages copy four positions per bulk copy (8 KB at 8 kv heads: the
+// producer's own pattern streams 7.20 vs 6.98 TB/s with 8-KB over 4-KB
+// copies, tools/bulk_bw.cu; the C5 layer 0.630 -> 0.626 ms) at the price of
+// 2-way ldmatrix conflicts (rows of a slot share bank groups); int8 keeps
+// pair slots, which its 32-bit fragment loads need. SD_ATTN_PAIRS=1: pairs
+// for fp16 too.
+int attention_mma_rows_per_slot(const KvGeom& g) {
+  static const bool pairs = std::getenv("SD_ATTN_PAIRS") != nullptr;
+  return g.fmt == SD_KV_HALF && !pairs ? 4 : 2;
+}
+
 bool attention_mma_supported(const KvGeom& g, int G) {
   return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD &&
          (g.hc == 8 || g.hc == 4 || g.hc == 2 || g.hc == 1) && (G == 2 || G == 4 || G == 8) && g.P % kT == 0;
@@ -564,7 +580,8 @@ bool attention_mma_supported(const KvGeom& g, int G) {
 
 size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, int* nstages) {
   // kT/2 pair slots of two rows + a 16-B pad
-  *stage_region = (kT / 2) * (2 * g.pos_bytes + 16);
+  const int rps = attention_mma_rows_per_slot(g);
+  *stage_region = (kT / rps) * (rps * g.pos_bytes + 16);
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
   const size_t scratch = (g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0) +
@@ -577,10 +594,17 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
   const bool i8 = a.g.fmt == SD_KV_INT8;
+  const bool quad = attention_mma_rows_per_slot(a.g) == 4;
   switch (a.G) {
-    case 2: fn = i8 ? attn_mma_kernel<2, SD_KV_INT8> : attn_mma_kernel<2, SD_KV_HALF>; break;
-    case 4: fn = i8 ? attn_mma_kernel<4, SD_KV_INT8> : attn_mma_kernel<4, SD_KV_HALF>; break;
-    case 8: fn = i8 ? attn_mma_kernel<8, SD_KV_INT8> : attn_mma_kernel<8, SD_KV_HALF>; break;
+    case 2:
+      fn = i8 ? attn_mma_kernel<2, SD_KV_INT8, 2> : quad ? attn_mma_kernel<2, SD_KV_HALF, 4> : attn_mma_kernel<2, SD_KV_HALF, 2>;
+      break;
+    case 4:
+      fn = i8 ? attn_mma_kernel<4, SD_KV_INT8, 2> : quad ? attn_mma_kernel<4, SD_KV_HALF, 4> : attn_mma_kernel<4, SD_KV_HALF, 2>;
+      break;
+    case 8:
+      fn = i8 ? attn_mma_kernel<8, SD_KV_INT8, 2> : quad ? attn_mma_kernel<8, SD_KV_HALF, 4> : attn_mma_kernel<8, SD_KV_HALF, 2>;
+      break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));

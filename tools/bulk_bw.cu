@@ -39,7 +39,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
 constexpr int kCons = 8;
 
 __global__ void __launch_bounds__((kCons + 1) * 32, 1)
-    stream(const uint8_t* __restrict__ src, int64_t per_cta_stages, int64_t group, int nst) {
+    stream(const uint8_t* __restrict__ src, int64_t per_cta_stages, int64_t group, int nst, int copy) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + nst;
@@ -67,7 +67,8 @@ __global__ void __launch_bounds__((kCons + 1) * 32, 1)
         bar_expect(&full[s], kStage);
       }
       __syncwarp();
-      if (lane < 16) bulk(ring + s * kStage + lane * 4096, base + lane * 4096, 4096, &full[s], pol);
+      const int ncopy = static_cast<int>(kStage / copy);
+      if (lane < ncopy) bulk(ring + s * kStage + lane * copy, base + lane * copy, copy, &full[s], pol);
       if (++s == nst) {
         s = 0;
         ph ^= 1;
@@ -99,24 +100,26 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   for (int64_t group : {64LL * 1024, 2LL * 1024 * 1024}) {
-    for (int nst : {2, 3}) {
-      const size_t smem = 1024 + static_cast<size_t>(nst) * 64 * 1024;
-      cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      const int64_t total_stages = static_cast<int64_t>((bytes - 64 * 1024) / group);
-      const int64_t per = total_stages / sms;
-      float best = 1e9;
-      for (int r = 0; r < 4; ++r) {
-        cudaEventRecord(e0);
-        stream<<<sms, (kCons + 1) * 32, smem>>>(p, per, group, nst);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        float ms;
-        cudaEventElapsedTime(&ms, e0, e1);
-        best = ms < best ? ms : best;
+    for (int copy : {4096, 8192, 16384}) {
+      for (int nst : {2, 3}) {
+        const size_t smem = 1024 + static_cast<size_t>(nst) * 64 * 1024;
+        cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        const int64_t total_stages = static_cast<int64_t>((bytes - 64 * 1024) / group);
+        const int64_t per = total_stages / sms;
+        float best = 1e9;
+        for (int r = 0; r < 4; ++r) {
+          cudaEventRecord(e0);
+          stream<<<sms, (kCons + 1) * 32, smem>>>(p, per, group, nst, copy);
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          best = ms < best ? ms : best;
+        }
+        const double moved = static_cast<double>(per) * sms * 64 * 1024;
+        printf("{\"kernel\": \"bulk\", \"copy\": %d, \"group_stride\": %lld, \"stages\": %d, \"GBps\": %.0f, \"err\": \"%s\"}\n",
+               copy, static_cast<long long>(group), nst, moved / (best * 1e6), cudaGetErrorString(cudaGetLastError()));
       }
-      const double moved = static_cast<double>(per) * sms * 64 * 1024;
-      printf("{\"kernel\": \"bulk 4KB x16\", \"group_stride\": %lld, \"stages\": %d, \"GBps\": %.0f, \"err\": \"%s\"}\n",
-             static_cast<long long>(group), nst, moved / (best * 1e6), cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
