@@ -171,7 +171,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   pdl_trigger();
   __syncthreads();
-  pdl_wait();  // inputs of the previous kernel (q, plan, pool) from here on
+  // The plan (host-uploaded: a copy in the stream orders before this launch)
+  // and the KV of every position but the one this step appends are inputs
+  // no kernel still running can change, so the producer streams the first
+  // stages before the wait on the previous kernel (the QKV GEMM that writes
+  // q and the new position); the consumers wait first.
+  if (warp != kWarps) pdl_wait();
 
   const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
   const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
@@ -185,10 +190,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     const uint64_t pol = evict_first_policy();
     int stage = 0;
     uint32_t phase = 0;
+    bool waited = false;
     for (int w = cb; w < ce; ++w) {
       const Piece pc = a.pieces[w];
       const int32_t* pt = g.page_table + static_cast<int64_t>(a.item_slot[pc.item]) * g.max_pages;
       for (int pos = pc.p0; pos < pc.p1; pos += kT) {
+        // a stage ending before the piece's last position cannot hold the
+        // position being appended (the item's last) nor a page opened for it
+        if (!waited && pos + kT >= pc.p1) {
+          pdl_wait();
+          waited = true;
+        }
         const int cnt = min(kT, pc.p1 - pos);
         const uint8_t* base = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes +
                               static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
