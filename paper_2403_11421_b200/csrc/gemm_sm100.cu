@@ -433,9 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (cs > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // A operand / residual of the previous kernel from here on; the producer
-  // waits below, after requesting the first stages' weight tiles
-  if (warp != 0) pdl_wait();
+  pdl_wait();  // A operand / residual of the previous kernel from here on
 
   // first row of this CTA's block 0 (block b adds b * cs * BM)
   auto m_origin = [&](int it) { return ((it % mgroups) * cs * MB + rank) * BM; };
@@ -449,54 +447,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bytes = static_cast<uint32_t>(ATOMS * (MB * C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
                              (PAIR ? 2u : 1u);  // PAIR: both CTAs' bytes land on the leader's barrier
       const uint32_t full0 = PAIR ? mapa(&full[0], 0) : smem_u32(&full[0]);
-      auto load_b = [&](int stg, int kb, int n0, uint32_t fb) {
-#pragma unroll
-        for (int a = 0; a < ATOMS; ++a) {
-          const int kc = (kb * ATOMS + a) * KELEMS;
-          uint8_t* dB = sB + stg * C_::B_ST + a * C_::B_ATOM;
-          if (PAIR) {
-            e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
-          } else if (cs > 1) {
-            e_tma_load_mc(dB + rank * slice * BK_BYTES, &tma_b, fb, kc, n0 + rank * slice, mask);
-          } else {
-            e_tma_load(dB, &tma_b, fb, kc, n0);
-          }
-        }
-      };
-      // The weights (B) are never written by an earlier kernel: the first
-      // item's first stages request their B tiles before the wait on the
-      // previous kernel, so the HBM latency of the weights overlaps its
-      // tail; A (its output) is requested after the wait.
-      const int pre = cluster < items && !(p.diag & 1) ? (p.kb < STAGES ? p.kb : STAGES) : 0;
-      for (int kb = 0; kb < pre; ++kb) {  // fresh slots: no empty wait
-        if (!PAIR || leader) e_expect_tx(&full[kb], bytes);
-        load_b(kb, kb, (cluster / mgroups) * p.bn, full0 + kb * static_cast<uint32_t>(sizeof(uint64_t)));
-      }
-      pdl_wait();
       for (int it = cluster; it < items; it += nclusters) {
         const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         for (int kb = 0; kb < p.kb; ++kb) {
-          const bool early = it == cluster && kb < pre;  // B already requested
-          if (!early) mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
+          mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
           if ((p.diag & 1) && (kb >= STAGES || it != cluster)) {
             if (!PAIR || leader) e_arrive(&full[s]);
           } else {
-            if (!early && (!PAIR || leader)) e_expect_tx(&full[s], bytes);
+            if (!PAIR || leader) e_expect_tx(&full[s], bytes);
             const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
 #pragma unroll
             for (int a = 0; a < ATOMS; ++a) {
               const int kc = (kb * ATOMS + a) * KELEMS;
               uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
+              uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
               if (PAIR) {
 #pragma unroll
                 for (int b = 0; b < MB; ++b) {
                   e_tma_load_pair(dA + b * ATOMS * C_::A_ATOM, &tma_a, fb, kc, m0 + b * 2 * BM);
                 }
+                e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
               } else {
                 e_tma_load(dA, &tma_a, fb, kc, m0);
+                if (cs > 1) {
+                  e_tma_load_mc(dB + rank * slice * BK_BYTES, &tma_b, fb, kc, n0 + rank * slice, mask);
+                } else {
+                  e_tma_load(dB, &tma_b, fb, kc, n0);
+                }
               }
             }
-            if (!early) load_b(s, kb, n0, fb);
           }
           if (++s == STAGES) {
             s = 0;
