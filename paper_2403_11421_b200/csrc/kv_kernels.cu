@@ -622,7 +622,17 @@ __global__ void append_kernel(const AppendArgs a) {
     for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = src[e];
   } else if (g.fmt == SD_KV_HALF) {
     __half* d = reinterpret_cast<__half*>(row);
-    for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(src[e]);
+    if ((g.width & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) | (reinterpret_cast<uintptr_t>(d) & 7)) == 0) {
+      // 16-B loads, 8-B stores (same round-to-nearest-even as the scalar path)
+      for (int e = 4 * threadIdx.x; e < g.width; e += 4 * blockDim.x) {
+        const float4 x = *reinterpret_cast<const float4*>(src + e);
+        const __half2 lo = __floats2half2_rn(x.x, x.y), hi = __floats2half2_rn(x.z, x.w);
+        *reinterpret_cast<uint2*>(d + e) =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+      }
+    } else {
+      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(src[e]);
+    }
   } else {
     // one warp per head
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
