@@ -62,7 +62,10 @@ enum sd_kv_format { SD_KV_SINGLE = 0, SD_KV_HALF = 1, SD_KV_INT8 = 2 };
 enum sd_dense_mode {
   SD_DENSE_EXACT_F32 = 0, /* CUDA-core fp32, the reference's per-element op order (bitwise) */
   SD_DENSE_BF16 = 1,      /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
-  SD_DENSE_TF32 = 2       /* tcgen05 kind::tf32, fp32 operands, fp32 accumulate in TMEM */
+  SD_DENSE_TF32 = 2,      /* tcgen05 kind::tf32, fp32 operands (read truncated to tf32), fp32 accumulate */
+  SD_DENSE_F16 = 3        /* tcgen05 kind::f16, fp16 operands (RNE, 11-bit significand), fp32 accumulate:
+                             tf32-level operand precision at the bf16 rate; operands must stay within
+                             fp16 range (|x| < 65504) */
 };
 
 /* ShardMode (transport.hpp:150-170) */
@@ -167,9 +170,18 @@ int sd_kv_timing_read(sd_kv* kv, double* ms, int64_t* launches, double* bytes, i
  * then head (V x D); each Eigen column-major. */
 int sd_weights_upload(const sd_model_spec* spec, const float* const* tensors, int dense_mode,
                       int device, sd_weights** out);
-/* Device-side seed_random_weights (core.cpp:97-127) is not offered: weights
- * are generated on the host (mt19937 is sequential) and uploaded. */
+/* seed_random_weights (core.cpp:97-127, WeightSet core.hpp:85-90): the
+ * reference's deterministic weights (mt19937 seeded uint32(seed ^ seed>>32),
+ * uniform +-1/sqrt(fan_in), embedding +-1, memory-order fill), bit-identical
+ * to the reference's, generated on the host (~1 ns per value; the stream is
+ * sequential) and uploaded into `dense_mode`'s layout. */
+int sd_weights_seed_random(const sd_model_spec* spec, uint64_t seed, int dense_mode, int device,
+                           sd_weights** out);
 int sd_weights_destroy(sd_weights* w);
+/* The embedding as stored (fp32, D x V column-major: token t's column is
+ * host[t * D .. t * D + D)), for callers that build TokenBatch.features on
+ * the host (workers.cpp:629-638). count >= D * V. */
+int sd_weights_export_embedding(const sd_weights* w, float* host, size_t count);
 /* project_qkv (dense.hpp:26-27): x [B][D] -> q [B][D], k, v [B][Hkv*hd]. */
 int sd_s_project_qkv(sd_weights* w, int layer, int32_t B, const float* x, float* q, float* k,
                      float* v);
@@ -222,6 +234,16 @@ int sd_engine_timing_read(sd_engine* e, double* ms, double* flops, int64_t* laun
  * S-Part of the other on the remaining SMs. enable = 0: one batch, one
  * stream (default). */
 int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
+/* Process-wide tuning switches, for A/B measurements and the
+ * variant-equivalence tests (the defaults are the measured-best paths):
+ * "gemm_bn" (force the CTA-pair tile width, 64..256, multiple of 16; 0 = the
+ * wave cost model), "gemm_pair" (0: single-CTA tiles), "fused_append" (0:
+ * separate KV append kernel), "fused_argmax" (0: logits + argmax kernel),
+ * "dist_fuse" (0: scatter kernel for the peer exchange), "attn_mma" (0:
+ * CUDA-core attention), "pdl" (0: no programmatic dependent launch),
+ * "dist_phases" (1: per-phase DistEngine timing on stderr). Unknown names
+ * return SD_ERR_CONFIG. */
+int sd_tune(const char* name, int value);
 /* Kernel launches issued by this library in this process (all devices). */
 int64_t sd_launch_count(void);
 /* Synthetic device-generated weights (uniform +-1/sqrt(fan_in), counter
@@ -265,7 +287,11 @@ typedef struct sd_dist sd_dist;
 int sd_nccl_unique_id(void* out, size_t bytes);
 /* shard_mode (enum sd_shard_mode, over kv heads): BY_SEQUENCE (default,
  * NCCL or peer exchange), BY_HEAD or HYBRID (peer exchange only); `kv` must
- * hold this rank's head range (sd_shardmap_head_range). */
+ * hold this rank's head range (sd_shardmap_head_range). nccl_id may be NULL:
+ * no NCCL communicator is created and the rank must connect the peer
+ * exchange (sd_dist_p2p_*) before its first step; the per-layer exchange and
+ * the per-step next-token gather then run as peer stores only (this also
+ * lets several ranks share one device). */
 int sd_dist_create(sd_weights* weights_or_null, sd_kv* kv, int rank, int world,
                    const void* nccl_id, int s_ranks, int shard_mode, sd_dist** out);
 int sd_dist_destroy(sd_dist* d);
@@ -285,7 +311,7 @@ int sd_dist_timing_read(sd_dist* d, double* exchange_ms, double* exchange_bytes,
  * handles are gathered (rank order, world * SD_DIST_IPC_BYTES), connect maps
  * the peers' buffers. Every later step scatters rows with direct NVLink
  * stores and an epoch flag per (exchange, source). */
-#define SD_DIST_IPC_BYTES 320
+#define SD_DIST_IPC_BYTES 384
 int sd_dist_p2p_setup(sd_dist* d, int32_t max_rows, void* handles_out);
 int sd_dist_p2p_connect(sd_dist* d, const void* all_handles);
 /* Host-only row plan of a step (CPU-testable): home rows grouped by shard,

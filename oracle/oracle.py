@@ -84,6 +84,8 @@ _sig("orc_kv_destroy", None, P)
 _sig("orc_kv_append", C.c_int, P, C.c_uint64, C.c_int, C.c_uint32, FP, FP)
 _sig("orc_kv_append_request", C.c_int, P, C.c_int, C.c_int, U64P, U32P, FP, FP)
 _sig("orc_kv_attend", C.c_int, P, C.c_int, C.c_int, U64P, FP, FP)
+_sig("orc_kv_prefill_synthetic", C.c_int, P, C.c_int, U64P, C.c_int, C.c_uint64)
+_sig("orc_kv_prefill_index", C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int)
 _sig("orc_kv_drop", None, P, C.c_uint64)
 _sig("orc_kv_stored_length", C.c_int, P, C.c_uint64, C.c_int)
 _sig("orc_kv_token_count", C.c_long, P)
@@ -182,6 +184,11 @@ def synth_value(idx: int) -> float:
     return float(_lib.orc_synth_value(idx))
 
 
+def prefill_index(seq, layer, pos, kv, h, d, kv_heads, hd) -> int:
+    """Element index of the sequence-keyed synthetic prefill."""
+    return int(_lib.orc_kv_prefill_index(seq, layer, pos, kv, h, d, kv_heads, hd))
+
+
 class Weights:
     """seed_random_weights (core.cpp:97-127)."""
 
@@ -245,6 +252,12 @@ class KvShard:
         k, v = f32(k), f32(v)
         _check(_lib.orc_kv_append_request(self.h, layer, len(seqs_a), sp,
                                           pos.ctypes.data_as(U32P), _f(k), _f(v)))
+
+    def prefill_synthetic(self, seqs, length: int, salt: int = 0):
+        """Synthetic context (sequence-keyed) appended position by
+        position in every layer: the bench / GPU prefill restated."""
+        seqs_a, sp = _u64(seqs)
+        _check(_lib.orc_kv_prefill_synthetic(self.h, len(seqs_a), sp, length, salt))
 
     def attend(self, layer, seqs, q) -> np.ndarray:
         seqs_a, sp = _u64(seqs)

@@ -328,6 +328,8 @@ class KvShard {
     if (fmt < 0 || fmt > 2) throw Error(kConfig, "unknown kv storage format");
   }
   int width() const { return hc_ * s_.head_dim; }  // kv width
+  int head_start() const { return h0_; }
+  const Spec& spec() const { return s_; }
   int group() const { return s_.num_heads / s_.num_kv_heads; }
   int q_width() const { return width() * group(); }
   long token_count() const { return total_ / s_.num_layers; }
@@ -1027,6 +1029,15 @@ inline float synth_value(uint64_t idx) {
   return 2.0f * (static_cast<float>(mix64(0x5EEDull ^ idx) >> 40) * 0x1p-24f) - 1.0f;
 }
 
+// Sequence-keyed element index of the synthetic prefill (the
+// repo's fixed definition; not a reference function): sequence id, layer
+// (< 4096), position (< 2^20), K (0) / V (1), global kv head h, element d.
+inline uint64_t prefill_index(uint64_t seq, int layer, int pos, int kv, int h, int d, int kv_heads, int hd) {
+  return ((((seq * 4096u + static_cast<uint64_t>(layer)) * 1048576u + static_cast<uint64_t>(pos)) * 2u +
+           static_cast<uint64_t>(kv)) * static_cast<uint64_t>(kv_heads) + static_cast<uint64_t>(h)) *
+             static_cast<uint64_t>(hd) + static_cast<uint64_t>(d);
+}
+
 }  // namespace orc
 
 // ============================================================ C interface ===
@@ -1092,6 +1103,34 @@ int orc_kv_create(const orc_spec* s, int head_start, int head_count, long cap, i
 void orc_kv_destroy(void* kv) { delete static_cast<KvShard*>(kv); }
 int orc_kv_append(void* kv, uint64_t seq, int layer, uint32_t pos, const float* k, const float* v) {
   return guard([&] { static_cast<KvShard*>(kv)->append(seq, layer, pos, k, v); });
+}
+// Synthetic context of `length` positions for each sequence in every layer,
+// appended through KvShard::append (so the stored bytes follow the reference
+// conversions): K/V element (seq, layer, pos, kv, h0 + head, d) =
+// synth_value(salt ^ prefill_index(...)).
+int orc_kv_prefill_synthetic(void* kvp, int n, const uint64_t* seqs, int length, uint64_t salt) {
+  return guard([&] {
+    KvShard* kv = static_cast<KvShard*>(kvp);
+    const Spec& sp = kv->spec();
+    const int w = kv->width(), hd = sp.head_dim, h0 = kv->head_start();
+    std::vector<float> k(static_cast<size_t>(w)), v(static_cast<size_t>(w));
+    for (int i = 0; i < n; ++i) {
+      for (int l = 0; l < sp.num_layers; ++l) {
+        for (int pos = 0; pos < length; ++pos) {
+          const uint64_t bk = prefill_index(seqs[i], l, pos, 0, h0, 0, sp.num_kv_heads, hd);
+          const uint64_t bv = prefill_index(seqs[i], l, pos, 1, h0, 0, sp.num_kv_heads, hd);
+          for (int e = 0; e < w; ++e) {
+            k[static_cast<size_t>(e)] = synth_value(salt ^ (bk + static_cast<uint64_t>(e)));
+            v[static_cast<size_t>(e)] = synth_value(salt ^ (bv + static_cast<uint64_t>(e)));
+          }
+          kv->append(seqs[i], l, static_cast<uint32_t>(pos), k.data(), v.data());
+        }
+      }
+    }
+  });
+}
+uint64_t orc_kv_prefill_index(uint64_t seq, int layer, int pos, int kv, int h, int d, int kv_heads, int hd) {
+  return prefill_index(seq, layer, pos, kv, h, d, kv_heads, hd);
 }
 int orc_kv_append_request(void* kv, int layer, int n, const uint64_t* seqs, const uint32_t* pos,
                           const float* k, const float* v) {

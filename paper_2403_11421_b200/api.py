@@ -67,7 +67,7 @@ def _check(rc: int):
 
 
 FORMATS = {"single": 0, "half": 1, "int8": 2}
-DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2}
+DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2, "fp16": 3}
 SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2, "sequence": 0, "head": 1}
 # home (S-Part) placement with data-parallel S-ranks (SD_HOME_MODULO, include/sd_abi.h)
 HOME_POLICIES = {"affinity": 0, "modulo": 0x100}
@@ -99,6 +99,32 @@ def make_model_spec(num_layers: int, model_dim: int, num_heads: int, mlp_dim: in
 def launch_count() -> int:
     """Kernel launches issued by libsd_b200 in this process."""
     return int(lib.sd_launch_count())
+
+
+_TUNED = {"gemm_bn": 0, "gemm_pair": 1, "fused_append": 1, "fused_argmax": 1, "dist_fuse": 1,
+          "attn_mma": 1, "pdl": 1, "dist_phases": 0}
+
+
+def tune(name: str, value: int):
+    """Process-wide tuning switch (sd_tune); defaults are the measured-best paths."""
+    _check(lib.sd_tune(name.encode(), int(value)))
+
+
+class tuned:
+    """Context manager: set tuning switches, restore the defaults on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            tune(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.kw:
+            tune(k, _TUNED[k])
+        return False
 
 
 def mix64(x: int) -> int:
@@ -292,14 +318,23 @@ class DeviceWeights:
     """WeightSet (core.hpp:85-90) uploaded to a device. `tensors` follow the
     reference storage: [embedding (D x V), per layer w_q, w_k, w_v, w_o,
     w_mlp_in, w_mlp_out, head (V x D)], each a flat column-major buffer.
-    tensors=None generates synthetic weights on the device."""
+    tensors=None generates the weights: generator "reference" is
+    seed_random_weights(spec, seed) (core.cpp:97-127), bit-identical to the
+    reference's WeightSet (host mt19937 stream, uploaded); "counter" is a
+    device-side counter hash of the same distribution (fast, not the
+    reference's values)."""
 
     def __init__(self, spec: ModelSpec, tensors: Sequence[np.ndarray] | None, mode: str = "exact",
-                 device: int = 0, seed: int = 0):
+                 device: int = 0, seed: int = 0, generator: str = "counter"):
         self.spec = spec
         self.mode = mode
         self.h = C.c_void_p()
-        if tensors is None:
+        if tensors is None and generator == "reference":
+            _check(lib.sd_weights_seed_random(C.byref(spec), seed, DENSE_MODES[mode], device,
+                                              C.byref(self.h)))
+        elif tensors is None:
+            if generator != "counter":
+                raise ConfigError(f"unknown weight generator {generator!r}")
             _check(lib.sd_weights_synthetic(C.byref(spec), DENSE_MODES[mode], seed, device,
                                             C.byref(self.h)))
         else:
@@ -308,6 +343,16 @@ class DeviceWeights:
             _check(lib.sd_weights_upload(C.byref(spec), arr, DENSE_MODES[mode], device,
                                          C.byref(self.h)))
             self._keep = None
+
+    def embedding_host(self, out=None) -> np.ndarray:
+        """The embedding as stored, as a (vocab, model_dim) array whose row t is
+        embedding column t (the TokenBatch.features of token t)."""
+        shape = (self.spec.vocab_size, self.spec.model_dim)
+        if out is None:
+            out = np.empty(shape, np.float32)
+        assert out.dtype == np.float32 and out.flags["C_CONTIGUOUS"] and out.size >= shape[0] * shape[1]
+        _check(lib.sd_weights_export_embedding(self.h, _fp(out), out.size))
+        return out.reshape(shape)
 
     def close(self):
         if getattr(self, "h", None):
@@ -362,7 +407,7 @@ def apply_linear(w: DeviceWeights, layer: int, which: int, x):
 def gemm_dev(kind: str, M: int, N: int, K: int, A, lda, B, ldb, C=None, ldc=0, Cb=None, ldcb=0,
              epi: int = 0, res=None, ldr=0, stream=0):
     """tcgen05 GEMM on device pointers (ints, e.g. torch .data_ptr()):
-    C = A . B^T (+ epilogue). kind: "bf16" | "tf32"."""
+    C = A . B^T (+ epilogue). kind: "bf16" | "fp16" | "tf32"."""
     _check(lib.sd_gemm_dev(DENSE_MODES[kind], M, N, K, A, lda, B, ldb, C, ldc, Cb, ldcb, epi, res,
                            ldr, stream))
 
@@ -383,12 +428,17 @@ class Engine:
 
     __del__ = close
 
-    def compute(self, seqs, tokens=None, features=None, want_final=False, want_logits=False):
-        """StepComputation::compute -> DecodeStepResult(next_tokens, final_activations)."""
+    def compute(self, seqs, tokens=None, features=None, want_final=False, want_logits=False,
+                out_next=None, out_final=None):
+        """StepComputation::compute -> DecodeStepResult(next_tokens, final_activations).
+        out_next / out_final: caller-owned result buffers (e.g. pinned)."""
         s, sp = _u64(seqs)
         B = len(s)
-        nxt = np.zeros(B, np.int32)
-        fx = np.zeros((B, self.weights.spec.model_dim), np.float32) if want_final else None
+        nxt = out_next if out_next is not None else np.zeros(B, np.int32)
+        if out_final is not None:
+            fx = out_final
+        else:
+            fx = np.zeros((B, self.weights.spec.model_dim), np.float32) if want_final else None
         if features is not None:
             x = _f32(features)
             lg = np.zeros((B, self.weights.spec.vocab_size), np.float32) if want_logits else None
@@ -516,7 +566,7 @@ class DistEngine:
         _check(lib.sd_dist_timing_read(self.h, C.byref(ms), C.byref(b), int(reset)))
         return ms.value, b.value
 
-    IPC_BYTES = 320
+    IPC_BYTES = 384
 
     def p2p_handles(self, max_rows: int) -> bytes:
         """Allocate this rank's peer-exchange receive buffers (up to `max_rows`

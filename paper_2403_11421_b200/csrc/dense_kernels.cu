@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kCols) linear_exact_kernel(int B, int in, int 
 
 __global__ void embed_kernel(int B, int D, const int32_t* __restrict__ tokens,
                              const float* __restrict__ emb, float* __restrict__ x, int64_t ldx,
-                             __nv_bfloat16* __restrict__ xb) {
+                             uint16_t* __restrict__ xb, int f16) {
   pdl_trigger();
   pdl_wait();
   const int b = blockIdx.x;
@@ -76,7 +76,7 @@ __global__ void embed_kernel(int B, int D, const int32_t* __restrict__ tokens,
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     const float v = col[d];
     x[static_cast<int64_t>(b) * ldx + d] = v;
-    if (xb) xb[static_cast<int64_t>(b) * D + d] = __float2bfloat16_rn(v);
+    if (xb) xb[static_cast<int64_t>(b) * D + d] = to16(v, f16);
   }
 }
 
@@ -130,17 +130,31 @@ __global__ void argmax_kernel(int V, const float* __restrict__ logits, int64_t l
   }
 }
 
-__global__ void to_bf16_kernel(int rows, int cols, const float* __restrict__ x, int64_t ldx,
-                               __nv_bfloat16* __restrict__ y, int64_t ldy) {
+__global__ void to16_kernel(int rows, int cols, const float* __restrict__ x, int64_t ldx,
+                            uint16_t* __restrict__ y, int64_t ldy, int f16) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.y;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    y[static_cast<int64_t>(r) * ldy + c] = __float2bfloat16_rn(x[static_cast<int64_t>(r) * ldx + c]);
+    y[static_cast<int64_t>(r) * ldy + c] = to16(x[static_cast<int64_t>(r) * ldx + c], f16);
   }
 }
 
 }  // namespace
+
+__global__ void fill_synthetic_kernel(float* p, int64_t n, uint64_t salt) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    p[i] = synth_value(salt + static_cast<uint64_t>(i));
+  }
+}
+
+void launch_fill_synthetic(float* p, int64_t n, uint64_t salt, cudaStream_t s) {
+  if (n <= 0) return;
+  fill_synthetic_kernel<<<148 * 4, 256, 0, s>>>(p, n, salt);
+  SD_CUDA(cudaGetLastError());
+  ::sd::count_launch();
+}
 
 void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, const float* w,
                          int64_t ldw, float* y, int64_t ldy, int epi, const float* res,
@@ -153,9 +167,10 @@ void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, co
 }
 
 void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
-                  __nv_bfloat16* xb, cudaStream_t s) {
+                  void* xb, int f16, cudaStream_t s) {
   if (B == 0) return;
-  SD_CUDA(launch_pdl(embed_kernel, dim3(B), dim3(256), 0, s, 1, B, D, tokens, emb, x, ldx, xb));
+  SD_CUDA(launch_pdl(embed_kernel, dim3(B), dim3(256), 0, s, 1, B, D, tokens, emb, x, ldx,
+                     static_cast<uint16_t*>(xb), f16));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }
@@ -186,11 +201,12 @@ void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* token
   ::sd::count_launch();
 }
 
-void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat16* y,
-                    int64_t ldy, cudaStream_t s) {
+void launch_to_16(int rows, int cols, const float* x, int64_t ldx, void* y, int64_t ldy, int f16,
+                  cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
   dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, rows);
-  SD_CUDA(launch_pdl(to_bf16_kernel, grid, dim3(256), 0, s, 1, rows, cols, x, ldx, y, ldy));
+  SD_CUDA(launch_pdl(to16_kernel, grid, dim3(256), 0, s, 1, rows, cols, x, ldx, static_cast<uint16_t*>(y), ldy,
+                     f16));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }

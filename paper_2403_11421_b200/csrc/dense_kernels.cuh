@@ -20,22 +20,26 @@ enum Epilogue : int {
 void launch_linear_exact(int B, int in, int out, const float* x, int64_t ldx, const float* w,
                          int64_t ldw, float* y, int64_t ldy, int epi, const float* res,
                          int64_t ldr, cudaStream_t s);
-// x[b][:] = embedding(:, tokens[b]); embedding is D x V column-major.
+// x[b][:] = embedding(:, tokens[b]); embedding is D x V column-major;
+// xb (optional): its 16-bit copy (fp16 when f16, else bf16)
 void launch_embed(int B, int D, const int32_t* tokens, const float* emb, float* x, int64_t ldx,
-                  __nv_bfloat16* xb, cudaStream_t s);
+                  void* xb, int f16, cudaStream_t s);
 // argmax_token per row (first index wins ties, dense.cpp:78-88)
 // tokens[i] from the fused-argmax keys (first maximum wins, as
 // argmax_token dense.cpp:80-88); resets the keys to zero for the next launch
 void launch_argmax_keys(int B, unsigned long long* keys, int32_t* tokens, cudaStream_t s);
 void launch_argmax(int B, int V, const float* logits, int64_t ld, int32_t* tokens,
                    cudaStream_t s);
-// fp32 -> bf16 copy (activation staging for the tensor-core GEMMs)
-void launch_to_bf16(int rows, int cols, const float* x, int64_t ldx, __nv_bfloat16* y,
-                    int64_t ldy, cudaStream_t s);
+// counter-hash values in [-1, 1) (synth_value(salt + i)): benchmark operands
+void launch_fill_synthetic(float* p, int64_t n, uint64_t salt, cudaStream_t s);
+// fp32 -> 16-bit copy (the A operand of a kind::f16 GEMM; fp16 when f16, else bf16)
+void launch_to_16(int rows, int cols, const float* x, int64_t ldx, void* y, int64_t ldy, int f16,
+                  cudaStream_t s);
 
 // tcgen05 GEMM: C[M][N] = A[M][K] . B[N][K]^T with fused epilogue; A, B
-// K-major (bf16 for kind::f16, fp32 bits for kind::tf32). Writes fp32 C and,
-// if cb != nullptr, a bf16 copy for the next GEMM's A operand.
+// K-major (bf16 / fp16 for kind::f16, fp32 bits for kind::tf32). Writes fp32 C
+// and, if Cb != nullptr, a 16-bit copy (the operand format) for the next
+// GEMM's A operand.
 // Multi-GPU exchange fused into a producer's epilogue (dist.cpp): output row
 // m is stored straight into base[rank[m]] + row[m] * ld (a peer's receive
 // buffer through its CUDA IPC mapping, or this rank's own), and the last CTA
@@ -74,12 +78,12 @@ struct GemmArgs {
   int64_t ldb;
   float* C;
   int64_t ldc;
-  __nv_bfloat16* Cb;
+  void* Cb;      // 16-bit copy of C in the operand format (bf16 / fp16)
   int64_t ldcb;
   int epi;
   const float* res;
   int64_t ldr;
-  int kind;      // 1 = bf16 (kind::f16), 2 = tf32
+  int kind;      // SD_DENSE_BF16 (kind::f16, bf16), SD_DENSE_TF32 (kind::tf32), SD_DENSE_F16 (kind::f16, fp16)
   int max_ctas;  // SM budget of the persistent grid (0 = every SM)
   const RowRoute* route = nullptr;  // fp32 C rows routed to peers (C unused)
   // argmax_token fused into the epilogue: per row, atomicMax of (ordered
@@ -91,19 +95,5 @@ struct GemmArgs {
 bool gemm_sm100_supported(const GemmArgs& g);
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s);
 
-// The GEMMs between two attentions (W_o, MLP-in, MLP-out, next QKV / head)
-// as one persistent launch with per-(GEMM, row block) completion counters
-// (gemm_sm100.cu). bf16, equal M >= 256. `done` holds kChainMax x 64 counters
-// zeroed at the start of the step; `epoch` = chain launches since then.
-struct ChainArgs {
-  int n;
-  GemmArgs g[4];
-  unsigned long long* done;
-  unsigned long long epoch;
-  int max_ctas;
-};
-bool gemm_chain_supported(const ChainArgs& c);
-void launch_gemm_chain(const ChainArgs& c, cudaStream_t s);
-// argmax over rows of C fused as a second pass (kept separate: logits stay in HBM for callers)
 
 }  // namespace sd

@@ -187,9 +187,9 @@ DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void*
     }
   }
   DeviceGuard dg(device_);
-  phases_ = std::getenv("SD_DIST_PHASES") != nullptr;
+  phases_ = tuning().dist_phases != 0;
   SD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  if (world > 1) {
+  if (world > 1 && nccl_id) {  // NULL: no communicator, the peer exchange carries everything
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     nccl_check(Nccl::get().CommInitRank(&comm_, world, id, rank), "ncclCommInitRank");
@@ -220,7 +220,7 @@ DistEngine::~DistEngine() {
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
                   static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_)}) {
+                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_)}) {
     if (p) cudaFree(p);
   }
   if (comm_) Nccl::get().CommDestroy(comm_);
@@ -290,6 +290,9 @@ void DistEngine::plan_for(int B, const uint64_t* seqs) {
   if (mode_ != SD_SHARD_BY_SEQUENCE && !p2p_) {
     fail(SD_ERR_CONFIG, "by-head / hybrid sharding needs the peer exchange (sd_dist_p2p_connect)");
   }
+  if (world_ > 1 && !comm_ && !p2p_) {
+    fail(SD_ERR_CONFIG, "a distributed engine without an NCCL id needs the peer exchange (sd_dist_p2p_connect)");
+  }
   if (p2p_) {
     // where this rank's rows land in each peer's receive buffers (every rank
     // derives every plan from the same batch)
@@ -337,14 +340,15 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaStreamSynchronize(stream_));
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
                   static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_)}) {
+                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_)}) {
     if (p) cudaFree(p);
   }
   const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_qkv_), rows * spec_.qkv_width() * 4));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), rows * spec_.D * 4));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_ob_), rows * spec_.D * 2));
-  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), 2 * kMaxWorld * sizeof(int64_t)));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_tok_), 2 * rows * sizeof(int32_t)));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), kFlagSlots * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&done_), sizeof(int32_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&gemm_done_), sizeof(int32_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&attn_done_), sizeof(int32_t)));
@@ -352,11 +356,13 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaMemset(attn_done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaMemset(rx_qkv_, 0, rows * spec_.qkv_width() * 4));
   SD_CUDA(cudaMemset(rx_o_, 0, rows * spec_.D * 4));
-  SD_CUDA(cudaMemset(flags_, 0, 2 * kMaxWorld * sizeof(int64_t)));
+  SD_CUDA(cudaMemset(flags_, 0, kFlagSlots * kMaxWorld * sizeof(int64_t)));
+  SD_CUDA(cudaMemset(rx_tok_, 0, 2 * rows * sizeof(int32_t)));
   SD_CUDA(cudaMemset(done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaDeviceSynchronize());
   SD_CUDA(cudaMemset(rx_ob_, 0, rows * spec_.D * 2));
-  cudaIpcMemHandle_t h[4];
+  cudaIpcMemHandle_t h[kIpcHandles];
+  SD_CUDA(cudaIpcGetMemHandle(&h[4], rx_tok_));
   SD_CUDA(cudaIpcGetMemHandle(&h[0], rx_qkv_));
   SD_CUDA(cudaIpcGetMemHandle(&h[1], rx_o_));
   SD_CUDA(cudaIpcGetMemHandle(&h[2], flags_));
@@ -366,7 +372,9 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   const int32_t mode = w_ ? w_->mode() : -1;
   std::memcpy(static_cast<uint8_t*>(handles_out) + sizeof(h), &mode, sizeof(mode));
   p2p_cap_ = max_rows;
+  tok_rows_ = static_cast<int>(rows);
   epoch_ = 0;
+  tok_epoch_ = 0;
 }
 
 void DistEngine::p2p_connect(const void* all_handles) {
@@ -374,7 +382,7 @@ void DistEngine::p2p_connect(const void* all_handles) {
   DeviceGuard dg(device_);
   const auto* hb = static_cast<const uint8_t*>(all_handles);
   for (int p = 0; p < world_; ++p) {
-    cudaIpcMemHandle_t h[4];
+    cudaIpcMemHandle_t h[kIpcHandles];
     std::memcpy(h, hb + static_cast<size_t>(p) * kIpcBytes, sizeof(h));
     std::memcpy(&peer_mode_[p], hb + static_cast<size_t>(p) * kIpcBytes + sizeof(h), sizeof(int32_t));
     if (p == rank_) {
@@ -382,21 +390,23 @@ void DistEngine::p2p_connect(const void* all_handles) {
       peer_o_[p] = rx_o_;
       peer_flags_[p] = flags_;
       peer_ob_[p] = rx_ob_;
+      peer_tok_[p] = rx_tok_;
       continue;
     }
-    void* ptr[4];
-    for (int i = 0; i < 4; ++i) {
+    void* ptr[kIpcHandles];
+    for (int i = 0; i < kIpcHandles; ++i) {
       SD_CUDA(cudaIpcOpenMemHandle(&ptr[i], h[i], cudaIpcMemLazyEnablePeerAccess));
       opened_.push_back(ptr[i]);
     }
     peer_qkv_[p] = static_cast<float*>(ptr[0]);
     peer_o_[p] = static_cast<float*>(ptr[1]);
     peer_flags_[p] = static_cast<int64_t*>(ptr[2]);
-    peer_ob_[p] = static_cast<__nv_bfloat16*>(ptr[3]);
+    peer_ob_[p] = static_cast<act16*>(ptr[3]);
+    peer_tok_[p] = static_cast<int32_t*>(ptr[4]);
   }
   p2p_ = true;
   // the exchange is fused into the producers when both have a routed form
-  fused_ = std::getenv("SD_DIST_NO_FUSE") == nullptr && mode_ == SD_SHARD_BY_SEQUENCE && kv_->tensor_core_path();
+  fused_ = tuning().dist_fuse != 0 && mode_ == SD_SHARD_BY_SEQUENCE && kv_->tensor_core_path();
   plan_key_.clear();  // recompute the peer offsets
 }
 
@@ -580,8 +590,10 @@ void DistEngine::run_step() {
   const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
   const int nh = static_cast<int>(plan_.home_rows.size());
   const int ns = static_cast<int>(plan_.shard_rows.size());
-  const bool bf = w_ && w_->mode() == SD_DENSE_BF16;
-  if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, stream_);
+  // kind::f16 homes keep 16-bit copies of the GEMM A operands (bf16 or fp16)
+  const bool bf = w_ && (w_->mode() == SD_DENSE_BF16 || w_->mode() == SD_DENSE_F16);
+  const int f16 = w_ && w_->mode() == SD_DENSE_F16 ? 1 : 0;
+  if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, f16, stream_);
   const bool fused = p2p_ && fused_;
   const bool route_qkv = fused && nh && w_->mode() != SD_DENSE_EXACT_F32;  // exact mode: scatter kernel
   const int32_t* tbl = static_cast<const int32_t*>(route_.p);
@@ -648,9 +660,10 @@ void DistEngine::run_step() {
       orr.row = tbl + 2 * nh + ns;
       orr.ld = D;
       for (int d = 0; d < world_; ++d) {
-        // a bf16 home takes its W_o operand straight from the attention
-        if (peer_mode_[d] == SD_DENSE_BF16) {
+        // a kind::f16 home takes its W_o operand straight from the attention
+        if (peer_mode_[d] == SD_DENSE_BF16 || peer_mode_[d] == SD_DENSE_F16) {
           orr.bbase[d] = peer_ob_[d];
+          if (peer_mode_[d] == SD_DENSE_F16) orr.f16_mask |= 1u << d;
         } else {
           orr.base[d] = peer_o_[d];
         }
@@ -683,8 +696,8 @@ void DistEngine::run_step() {
       exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h, plan_.send_cnt, plan_.send_off, D);
     }
     if (nh) {
-      __nv_bfloat16* ob = fused && bf ? rx_ob_ : ob_;  // fused: the attention wrote it
-      if (bf && !fused) launch_to_bf16(nh, D, o_h, D, ob_, D, stream_);
+      act16* ob = fused && bf ? rx_ob_ : ob_;  // fused: the attention wrote it
+      if (bf && !fused) launch_to_16(nh, D, o_h, D, ob_, D, f16, stream_);
       mark(6);
       w_->linear(l, 4, nh, o_h, D, ob, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
       mark(7);
@@ -695,7 +708,7 @@ void DistEngine::run_step() {
     }
   }
   if (nh) {
-    if (w_->mode() != SD_DENSE_EXACT_F32 && getenv("SD_NO_FUSED_ARGMAX") == nullptr) {
+    if (w_->mode() != SD_DENSE_EXACT_F32 && tuning().fused_argmax) {
       // argmax_token in the head GEMM's epilogue: no logits round trip
       GemmArgs ga = w_->gemm_args(0, 7, nh, x_, D, xb_, D, nullptr, s.V, nullptr, 0, kEpiNone, nullptr, 0);
       ga.amax = amax_;
@@ -708,8 +721,20 @@ void DistEngine::run_step() {
   }
 }
 
-void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next, float* final_x) {
+// validate_batch (core.cpp:37-54): a repeated sequence id is a ConfigError
+// before anything is planned or appended
+static void check_unique(int B, const uint64_t* seqs) {
   if (B == 0) fail(SD_ERR_CONFIG, "project_qkv: empty batch");
+  std::unordered_set<uint64_t> seen;
+  for (int i = 0; i < B; ++i) {
+    if (!seen.insert(seqs[i]).second) {
+      fail(SD_ERR_CONFIG, "token batch: duplicate sequence id " + std::to_string(seqs[i]));
+    }
+  }
+}
+
+void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next, float* final_x) {
+  check_unique(B, seqs);
   DeviceGuard dg(device_);
   ensure(B);
   plan_for(B, seqs);
@@ -727,7 +752,30 @@ void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int
   // between steps (balanced homes follow the batch), so each rank's caller
   // keeps every sequence's last token. Homes write their rows into a zeroed
   // batch vector, summed across ranks (B int32 per step).
-  if (world_ > 1) {
+  if (world_ > 1 && p2p_) {
+    // peer stores of the home rows' tokens into every rank's batch vector
+    // (double-buffered by step parity: a rank can be at most one step ahead)
+    const int64_t ep = ++tok_epoch_;
+    const int half = static_cast<int>(ep & 1) * tok_rows_;
+    P2PTokens a{};
+    a.idx = home_idx_;
+    a.src = tok_;
+    a.n = nh;
+    a.world = world_;
+    a.self = rank_;
+    a.slot = kTokSlot;
+    a.epoch = ep;
+    uint32_t others = 0;
+    for (int d = 0; d < world_; ++d) {
+      a.dst[d] = peer_tok_[d] + half;
+      a.flag[d] = peer_flags_[d];
+      if (d != rank_) others |= 1u << d;
+    }
+    a.notify = others;
+    launch_p2p_tokens(a, stream_);
+    launch_p2p_wait(flags_, kTokSlot, others, world_, ep, stream_);
+    SD_CUDA(cudaMemcpyAsync(next, rx_tok_ + half, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
+  } else if (world_ > 1) {
     SD_CUDA(cudaMemsetAsync(all_tok_, 0, static_cast<size_t>(B) * 4, stream_));
     launch_scatter_i32(nh, home_idx_, tok_, all_tok_, stream_);
     nccl_check(Nccl::get().AllReduce(all_tok_, all_tok_, static_cast<size_t>(B), ncclInt32, ncclSum, comm_, stream_),
@@ -753,6 +801,7 @@ void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int
 }
 
 double DistEngine::bench(int B, const uint64_t* seqs, const int32_t* tokens, int steps) {
+  check_unique(B, seqs);
   DeviceGuard dg(device_);
   ensure(B);
   plan_for(B, seqs);
@@ -776,11 +825,23 @@ double DistEngine::bench(int B, const uint64_t* seqs, const int32_t* tokens, int
   return ms;
 }
 
-// DROP_SEQ routed to worker_for(seq, 0) under by-sequence sharding
-// (workers.cpp:482-501): each rank drops the retiring sequences it stores.
+// DROP_SEQ (workers.cpp:482-501): routed to worker_for(seq, 0) under
+// by-sequence sharding, to every link otherwise. Each rank drops the retiring
+// sequences it stores: by-sequence mix64(seq) % world == rank; by-head every
+// rank holds every sequence; hybrid the ranks of sequence group
+// mix64(seq) % SG (worker w = hg * SG + sg).
+bool DistEngine::holds(uint64_t seq) const {
+  if (mode_ == SD_SHARD_BY_HEAD) return true;
+  if (mode_ == SD_SHARD_HYBRID) {
+    const int hg = std::gcd(world_, spec_.Hkv), sg = world_ / hg;
+    return sg == 1 || static_cast<int>(mix64(seq) % static_cast<uint64_t>(sg)) == rank_ % sg;
+  }
+  return shard_of(seq, world_) == rank_;
+}
+
 void DistEngine::retire(int n, const uint64_t* seqs) {
   for (int i = 0; i < n; ++i) {
-    if (shard_of(seqs[i], world_) == rank_) kv_->drop(seqs[i]);
+    if (holds(seqs[i])) kv_->drop(seqs[i]);
   }
 }
 

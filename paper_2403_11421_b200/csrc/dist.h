@@ -58,6 +58,8 @@ class DistEngine : public StepComputation {
   void compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next,
                float* final_x) override;
   void retire(int n, const uint64_t* seqs) override;
+  // whether this rank's R-shard stores `seq` (ShardMap mode and rank)
+  bool holds(uint64_t seq) const;
   // whether this rank produced `seq`'s token in the last step (homes are
   // assigned per step batch)
   bool owns(uint64_t seq) const override { return home_set_.count(seq) != 0; }
@@ -71,8 +73,11 @@ class DistEngine : public StepComputation {
   // Peer-memory exchange (dist_p2p.cu): allocate fixed receive buffers for
   // up to `max_rows` rows and export their CUDA IPC handles (kIpcBytes);
   // connect() maps every rank's buffers (world x kIpcBytes, rank order).
-  // [rx_qkv | rx_o | flags | rx_ob handles][int32 dense mode of this rank, -1 none][pad]
-  static constexpr size_t kIpcBytes = 4 * sizeof(cudaIpcMemHandle_t) + 64;
+  // [rx_qkv | rx_o | flags | rx_ob | rx_tok handles][int32 dense mode of this rank, -1 none][pad]
+  static constexpr int kIpcHandles = 5;
+  static constexpr size_t kIpcBytes = kIpcHandles * sizeof(cudaIpcMemHandle_t) + 64;
+  // flag slots: 0 Q/K/V rows, 1 attention rows, 2 next tokens
+  static constexpr int kFlagSlots = 3, kTokSlot = 2;
   void p2p_setup(int max_rows, void* handles_out);
   void p2p_connect(const void* all_handles);
   bool p2p() const { return p2p_; }
@@ -109,7 +114,7 @@ class DistEngine : public StepComputation {
   int cap_ = 0;
   float *x_ = nullptr, *qkv_h_ = nullptr, *qkv_s_ = nullptr, *o_s_ = nullptr, *o_h_ = nullptr,
         *y_ = nullptr, *h_ = nullptr, *logits_ = nullptr;
-  __nv_bfloat16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
+  act16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
   int32_t* tok_ = nullptr;
   int32_t* all_tok_ = nullptr;   // [B] next tokens of the whole batch (compute)
   int32_t* home_idx_ = nullptr;  // [home rows] batch row of each home row
@@ -124,7 +129,7 @@ class DistEngine : public StepComputation {
   bool p2p_ = false;
   int p2p_cap_ = 0;
   float *rx_qkv_ = nullptr, *rx_o_ = nullptr;  // receive buffers (shard rows / home rows)
-  __nv_bfloat16* rx_ob_ = nullptr;             // home rows' attention output as the bf16 W_o operand
+  act16* rx_ob_ = nullptr;             // home rows' attention output as the bf16 W_o operand
   // fused exchange: the QKV GEMM and the attention store rows straight into
   // the peers' buffers (RowRoute / ORoute) and publish the epoch themselves.
   // Decided from rank-independent facts (a sender may still use the scatter
@@ -138,9 +143,13 @@ class DistEngine : public StepComputation {
   int32_t* done_ = nullptr;
   float* peer_qkv_[kMaxWorld] = {};
   float* peer_o_[kMaxWorld] = {};
-  __nv_bfloat16* peer_ob_[kMaxWorld] = {};
+  act16* peer_ob_[kMaxWorld] = {};
   int peer_mode_[kMaxWorld] = {};  // each rank's dense mode (-1: no weights)
   int64_t* peer_flags_[kMaxWorld] = {};
+  int32_t* rx_tok_ = nullptr;  // [2][tok_rows_] next tokens of the batch (double-buffered)
+  int32_t* peer_tok_[kMaxWorld] = {};
+  int tok_rows_ = 0;
+  int64_t tok_epoch_ = 0;
   std::vector<void*> opened_;
   int64_t epoch_ = 0;
   std::vector<int32_t> peer_qkv_off_, peer_o_off_;  // row offset of this rank's rows in each peer's buffer

@@ -83,7 +83,27 @@ __global__ void p2p_wait_kernel(const int64_t* flags, int slot, uint32_t expect,
   }
 }
 
+__global__ void p2p_tokens_kernel(const P2PTokens a) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+    const int32_t t = a.src[i], r = a.idx[i];
+    for (int d = 0; d < a.world; ++d) a.dst[d][r] = t;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.world && (a.notify >> threadIdx.x & 1)) {
+    st_release_sys(a.flag[threadIdx.x] + a.slot * kMaxWorld + a.self, a.epoch);
+  }
+}
+
 }  // namespace
+
+void launch_p2p_tokens(const P2PTokens& a, cudaStream_t s) {
+  SD_CUDA(launch_pdl(p2p_tokens_kernel, dim3(1), dim3(1024), 0, s, 1, a));
+  SD_CUDA(cudaGetLastError());
+  count_launch();
+}
 
 void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s) {
   int64_t work = 0;

@@ -35,6 +35,20 @@ struct P2PScatter {
 void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s);
 // dst[idx[i]] = src[i] for i < n (a rank's next tokens into the batch vector)
 void launch_scatter_i32(int n, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s);
+// The next-token gather of a distributed step over peer memory: every rank
+// stores its home rows' tokens at their batch rows into every rank's token
+// buffer (dst[d] + idx[i] = src[i]), then publishes flag[d][slot][self] =
+// epoch for every d in `notify` (one block; B int32 per step).
+struct P2PTokens {
+  const int32_t* idx;
+  const int32_t* src;
+  int n, world, self, slot;
+  int64_t epoch;
+  uint32_t notify;
+  int32_t* dst[kMaxWorld];
+  int64_t* flag[kMaxWorld];
+};
+void launch_p2p_tokens(const P2PTokens& a, cudaStream_t s);
 // wait until flags[slot][src] >= epoch for every src bit in `expect`
 void launch_p2p_wait(const int64_t* flags, int slot, uint32_t expect, int world, int64_t epoch, cudaStream_t s);
 

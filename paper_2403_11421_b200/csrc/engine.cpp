@@ -39,8 +39,8 @@ __global__ void pack_kernel(const float* __restrict__ src, int in, int out, void
       if (k < in && j < out) {
         const float v = tile[threadIdx.x][r];
         const int64_t idx = static_cast<int64_t>(off + j) * ld + k;
-        if (mode == SD_DENSE_BF16) {
-          static_cast<__nv_bfloat16*>(dst)[idx] = __float2bfloat16_rn(v);
+        if (mode == SD_DENSE_BF16 || mode == SD_DENSE_F16) {
+          static_cast<uint16_t*>(dst)[idx] = to16(v, mode == SD_DENSE_F16);
         } else {
           static_cast<float*>(dst)[idx] = v;
         }
@@ -60,8 +60,8 @@ __global__ void synth_weight_kernel(int in, int out, void* dst, int64_t ld, int 
     const float v = synth_value(salt + static_cast<uint64_t>(e)) * scale;
     if (mode == SD_DENSE_EXACT_F32) {
       static_cast<float*>(dst)[static_cast<int64_t>(k) * ld + off + j] = v;
-    } else if (mode == SD_DENSE_BF16) {
-      static_cast<__nv_bfloat16*>(dst)[static_cast<int64_t>(off + j) * ld + k] = __float2bfloat16_rn(v);
+    } else if (mode == SD_DENSE_BF16 || mode == SD_DENSE_F16) {
+      static_cast<uint16_t*>(dst)[static_cast<int64_t>(off + j) * ld + k] = to16(v, mode == SD_DENSE_F16);
     } else {
       static_cast<float*>(dst)[static_cast<int64_t>(off + j) * ld + k] = v;
     }
@@ -95,7 +95,7 @@ int Weights::in_dim(int which) const { return which == 6 ? spec_.F : spec_.D; }
 
 void Weights::alloc() {
   DeviceGuard dg(device_);
-  const size_t es = mode_ == SD_DENSE_BF16 ? 2 : 4;
+  const size_t es = mode_ == SD_DENSE_BF16 || mode_ == SD_DENSE_F16 ? 2 : 4;
   size_t off = 0;
   auto take = [&](size_t elems) {
     const size_t o = off;
@@ -117,7 +117,7 @@ void Weights::alloc() {
 const void* Weights::tensor(int layer, int which) const {
   const uint8_t* b = static_cast<const uint8_t*>(blob_);
   if (which == 7) return b + head_off_;
-  const size_t es = mode_ == SD_DENSE_BF16 ? 2 : 4;
+  const size_t es = mode_ == SD_DENSE_BF16 || mode_ == SD_DENSE_F16 ? 2 : 4;
   const int D = spec_.D, kvw = spec_.kv_width();
   const size_t base = off_[static_cast<size_t>(layer) * 8 + (which <= 3 ? 0 : which)];
   if (which <= 3) {
@@ -131,7 +131,7 @@ const void* Weights::tensor(int layer, int which) const {
 
 Weights::Weights(const Spec& spec, const float* const* tensors, int mode, int device)
     : spec_(spec), mode_(mode), device_(device) {
-  if (mode < SD_DENSE_EXACT_F32 || mode > SD_DENSE_TF32) fail(SD_ERR_CONFIG, "unknown dense mode");
+  if (mode < SD_DENSE_EXACT_F32 || mode > SD_DENSE_F16) fail(SD_ERR_CONFIG, "unknown dense mode");
   alloc();
   DeviceGuard dg(device_);
   const int D = spec.D, F = spec.F, V = spec.V, kvw = spec.kv_width();
@@ -164,7 +164,7 @@ Weights::Weights(const Spec& spec, const float* const* tensors, int mode, int de
 
 Weights::Weights(const Spec& spec, int mode, uint64_t seed, int device)
     : spec_(spec), mode_(mode), device_(device) {
-  if (mode < SD_DENSE_EXACT_F32 || mode > SD_DENSE_TF32) fail(SD_ERR_CONFIG, "unknown dense mode");
+  if (mode < SD_DENSE_EXACT_F32 || mode > SD_DENSE_F16) fail(SD_ERR_CONFIG, "unknown dense mode");
   alloc();
   DeviceGuard dg(device_);
   const int D = spec.D, F = spec.F, V = spec.V, kvw = spec.kv_width();
@@ -194,6 +194,131 @@ Weights::Weights(const Spec& spec, int mode, uint64_t seed, int device)
   SD_CUDA(cudaDeviceSynchronize());
 }
 
+namespace {
+
+// UniformSource (core.cpp:72-93): std::mt19937 seeded with
+// uint32(seed ^ (seed >> 32)); u = (gen() >> 8) * 2^-24; value (2u - 1) *
+// scale; tensors filled in memory (Eigen column-major) order. The 624-word
+// twist is done in bulk and the tempering in a loop the compiler vectorizes
+// (~1 ns per value; bit-identical to std::mt19937's stream).
+class Mt19937Source {
+ public:
+  explicit Mt19937Source(uint64_t seed) {
+    s_[0] = static_cast<uint32_t>(seed ^ (seed >> 32));
+    for (int k = 1; k < 624; ++k) s_[k] = 1812433253u * (s_[k - 1] ^ (s_[k - 1] >> 30)) + static_cast<uint32_t>(k);
+    i_ = 624;
+  }
+  void fill(float* out, size_t n, float scale) {
+    size_t o = 0;
+    while (o < n) {
+      if (i_ == 624) twist();
+      const size_t m = std::min<size_t>(static_cast<size_t>(624 - i_), n - o);
+      const uint32_t* st = s_ + i_;
+      for (size_t k = 0; k < m; ++k) {
+        uint32_t y = st[k];
+        y ^= y >> 11;
+        y ^= (y << 7) & 0x9d2c5680u;
+        y ^= (y << 15) & 0xefc60000u;
+        y ^= y >> 18;
+        out[o + k] = (2.0f * (static_cast<float>(y >> 8) * 0x1p-24f) - 1.0f) * scale;
+      }
+      i_ += static_cast<int>(m);
+      o += m;
+    }
+  }
+
+ private:
+  void twist() {
+    auto mix = [](uint32_t a, uint32_t b, uint32_t c) {
+      const uint32_t y = (a & 0x80000000u) | (b & 0x7fffffffu);
+      return c ^ (y >> 1) ^ ((y & 1u) ? 0x9908b0dfu : 0u);
+    };
+    for (int k = 0; k < 227; ++k) s_[k] = mix(s_[k], s_[k + 1], s_[k + 397]);
+    for (int k = 227; k < 623; ++k) s_[k] = mix(s_[k], s_[k + 1], s_[k - 227]);
+    s_[623] = mix(s_[623], s_[0], s_[396]);
+    i_ = 0;
+  }
+  uint32_t s_[624];
+  int i_;
+};
+
+}  // namespace
+
+// seed_random_weights (core.cpp:97-127): the reference's generator on the
+// host, streamed tensor by tensor through two pinned chunks into a device
+// staging copy of the reference storage, then packed into the mode's layout.
+Weights::Weights(const Spec& spec, int mode, uint64_t seed, int device, SeedRandom)
+    : spec_(spec), mode_(mode), device_(device) {
+  if (mode < SD_DENSE_EXACT_F32 || mode > SD_DENSE_F16) fail(SD_ERR_CONFIG, "unknown dense mode");
+  alloc();
+  DeviceGuard dg(device_);
+  const int D = spec.D, F = spec.F, V = spec.V, kvw = spec.kv_width();
+  const float ds = 1.0f / std::sqrt(static_cast<float>(D));
+  const float ms = 1.0f / std::sqrt(static_cast<float>(F));
+  constexpr size_t kChunk = size_t{1} << 23;  // floats per pinned chunk (32 MB)
+  float* pin[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  SD_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    SD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&pin[i]), kChunk * 4, cudaHostAllocDefault));
+    SD_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  }
+  Mt19937Source src(seed);
+  int cur = 0;
+  // the next n values of the stream into dst (device), in order
+  auto stream_into = [&](float* dst, size_t n, float scale) {
+    for (size_t o = 0; o < n; o += kChunk) {
+      const size_t m = std::min(kChunk, n - o);
+      SD_CUDA(cudaEventSynchronize(ev[cur]));  // the chunk's previous copy is done
+      src.fill(pin[cur], m, scale);
+      SD_CUDA(cudaMemcpyAsync(dst + o, pin[cur], m * 4, cudaMemcpyHostToDevice, st));
+      SD_CUDA(cudaEventRecord(ev[cur], st));
+      cur ^= 1;
+    }
+  };
+  DevBuf tmp;
+  auto gen = [&](int in, int out, void* dst, int64_t ld, int off, float scale) {
+    const size_t n = static_cast<size_t>(in) * out;
+    tmp.get(n * 4);
+    stream_into(static_cast<float*>(tmp.p), n, scale);
+    dim3 grid((out + 31) / 32, (in + 31) / 32);
+    pack_kernel<<<grid, dim3(32, 8), 0, st>>>(static_cast<const float*>(tmp.p), in, out, dst, ld, off, mode_);
+    SD_CUDA(cudaGetLastError());
+    ::sd::count_launch();
+    SD_CUDA(cudaStreamSynchronize(st));  // tmp is reused by the next tensor
+  };
+  try {
+    stream_into(emb_, static_cast<size_t>(D) * V, 1.0f);  // embedding (D x V), scale 1
+    uint8_t* b = static_cast<uint8_t*>(blob_);
+    for (int l = 0; l < spec.L; ++l) {
+      void* qkv = b + off_[l * 8 + 0];
+      const int64_t ld_qkv = mode == SD_DENSE_EXACT_F32 ? spec.qkv_width() : D;
+      gen(D, D, qkv, ld_qkv, 0, ds);           // w_q
+      gen(D, kvw, qkv, ld_qkv, D, ds);         // w_k
+      gen(D, kvw, qkv, ld_qkv, D + kvw, ds);   // w_v
+      gen(D, D, b + off_[l * 8 + 4], D, 0, ds);                                 // w_o
+      gen(D, F, b + off_[l * 8 + 5], mode == SD_DENSE_EXACT_F32 ? F : D, 0, ds);  // w_mlp_in
+      gen(F, D, b + off_[l * 8 + 6], mode == SD_DENSE_EXACT_F32 ? D : F, 0, ms);  // w_mlp_out
+    }
+    gen(D, V, b + head_off_, mode == SD_DENSE_EXACT_F32 ? V : D, 0, ds);  // head (V x D)
+    SD_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    for (int i = 0; i < 2; ++i) {
+      cudaFreeHost(pin[i]);
+      cudaEventDestroy(ev[i]);
+    }
+    cudaStreamDestroy(st);
+    throw;
+  }
+  for (int i = 0; i < 2; ++i) {
+    cudaFreeHost(pin[i]);
+    cudaEventDestroy(ev[i]);
+  }
+  cudaStreamDestroy(st);
+}
+
 Weights::~Weights() {
   DeviceGuard dg(device_);
   cudaFree(blob_);
@@ -201,8 +326,8 @@ Weights::~Weights() {
 }
 
 void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
-                     const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy,
-                     __nv_bfloat16* yb, int64_t ldyb, int epi, const float* res, int64_t ldr,
+                     const act16* xb, int64_t ldxb, float* y, int64_t ldy,
+                     act16* yb, int64_t ldyb, int epi, const float* res, int64_t ldr,
                      cudaStream_t s, int max_ctas) const {
   if (which != 7 && (layer < 0 || layer >= spec_.L)) fail(SD_ERR_CONFIG, "layer out of range");
   const int in = in_dim(which), out = out_dim(which);
@@ -211,15 +336,15 @@ void Weights::linear(int layer, int which, int B, const float* x, int64_t ldx,
     int64_t ldw = out;
     if (which <= 3) ldw = spec_.qkv_width();
     launch_linear_exact(B, in, out, x, ldx, static_cast<const float*>(W), ldw, y, ldy, epi, res, ldr, s);
-    if (yb) launch_to_bf16(B, out, y, ldy, yb, ldyb, s);
+    if (yb) launch_to_16(B, out, y, ldy, yb, ldyb, 0, s);
     return;
   }
   const GemmArgs g = gemm_args(layer, which, B, x, ldx, xb, ldxb, y, ldy, yb, ldyb, epi, res, ldr, max_ctas);
   launch_gemm_sm100(g, s);
 }
 
-GemmArgs Weights::gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
-                            int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+GemmArgs Weights::gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const act16* xb,
+                            int64_t ldxb, float* y, int64_t ldy, act16* yb, int64_t ldyb, int epi,
                             const float* res, int64_t ldr, int max_ctas) const {
   if (mode_ == SD_DENSE_EXACT_F32) fail(SD_ERR_INTERNAL, "gemm_args: exact mode has no tensor-core GEMM");
   if (which != 7 && (layer < 0 || layer >= spec_.L)) fail(SD_ERR_CONFIG, "layer out of range");
@@ -228,8 +353,8 @@ GemmArgs Weights::gemm_args(int layer, int which, int B, const float* x, int64_t
   g.N = out_dim(which);
   g.K = in_dim(which);
   g.kind = mode_;
-  if (mode_ == SD_DENSE_BF16) {
-    if (!xb) fail(SD_ERR_INTERNAL, "bf16 GEMM needs a bf16 A operand");
+  if (mode_ == SD_DENSE_BF16 || mode_ == SD_DENSE_F16) {
+    if (!xb) fail(SD_ERR_INTERNAL, "kind::f16 GEMM needs a 16-bit A operand");
     g.A = xb;
     g.lda = ldxb;
   } else {

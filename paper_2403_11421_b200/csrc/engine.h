@@ -24,6 +24,10 @@ class Weights {
   // Counter-based synthetic weights of the same distribution (uniform
   // +-1/sqrt(fan_in)); generated on device for the full-size benchmark.
   Weights(const Spec& spec, int mode, uint64_t seed, int device);
+  // seed_random_weights (core.cpp:97-127): the reference's mt19937 stream,
+  // bit-identical to its WeightSet, generated on the host and uploaded.
+  struct SeedRandom {};
+  Weights(const Spec& spec, int mode, uint64_t seed, int device, SeedRandom);
   ~Weights();
   Weights(const Weights&) = delete;
   Weights& operator=(const Weights&) = delete;
@@ -36,14 +40,14 @@ class Weights {
   // 5 = w_mlp_in, 6 = w_mlp_out, 7 = head, 1/2/3 = q/k/v slices.
   // x_bf16 is required in BF16 mode (A operand), ignored otherwise.
   // the tensor-core GEMM of linear() without launching it (chained S-Part)
-  GemmArgs gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
-                     int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+  GemmArgs gemm_args(int layer, int which, int B, const float* x, int64_t ldx, const act16* xb,
+                     int64_t ldxb, float* y, int64_t ldy, act16* yb, int64_t ldyb, int epi,
                      const float* res, int64_t ldr, int max_ctas = 0) const;
   void linear(int layer, int which, int B, const float* x, int64_t ldx,
-              const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
+              const act16* xb, int64_t ldxb, float* y, int64_t ldy, act16* yb,
               int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s,
               int max_ctas = 0) const;
-  const float* embedding() const { return emb_; }
+  const float* embedding() const { return emb_; }  // fp32 D x V column-major (the reference storage)
   int out_dim(int which) const;
   int in_dim(int which) const;
 
@@ -113,7 +117,7 @@ class Engine : public StepComputation {
     std::vector<uint64_t> seqs;
     int cap = 0;
     float *x = nullptr, *qkv = nullptr, *o = nullptr, *y = nullptr, *h = nullptr, *logits = nullptr;
-    __nv_bfloat16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
+    act16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
     int32_t* tok = nullptr;
     unsigned long long* amax = nullptr;  // fused-argmax keys of the head GEMM
     std::vector<char> appended;          // per layer: K/V already stored by the QKV GEMM
@@ -125,14 +129,9 @@ class Engine : public StepComputation {
   void ensure(Group& g, int n);
   void free_group(Group& g);
   void run(int ng, bool embed);
-  void chain(const ChainArgs& c);
-  static constexpr int kChainCounters = 4 * 64;
-  unsigned long long* chain_done_ = nullptr;
-  unsigned long long chain_epoch_ = 0;
-  bool chain_on_ = true;
   int timing_every_ = 1;
-  void gemm(int layer, int which, int B, const float* x, int64_t ldx, const __nv_bfloat16* xb,
-            int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb, int64_t ldyb, int epi,
+  void gemm(int layer, int which, int B, const float* x, int64_t ldx, const act16* xb,
+            int64_t ldxb, float* y, int64_t ldy, act16* yb, int64_t ldyb, int epi,
             const float* res, int64_t ldr, unsigned long long* amax = nullptr,
             const KvAppendOut* kvapp = nullptr);
   // the next layer's project_qkv with append_lane folded into its epilogue

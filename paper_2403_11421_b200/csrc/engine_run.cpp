@@ -32,13 +32,6 @@ Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_s, cudaEventDisableTiming));
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_r, cudaEventDisableTiming));
   }
-  // opt-in (SD_CHAIN=1): bitwise equal to the separate launches and faster
-  // when per-kernel timing events sit between them, but not end to end,
-  // where programmatic dependent launch already hides the launch/prologue cost
-  chain_on_ = std::getenv("SD_CHAIN") != nullptr;
-  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&chain_done_), kChainCounters * sizeof(unsigned long long)));
-  SD_CUDA(cudaMemset(chain_done_, 0, kChainCounters * sizeof(unsigned long long)));
-  SD_CUDA(cudaDeviceSynchronize());
 }
 
 void Engine::free_group(Group& g) {
@@ -69,7 +62,6 @@ Engine::~Engine() {
     cudaEventDestroy(e.second);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
-  if (chain_done_) cudaFree(chain_done_);
   cudaStreamDestroy(stream_);
   cudaStreamDestroy(stream_r_);
 }
@@ -145,7 +137,7 @@ int Engine::split(int B, const uint64_t* seqs) {
 }
 
 void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
-                  const __nv_bfloat16* xb, int64_t ldxb, float* y, int64_t ldy, __nv_bfloat16* yb,
+                  const act16* xb, int64_t ldxb, float* y, int64_t ldy, act16* yb,
                   int64_t ldyb, int epi, const float* res, int64_t ldr, unsigned long long* amax,
                   const KvAppendOut* kvapp) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -179,29 +171,6 @@ void Engine::gemm(int layer, int which, int B, const float* x, int64_t ldx,
   }
 }
 
-void Engine::chain(const ChainArgs& c) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing_) {
-    for (cudaEvent_t* e : {&e0, &e1}) {
-      if (ev_pool_.empty()) {
-        SD_CUDA(cudaEventCreate(e));
-      } else {
-        *e = ev_pool_.back();
-        ev_pool_.pop_back();
-      }
-    }
-    SD_CUDA(cudaEventRecord(e0, stream_));
-  }
-  launch_gemm_chain(c, stream_);
-  if (timing_) {
-    SD_CUDA(cudaEventRecord(e1, stream_));
-    ev_.emplace_back(e0, e1);
-    double f = 0;
-    for (int i = 0; i < c.n; ++i) f += 2.0 * c.g[i].M * c.g[i].N * c.g[i].K;
-    ev_flops_.push_back(f);
-  }
-}
-
 void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool reset) {
   for (size_t i = 0; i < ev_.size(); ++i) {
     SD_CUDA(cudaEventSynchronize(ev_[i].second));
@@ -227,8 +196,10 @@ void Engine::read_timing(double* ms, double* flops, int64_t* launches, bool rese
 bool Engine::qkv_fused_append(int layer, Group& g) {
   const Spec& s = w_->spec();
   const int n = static_cast<int>(g.rows.size());
-  const bool off = getenv("SD_NO_FUSED_APPEND") != nullptr;
-  if (off || pipeline_ || w_->mode() == SD_DENSE_EXACT_F32 || n == 0) return false;
+  if (!tuning().fused_append || pipeline_ || w_->mode() == SD_DENSE_EXACT_F32 || n == 0) return false;
+  // the epilogue's K/V stores need the TMA-store path and 16-column-aligned
+  // fp16 K/V rows: decided before anything is staged
+  if (s.D % 16 || s.kv_width() % 16 || s.qkv_width() % 4) return false;
   for (int i = 0; i < n; ++i) {
     g.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(g.seqs[static_cast<size_t>(i)], layer));
   }
@@ -236,7 +207,12 @@ bool Engine::qkv_fused_append(int layer, Group& g) {
   if (!kv_->stage_fused_append(layer, n, g.seqs.data(), g.pos.data(), &ka)) return false;
   ka.col_k = s.D;
   ka.width = s.kv_width();
-  gemm(layer, 0, n, g.x, s.D, g.xb, s.D, g.qkv, s.qkv_width(), nullptr, 0, kEpiNone, nullptr, 0, nullptr, &ka);
+  try {
+    gemm(layer, 0, n, g.x, s.D, g.xb, s.D, g.qkv, s.qkv_width(), nullptr, 0, kEpiNone, nullptr, 0, nullptr, &ka);
+  } catch (...) {
+    kv_->abort_fused_append();  // lengths back: a later append / attend sees the store as before
+    throw;
+  }
   kv_->end_fused_append(stream_);
   return true;
 }
@@ -249,16 +225,14 @@ bool Engine::qkv_fused_append(int layer, Group& g) {
 void Engine::run(int ng, bool embed) {
   const Spec& s = w_->spec();
   const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
-  const bool bf = w_->mode() == SD_DENSE_BF16;
+  // kind::f16 modes keep 16-bit copies of the GEMM A operands (bf16 or fp16)
+  const bool bf = w_->mode() == SD_DENSE_BF16 || w_->mode() == SD_DENSE_F16;
+  const int f16 = w_->mode() == SD_DENSE_F16 ? 1 : 0;
   cudaStream_t rs = pipeline_ ? stream_r_ : stream_;
-  // chain counters restart every step (ChainArgs::done / epoch)
-  bool head_done = false;
-  if (chain_done_) SD_CUDA(cudaMemsetAsync(chain_done_, 0, kChainCounters * sizeof(unsigned long long), stream_));
-  chain_epoch_ = 0;
   for (int gi = 0; gi < ng; ++gi) {
     Group& g = groups_[gi];
     const int n = static_cast<int>(g.rows.size());
-    if (embed) launch_embed(n, D, g.tok, w_->embedding(), g.x, D, bf ? g.xb : nullptr, stream_);
+    if (embed) launch_embed(n, D, g.tok, w_->embedding(), g.x, D, bf ? g.xb : nullptr, f16, stream_);
     gemm(0, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
     if (pipeline_) SD_CUDA(cudaEventRecord(g.ev_s, stream_));
   }
@@ -274,31 +248,13 @@ void Engine::run(int ng, bool embed) {
         }
         kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
       }
-      // the attention also writes the bf16 copy of o that W_o consumes
-      kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi, bf ? g.ob : nullptr, D);
+      // the attention also writes the 16-bit copy of o that W_o consumes
+      kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi, bf ? g.ob : nullptr, D, nullptr, f16);
       if (pipeline_) {
         SD_CUDA(cudaEventRecord(g.ev_r, rs));
         SD_CUDA(cudaStreamWaitEvent(stream_, g.ev_r, 0));
       }
       // finish_block (dense.cpp:51-70), then the next layer's project_qkv
-      // (or the head): one chained launch when the S-Part is bf16 at n >= 256
-      if (bf && !pipeline_ && chain_on_ && n >= 256) {
-        ChainArgs c{};
-        c.n = 4;
-        c.g[0] = w_->gemm_args(l, 4, n, g.o, D, g.ob, D, g.y, D, g.yb, D, kEpiResidual, g.x, D);
-        c.g[1] = w_->gemm_args(l, 5, n, g.y, D, g.yb, D, nullptr, F, g.hb, F, kEpiSilu, nullptr, 0);
-        c.g[2] = w_->gemm_args(l, 6, n, g.h, F, g.hb, F, g.x, D, g.xb, D, kEpiResidual, g.y, D);
-        c.g[3] = l + 1 < s.L
-                     ? w_->gemm_args(l + 1, 0, n, g.x, D, g.xb, D, g.qkv, qkvw, nullptr, 0, kEpiNone, nullptr, 0)
-                     : w_->gemm_args(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
-        c.done = chain_done_;
-        if (gemm_chain_supported(c)) {
-          c.epoch = chain_epoch_++;
-          chain(c);
-          if (l + 1 == s.L) head_done = true;
-          continue;
-        }
-      }
       gemm(l, 4, n, g.o, D, g.ob, D, g.y, D, bf ? g.yb : nullptr, D, kEpiResidual, g.x, D);
       gemm(l, 5, n, g.y, D, g.yb, D, bf ? nullptr : g.h, F, bf ? g.hb : nullptr, F, kEpiSilu, nullptr, 0);
       gemm(l, 6, n, g.h, F, g.hb, F, g.x, D, bf ? g.xb : nullptr, D, kEpiResidual, g.y, D);
@@ -317,13 +273,12 @@ void Engine::run(int ng, bool embed) {
     const int n = static_cast<int>(g.rows.size());
     // tensor-core modes: argmax_token folded into the head GEMM's epilogue
     // (no logits round trip through HBM) unless the caller wants the logits
-    static const bool no_fuse = getenv("SD_NO_FUSED_ARGMAX") != nullptr;
-    if (!head_done && !want_logits_ && !no_fuse && w_->mode() != SD_DENSE_EXACT_F32) {
+    if (!want_logits_ && tuning().fused_argmax && w_->mode() != SD_DENSE_EXACT_F32) {
       gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0, g.amax);
       launch_argmax_keys(n, g.amax, g.tok, stream_);
       continue;
     }
-    if (!head_done) gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+    gemm(0, 7, n, g.x, D, g.xb, D, g.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0);
     launch_argmax(n, s.V, g.logits, s.V, g.tok, stream_);
   }
 }
@@ -347,7 +302,8 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
   }
   DeviceGuard dg(w_->device());
   const int ng = split(B, seqs);
-  const bool bf = w_->mode() == SD_DENSE_BF16;
+  const bool bf = w_->mode() == SD_DENSE_BF16 || w_->mode() == SD_DENSE_F16;
+  const int f16 = w_->mode() == SD_DENSE_F16 ? 1 : 0;
   std::vector<float> xrows;
   for (int gi = 0; gi < ng; ++gi) {
     Group& g = groups_[gi];
@@ -356,6 +312,11 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
       g.host_tok.resize(static_cast<size_t>(n));
       for (int i = 0; i < n; ++i) g.host_tok[static_cast<size_t>(i)] = tokens_host[g.rows[static_cast<size_t>(i)]];
       SD_CUDA(cudaMemcpyAsync(g.tok, g.host_tok.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, stream_));
+    } else if (ng == 1) {
+      // one group holds the batch in row order: the caller's rows go
+      // straight to the device (a DMA from pinned memory when it is pinned)
+      SD_CUDA(cudaMemcpyAsync(g.x, x_host, static_cast<size_t>(n) * s.D * 4, cudaMemcpyHostToDevice, stream_));
+      if (bf) launch_to_16(n, s.D, g.x, s.D, g.xb, s.D, f16, stream_);
     } else {
       xrows.resize(static_cast<size_t>(n) * s.D);
       for (int i = 0; i < n; ++i) {
@@ -364,31 +325,12 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
       }
       SD_CUDA(cudaMemcpyAsync(g.x, xrows.data(), xrows.size() * 4, cudaMemcpyHostToDevice, stream_));
       SD_CUDA(cudaStreamSynchronize(stream_));  // xrows is reused by the next group
-      if (bf) launch_to_bf16(n, s.D, g.x, s.D, g.xb, s.D, stream_);
+      if (bf) launch_to_16(n, s.D, g.x, s.D, g.xb, s.D, f16, stream_);
     }
-  }
-  static const bool step_log = getenv("SD_STEP_LOG") != nullptr;
-  cudaEvent_t l0 = nullptr, l1 = nullptr;
-  const auto h0 = std::chrono::steady_clock::now();
-  if (step_log) {
-    SD_CUDA(cudaEventCreate(&l0));
-    SD_CUDA(cudaEventCreate(&l1));
-    SD_CUDA(cudaEventRecord(l0, stream_));
   }
   want_logits_ = logits_host != nullptr;
   run(ng, tokens_host != nullptr);
   want_logits_ = false;
-  if (step_log) {
-    const double enq = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-    SD_CUDA(cudaEventRecord(l1, stream_));
-    SD_CUDA(cudaEventSynchronize(l1));
-    float d = 0;
-    SD_CUDA(cudaEventElapsedTime(&d, l0, l1));
-    const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-    fprintf(stderr, "[step] device %.2f ms, host enqueue %.2f ms, host total %.2f ms\n", d, enq, tot);
-    cudaEventDestroy(l0);
-    cudaEventDestroy(l1);
-  }
   std::vector<int32_t> nt;
   std::vector<float> buf;
   for (int gi = 0; gi < ng; ++gi) {
@@ -401,6 +343,11 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
       if (next_host) next_host[g.rows[static_cast<size_t>(i)]] = nt[static_cast<size_t>(i)];
     }
     auto scatter = [&](const float* dev, int width, float* dst) {
+      if (ng == 1) {  // rows in batch order: straight into the caller's buffer
+        SD_CUDA(cudaMemcpyAsync(dst, dev, static_cast<size_t>(n) * width * 4, cudaMemcpyDeviceToHost, stream_));
+        SD_CUDA(cudaStreamSynchronize(stream_));
+        return;
+      }
       buf.resize(static_cast<size_t>(n) * width);
       SD_CUDA(cudaMemcpy(buf.data(), dev, buf.size() * 4, cudaMemcpyDeviceToHost));
       for (int i = 0; i < n; ++i) {
@@ -428,36 +375,12 @@ double Engine::bench(int B, const uint64_t* seqs, const int32_t* tokens_host, in
   SD_CUDA(cudaEventCreate(&e0));
   SD_CUDA(cudaEventCreate(&e1));
   SD_CUDA(cudaStreamSynchronize(stream_));
-  // SD_STEP_LOG=1: per-step device times (stderr) for diagnosing host stalls
-  static const bool step_log = getenv("SD_STEP_LOG") != nullptr;
-  std::vector<cudaEvent_t> marks;
-  std::vector<double> host_ms;
   SD_CUDA(cudaEventRecord(e0, stream_));
-  const auto h0 = std::chrono::steady_clock::now();
-  for (int i = 0; i < steps; ++i) {
-    run(ng, true);  // tokens fed back on device
-    if (step_log) {
-      cudaEvent_t ev;
-      SD_CUDA(cudaEventCreate(&ev));
-      SD_CUDA(cudaEventRecord(ev, stream_));
-      marks.push_back(ev);
-      host_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
-    }
-  }
+  for (int i = 0; i < steps; ++i) run(ng, true);  // tokens fed back on device
   SD_CUDA(cudaEventRecord(e1, stream_));
   SD_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
   SD_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-  if (step_log) {
-    cudaEvent_t prev = e0;
-    for (size_t i = 0; i < marks.size(); ++i) {
-      float d = 0;
-      SD_CUDA(cudaEventElapsedTime(&d, prev, marks[i]));
-      fprintf(stderr, "[step %zu] device %.2f ms, host enqueue done at %.2f ms\n", i, d, host_ms[i]);
-      prev = marks[i];
-    }
-    for (cudaEvent_t ev : marks) cudaEventDestroy(ev);
-  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (next_host) {

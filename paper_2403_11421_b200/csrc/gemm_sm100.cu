@@ -7,14 +7,15 @@
 //           so a weight tile crosses L2 once per cluster instead of once per
 //           M-block (decode batches make M small and L2 bandwidth the limit).
 //   warp 1  MMA issuer: one elected lane issues tcgen05.mma (kind::f16 for
-//           bf16 operands, kind::tf32 for fp32) into one of two TMEM
+//           bf16 or fp16 operands, kind::tf32 for fp32) into one of two TMEM
 //           accumulators (128 lanes x BN fp32 columns) and releases the smem
 //           slot in every cluster CTA with a multicast tcgen05.commit.
 //   warps 2-5 epilogue: tcgen05.ld the accumulator, fuse the finish_block
 //           epilogues (residual add, SiLU; dense.cpp:51-70), transpose through
-//           shared memory and write coalesced fp32 and/or bf16 rows.
+//           shared memory and write coalesced fp32 and/or 16-bit rows.
 // Accumulation is fp32 in TMEM; results match the fp32 reference within
-// the operand rounding (bf16 2^-9, tf32 2^-11 relative per product).
+// the operand rounding (bf16 2^-9, fp16 2^-11 RNE, tf32 2^-11 truncated,
+// relative per operand).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,20 +45,19 @@ struct Params {
   int cs;          // cluster size along M (1, 2, 4)
   float* C;
   int64_t ldc;
-  __nv_bfloat16* Cb;
+  uint16_t* Cb;  // 16-bit copy of C (the next GEMM's A operand): bf16, or fp16 when f16
   int64_t ldcb;
   int epi;
   const float* res;
   int64_t ldr;
   uint32_t idesc;
   int kind;
+  int f16;   // kind::f16 operands are fp16 (else bf16); Cb is written in the same format
   int bn;    // tile width along N (<= BN; a multiple of 16 in PAIR mode)
   int vec;   // outputs / residual 16-B aligned: vector epilogue
   int tma_out;  // outputs written by TMA tensor stores
-  int diag;  // 1: reuse resident smem after the first ring fill (MMA-rate probe)
   int routed;      // C rows go to route.base[route.rank[m]] (fused multi-GPU exchange)
-  int route_bulk;  // routed rows leave through bulk copies (else smem-transposed st.global)
-  int route_tma;   // contiguous 32-row slabs leave as tensor stores (RouteMaps)
+  int route_tma;   // contiguous 32-row slabs leave as tensor stores (RouteMaps), other rows as bulk copies
   RowRoute route;
   unsigned long long* amax;  // fused argmax keys per row (GemmArgs::amax)
   int kvapp;                 // K/V columns go to the KV pages (kva)
@@ -328,41 +328,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // MMAs take; tools/mma_rate.cu). PAIR: a CTA pair computes a 256 x bn tile
 // with cta_group::2 MMAs, each CTA staging its own 128 A rows and half of
 // the B tile.
-// MB: 128-row A blocks per CTA (MB = 2, opt-in SD_GEMM_MB=2: a pair computes
-// a 512 x bn tile as two 256 x bn accumulators sharing every B stage, 1.5x
-// the MACs per staged byte; measured no faster at the decode shapes, see
-// pick_pair_bn_mb2).
-template <int BN, bool PAIR, int ATOMS, int MB = 1>
+template <int BN, bool PAIR, int ATOMS>
 struct Cfg {
   static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows staged per CTA (max)
   static constexpr int A_ATOM = BM * BK_BYTES;
   static constexpr int B_ATOM = B_ROWS * BK_BYTES;
-  static constexpr int A_ST = MB * ATOMS * A_ATOM;
+  static constexpr int A_ST = ATOMS * A_ATOM;
   static constexpr int B_ST = ATOMS * B_ATOM;
   static constexpr int STAGES = (196 * 1024 / (A_ST + B_ST)) > 8 ? 8 : (196 * 1024 / (A_ST + B_ST));
   // two accumulators, allocated in a power-of-two column count
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   // epilogue staging for TMA stores: per epilogue warp, two buffers of
-  // 32 rows x 16 columns in fp32 (2 KB, 64-B swizzle) and bf16 (1 KB, 32-B swizzle)
+  // 32 rows x 16 columns in fp32 (2 KB, 64-B swizzle) and 16-bit (1 KB, 32-B swizzle)
   static constexpr int OUT_F32 = 32 * 16 * 4, OUT_BF16 = 32 * 16 * 2;
   static constexpr int OUT_WARP = 2 * (OUT_F32 + OUT_BF16);
   static constexpr size_t SMEM = 1024 + STAGES * (A_ST + B_ST) + 4 * OUT_WARP + 256;
 };
-
-template <int KIND, bool PAIR>
-__device__ __forceinline__ void mma_issue(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  if (PAIR) {
-    if (KIND == 2) {
-      mma_tf32_pair(d, a, b, idesc, acc);
-    } else {
-      mma_f16_pair(d, a, b, idesc, acc);
-    }
-  } else if (KIND == 2) {
-    mma_tf32(d, a, b, idesc, acc);
-  } else {
-    mma_f16(d, a, b, idesc, acc);
-  }
-}
 
 // fp32 tensor maps (64-B swizzle, 16-column x 32-row boxes) of a routed
 // GEMM's destination buffers, one per rank
@@ -370,13 +351,12 @@ struct RouteMaps {
   CUtensorMap m[8];
 };
 
-template <int BN, bool PAIR, int ATOMS, int KIND, int MB>
+template <int BN, bool PAIR, int ATOMS, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_cb, const Params p,
                 const __grid_constant__ RouteMaps rmaps) {
-  static_assert(MB == 1 || PAIR, "two A blocks per CTA only in pair mode");
-  using C_ = Cfg<BN, PAIR, ATOMS, MB>;
+  using C_ = Cfg<BN, PAIR, ATOMS>;
   constexpr int STAGES = C_::STAGES;
   constexpr int KELEMS = BK_BYTES / (KIND == 2 ? 4 : 2);  // elements per atom row
   extern __shared__ uint8_t smem_raw[];
@@ -400,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x / cs, nclusters = gridDim.x / cs;
   // PAIR: a cluster item is a 256-row M block (rank r owns rows r*128..);
   // otherwise cs consecutive 128-row M blocks sharing one B tile (multicast)
-  const int mgroups = PAIR ? (p.mb + 2 * MB - 1) / (2 * MB) : p.mb / cs;
+  const int mgroups = PAIR ? (p.mb + 1) / 2 : p.mb / cs;
   const int items = mgroups * p.nb;
 
   if (warp == 0 && lane == 0) {
@@ -436,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_wait();  // A operand / residual of the previous kernel from here on
 
   // first row of this CTA's block 0 (block b adds b * cs * BM)
-  auto m_origin = [&](int it) { return ((it % mgroups) * cs * MB + rank) * BM; };
+  auto m_origin = [&](int it) { return ((it % mgroups) * cs + rank) * BM; };
 
   if (warp == 0) {
     // ------------------------------------------------------- TMA producer
@@ -444,36 +424,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const int slice = PAIR ? p.bn / 2 : BN / cs;
-      const uint32_t bytes = static_cast<uint32_t>(ATOMS * (MB * C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
+      const uint32_t bytes = static_cast<uint32_t>(ATOMS * (C_::A_ATOM + (PAIR ? slice : BN) * BK_BYTES)) *
                              (PAIR ? 2u : 1u);  // PAIR: both CTAs' bytes land on the leader's barrier
       const uint32_t full0 = PAIR ? mapa(&full[0], 0) : smem_u32(&full[0]);
       for (int it = cluster; it < items; it += nclusters) {
         const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);  // slot s released (by every cluster CTA / the pair leader)
-          if ((p.diag & 1) && (kb >= STAGES || it != cluster)) {
-            if (!PAIR || leader) e_arrive(&full[s]);
-          } else {
-            if (!PAIR || leader) e_expect_tx(&full[s], bytes);
-            const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
+          if (!PAIR || leader) e_expect_tx(&full[s], bytes);
+          const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
 #pragma unroll
-            for (int a = 0; a < ATOMS; ++a) {
-              const int kc = (kb * ATOMS + a) * KELEMS;
-              uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
-              uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
-              if (PAIR) {
-#pragma unroll
-                for (int b = 0; b < MB; ++b) {
-                  e_tma_load_pair(dA + b * ATOMS * C_::A_ATOM, &tma_a, fb, kc, m0 + b * 2 * BM);
-                }
-                e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
+          for (int a = 0; a < ATOMS; ++a) {
+            const int kc = (kb * ATOMS + a) * KELEMS;
+            uint8_t* dA = sA + s * C_::A_ST + a * C_::A_ATOM;
+            uint8_t* dB = sB + s * C_::B_ST + a * C_::B_ATOM;
+            if (PAIR) {
+              e_tma_load_pair(dA, &tma_a, fb, kc, m0);
+              e_tma_load_pair(dB, &tma_b, fb, kc, n0 + rank * slice);
+            } else {
+              e_tma_load(dA, &tma_a, fb, kc, m0);
+              if (cs > 1) {
+                e_tma_load_mc(dB + rank * slice * BK_BYTES, &tma_b, fb, kc, n0 + rank * slice, mask);
               } else {
-                e_tma_load(dA, &tma_a, fb, kc, m0);
-                if (cs > 1) {
-                  e_tma_load_mc(dB + rank * slice * BK_BYTES, &tma_b, fb, kc, n0 + rank * slice, mask);
-                } else {
-                  e_tma_load(dB, &tma_b, fb, kc, n0);
-                }
+                e_tma_load(dB, &tma_b, fb, kc, n0);
               }
             }
           }
@@ -501,16 +474,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int local = 0;
       const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
       const uint16_t cmask = PAIR ? static_cast<uint16_t>(3) : mask;
-      for (int it = cluster; it < items; it += nclusters, local += MB) {
-        // accumulator slots alternate per 256-row block: MB = 1 double-buffers
-        // across items, MB = 2 gives an item's two blocks one slot each
-        for (int b = 0; b < MB; ++b) {
-          const int acc = (local + b) & 1;
-          const uint32_t use = static_cast<uint32_t>((local + b) >> 1);
-          mbar_wait(&tempty[acc], (use & 1) ^ 1);
-        }
+      for (int it = cluster; it < items; it += nclusters, ++local) {
+        // two accumulator slots alternate across this CTA's items
+        const int acc = local & 1;
+        mbar_wait(&tempty[acc], (static_cast<uint32_t>(local >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dcol = tmem_base + (local & 1) * BN;  // block b: slot (local + b) & 1
+        const uint32_t dcol = tmem_base + acc * BN;
         for (int kb = 0; kb < p.kb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -521,12 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int a = 0; a < ATOMS; ++a) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 x 32 B along the 128-B swizzle row
-#pragma unroll
-              for (int b = 0; b < MB; ++b) {
-                e_mma<KIND, PAIR>(MB == 1 ? dcol : tmem_base + ((local + b) & 1) * BN,
-                                  da + (b * ATOMS + a) * (C_::A_ATOM >> 4) + 2 * k,
-                                  db + a * (C_::B_ATOM >> 4) + 2 * k, p.idesc, (kb | a | k) != 0);
-              }
+              e_mma<KIND, PAIR>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k,
+                                p.idesc, (kb | a | k) != 0);
             }
           }
           e_commit<PAIR>(&empty[s], cmask);  // release slot s (both pair CTAs / every cluster CTA)
@@ -535,10 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ph ^= 1;
           }
         }
-#pragma unroll
-        for (int b = 0; b < MB; ++b) {
-          e_commit<PAIR>(&tfull[(local + b) & 1], PAIR ? static_cast<uint16_t>(3) : static_cast<uint16_t>(1));
-        }
+        e_commit<PAIR>(&tfull[acc], PAIR ? static_cast<uint16_t>(3) : static_cast<uint16_t>(1));
       }
     }
   } else {
@@ -555,11 +517,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the tensor maps clip rows >= M and columns >= N
       uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
       int nchunk = 0;
-      for (int itb = cluster * MB; itb < items * MB; itb += itb % MB == MB - 1 ? (nclusters - 1) * MB + 1 : 1, ++local) {
-        const int it = itb / MB, blk = itb % MB;  // item, 256-row block of the item
+      for (int it = cluster; it < items; it += nclusters, ++local) {
         const int acc = local & 1;
         const uint32_t use = static_cast<uint32_t>(local >> 1);
-        const int m0 = m_origin(it) + blk * 2 * BM, n0 = (it / mgroups) * p.bn;
+        const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
         const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
         mbar_wait(&tfull[acc], use & 1);
         __syncwarp();
@@ -631,10 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.Cb) {  // 32 B = two 16-B chunks, 32-B swizzle
             uint32_t w[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-              w[e] = *reinterpret_cast<const uint32_t*>(&h);
-            }
+            for (int e = 0; e < 8; ++e) w[e] = pack16x2(v[2 * e], v[2 * e + 1], p.f16);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               sts128(bb + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
@@ -661,17 +619,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (lane == 0) bulk_wait_all();  // stores complete before the CTA retires
     } else
-    for (int itb = cluster * MB; itb < items * MB; itb += itb % MB == MB - 1 ? (nclusters - 1) * MB + 1 : 1, ++local) {
-      const int it = itb / MB, blk = itb % MB;
+    for (int it = cluster; it < items; it += nclusters, ++local) {
       const int acc = local & 1;
       const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int m0 = m_origin(it) + blk * 2 * BM, n0 = (it / mgroups) * p.bn;
+      const int m0 = m_origin(it), n0 = (it / mgroups) * p.bn;
       const int nend = n0 + p.bn < p.N ? n0 + p.bn : p.N;
       mbar_wait(&tfull[acc], use & 1);
       __syncwarp();  // lanes leave the try_wait spin independently; .sync.aligned needs convergence
       tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
-      const bool rowok = row < p.M && !(p.diag & 4);
+      const bool rowok = row < p.M;
       // routed rows (peer memory over NVLink): each lane's destination row,
       // resolved once per tile
       float* rrow = p.routed && rowok ? p.route.base[p.route.rank[row]] + p.route.row[row] * p.route.ld : nullptr;
@@ -716,11 +673,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (p.routed) {
-          // transpose the 32x32 chunk through smem so that every store
-          // instruction writes 128 contiguous bytes of one row (4 rows per
-          // instruction) instead of 32 rows x 16 B: remote NVLink writes
-          // are packetised per contiguous run. 16-B chunks XOR-swizzled by
-          // row, conflict-free on both sides. (kEpiNone; host-checked)
+          // remote NVLink writes are packetised per contiguous run: a warp
+          // slab bound for 32 consecutive rows of one buffer leaves as tensor
+          // stores, any other row as one bulk copy of its 32 columns
+          // (kEpiNone; host-checked)
           float* st = reinterpret_cast<float*>(sOut + (warp - 2) * C_::OUT_WARP);
           const int ncols = nend - col0 < 32 ? nend - col0 : 32;  // multiple of 16
           if (slab) {
@@ -747,43 +703,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
-          if (p.route_bulk) {
-            // each lane stages its own row (144-B stride, conflict-free) and
-            // hands it to the bulk-copy engine: one async smem->peer copy per
-            // row, no LSU slots held while the NVLink writes drain
-            float* mine = st + lane * 36;
-            bulk_wait_read<0>();  // this lane's previous copy has read its row
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              sts128(mine + 4 * k, __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
-                     __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
-            }
-            if (rrow) {
-              fence_async_smem();
-              bulk_s2g(rrow + col0, mine, static_cast<uint32_t>(ncols) * 4u);
-              bulk_commit();
-            }
-            __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
-            continue;
-          }
-          __syncwarp();  // the previous chunk's reads are done
+          // each lane stages its own row (144-B stride, conflict-free) and
+          // hands it to the bulk-copy engine: one async smem->peer copy per
+          // row, no LSU slots held while the NVLink writes drain
+          float* mine = st + lane * 36;
+          bulk_wait_read<0>();  // this lane's previous copy has read its row
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            sts128(st + lane * 32 + ((k ^ (lane & 7)) << 2), __float_as_uint(v[4 * k]),
-                   __float_as_uint(v[4 * k + 1]), __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
+            sts128(mine + 4 * k, __float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                   __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3]));
           }
-          __syncwarp();
-          const int c4 = lane & 7;
-#pragma unroll 4
-          for (int r = 0; r < 32; r += 4) {
-            const int rr = r + (lane >> 3);
-            float* dst = reinterpret_cast<float*>(
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rrow), rr));
-            if (dst && c4 * 4 < ncols) {
-              const float4 t = *reinterpret_cast<const float4*>(st + rr * 32 + ((c4 ^ (rr & 7)) << 2));
-              *reinterpret_cast<float4*>(dst + col0 + c4 * 4) = t;
-            }
+          if (rrow) {
+            fence_async_smem();
+            bulk_s2g(rrow + col0, mine, static_cast<uint32_t>(ncols) * 4u);
+            bulk_commit();
           }
+          __syncwarp();  // reconverge before the next .sync.aligned tcgen05.ld
           continue;
         }
         if (!rowok) continue;
@@ -816,10 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int k = 0; k < 4; ++k) {
               uint32_t w[4];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const __nv_bfloat162 h = __floats2bfloat162_rn(v[8 * k + 2 * e], v[8 * k + 2 * e + 1]);
-                w[e] = *reinterpret_cast<const uint32_t*>(&h);
-              }
+              for (int e = 0; e < 4; ++e) w[e] = pack16x2(v[8 * k + 2 * e], v[8 * k + 2 * e + 1], p.f16);
               b4[k] = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
@@ -840,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if (p.C) {
               p.C[row * p.ldc + col] = x;
             }
-            if (p.Cb) p.Cb[row * p.ldcb + col] = __float2bfloat16_rn(x);
+            if (p.Cb) p.Cb[row * p.ldcb + col] = to16(x, p.f16);
           }
         }
       }
@@ -885,299 +817,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Chained S-Part (bf16, CTA pairs): the GEMMs between two attentions -
-// W_o, MLP-in, MLP-out and the next layer's QKV (or the head) - as one
-// persistent launch. Items are the GEMMs' pair tiles in order, each GEMM's
-// tiles ordered by 256-row block; an item of GEMM g > 0 waits until every
-// tile of GEMM g-1 in the same row block has stored its outputs (a counter
-// per (GEMM, row block), bumped by the 8 epilogue warps of each pair tile).
-// Dependencies only point to earlier items and every CTA walks its items in
-// order on a persistent grid, so the earliest unfinished item can always
-// run. This removes three launches, prologues and epilogue drains per layer
-// and lets the next GEMM's first row block start under the previous GEMM's
-// tail wave.
-constexpr int kChainMax = 4;
-
-struct ChainGemm {
-  int M, N, K, bn, nb, kb, mg;  // pair tiles: mg row blocks x nb n-tiles
-  int item0;                    // first item of this GEMM in the chain
-  float* C;
-  int64_t ldc;
-  __nv_bfloat16* Cb;
-  int64_t ldcb;
-  int epi;
-  const float* res;
-  int64_t ldr;
-  int vec_res;
-  uint32_t idesc;
-};
-struct ChainParams {
-  int n, items;
-  ChainGemm g[kChainMax];
-  unsigned long long* done;  // [kChainMax][64] tile-completion counts, this step
-  unsigned long long epoch;  // chain launches so far this step (targets scale with it)
-};
-struct ChainMaps {
-  CUtensorMap m[kChainMax][4];  // A, B, C (fp32 out), Cb (bf16 out)
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_chain_kernel(const __grid_constant__ ChainMaps maps, const ChainParams p) {
-  using C_ = Cfg<BN, true, 2>;
-  constexpr int STAGES = C_::STAGES;
-  constexpr int KELEMS = BK_BYTES / 2;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * C_::A_ST;
-  uint8_t* sOut = sB + STAGES * C_::B_ST;
-  uint8_t* tail = sOut + 4 * C_::OUT_WARP;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int rank = static_cast<int>(cluster_rank());
-  const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
-
-  // item -> (gemm, row block, n-tile); row-block-major inside a GEMM
-  auto locate = [&](int it, int& gi, int& r, int& n) {
-    gi = 0;
-    while (gi + 1 < p.n && it >= p.g[gi + 1].item0) ++gi;
-    const int li = it - p.g[gi].item0;
-    r = li / p.g[gi].nb;
-    n = li - r * p.g[gi].nb;
-  };
-
-  if (warp == 0 && lane == 0) {
-    for (int gi = 0; gi < p.n; ++gi)
-      for (int t = 0; t < 4; ++t) asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.m[gi][t]) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C_::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  pdl_trigger();
-  __syncthreads();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  pdl_wait();
-
-  if (warp == 0) {
-    // ------------------------------------------------------- TMA producer
-    int s = 0;
-    uint32_t ph = 0;
-    const uint32_t full0 = mapa(&full[0], 0);
-    for (int it = cluster; it < p.items; it += nclusters) {
-      int gi, r, n;
-      locate(it, gi, r, n);
-      const ChainGemm& G = p.g[gi];
-      if (gi > 0) {
-        // GEMM gi-1 finished this row block (its outputs are this A operand)
-        const unsigned long long target = (p.epoch + 1ull) * static_cast<unsigned long long>(p.g[gi - 1].nb) * 8ull;
-        const unsigned long long* ctr = p.done + (gi - 1) * 64 + r;
-        const long long t0 = clock64();
-        while (ld_acquire_gpu(ctr) < target) {
-          if (clock64() - t0 > 20'000'000'000LL) __trap();  // ~10 s: a lost tile
-          __nanosleep(128);
-        }
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA (async proxy) reads follow
-      }
-      const int slice = G.bn / 2;
-      const uint32_t bytes = 2u * static_cast<uint32_t>(2 * (C_::A_ATOM + slice * BK_BYTES));
-      const int m0 = (r * 2 + rank) * BM, n0 = n * G.bn;
-      const CUtensorMap* ta = &maps.m[gi][0];
-      const CUtensorMap* tb = &maps.m[gi][1];
-      for (int kb = 0; kb < G.kb; ++kb) {
-        mbar_wait(&empty[s], ph ^ 1);
-        if (leader) e_expect_tx(&full[s], bytes);
-        const uint32_t fb = full0 + s * static_cast<uint32_t>(sizeof(uint64_t));
-#pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const int kc = (kb * 2 + a) * KELEMS;
-          e_tma_load_pair(sA + s * C_::A_ST + a * C_::A_ATOM, ta, fb, kc, m0);
-          e_tma_load_pair(sB + s * C_::B_ST + a * C_::B_ATOM, tb, fb, kc, n0 + rank * slice);
-        }
-        if (++s == STAGES) {
-          s = 0;
-          ph ^= 1;
-        }
-      }
-    }
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_wait(&empty[s], ph ^ 1);
-      if (++s == STAGES) {
-        s = 0;
-        ph ^= 1;
-      }
-    }
-  } else if (warp == 1) {
-    // --------------------------------------------------------- MMA issuer
-    if (leader) {
-      int s = 0;
-      uint32_t ph = 0;
-      int local = 0;
-      const uint64_t da0 = make_desc(smem_u32(sA)), db0 = make_desc(smem_u32(sB));
-      for (int it = cluster; it < p.items; it += nclusters, ++local) {
-        int gi, r, n;
-        locate(it, gi, r, n);
-        const ChainGemm& G = p.g[gi];
-        const int acc = local & 1;
-        const uint32_t use = static_cast<uint32_t>(local >> 1);
-        mbar_wait(&tempty[acc], (use & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tmem_base + acc * BN;
-        for (int kb = 0; kb < G.kb; ++kb) {
-          mbar_wait(&full[s], ph);
-          tc_fence_after();
-          const uint64_t da = da0 + static_cast<uint64_t>(s * (C_::A_ST >> 4));
-          const uint64_t db = db0 + static_cast<uint64_t>(s * (C_::B_ST >> 4));
-#pragma unroll
-          for (int a = 0; a < 2; ++a) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              e_mma<1, true>(dcol, da + a * (C_::A_ATOM >> 4) + 2 * k, db + a * (C_::B_ATOM >> 4) + 2 * k, G.idesc,
-                             (kb | a | k) != 0);
-            }
-          }
-          e_commit<true>(&empty[s], 3);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-        e_commit<true>(&tfull[acc], 3);
-      }
-    }
-  } else {
-    // ----------------------------------------------------------- epilogue
-    const int q = warp & 3;
-    const uint32_t tempty_leader0 = mapa(&tempty[0], 0);
-    uint8_t* myout = sOut + (warp - 2) * C_::OUT_WARP;
-    int nchunk = 0;
-    int local = 0;
-    for (int it = cluster; it < p.items; it += nclusters, ++local) {
-      int gi, r, n;
-      locate(it, gi, r, n);
-      const ChainGemm& G = p.g[gi];
-      const int acc = local & 1;
-      const uint32_t use = static_cast<uint32_t>(local >> 1);
-      const int m0 = (r * 2 + rank) * BM, n0 = n * G.bn;
-      const int nend = n0 + G.bn < G.N ? n0 + G.bn : G.N;
-      mbar_wait(&tfull[acc], use & 1);
-      __syncwarp();
-      tc_fence_after();
-      const int rowb = m0 + q * 32;
-      const int64_t row = rowb + lane;
-      const bool rin = row < G.M;
-#pragma unroll 1
-      for (int c = 0; c < (G.bn + 15) / 16; ++c) {
-        const int col0 = n0 + c * 16;
-        if (col0 >= nend) break;
-        float v[16];
-        tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 16, v);
-        if (G.epi == kEpiResidual) {
-          if (rin && G.vec_res && col0 + 16 <= G.N) {
-            const float4* r4 = reinterpret_cast<const float4*>(G.res + row * G.ldr + col0);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float4 t = r4[k];
-              v[4 * k] = v[4 * k] + t.x;
-              v[4 * k + 1] = v[4 * k + 1] + t.y;
-              v[4 * k + 2] = v[4 * k + 2] + t.z;
-              v[4 * k + 3] = v[4 * k + 3] + t.w;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-              if (rin && col0 + k < G.N) v[k] = v[k] + G.res[row * G.ldr + col0 + k];
-            }
-          }
-        } else if (G.epi == kEpiSilu) {
-#pragma unroll
-          for (int k = 0; k < 16; ++k) v[k] = v[k] / (1.0f + expf(-v[k]));
-        }
-        uint8_t* bf = myout + (nchunk & 1) * (C_::OUT_F32 + C_::OUT_BF16);
-        uint8_t* bb = bf + C_::OUT_F32;
-        ++nchunk;
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        if (G.C) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            sts128(bf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), __float_as_uint(v[4 * j]),
-                   __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
-          }
-        }
-        if (G.Cb) {
-          uint32_t w[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
-            w[e] = *reinterpret_cast<const uint32_t*>(&h);
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            sts128(bb + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2],
-                   w[4 * j + 3]);
-          }
-        }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          if (G.C) tma_store_2d(&maps.m[gi][2], bf, col0, rowb);
-          if (G.Cb) tma_store_2d(&maps.m[gi][3], bb, col0, rowb);
-          bulk_commit();
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_cluster(tempty_leader0 + acc * static_cast<uint32_t>(sizeof(uint64_t)));
-        // this warp's part of the tile is in global memory: count it
-        bulk_wait_all();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        atomicAdd(p.done + gi * 64 + r, 1ull);
-      }
-      __syncwarp();
-    }
-    if (lane == 0) bulk_wait_all();
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C_::TMEM_COLS));
   }
 }
 
@@ -1241,7 +880,10 @@ CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kin
   cuuint32_t estr[2] = {1, 1};
   const CUtensorMapSwizzle sw =
       swb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : (swb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
-  const CUresult r = get_encode()(&m, kind == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+  const CUtensorMapDataType dt = kind == 2   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : kind == 3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUresult r = get_encode()(&m, dt, 2,
                                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1249,10 +891,6 @@ CUtensorMap encode_map(const void* base, int rows, int cols, int64_t ld, int kin
   return m;
 }
 
-int env_int(const char* name) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : 0;
-}
 
 int num_sms() {
   static int n = 0;
@@ -1264,13 +902,11 @@ int num_sms() {
   return n;
 }
 
-
-// Tile choice (measured at decode batches, tools/tune_gemm.py, tools/gemm_diag.py,
-// tools/splitk_probe.py): the S-Part GEMMs at M = 512 are neither L2- nor
-// HBM-bandwidth-bound; within a tile the operand loads are latency-bound
-// (bytes in flight per SM / load latency: one more stage of the same smem
-// is -14% on the bn = 112 GEMMs), and across tiles the cost is quantized
-// into waves of CTA pairs. So when M spans at
+// Tile choice (measured at decode batches): the S-Part
+// GEMMs at M = 512 are neither L2- nor HBM-bandwidth-bound; within a tile the
+// operand loads are latency-bound (bytes in flight per SM / load latency: one
+// more stage of the same smem is -14% on the bn = 112 GEMMs), and across
+// tiles the cost is quantized into waves of CTA pairs. So when M spans at
 // least two 128-row blocks, a CTA pair (cta_group::2, 256 x bn tiles) is used
 // with the tile width bn (a multiple of 16, 64..256) that minimizes
 // waves x (bn + fixed per-tile cost); e.g. N = 14336 -> bn 208 (138 tiles on
@@ -1290,35 +926,32 @@ int pick_pair_bn(int mgroups, int N, int pairs) {
   return best;
 }
 
-// Tile width of the two-block pair tile (MB = 2, opt-in): the same
-// waves x (bn + fixed) rule over half as many tile rows. Measured at M = 512
-// (tools/splitk_probe.py): MLP-in 49.4 vs 50.9 us, the head slower, the other
-// shapes slower — staging 1.5x fewer bytes per MAC did not shorten the tiles,
-// so operand ingress is not what bounds them; kept for experiments.
-int pick_pair_bn_mb2(int mb, int N, int pairs) {
-  return pick_pair_bn((mb + 3) / 4, N, pairs);
+// Kernel attributes are set once per instantiation (first launch).
+template <typename K>
+void set_smem_once(K* kern, size_t smem) {
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
 }
 
-template <int BN, bool PAIR, int ATOMS, int KIND, int MB = 1>
+template <int BN, bool PAIR, int ATOMS, int KIND>
 void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
-  using C_ = Cfg<BN, PAIR, ATOMS, MB>;
-  auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND, MB>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_set = true;
-  }
+  using C_ = Cfg<BN, PAIR, ATOMS>;
+  auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND>;
+  set_smem_once(kern, C_::SMEM);
   if (PAIR) cs = 2;
   if (!PAIR) bn = BN;
   if (bn < 16 || bn > BN || (PAIR && bn % 16)) fail(SD_ERR_CONFIG, "gemm: bad tile width");
+  const int f16 = g.kind == 3 ? 1 : 0;
   const CUtensorMap ta = make_map(g.A, g.M, g.K, g.lda, g.kind, BM);
-  // output tensor maps (16-column boxes: fp32 rows 64 B, bf16 rows 32 B)
+  // output tensor maps (16-column boxes: fp32 rows 64 B, 16-bit rows 32 B)
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  const bool tma_out = env_int("SD_GEMM_NO_TMA_OUT") == 0 && (g.C || g.Cb) &&
-                       (!g.C || (al16(g.C) && g.ldc % 4 == 0)) && (!g.Cb || (al16(g.Cb) && g.ldcb % 8 == 0));
+  const bool tma_out = (g.C || g.Cb) && (!g.C || (al16(g.C) && g.ldc % 4 == 0)) &&
+                       (!g.Cb || (al16(g.Cb) && g.ldcb % 8 == 0));
   const CUtensorMap tc = tma_out && g.C ? make_map(g.C, g.M, g.N, g.ldc, 2, 32, 64) : ta;
-  const CUtensorMap tcb = tma_out && g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, 1, 32, 32) : ta;
+  const CUtensorMap tcb = tma_out && g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, f16 ? 3 : 1, 32, 32) : ta;
   const CUtensorMap tb = make_map(g.B, g.N, g.K, g.ldb, g.kind, PAIR ? bn / 2 : BN / cs);
   Params p{};
   RouteMaps rmaps{};
@@ -1332,19 +965,18 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   p.cs = cs;
   p.C = g.C;
   p.ldc = g.ldc;
-  p.Cb = g.Cb;
+  p.Cb = reinterpret_cast<uint16_t*>(g.Cb);
   p.ldcb = g.ldcb;
   p.epi = g.epi;
   p.res = g.res;
   p.ldr = g.ldr;
   p.kind = KIND;
+  p.f16 = f16;
   p.bn = bn;
-  p.diag = env_int("SD_GEMM_DIAG");
-  p.tma_out = tma_out && !g.route ? 1 : 0;  // routed rows use the smem-transposed row stores
+  p.tma_out = tma_out && !g.route ? 1 : 0;  // routed rows use the smem-staged row stores
   if (g.route) {
     p.routed = 1;
-    p.route_bulk = env_int("SD_ROUTE_ST") == 0 ? 1 : 0;
-    p.route_tma = env_int("SD_ROUTE_NO_TMA") == 0 && g.route->rows > 0 ? 1 : 0;
+    p.route_tma = g.route->rows > 0 ? 1 : 0;
     p.route = *g.route;
     for (int d = 0; d < 8 && p.route_tma; ++d) {
       if (g.route->base[d]) {
@@ -1357,7 +989,7 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   }
   p.amax = g.amax;
   if (g.kvapp) {
-    if (!p.tma_out || KIND != 1 && KIND != 2 || g.kvapp->col_k % 16 || g.kvapp->width % 16 || (g.kvapp->pos_bytes % 16)) {
+    if (!p.tma_out || g.kvapp->col_k % 16 || g.kvapp->width % 16 || (g.kvapp->pos_bytes % 16)) {
       fail(SD_ERR_INTERNAL, "fused append: needs the TMA-store epilogue and 16-column-aligned K/V");
     }
     p.kvapp = 1;
@@ -1366,10 +998,11 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   if (g.amax && (g.route || g.C || g.Cb)) fail(SD_ERR_CONFIG, "fused-argmax GEMM: no other output");
   p.vec = (!g.C || (g.ldc % 4 == 0 && al16(g.C))) && (!g.Cb || (g.ldcb % 8 == 0 && al16(g.Cb))) &&
           (g.epi != kEpiResidual || (g.ldr % 4 == 0 && al16(g.res)));
-  const uint32_t fmt = KIND == 2 ? 2u : 1u;  // TF32 : BF16
+  // instruction descriptor: A/B format (kind::f16: 0 F16, 1 BF16; kind::tf32: 2), fp32 D, N >> 3, M >> 4
+  const uint32_t fmt = KIND == 2 ? 2u : (f16 ? 0u : 1u);
   p.idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (static_cast<uint32_t>(bn >> 3) << 17) |
             (static_cast<uint32_t>((PAIR ? 2 * BM : BM) >> 4) << 24);
-  const int items = (PAIR ? (p.mb + 2 * MB - 1) / (2 * MB) : p.mb / cs) * p.nb;
+  const int items = (PAIR ? (p.mb + 1) / 2 : p.mb / cs) * p.nb;
   const int budget = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
   const int max_clusters = budget / cs > 0 ? budget / cs : 1;
   const int clusters = items < max_clusters ? items : max_clusters;
@@ -1380,51 +1013,34 @@ void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
 
 template <int KIND>
 void dispatch(const GemmArgs& g, cudaStream_t s) {
+  const Tuning& t = tuning();
   const int mb = (g.M + BM - 1) / BM;
-  const int force_cs = env_int("SD_GEMM_CS");
-  const int force_bn = env_int("SD_GEMM_BN");
-  const char* pair_env = getenv("SD_GEMM_PAIR");
   const int sms = g.max_ctas > 0 && g.max_ctas < num_sms() ? g.max_ctas : num_sms();
-  const bool pair = pair_env ? atoi(pair_env) > 0 : (mb >= 2 && sms >= 2);
-  if (pair) {
-    int MB = 1, bn = pick_pair_bn((mb + 1) / 2, g.N, sms / 2);
-    if (env_int("SD_GEMM_MB") == 2 && mb >= 3) {  // 512-row pair tiles (experimental)
-      MB = 2;
-      bn = pick_pair_bn_mb2(mb, g.N, sms / 2);
-    }
-    if (force_bn >= 16 && force_bn <= 256 && force_bn % 16 == 0) bn = force_bn;
+  if (t.gemm_pair && mb >= 2 && sms >= 2) {
+    int bn = pick_pair_bn((mb + 1) / 2, g.N, sms / 2);
+    if (t.gemm_bn >= 64 && t.gemm_bn <= 256 && t.gemm_bn % 16 == 0) bn = t.gemm_bn;
     // The stage ring is sized for the widest tile of the instantiation, so
     // the tile width picks the instantiation: one swizzle atom per stage and
     // a B stage no wider than needed gives the most stages in the same smem
     // (bn <= 128: 8, <= 192: 7, else 6; the loads are latency-bound, so more,
     // smaller stages keep more of them in flight). Measured at M = 512 with
-    // the weights streamed from HBM (tools/wide_probe.py, splitk_probe.py):
-    // QKV 25.1 -> 22.5 us, MLP-in 50.5 -> 48.2, MLP-out 58.8 -> 50.1, W_o
-    // 20.8 -> 18.2 against the two-atom stages of the 256-wide instantiation
-    // (3 stages). SD_GEMM_ATOMS2=1: two atoms per stage (3-4 stages).
-    const bool two = env_int("SD_GEMM_ATOMS2") == 1;
-    if (MB == 2) {
-      launch<256, true, 1, KIND, 2>(g, 2, bn, s);
-    } else if (bn <= 128) {
-      if (two) {
-        launch<128, true, 2, KIND>(g, 2, bn, s);
-      } else {
-        launch<128, true, 1, KIND>(g, 2, bn, s);
-      }
-    } else if (bn <= 192 && !two) {
+    // the weights streamed from HBM: QKV 25.1 -> 22.5 us, MLP-in 50.5 -> 48.2,
+    // MLP-out 58.8 -> 50.1, W_o 20.8 -> 18.2 against two-atom stages of the
+    // 256-wide instantiation (3 stages).
+    if (bn <= 128) {
+      launch<128, true, 1, KIND>(g, 2, bn, s);
+    } else if (bn <= 192) {
       launch<192, true, 1, KIND>(g, 2, bn, s);
-    } else if (two) {
-      launch<256, true, 2, KIND>(g, 2, bn, s);
     } else {
       launch<256, true, 1, KIND>(g, 2, bn, s);
     }
     return;
   }
+  // one 128-row block (or an SM budget of one): single-CTA tiles, B
+  // multicast over a cluster of M blocks when that fills the machine
   const int tiles256 = mb * ((g.N + 255) / 256);
-  int bn = tiles256 * 2 <= sms ? 128 : 256;
-  int cs = (bn == 256 && mb % 2 == 0) ? 2 : 1;
-  if (force_cs > 0 && mb % force_cs == 0) cs = force_cs;
-  if (force_bn == 128 || force_bn == 256) bn = force_bn;
+  const int bn = tiles256 * 2 <= sms ? 128 : 256;
+  const int cs = (bn == 256 && mb % 2 == 0) ? 2 : 1;
   if (bn == 128) {
     launch<128, false, 2, KIND>(g, cs, 128, s);
   } else {
@@ -1436,7 +1052,7 @@ void dispatch(const GemmArgs& g, cudaStream_t s) {
 
 bool gemm_sm100_supported(const GemmArgs& g) {
   const int es = g.kind == 2 ? 4 : 2;
-  if (g.kind != 1 && g.kind != 2) return false;
+  if (g.kind < 1 || g.kind > 3) return false;
   if (g.M < 1 || g.N < 1 || g.K < 1) return false;
   if ((g.lda * es) % 16 || (g.ldb * es) % 16) return false;
   if (reinterpret_cast<uintptr_t>(g.A) % 16 || reinterpret_cast<uintptr_t>(g.B) % 16) return false;
@@ -1444,74 +1060,11 @@ bool gemm_sm100_supported(const GemmArgs& g) {
   return true;
 }
 
-bool gemm_chain_supported(const ChainArgs& c) {
-  if (c.n < 1 || c.n > kChainMax || !c.done) return false;
-  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  for (int i = 0; i < c.n; ++i) {
-    const GemmArgs& g = c.g[i];
-    if (g.kind != 1 || !gemm_sm100_supported(g) || g.M != c.g[0].M || g.M < 2 * BM || g.M > 64 * 2 * BM) return false;
-    if (!(g.C || g.Cb) || (g.C && (!al16(g.C) || g.ldc % 4)) || (g.Cb && (!al16(g.Cb) || g.ldcb % 8))) return false;
-    if (g.K % (2 * BK_BYTES / 2)) return false;  // whole two-atom stages
-  }
-  return true;
-}
-
-void launch_gemm_chain(const ChainArgs& c, cudaStream_t s) {
-  if (!gemm_chain_supported(c)) fail(SD_ERR_INTERNAL, "gemm chain: unsupported shapes");
-  using C_ = Cfg<256, true, 2>;
-  auto* kern = gemm_chain_kernel<256>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr_set = true;
-  }
-  const int sms = c.max_ctas > 0 && c.max_ctas < num_sms() ? c.max_ctas : num_sms();
-  ChainMaps maps{};
-  ChainParams p{};
-  p.n = c.n;
-  p.done = c.done;
-  p.epoch = c.epoch;
-  int items = 0;
-  for (int i = 0; i < c.n; ++i) {
-    const GemmArgs& g = c.g[i];
-    ChainGemm& G = p.g[i];
-    G.M = g.M;
-    G.N = g.N;
-    G.K = g.K;
-    G.mg = (g.M + 2 * BM - 1) / (2 * BM);
-    G.bn = pick_pair_bn(G.mg, g.N, sms / 2);
-    G.nb = (g.N + G.bn - 1) / G.bn;
-    G.kb = g.K / (2 * (BK_BYTES / 2));
-    G.item0 = items;
-    items += G.mg * G.nb;
-    G.C = g.C;
-    G.ldc = g.ldc;
-    G.Cb = g.Cb;
-    G.ldcb = g.ldcb;
-    G.epi = g.epi;
-    G.res = g.res;
-    G.ldr = g.ldr;
-    G.vec_res = g.epi == kEpiResidual && g.ldr % 4 == 0 && (reinterpret_cast<uintptr_t>(g.res) & 15) == 0;
-    G.idesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(G.bn >> 3) << 17) |
-              (static_cast<uint32_t>((2 * BM) >> 4) << 24);
-    maps.m[i][0] = make_map(g.A, g.M, g.K, g.lda, 1, BM);
-    maps.m[i][1] = make_map(g.B, g.N, g.K, g.ldb, 1, G.bn / 2);
-    maps.m[i][2] = g.C ? make_map(g.C, g.M, g.N, g.ldc, 2, 32, 64) : maps.m[i][0];
-    maps.m[i][3] = g.Cb ? make_map(g.Cb, g.M, g.N, g.ldcb, 1, 32, 32) : maps.m[i][0];
-  }
-  p.items = items;
-  const int max_clusters = sms / 2 > 0 ? sms / 2 : 1;
-  const int clusters = items < max_clusters ? items : max_clusters;
-  SD_CUDA(launch_pdl(kern, dim3(static_cast<unsigned>(clusters * 2)), dim3(kThreads), C_::SMEM, s, 2u, maps, p));
-  count_launch();
-}
-
 void launch_gemm_sm100(const GemmArgs& g, cudaStream_t s) {
   if (g.kind == 2) {
     dispatch<2>(g, s);
   } else {
-    dispatch<1>(g, s);
+    dispatch<1>(g, s);  // bf16 and fp16 operands: kind::f16
   }
 }
 

@@ -661,9 +661,13 @@ __global__ void append_kernel(const AppendArgs a) {
   }
 }
 
-// Synthetic prefill: element (slot, layer, pos, kv, i) = synth_value(idx).
-__global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* slots, int n,
-                               int length, uint64_t salt) {
+// Synthetic prefill, keyed by sequence id, not by store slot,
+// so a sequence's context is the same in any shard and any allocation order:
+// element (seq, layer, pos, kv, global kv head h, d) = synth_value(salt ^ idx),
+// idx = ((((seq * 4096 + layer) * 2^20 + pos) * 2 + kv) * Hkv_total + h) * hd + d
+// (kv_prefill_index in sd_common.h; the oracle restates it).
+__global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* slots, const uint64_t* seq_ids,
+                               int n, int length, uint64_t salt, int h0, int kv_heads_total) {
   pdl_trigger();
   pdl_wait();
   const int64_t rows = static_cast<int64_t>(n) * num_layers * length * 2;
@@ -681,28 +685,26 @@ __global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* sl
     uint8_t* lb = g.pool + static_cast<int64_t>(grp) * g.group_bytes +
                   static_cast<int64_t>(layer) * g.layer_bytes;
     uint8_t* row = lb + (kv ? g.v_off : 0) + static_cast<int64_t>(off) * g.pos_bytes;
-    const uint64_t base =
-        salt ^ ((((static_cast<uint64_t>(slot) * 4096u + layer) * 1048576u + pos) * 2u + kv) *
-                static_cast<uint64_t>(g.width));
+    const uint64_t base = kv_prefill_index(seq_ids[item], layer, pos, kv, h0, 0, kv_heads_total, g.hd);
     if (g.fmt == SD_KV_SINGLE) {
       float* d = reinterpret_cast<float*>(row);
-      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = synth_value(base + e);
+      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = synth_value(salt ^ (base + e));
     } else if (g.fmt == SD_KV_HALF) {
       __half* d = reinterpret_cast<__half*>(row);
-      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(synth_value(base + e));
+      for (int e = threadIdx.x; e < g.width; e += blockDim.x) d[e] = __float2half_rn(synth_value(salt ^ (base + e)));
     } else {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       float* scales = reinterpret_cast<float*>(lb + (kv ? g.vs_off : g.ks_off)) + off * g.hc;
       int8_t* d = reinterpret_cast<int8_t*>(row);
       for (int h = warp; h < g.hc; h += nw) {
         float mx = 0.0f;
-        for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(synth_value(base + h * g.hd + e)));
+        for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(synth_value(salt ^ (base + h * g.hd + e))));
 #pragma unroll
         for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
         const float sc = mx == 0.0f ? 0.0f : __fdiv_rn(mx, 127.0f);
         const double inv = sc == 0.0f ? 0.0 : 1.0 / static_cast<double>(sc);
         for (int e = lane; e < g.hd; e += 32) {
-          double rr = rint(static_cast<double>(synth_value(base + h * g.hd + e)) * inv);
+          double rr = rint(static_cast<double>(synth_value(salt ^ (base + h * g.hd + e))) * inv);
           rr = fmin(fmax(rr, -127.0), 127.0);
           d[h * g.hd + e] = static_cast<int8_t>(rr);
         }
@@ -853,10 +855,11 @@ void launch_append(const AppendArgs& a, cudaStream_t s) {
   ::sd::count_launch();
 }
 
-void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, int n,
-                              int length, uint64_t salt, cudaStream_t s) {
+void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, const uint64_t* seq_ids,
+                              int n, int length, uint64_t salt, int h0, int kv_heads_total, cudaStream_t s) {
   if (n == 0 || length == 0) return;
-  SD_CUDA(launch_pdl(prefill_kernel, dim3(148 * 16), dim3(256), 0, s, 1, g, num_layers, slots, n, length, salt));
+  SD_CUDA(launch_pdl(prefill_kernel, dim3(148 * 16), dim3(256), 0, s, 1, g, num_layers, slots, seq_ids, n, length,
+                     salt, h0, kv_heads_total));
   SD_CUDA(cudaGetLastError());
   ::sd::count_launch();
 }

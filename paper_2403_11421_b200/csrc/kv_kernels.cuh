@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "sd_common.h"
+
 namespace sd {
 
 // Geometry of the paged KV pool.
@@ -63,7 +65,8 @@ struct ORoute {
   const int32_t* rank;
   const int32_t* row;
   float* base[8];
-  __nv_bfloat16* bbase[8];
+  act16* bbase[8];      // 16-bit copy (the home's W_o operand) instead of fp32
+  uint32_t f16_mask;    // destinations whose 16-bit copy is fp16 (else bf16)
   int64_t ld, bld;
   int64_t* flag[8];
   int32_t* done;
@@ -94,8 +97,9 @@ struct AttnArgs {
   // arithmetic) and resets its counter
   const int4* comb;           // [ncombine] (item, first piece, piece count, -)
   int32_t* comb_cnt;          // [ncombine][hc] arrival counters, zero between launches
-  __nv_bfloat16* ob;          // optional bf16 copy of o (the W_o GEMM operand)
+  act16* ob;          // optional 16-bit copy of o (the W_o GEMM operand)
   int64_t ob_stride;
+  int ob_f16;                 // the copy is fp16 (else bf16)
   int routed;                 // o rows go to the home ranks (oroute), o/ob unused
   ORoute oroute;
 };
@@ -123,8 +127,8 @@ void launch_append(const AppendArgs& a, cudaStream_t s);
 bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s);
 void launch_attention_generic(const AttnArgs& a, int npieces, cudaStream_t s);
 void launch_combine(const CombineArgs& a, cudaStream_t s);
-void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots,
-                              int n, int length, uint64_t salt, cudaStream_t s);
+void launch_prefill_synthetic(const KvGeom& g, int num_layers, const int32_t* slots, const uint64_t* seq_ids,
+                              int n, int length, uint64_t salt, int h0, int kv_heads_total, cudaStream_t s);
 int attention_consumer_warps();
 // tensor-core GQA path (kv_mma.cu): fp16 KV, hd 128, 8 kv heads per shard, G in {2, 4, 8}
 bool attention_mma_supported(const KvGeom& g, int G);

@@ -22,6 +22,8 @@
 #include <cuda_fp16.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "kv_kernels.cuh"
 #include "pdl.cuh"
@@ -451,12 +453,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const int qh = hk * G + hq;
       if (direct) {
         float* orow;
-        __nv_bfloat16* brow;
+        act16* brow;
+        int f16 = a.ob_f16;  // format of the 16-bit copy (fp16 when set)
         if (a.routed) {
           const int rk = a.oroute.rank[pc.item];
           const int64_t rr = a.oroute.row[pc.item];
           orow = a.oroute.base[rk] ? a.oroute.base[rk] + rr * a.oroute.ld + qh * kHD : nullptr;
           brow = a.oroute.bbase[rk] ? a.oroute.bbase[rk] + rr * a.oroute.bld + qh * kHD : nullptr;
+          f16 = static_cast<int>(a.oroute.f16_mask >> rk & 1u);
         } else {
           orow = a.o + static_cast<int64_t>(pc.item) * a.o_stride + qh * kHD;
           brow = a.ob ? a.ob + static_cast<int64_t>(pc.item) * a.ob_stride + qh * kHD : nullptr;
@@ -470,8 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
             orow[16 * mt + gq + 8] = x1;
           }
           if (brow) {
-            brow[16 * mt + gq] = __float2bfloat16_rn(x0);
-            brow[16 * mt + gq + 8] = __float2bfloat16_rn(x1);
+            brow[16 * mt + gq] = to16(x0, f16);
+            brow[16 * mt + gq + 8] = to16(x1, f16);
           }
         }
       } else {
@@ -529,12 +533,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           }
         }
         float* orow;
-        __nv_bfloat16* bro;
+        act16* bro;
+        int f16 = a.ob_f16;
         if (a.routed) {
           const int rk = a.oroute.rank[it.x];
           const int64_t rr = a.oroute.row[it.x];
           orow = a.oroute.base[rk] ? a.oroute.base[rk] + rr * a.oroute.ld + qh * kHD + d0 : nullptr;
           bro = a.oroute.bbase[rk] ? a.oroute.bbase[rk] + rr * a.oroute.bld + qh * kHD + d0 : nullptr;
+          f16 = static_cast<int>(a.oroute.f16_mask >> rk & 1u);
         } else {
           orow = a.o + static_cast<int64_t>(it.x) * a.o_stride + qh * kHD + d0;
           bro = a.ob ? a.ob + static_cast<int64_t>(it.x) * a.ob_stride + qh * kHD + d0 : nullptr;
@@ -544,9 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           const float4 x = make_float4(acc[4 * k] / L, acc[4 * k + 1] / L, acc[4 * k + 2] / L, acc[4 * k + 3] / L);
           if (orow) *reinterpret_cast<float4*>(orow + 4 * k) = x;
           if (bro) {
-            __nv_bfloat16* brow = bro + 4 * k;
-            *reinterpret_cast<__nv_bfloat162*>(brow) = __floats2bfloat162_rn(x.x, x.y);
-            *reinterpret_cast<__nv_bfloat162*>(brow + 2) = __floats2bfloat162_rn(x.z, x.w);
+            act16* brow = bro + 4 * k;
+            *reinterpret_cast<uint2*>(brow) = make_uint2(pack16x2(x.x, x.y, f16), pack16x2(x.z, x.w, f16));
           }
         }
         if (lane == 0) a.comb_cnt[ci * g.hc + hk] = 0;  // ready for the next launch
@@ -578,12 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 // producer's own pattern streams 7.20 vs 6.98 TB/s with 8-KB over 4-KB
 // copies, tools/bulk_bw.cu; the C5 layer 0.630 -> 0.626 ms) at the price of
 // 2-way ldmatrix conflicts (rows of a slot share bank groups); int8 keeps
-// pair slots, which its 32-bit fragment loads need. SD_ATTN_PAIRS=1: pairs
-// for fp16 too.
-int attention_mma_rows_per_slot(const KvGeom& g) {
-  static const bool pairs = std::getenv("SD_ATTN_PAIRS") != nullptr;
-  return g.fmt == SD_KV_HALF && !pairs ? 4 : 2;
-}
+// pair slots, which its 32-bit fragment loads need.
+int attention_mma_rows_per_slot(const KvGeom& g) { return g.fmt == SD_KV_HALF ? 4 : 2; }
 
 bool attention_mma_supported(const KvGeom& g, int G) {
   return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD &&
@@ -606,20 +607,24 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
   const bool i8 = a.g.fmt == SD_KV_INT8;
-  const bool quad = attention_mma_rows_per_slot(a.g) == 4;
   switch (a.G) {
-    case 2:
-      fn = i8 ? attn_mma_kernel<2, SD_KV_INT8, 2> : quad ? attn_mma_kernel<2, SD_KV_HALF, 4> : attn_mma_kernel<2, SD_KV_HALF, 2>;
-      break;
-    case 4:
-      fn = i8 ? attn_mma_kernel<4, SD_KV_INT8, 2> : quad ? attn_mma_kernel<4, SD_KV_HALF, 4> : attn_mma_kernel<4, SD_KV_HALF, 2>;
-      break;
-    case 8:
-      fn = i8 ? attn_mma_kernel<8, SD_KV_INT8, 2> : quad ? attn_mma_kernel<8, SD_KV_HALF, 4> : attn_mma_kernel<8, SD_KV_HALF, 2>;
-      break;
+    case 2: fn = i8 ? attn_mma_kernel<2, SD_KV_INT8, 2> : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
+    case 4: fn = i8 ? attn_mma_kernel<4, SD_KV_INT8, 2> : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
+    case 8: fn = i8 ? attn_mma_kernel<8, SD_KV_INT8, 2> : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
-  SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  // the dynamic-smem opt-in once per instantiation and size
+  static std::mutex mu;
+  static std::vector<std::pair<void (*)(const AttnArgs), size_t>> set;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    bool have = false;
+    for (auto& e : set) have = have || (e.first == fn && e.second >= smem);
+    if (!have) {
+      SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      set.emplace_back(fn, smem);
+    }
+  }
   SD_CUDA(launch_pdl(fn, dim3(grid), dim3(kThreads), smem, s, 1, a));
   SD_CUDA(cudaGetLastError());
   count_launch();

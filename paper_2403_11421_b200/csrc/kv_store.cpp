@@ -74,15 +74,9 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   // allocated in order, so one layer's K/V of a sequence is one contiguous
   // stream for the attention (bulk copies walking 64-KB regions back to back
   // read 7.0-7.4 TB/s, at a 2-MB stride 6.5-6.8: tools/bulk_bw.cu).
-  // SD_KV_GROUP_MAJOR=1: [page group][layer][region].
   const int64_t rbytes = round_up(lb, 128);
-  if (std::getenv("SD_KV_GROUP_MAJOR")) {
-    g.layer_bytes = rbytes;
-    g.group_bytes = rbytes * spec.L;
-  } else {
-    g.group_bytes = rbytes;
-    g.layer_bytes = rbytes * static_cast<int64_t>(pool_groups_);
-  }
+  g.group_bytes = rbytes;
+  g.layer_bytes = rbytes * static_cast<int64_t>(pool_groups_);
 
   const size_t pool_bytes = static_cast<size_t>(rbytes) * spec.L * static_cast<size_t>(pool_groups_);
   void* pool = nullptr;
@@ -94,7 +88,6 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
                               cudaGetErrorString(e));
   }
   g.pool = static_cast<uint8_t*>(pool);
-  if (std::getenv("SD_DEBUG_ZERO_POOL")) SD_CUDA(cudaMemset(pool, 0, pool_bytes));
   const size_t pt_bytes = static_cast<size_t>(max_seqs_) * max_pages * sizeof(int32_t);
   SD_CUDA(cudaMalloc(&g.page_table, pt_bytes));
   SD_CUDA(cudaMemset(g.page_table, 0, pt_bytes));
@@ -117,7 +110,7 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
     --nstages_;
   }
   attn_smem_ = attention_smem_bytes(g, T_, nstages_, G_, &stage_region_, &sc_region_);
-  use_mma_ = attention_mma_supported(g, G_) && std::getenv("SD_ATTN_NO_MMA") == nullptr;
+  use_mma_ = attention_mma_supported(g, G_) && tuning().attn_mma != 0;
   if (use_mma_) {
     T_ = 16;
     attn_smem_ = attention_mma_smem(g, &stage_region_, &sc_region_, &nstages_);
@@ -388,6 +381,7 @@ bool KvStore::stage_fused_append(int layer, int n, const uint64_t* seqs, const u
   }
   for (int i = 0; i < n; ++i) len_[static_cast<size_t>(fm->slots[static_cast<size_t>(i)]) * L + layer] += 1;
   total_ += n;
+  fused_prev_layer_ = fm->layer;
   const int32_t* d = static_cast<const int32_t*>(fm->blob->dev.p);
   out->layer_base = geom_.pool + static_cast<int64_t>(layer) * geom_.layer_bytes;
   out->group_bytes = geom_.group_bytes;
@@ -400,6 +394,16 @@ bool KvStore::stage_fused_append(int layer, int n, const uint64_t* seqs, const u
   fm->used = ++fast_clock_;
   fused_pending_ = fm;
   return true;
+}
+
+void KvStore::abort_fused_append() {
+  Fast* fm = fused_pending_;
+  if (!fm) return;
+  const int L = spec_.L, layer = fm->layer;
+  for (int i = 0; i < fm->n; ++i) len_[static_cast<size_t>(fm->slots[static_cast<size_t>(i)]) * L + layer] -= 1;
+  total_ -= fm->n;
+  fm->layer = fused_prev_layer_;
+  fused_pending_ = nullptr;
 }
 
 void KvStore::end_fused_append(cudaStream_t s) {
@@ -420,7 +424,7 @@ const KvStore::Fast* KvStore::fast_match(int n, const uint64_t* seqs) const {
 // --------------------------------------------------------------- attend ---
 void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
                      int64_t q_stride, float* o_dev, int64_t o_stride, cudaStream_t s, int slot,
-                     __nv_bfloat16* ob, int64_t ob_stride, const ORoute* oroute) {
+                     act16* ob, int64_t ob_stride, const ORoute* oroute, int ob_f16) {
   if (oroute && !use_mma_) fail(SD_ERR_INTERNAL, "routed attention output needs the tensor-core path");
   DeviceGuard dg(device_);
   const int L = spec_.L;
@@ -537,12 +541,12 @@ void KvStore::attend(int layer, int n, const uint64_t* seqs, const float* q_dev,
       SD_CUDA(cudaMemsetAsync(P.comb_cnt.p, 0, P.comb_cnt.bytes, s));
     }
   }
-  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, ob, ob_stride, s, oroute);
+  launch_attention_plan(P, layer, q_dev, q_stride, o_dev, o_stride, ob, ob_stride, s, oroute, ob_f16);
 }
 
 void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o,
-                                    int64_t os, __nv_bfloat16* ob, int64_t obs, cudaStream_t s,
-                                    const ORoute* oroute) {
+                                    int64_t os, act16* ob, int64_t obs, cudaStream_t s,
+                                    const ORoute* oroute, int ob_f16) {
   const uint8_t* base = static_cast<const uint8_t*>(P.blob.dev.p);
   AttnArgs a{};
   a.g = geom_;
@@ -562,14 +566,13 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   a.nstages = nstages_;
   a.stage_region = stage_region_;
   a.sc_region = sc_region_;
-  // the tensor-core kernel fuses the combine and the bf16 copy
-  // (SD_ATTN_SEPARATE_COMBINE=1 keeps the separate combine kernel)
-  static const bool separate = std::getenv("SD_ATTN_SEPARATE_COMBINE") != nullptr;
-  const bool fused = use_mma_ && !separate;
+  // the tensor-core kernel fuses the combine and the 16-bit copy of o
+  const bool fused = use_mma_;
   a.comb = reinterpret_cast<const int4*>(base + P.off_comb);
   a.comb_cnt = fused ? static_cast<int32_t*>(P.comb_cnt.p) : nullptr;
   a.ob = fused ? ob : nullptr;
   a.ob_stride = obs;
+  a.ob_f16 = ob_f16;
   if (oroute) {
     if (!fused) fail(SD_ERR_INTERNAL, "routed attention output needs the fused combine");
     a.routed = 1;
@@ -621,7 +624,7 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   c.Hq = head_count_ * G_;
   c.hd = spec_.hd;
   launch_combine(c, s);
-  if (ob) launch_to_bf16(static_cast<int>(P.slots.size()), q_width(), o, os, ob, obs, s);
+  if (ob) launch_to_16(static_cast<int>(P.slots.size()), q_width(), o, os, ob, obs, ob_f16, s);
   SD_CUDA(cudaEventRecord(P.blob.done, s));
 }
 
@@ -710,18 +713,20 @@ void KvStore::prefill_synthetic(int n, const uint64_t* seqs, int length, uint64_
     npages_[static_cast<size_t>(slot)] = npg;
   }
   DevBuf d;
-  const size_t bytes = (upd.size() + slots.size()) * 4;
-  d.get(bytes);
+  const size_t ints = (upd.size() + slots.size() + 1) / 2 * 2;  // 8-B aligned sequence ids follow
+  d.get(ints * 4 + static_cast<size_t>(n) * 8);
   SD_CUDA(cudaMemcpy(d.p, upd.data(), upd.size() * 4, cudaMemcpyHostToDevice));
   int32_t* dslots = static_cast<int32_t*>(d.p) + upd.size();
   SD_CUDA(cudaMemcpy(dslots, slots.data(), slots.size() * 4, cudaMemcpyHostToDevice));
+  uint64_t* dseqs = reinterpret_cast<uint64_t*>(static_cast<int32_t*>(d.p) + ints);
+  SD_CUDA(cudaMemcpy(dseqs, seqs, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice));
   AppendArgs a{};
   a.g = geom_;
   a.n = 0;
   a.upd = static_cast<const int32_t*>(d.p);
   a.nupd = static_cast<int>(upd.size() / 2);
   launch_append(a, s);
-  launch_prefill_synthetic(geom_, L, dslots, n, length, salt, s);
+  launch_prefill_synthetic(geom_, L, dslots, dseqs, n, length, salt, head_start_, spec_.Hkv, s);
   SD_CUDA(cudaStreamSynchronize(s));
   for (Plan& P : plans_) {
     P.slots.clear();

@@ -54,13 +54,16 @@ class KvStore {
   bool stage_fused_append(int layer, int n, const uint64_t* seqs, const uint32_t* positions,
                           struct KvAppendOut* out);
   void end_fused_append(cudaStream_t s);
+  // undo a staged append whose producer could not be launched (lengths,
+  // totals and the fast-path layer return to their state before staging)
+  void abort_fused_append();
   // KvShard::attend semantics (attention.cpp:204-282).
   // `slot` selects one of the cached split plans (one per interleaved
   // mini-batch, so alternating batches do not rebuild each other's plan).
   // `ob` (optional): also write o in bf16 (the W_o GEMM operand).
   void attend(int layer, int n, const uint64_t* seqs, const float* q_dev, int64_t q_stride,
               float* o_dev, int64_t o_stride, cudaStream_t s, int slot = 0,
-              __nv_bfloat16* ob = nullptr, int64_t ob_stride = 0, const ORoute* oroute = nullptr);
+              act16* ob = nullptr, int64_t ob_stride = 0, const ORoute* oroute = nullptr, int ob_f16 = 0);
   bool tensor_core_path() const { return use_mma_; }
   // SM budget of the attention grid (0 = every SM): the R-Part's share when
   // it runs beside the S-Part of the other mini-batch
@@ -99,7 +102,7 @@ class KvStore {
   };
   static constexpr int kPlanSlots = 2;
   void launch_attention_plan(Plan& P, int layer, const float* q, int64_t qs, float* o, int64_t os,
-                             __nv_bfloat16* ob, int64_t obs, cudaStream_t s, const ORoute* oroute);
+                             act16* ob, int64_t obs, cudaStream_t s, const ORoute* oroute, int ob_f16);
 
   Spec spec_;
   int head_start_, head_count_, G_;
@@ -141,6 +144,7 @@ class KvStore {
   };
   Fast fast_[2];
   Fast* fused_pending_ = nullptr;
+  int fused_prev_layer_ = -1;
   uint64_t fast_clock_ = 0;
   const Fast* fast_match(int n, const uint64_t* seqs) const;
 

@@ -10,17 +10,14 @@
 
 #include <cuda_runtime.h>
 
-#include <cstdlib>
+#include "sd_common.h"
 
 namespace sd {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-inline bool pdl_enabled() {
-  static const bool on = std::getenv("SD_NO_PDL") == nullptr;
-  return on;
-}
+inline bool pdl_enabled() { return tuning().pdl != 0; }
 
 // cudaLaunchKernelEx with the programmatic-serialization attribute (and an
 // optional cluster dimension)

@@ -51,7 +51,8 @@ void bench_dense_block(Weights& w, const int* batches, int n, int reps, double* 
   DeviceGuard dg(w.device());
   const Spec& sp = w.spec();
   const size_t bmax = (static_cast<size_t>(batches[n - 1]) + 127) / 128 * 128;
-  const bool bf = w.mode() == SD_DENSE_BF16;
+  const bool bf = w.mode() == SD_DENSE_BF16 || w.mode() == SD_DENSE_F16;
+  const int f16 = w.mode() == SD_DENSE_F16 ? 1 : 0;
   DevBuf x, qkv, y, h, xo, xb, ob, yb, hb;
   const size_t D = sp.D, F = sp.F, Q = sp.qkv_width();
   for (auto* b : {&x, &y, &xo}) SD_CUDA(cudaMemset(b->get(bmax * D * 4), 0, bmax * D * 4));
@@ -62,15 +63,21 @@ void bench_dense_block(Weights& w, const int* batches, int n, int reps, double* 
   SD_CUDA(cudaDeviceSynchronize());
   cudaStream_t s;
   SD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // data-dependent tensor-core power: the features are random values (the
+  // reference feeds deterministic_batch features, dense.cpp:145-196), not zeros
+  launch_fill_synthetic(static_cast<float*>(x.p), static_cast<int64_t>(bmax * D), 0xB0B5ull, s);
+  if (bf) launch_to_16(static_cast<int>(bmax), static_cast<int>(D), static_cast<float*>(x.p), D, xb.p, D,
+                       w.mode() == SD_DENSE_F16, s);
+  SD_CUDA(cudaStreamSynchronize(s));
   auto f = [](DevBuf& b) { return static_cast<float*>(b.p); };
-  auto hbf = [](DevBuf& b) { return static_cast<__nv_bfloat16*>(b.p); };
+  auto hbf = [](DevBuf& b) { return static_cast<act16*>(b.p); };
   for (int i = 0; i < n; ++i) {
     const int B = batches[i];
     // project_qkv + finish_block of layer 0 (the reference's run_once); the
     // attention output o is taken as the q block as in the reference
     auto once = [&] {
       w.linear(0, 0, B, f(x), D, hbf(xb), D, f(qkv), Q, nullptr, 0, kEpiNone, nullptr, 0, s);
-      if (bf) launch_to_bf16(B, static_cast<int>(D), f(qkv), Q, hbf(ob), D, s);
+      if (bf) launch_to_16(B, static_cast<int>(D), f(qkv), Q, hbf(ob), D, f16, s);
       w.linear(0, 4, B, f(qkv), Q, hbf(ob), D, f(y), D, bf ? hbf(yb) : nullptr, D, kEpiResidual, f(x), D, s);
       w.linear(0, 5, B, f(y), D, hbf(yb), D, bf ? nullptr : f(h), F, bf ? hbf(hb) : nullptr, F, kEpiSilu, nullptr, 0, s);
       w.linear(0, 6, B, f(h), F, hbf(hb), F, f(xo), D, nullptr, 0, kEpiResidual, f(y), D, s);

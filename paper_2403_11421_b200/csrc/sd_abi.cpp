@@ -331,11 +331,11 @@ void host_linear(sd_weights* w, int layer, int which, int B, const float* x, flo
   float* dy = static_cast<float*>(g_scr.b.get(bp * out * 4));
   const float* dr = nullptr;
   if (res) dr = stage(g_scr.c, res, static_cast<size_t>(B) * out);
-  __nv_bfloat16* dxb = nullptr;
-  if (W.mode() == SD_DENSE_BF16) {
-    dxb = static_cast<__nv_bfloat16*>(g_scr.ab.get(bp * in * 2));
+  sd::act16* dxb = nullptr;
+  if (W.mode() == SD_DENSE_BF16 || W.mode() == SD_DENSE_F16) {
+    dxb = static_cast<sd::act16*>(g_scr.ab.get(bp * in * 2));
     SD_CUDA(cudaMemset(dxb, 0, bp * in * 2));
-    sd::launch_to_bf16(B, in, dx, in, dxb, in, nullptr);
+    sd::launch_to_16(B, in, dx, in, dxb, in, W.mode() == SD_DENSE_F16, nullptr);
   }
   W.linear(layer, which, B, dx, in, dxb, in, dy, out, nullptr, 0, epi, dr, out, nullptr);
   SD_CUDA(cudaMemcpy(y, dy, static_cast<size_t>(B) * out * 4, cudaMemcpyDeviceToHost));
@@ -421,7 +421,7 @@ int sd_gemm_dev(int kind, int M, int N, int K, const void* A, int64_t lda, const
     g.ldb = ldb;
     g.C = C;
     g.ldc = ldc;
-    g.Cb = static_cast<__nv_bfloat16*>(Cb);
+    g.Cb = static_cast<sd::act16*>(Cb);
     g.ldcb = ldcb;
     g.epi = epi;
     g.res = res;
@@ -508,6 +508,47 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms) {
   });
 }
 
+int sd_tune(const char* name, int value) {
+  return guard([&] {
+    need(name, "name");
+    sd::Tuning& t = sd::tuning();
+    const std::string n(name);
+    int* f = n == "gemm_bn"        ? &t.gemm_bn
+             : n == "gemm_pair"    ? &t.gemm_pair
+             : n == "fused_append" ? &t.fused_append
+             : n == "fused_argmax" ? &t.fused_argmax
+             : n == "dist_fuse"    ? &t.dist_fuse
+             : n == "attn_mma"     ? &t.attn_mma
+             : n == "pdl"          ? &t.pdl
+             : n == "dist_phases"  ? &t.dist_phases
+                                   : nullptr;
+    if (!f) sd::fail(SD_ERR_CONFIG, "sd_tune: unknown switch " + n);
+    *f = value;
+  });
+}
+
+int sd_weights_seed_random(const sd_model_spec* spec, uint64_t seed, int mode, int device, sd_weights** out) {
+  return guard([&] {
+    need(out, "out");
+    sd::Spec s = sd::from_abi(spec);
+    auto h = std::make_unique<sd_weights>();
+    h->w = std::make_unique<sd::Weights>(s, mode, seed, device, sd::Weights::SeedRandom{});
+    *out = h.release();
+  });
+}
+
+int sd_weights_export_embedding(const sd_weights* w, float* host, size_t count) {
+  return guard([&] {
+    need(w, "weights");
+    need(host, "host");
+    const sd::Spec& s = w->w->spec();
+    const size_t n = static_cast<size_t>(s.D) * s.V;
+    if (count < n) sd::fail(SD_ERR_CONFIG, "export_embedding: buffer holds fewer than model_dim * vocab floats");
+    sd::DeviceGuard dg(w->w->device());
+    SD_CUDA(cudaMemcpy(host, w->w->embedding(), n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
 int sd_weights_synthetic(const sd_model_spec* spec, int mode, uint64_t seed, int device,
                          sd_weights** out) {
   return guard([&] {
@@ -571,7 +612,6 @@ int sd_dist_create(sd_weights* w, sd_kv* kv, int rank, int world, const void* nc
   return guard([&] {
     need(kv, "kv");
     need(out, "out");
-    if (world > 1) need(nccl_id, "nccl_id");
     auto h = std::make_unique<sd_dist>();
     h->d = std::make_unique<sd::DistEngine>(w ? w->w.get() : nullptr, kv->s.get(), rank, world, nccl_id,
                                             s_ranks, shard_mode);

@@ -1,6 +1,8 @@
 // Internal shared definitions for libsd_b200 (host C++ and CUDA).
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -71,9 +73,49 @@ __host__ __device__ inline uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// Process-wide tuning switches (sd_tune in sd_abi.h). The defaults are the
+// measured-best paths; A/B measurements and the variant-equivalence tests
+// flip them. Read on the host when a launch is planned.
+struct Tuning {
+  int gemm_bn = 0;       // force the pair-tile width (16 | bn, 64..256); 0 = the wave cost model
+  int gemm_pair = 1;     // 0: single-CTA tiles even when M spans two 128-row blocks
+  int fused_append = 1;  // append_lane in the QKV GEMM epilogue (lockstep fp16 pages)
+  int fused_argmax = 1;  // argmax_token in the head GEMM epilogue
+  int dist_fuse = 1;     // multi-GPU exchange fused into its producers (else a scatter kernel)
+  int attn_mma = 1;      // tensor-core attention where the geometry allows it
+  int pdl = 1;           // programmatic dependent launch between the step's kernels
+  int dist_phases = 0;   // per-phase CUDA events in DistEngine, printed to stderr at destroy
+};
+inline Tuning& tuning() {
+  static Tuning t;
+  return t;
+}
+
+// Bits of a 16-bit activation copy (bf16 or fp16 per the S-Part's dense mode).
+using act16 = uint16_t;
+
+// The 16-bit copy of an activation that a kind::f16 GEMM reads as its A
+// operand: bf16, or fp16 when the S-Part runs fp16 operands; RNE either way.
+__device__ __forceinline__ uint16_t to16(float x, int f16) {
+  return f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+__device__ __forceinline__ uint32_t pack16x2(float lo, float hi, int f16) {
+  return static_cast<uint32_t>(to16(lo, f16)) | (static_cast<uint32_t>(to16(hi, f16)) << 16);
+}
+
 // Counter-based synthetic value in [-1, 1) (SURVEY §8d bench prefill)
 __host__ __device__ inline float synth_value(uint64_t idx) {
   return 2.0f * (static_cast<float>(mix64(0x5EEDull ^ idx) >> 40) * 0x1p-24f) - 1.0f;
+}
+
+// Element index of the synthetic KV prefill: sequence id,
+// layer (< 4096), position (< 2^20), K (0) / V (1), global kv head h of
+// Hkv, element d of hd. Shard- and slot-independent.
+__host__ __device__ inline uint64_t kv_prefill_index(uint64_t seq, int layer, int pos, int kv, int h, int d,
+                                                     int kv_heads_total, int hd) {
+  return ((((seq * 4096u + static_cast<uint64_t>(layer)) * 1048576u + static_cast<uint64_t>(pos)) * 2u +
+           static_cast<uint64_t>(kv)) * static_cast<uint64_t>(kv_heads_total) + static_cast<uint64_t>(h)) *
+             static_cast<uint64_t>(hd) + static_cast<uint64_t>(d);
 }
 
 // Device scratch buffer that only grows.

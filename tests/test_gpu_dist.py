@@ -28,7 +28,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence"):
+def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence", drain=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -37,29 +37,37 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mo
     import oracle as o
     import paper_2403_11421_b200 as sd
     from conftest import upload_oracle_weights
-    torch.cuda.set_device(rank)
+    # "p2p-one-device": every rank on cuda:0, no NCCL communicator; the
+    # exchange and the next-token gather run as CUDA-IPC peer stores
+    dev = 0 if exchange == "p2p-one-device" else rank
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    obj = [sd.nccl_unique_id() if rank == 0 else None]
+    obj = [sd.nccl_unique_id() if rank == 0 and exchange != "p2p-one-device" else None]
     dist.broadcast_object_list(obj, src=0)
     W = o.Weights(o.make_spec(2, 64, 4, 256, 128), 0)
     is_s = s_ranks == world or rank == 0
-    dw = upload_oracle_weights(W, "exact", device=rank) if is_s else None
+    dw = upload_oracle_weights(W, "exact", device=dev) if is_s else None
     spec = sd.make_model_spec(2, 64, 4, 256, 128)
     if shard_mode == "sequence":
         h0, hc = 0, 4
     else:
         h0, hc = sd.ShardMap(shard_mode, 4, world).head_range(rank)
-    kv = sd.KvShard(spec, h0, hc, 1 << 16, "single", rank)
+    kv = sd.KvShard(spec, h0, hc, 1 << 16, "single", dev)
     eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks, shard_mode=shard_mode)
-    if exchange == "p2p":
+    if exchange.startswith("p2p"):
         eng.enable_p2p(64)
     recs, acts, _ = sd.run_generation(eng, *cfg, seed=0, record_activations=True)
     rows = [(r, acts[i].tolist()) for i, r in enumerate(recs)]
-    allr = [None] * world
+    # after a run to completion every sequence has retired on every rank
+    # that stores it (DROP_SEQ to all links outside by-sequence sharding,
+    # workers.cpp:482-501)
+    left = (kv.token_count(), kv.warning_count()) if drain else None
+    allr, alll = [None] * world, [None] * world
     dist.all_gather_object(allr, rows)
+    dist.all_gather_object(alll, left)
     if rank == 0:
         with open(out_path, "wb") as f:
-            pickle.dump([x for part in allr for x in part], f)
+            pickle.dump(([x for part in allr for x in part], alll), f)
     eng.close()
     dist.destroy_process_group()
 
@@ -77,7 +85,11 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
     mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode), nprocs=2, join=True)
-    rows = pickle.load(open(out, "rb"))
+    _check_rows(oracle, out, cfg)
+
+
+def _check_rows(oracle, out, cfg):
+    rows, left = pickle.load(open(out, "rb"))
     W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 128), 0)
     orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
     ref = {(s, q): (t, oacts[i]) for i, (s, q, t) in enumerate(orecs)}
@@ -88,6 +100,7 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
         assert t == rt
         worst = max(worst, float(np.abs(np.asarray(x, np.float32) - rx).max()))
     assert worst <= 1e-5
+    return left
 
 
 def _fused_worker(rank, world, port, out_path, s_ranks):
@@ -107,18 +120,13 @@ def _fused_worker(rank, world, port, out_path, s_ranks):
     homes = ("affinity", "modulo") if s_ranks == world else ("affinity",)
     for home_policy in homes:
         for fused in (True, False):
-            if fused:
-                os.environ.pop("SD_DIST_NO_FUSE", None)
-            else:
-                os.environ["SD_DIST_NO_FUSE"] = "1"
+            sd.tune("dist_fuse", int(fused))
             obj = [sd.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             is_s = s_ranks == world or rank == 0
             w = sd.DeviceWeights(spec, None, "bf16", rank, seed=5) if is_s else None
             plan = sd.dist_plan(world, rank, s_ranks, seqs, home=home_policy)
-            # the synthetic prefill is keyed by KV slot: allocate slots in sequence
-            # order so both placements hold the same context per sequence
-            mine = sorted(seqs[i] for i in plan["shard_rows"])
+            mine = [seqs[i] for i in plan["shard_rows"]]  # prefill is sequence-keyed
             kv = sd.KvShard(spec, 0, 2, 96 * 64, "half", rank, max_sequences=96, max_seq_len=64)
             kv.prefill_synthetic(mine, 20, salt=0)
             eng = sd.DistEngine(w, kv, rank, world, obj[0], s_ranks, home=home_policy)
@@ -180,3 +188,22 @@ def test_two_gpu_fused_exchange_is_bitwise_equal(tmp_path, s_ranks):
     out = str(tmp_path / "fused.txt")
     mp.spawn(_fused_worker, args=(2, _free_port(), out, s_ranks), nprocs=2, join=True)
     assert open(out).read() == "ok"
+
+
+@pytest.mark.skipif(_ngpus() < 1, reason="needs a GPU")
+@pytest.mark.parametrize("s_ranks", [1, 2])
+@pytest.mark.parametrize("shard_mode", ["sequence", "head", "hybrid"])
+def test_two_ranks_one_device_distributed_equals_monolithic(oracle, tmp_path, s_ranks, shard_mode):
+    """DistributedComputation with two ranks on ONE device (two processes,
+    no NCCL: the per-layer Q/K/V and O exchange and the next-token gather are
+    CUDA-IPC peer stores with epoch flags), run to completion: tokens equal
+    the monolithic oracle's, activations <= 1e-5 (test_workers.cpp:280-321),
+    and every rank's shard is empty afterwards with no drop warnings, in all
+    three ShardMap modes (retire routing, workers.cpp:482-501)."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rows.pkl")
+    cfg = (8, 16, 4, 0)
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True),
+             nprocs=2, join=True)
+    left = _check_rows(oracle, out, cfg)
+    assert left == [(0, 0), (0, 0)]

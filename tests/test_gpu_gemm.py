@@ -23,6 +23,10 @@ def sd():
     return m
 
 
+def fp16(x):
+    return np.ascontiguousarray(x, np.float32).astype(np.float16).astype(np.float32)
+
+
 def bf16(x):
     u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
     u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
@@ -37,7 +41,7 @@ def tf32(x):
 
 
 def _ref(x, wT, mode):
-    r = bf16 if mode == "bf16" else tf32
+    r = {"bf16": bf16, "fp16": fp16, "tf32": tf32}[mode]
     xe, we = r(x).astype(np.float64), r(wT).astype(np.float64)
     return xe @ we, np.abs(xe) @ np.abs(we)
 
@@ -45,7 +49,7 @@ def _ref(x, wT, mode):
 SHAPES = [(2, 64, 4, 256, 128), (1, 512, 8, 1024, 1000), (1, 256, 2, 512, 300)]
 
 
-@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+@pytest.mark.parametrize("mode", ["bf16", "fp16", "tf32"])
 @pytest.mark.parametrize("shape", SHAPES, ids=["toy", "d512", "d256"])
 @pytest.mark.parametrize("B", [1, 3, 130, 257])
 def test_linear_matches_rounded_reference(sd, oracle, mode, shape, B):
@@ -58,11 +62,11 @@ def test_linear_matches_rounded_reference(sd, oracle, mode, shape, B):
         y = sd.apply_linear(dw, 0, which, x)
         wT = W.tensor(name).T  # (in, out)
         ref, scale = _ref(x, wT, mode)
-        tol = 2e-5 if mode == "bf16" else 1e-3  # tf32: rounding mode of operands unspecified
+        tol = 1e-3 if mode == "tf32" else 2e-5  # tf32: rounding mode of operands unspecified
         assert np.all(np.abs(y - ref) <= tol * scale + 1e-6), (which, float(np.abs(y - ref).max()))
 
 
-@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+@pytest.mark.parametrize("mode", ["bf16", "fp16", "tf32"])
 def test_fused_epilogues(sd, oracle, mode):
     W = oracle.Weights(oracle.make_spec(1, 512, 8, 1024, 64), 5)
     dw = upload_oracle_weights(W, mode)
@@ -71,11 +75,11 @@ def test_fused_epilogues(sd, oracle, mode):
     res = rng.uniform(-1, 1, (77, 512)).astype(np.float32)
     got = sd.finish_block(dw, 0, o, res)
     exact = oracle.finish_block(W, 0, o, res)
-    rel = 2.0**-7 if mode == "bf16" else 2.0**-9
+    rel = 2.0**-7 if mode == "bf16" else 2.0**-9  # fp16 / tf32: 11-bit significands
     assert np.abs(got - exact).max() <= rel * max(1.0, float(np.abs(exact).max()))
 
 
-@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+@pytest.mark.parametrize("mode", ["bf16", "fp16", "tf32"])
 def test_golden_transcript_tensor_core_modes(sd, oracle, mode):
     """The reference transcript survives tensor-core operand rounding
     (SURVEY §0 finding 2: minimum top-1/top-2 logit margin 4.3e-3)."""
@@ -88,47 +92,63 @@ def test_golden_transcript_tensor_core_modes(sd, oracle, mode):
         assert sd.transcript_csv(recs) == f.read()
 
 
-@pytest.mark.parametrize("kind", ["bf16", "tf32"])
+@pytest.mark.parametrize("kind", ["bf16", "fp16", "tf32"])
 @pytest.mark.parametrize("M,N,K", [(512, 1024, 512), (300, 640, 256), (1000, 2080, 384), (384, 96, 128)])
-def test_pair_tile_variants_are_bitwise_equal(sd, monkeypatch, kind, M, N, K):
+def test_pair_tile_variants_are_bitwise_equal(sd, kind, M, N, K):
     """Every pair-tile variant accumulates each output over the same K
-    sequence of MMAs: one or two swizzle atoms per stage (the 128 / 192 / 256
-    instantiations picked by tile width), tile widths 112 / 176 / 208, and the
-    512-row tile (two 256-row accumulators per CTA pair sharing every B stage,
-    SD_GEMM_MB=2). Outputs are bitwise equal for every epilogue (plain,
-    residual + bf16 copy, SiLU), ragged M included, and match the rounded
-    reference."""
+    sequence of MMAs: the 128 / 192 / 256 instantiations picked by tile width
+    (tile widths 112 / 176 / 208 and the cost model's choice), and single-CTA
+    tiles. Outputs are bitwise equal for every epilogue (plain, residual +
+    16-bit copy, SiLU), ragged M included, and match the rounded reference."""
     import torch
     dev = torch.device("cuda")
     g = torch.Generator(device="cpu").manual_seed(M + N + K)
-    dt = torch.bfloat16 if kind == "bf16" else torch.float32
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "tf32": torch.float32}[kind]
+    cdt = torch.float16 if kind == "fp16" else torch.bfloat16
     A = (torch.rand(M, K, generator=g) * 2 - 1).to(dt).to(dev)
     B = ((torch.rand(N, K, generator=g) * 2 - 1) / K**0.5).to(dt).to(dev)
     res = (torch.rand(M, N, generator=g) * 2 - 1).to(dev)
-    variants = [{}, {"SD_GEMM_ATOMS2": "1"}, {"SD_GEMM_MB": "2"}]
-    variants += [{"SD_GEMM_BN": str(bn), **v} for bn in (112, 176, 208) for v in ({}, {"SD_GEMM_ATOMS2": "1"})]
+    variants = [{}] + [{"gemm_bn": bn} for bn in (112, 176, 208)]
     outs = []
-    for env in variants:
-        for k in ("SD_GEMM_ATOMS2", "SD_GEMM_MB", "SD_GEMM_BN"):
-            monkeypatch.delenv(k, raising=False)
-        monkeypatch.setenv("SD_GEMM_PAIR", "1")
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        C0 = torch.empty(M, N, device=dev)
-        C1 = torch.empty(M, N, device=dev)
-        Cb1 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-        C2 = torch.empty(M, N, device=dev)
-        sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C0.data_ptr(), N)
-        sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C1.data_ptr(), N, Cb1.data_ptr(), N,
-                    epi=1, res=res.data_ptr(), ldr=N)
-        sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C2.data_ptr(), N, epi=2)
-        torch.cuda.synchronize()
-        outs.append([t.cpu() for t in (C0, C1, Cb1, C2)])
+    for tv in variants:
+        with sd.tuned(**tv):
+            C0 = torch.empty(M, N, device=dev)
+            C1 = torch.empty(M, N, device=dev)
+            Cb1 = torch.empty(M, N, device=dev, dtype=cdt)
+            C2 = torch.empty(M, N, device=dev)
+            sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C0.data_ptr(), N)
+            sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C1.data_ptr(), N, Cb1.data_ptr(), N,
+                        epi=1, res=res.data_ptr(), ldr=N)
+            sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C2.data_ptr(), N, epi=2)
+            torch.cuda.synchronize()
+            outs.append([t.cpu() for t in (C0, C1, Cb1, C2)])
     for o in outs[1:]:
         for a, b in zip(outs[0], o):
-            assert torch.equal(a.view(torch.int16) if a.dtype == torch.bfloat16 else a.view(torch.int32),
-                               b.view(torch.int16) if b.dtype == torch.bfloat16 else b.view(torch.int32))
+            assert torch.equal(a.view(torch.int16) if a.element_size() == 2 else a.view(torch.int32),
+                               b.view(torch.int16) if b.element_size() == 2 else b.view(torch.int32))
+    # the 16-bit copy is the RNE conversion of the fp32 result
+    assert torch.equal(outs[0][2].view(torch.int16), outs[0][1].to(cdt).view(torch.int16))
     ref = A.float().cpu().double() @ B.float().cpu().double().T
     scale = A.float().cpu().double().abs() @ B.float().cpu().double().abs().T
-    tol = 2e-5 if kind == "bf16" else 1e-3
+    tol = 1e-3 if kind == "tf32" else 2e-5
     assert bool(((outs[0][0].double() - ref).abs() <= tol * scale + 1e-6).all())
+
+
+@pytest.mark.parametrize("kind", ["bf16", "fp16", "tf32"])
+def test_single_cta_tiles_match_pair_tiles(sd, kind):
+    """gemm_pair=0 (single-CTA 128-row tiles) against the CTA-pair tiles: the
+    same MMAs per output, bitwise equal."""
+    import torch
+    M, N, K = 640, 1536, 512
+    g = torch.Generator(device="cpu").manual_seed(11)
+    dt = {"bf16": torch.bfloat16, "fp16": torch.float16, "tf32": torch.float32}[kind]
+    A = (torch.rand(M, K, generator=g) * 2 - 1).to(dt).cuda()
+    B = ((torch.rand(N, K, generator=g) * 2 - 1) / K**0.5).to(dt).cuda()
+    outs = []
+    for pair in (1, 0):
+        with sd.tuned(gemm_pair=pair):
+            C = torch.empty(M, N, device="cuda")
+            sd.gemm_dev(kind, M, N, K, A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N)
+            torch.cuda.synchronize()
+            outs.append(C.cpu())
+    assert torch.equal(outs[0].view(torch.int32), outs[1].view(torch.int32))

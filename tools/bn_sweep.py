@@ -14,9 +14,7 @@ dev = torch.device("cuda")
 
 
 def timed(N, K, bn):
-    os.environ.pop("SD_GEMM_BN", None)
-    if bn:
-        os.environ["SD_GEMM_BN"] = str(bn)
+    sd.tune("gemm_bn", bn)  # 0: the wave cost model
     nbuf = max(2, int(192e6 // (N * K * 2)) + 1)
     A = (torch.rand(M, K, device=dev) * 2 - 1).to(torch.bfloat16)
     Bs = [((torch.rand(N, K, device=dev) * 2 - 1) / K**0.5).to(torch.bfloat16) for _ in range(nbuf)]

@@ -4,7 +4,7 @@ cannot follow a multi-rank job:
 
   ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm \
       --csv python tools/dist1_probe.py
-  SD_DIST_NO_FUSE=1 ... (the same kernels without the routed epilogue)
+  PROBE_NO_FUSE=1 ... (the same kernels without the routed epilogue)
 """
 import os
 import sys
@@ -18,6 +18,8 @@ import paper_2403_11421_b200 as sd  # noqa: E402
 
 def main():
     B = int(os.environ.get("PROBE_B", "512"))
+    if os.environ.get("PROBE_NO_FUSE"):
+        sd.tune("dist_fuse", 0)
     ctx = int(os.environ.get("PROBE_CTX", "64"))
     spec = sd.make_model_spec(32, 4096, 32, 14336, 128256, 8)
     w = sd.DeviceWeights(spec, None, "bf16", 0, seed=0)
