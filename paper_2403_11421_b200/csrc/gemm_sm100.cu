@@ -926,21 +926,15 @@ int pick_pair_bn(int mgroups, int N, int pairs) {
   return best;
 }
 
-// Kernel attributes are set once per instantiation (first launch).
-template <typename K>
-void set_smem_once(K* kern, size_t smem) {
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  });
-}
-
 template <int BN, bool PAIR, int ATOMS, int KIND>
 void launch(const GemmArgs& g, int cs, int bn, cudaStream_t s) {
   using C_ = Cfg<BN, PAIR, ATOMS>;
   auto* kern = gemm_kernel<BN, PAIR, ATOMS, KIND>;
-  set_smem_once(kern, C_::SMEM);
+  static std::once_flag attrs;  // one per instantiation: the attributes are set at its first launch
+  std::call_once(attrs, [&] {
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C_::SMEM)));
+    SD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  });
   if (PAIR) cs = 2;
   if (!PAIR) bn = BN;
   if (bn < 16 || bn > BN || (PAIR && bn % 16)) fail(SD_ERR_CONFIG, "gemm: bad tile width");

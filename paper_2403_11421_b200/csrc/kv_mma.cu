@@ -9,9 +9,12 @@
 // K rows are the A operand (ldmatrix), V rows the transposed A operand
 // (ldmatrix.trans); Q^T is a register-resident B operand; P^T is built from
 // the S^T accumulators with movmatrix.trans. fp16 K/V are exact tensor-core
-// operands; q and p are split into fp16 hi + lo parts (two MMAs each), so the
-// products carry ~22 significant bits — fp32-level agreement with the
-// reference's fp32 attend (attention.cpp:204-282), not fp16 rounding.
+// operands; q and p are split into fp16 hi + lo parts, so the products carry
+// ~22 significant bits — fp32-level agreement with the reference's fp32
+// attend (attention.cpp:204-282), not fp16 rounding. With G <= 4 query heads
+// per kv head the hi and lo parts share one MMA: hi in N columns [0, G), lo
+// in [G, 2G) (an m16n8 tile has 8 columns), summed by one lane shuffle — half
+// the MMAs of issuing them separately.
 //
 // Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
@@ -145,6 +148,9 @@ template <int G, int FMT, int RPS>
 __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
   static_assert(!I8 || RPS == 2, "int8 fragments assume pair slots");
+  // hi / lo parts of q and p packed into the N columns of one MMA
+  constexpr bool PACK = 2 * G <= 8;
+  constexpr int XG = G / 2;  // lane xor between a column's hi and lo holders
   constexpr int NS = kT / RPS;  // slots per K (V) half of a stage
   extern __shared__ __align__(128) uint8_t smem[];
   const int nst = a.nstages;
@@ -248,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
   const int hk = warp % g.hc, cls = warp / g.hc;
   int jst = 0;  // stage sequence number (same order as the producer)
   const int gq = lane >> 2, tq = lane & 3;
+  const bool lo_role = PACK && (tq & XG) != 0;  // this lane's columns carry lo parts
   const int Hq = g.hc * G;
   float o[8][4];      // O^T fragments: hd rows 16*mt + {gq, gq+8}, heads {2tq, 2tq+1}
   float m[2], l[2];   // per head 2tq, 2tq+1 (replicated over gq lanes; l partial per lane)
@@ -269,8 +276,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           // int8 K fragments take 4 contiguous d per lane (a permutation of
           // the dot's k index); Q^T uses the same permutation
           const int d = I8 ? 16 * kk + 4 * tq + 2 * h : 16 * kk + 8 * h + 2 * tq;
-          if (gq < G) x = *reinterpret_cast<const float2*>(qrow + gq * kHD + d);
+          const int hq = PACK && gq >= G ? gq - G : gq;  // PACK: column gq >= G is head gq - G's lo part
+          if (hq < G && gq < (PACK ? 2 * G : G)) x = *reinterpret_cast<const float2*>(qrow + hq * kHD + d);
           split2(x.x * a.qscale, x.y * a.qscale, qb[kk][h][0], qb[kk][h][1]);
+          if (PACK && gq >= G) qb[kk][h][0] = qb[kk][h][1];  // the MMA's B column gets the lo part
         }
       }
     }
@@ -309,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
                                   i8x2_to_h2(w1, 0x5342)};
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
-          mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+          if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
         // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
@@ -342,8 +351,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           const int mr = lr + 8 * (lm & 1);  // MMA row: slot mr % NS, row mr / NS of the slot
           ldsm_x4(Ks + (mr % NS) * ppitch + (mr / NS) * g.pos_bytes + (16 * kk + 8 * (lm >> 1)) * 2, ka);
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
-          mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+          if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
+      }
+      if (PACK) {  // hi + lo columns: every lane of the pair holds the full score
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], XG);
       }
       // s[0], s[1]: (pos gq, heads 2tq, 2tq+1); s[2], s[3]: (pos gq+8, ...)
       // positions of MMA rows gq and gq + 8 (slot-major: row r is position (r % NS) * RPS + r / NS)
@@ -382,8 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       uint32_t h01, l01, h23, l23;
       split2(p0 * vs0, p1 * vs0, h01, l01);  // (pos gq, heads 2tq..): rows = pos
       split2(p2 * vs1, p3 * vs1, h23, l23);  // (pos gq+8, ...)
+      if (lo_role) {  // PACK: this lane's columns take the lo parts
+        h01 = l01;
+        h23 = l23;
+      }
       const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
-      const uint32_t bl0 = movm_t(l01), bl1 = movm_t(l23);
+      const uint32_t bl0 = PACK ? 0u : movm_t(l01), bl1 = PACK ? 0u : movm_t(l23);
       // ---- O^T += V^T . P^T  (8 tiles of 16 head-dims)
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         const uint32_t vaddr = vpitch ? Vs + vrow * vpitch : Vs + (vrow % NS) * ppitch + (vrow / NS) * g.pos_bytes;
         ldsm_x4_t(vaddr + (16 * mt + 8 * (lm & 1)) * 2, va);
         mma16816(o[mt], va, bh0, bh1);
-        mma16816(o[mt], va, bl0, bl1);
+        if (!PACK) mma16816(o[mt], va, bl0, bl1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -404,6 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
 
     // ---- finalize: full row sums, then direct output or partial
+    if (PACK) {  // O^T columns [G, 2G) hold V . P_lo: add them to the hi columns
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[mt][i] += __shfl_xor_sync(0xffffffffu, o[mt][i], XG);
+    }
 #pragma unroll
     for (int sh = 4; sh < 32; sh <<= 1) {
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], sh);
