@@ -295,6 +295,13 @@ int sd_nccl_unique_id(void* out, size_t bytes);
 int sd_dist_create(sd_weights* weights_or_null, sd_kv* kv, int rank, int world,
                    const void* nccl_id, int s_ranks, int shard_mode, sd_dist** out);
 int sd_dist_destroy(sd_dist* d);
+/* The reference's two interleaved mini-batches (DistributedComputation with
+ * pipelined_ = true, workers.cpp:405-452): rows split by seq % 2 (merged
+ * when one side is empty); per layer and mini-batch every rank runs its
+ * shard's attention, then the S-Part of that mini-batch's home rows and its
+ * next QKV, so one mini-batch's R-Part overlaps the other's S-Part across
+ * ranks. With world > 1 it needs the peer exchange (connected first). */
+int sd_dist_pipeline(sd_dist* d, int enable);
 int sd_dist_step(sd_dist* d, int32_t B, const uint64_t* seqs, const int32_t* tokens,
                  int32_t* next_tokens, float* final_x);
 int sd_dist_retire(sd_dist* d, int32_t n, const uint64_t* seqs);
@@ -307,7 +314,7 @@ int sd_dist_timing(sd_dist* d, int enable);
 int sd_dist_timing_read(sd_dist* d, double* exchange_ms, double* exchange_bytes, int reset);
 /* Peer-memory exchange over NVLink in place of NCCL send/recv (same rows,
  * same order): each rank allocates receive buffers for up to `max_rows`
- * rows and writes SD_DIST_IPC_BYTES of CUDA IPC handles; after every rank's
+ * rows per mini-batch and writes SD_DIST_IPC_BYTES of CUDA IPC handles; after every rank's
  * handles are gathered (rank order, world * SD_DIST_IPC_BYTES), connect maps
  * the peers' buffers. Every later step scatters rows with direct NVLink
  * stores and an epoch flag per (exchange, source). */

@@ -123,6 +123,7 @@ SIGNATURES = {
     "sd_weights_synthetic": (C.c_int, [SPEC_P, C.c_int, C.c_uint64, C.c_int, PP]),
     "sd_weights_seed_random": (C.c_int, [SPEC_P, C.c_uint64, C.c_int, C.c_int, PP]),
     "sd_tune": (C.c_int, [C.c_char_p, C.c_int]),
+    "sd_dist_pipeline": (C.c_int, [C.c_void_p, C.c_int]),
     "sd_weights_export_embedding": (C.c_int, [C.c_void_p, FP, C.c_size_t]),
     "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_drive_count": (C.c_int64, [P]),

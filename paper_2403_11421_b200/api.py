@@ -547,6 +547,11 @@ class DistEngine:
                                 _fp(fx) if fx is not None else None))
         return nxt, fx
 
+    def pipeline(self, enable: bool):
+        """The reference's two interleaved mini-batches (seq % 2,
+        workers.cpp:405-452); needs enable_p2p first when world > 1."""
+        _check(lib.sd_dist_pipeline(self.h, int(enable)))
+
     def retire(self, seqs):
         s, sp = _u64(seqs)
         _check(lib.sd_dist_retire(self.h, len(s), sp))

@@ -166,6 +166,7 @@ void make_plan(int world, int rank, int s_ranks, int B, const uint64_t* seqs, Di
   }
 }
 
+
 DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void* nccl_id, int s_ranks,
                        int shard_mode)
     : spec_(kv->spec()), w_(w), kv_(kv), rank_(rank), world_(world), s_ranks_(s_ranks),
@@ -196,6 +197,21 @@ DistEngine::DistEngine(Weights* w, KvStore* kv, int rank, int world, const void*
   }
 }
 
+void DistEngine::free_group(Group& G) {
+  for (void* p : {static_cast<void*>(G.x), static_cast<void*>(G.qkv_h), static_cast<void*>(G.qkv_s),
+                  static_cast<void*>(G.o_s), static_cast<void*>(G.o_h), static_cast<void*>(G.y),
+                  static_cast<void*>(G.h), static_cast<void*>(G.logits), static_cast<void*>(G.xb),
+                  static_cast<void*>(G.ob), static_cast<void*>(G.yb), static_cast<void*>(G.hb),
+                  static_cast<void*>(G.tok), static_cast<void*>(G.home_idx), static_cast<void*>(G.amax)}) {
+    if (p) cudaFree(p);
+  }
+  G.x = G.qkv_h = G.qkv_s = G.o_s = G.o_h = G.y = G.h = G.logits = nullptr;
+  G.xb = G.ob = G.yb = G.hb = nullptr;
+  G.tok = G.home_idx = nullptr;
+  G.amax = nullptr;
+  G.cap = 0;
+}
+
 DistEngine::~DistEngine() {
   DeviceGuard dg(device_);
   cudaStreamSynchronize(stream_);
@@ -206,7 +222,7 @@ DistEngine::~DistEngine() {
     }
   }
   if (phases_ && ph_layers_) {
-    static const char* names[] = {"", "qkv", "recv_qkv", "append", "attend", "recv_o", "to_bf16", "w_o", "mlp_in", "mlp_out"};
+    static const char* names[] = {"", "qkv", "recv_qkv", "append", "attend", "recv_o", "to_16", "w_o", "mlp_in", "mlp_out"};
     std::string line = "[dist phases] rank " + std::to_string(rank_) + ", " + std::to_string(ph_layers_) +
                        " layers, ms/layer:";
     for (int i = 1; i < 10; ++i) {
@@ -219,19 +235,12 @@ DistEngine::~DistEngine() {
   }
   for (void* p : opened_) cudaIpcCloseMemHandle(p);
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
-                  static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_)}) {
+                  static_cast<void*>(done_), static_cast<void*>(gemm_done_), static_cast<void*>(attn_done_),
+                  static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_), static_cast<void*>(all_tok_)}) {
     if (p) cudaFree(p);
   }
   if (comm_) Nccl::get().CommDestroy(comm_);
-  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_h_), static_cast<void*>(qkv_s_),
-                  static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
-                  static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
-                  static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_),
-                  static_cast<void*>(amax_)}) {
-    if (p) cudaFree(p);
-  }
+  for (Group& G : groups_) free_group(G);
   for (auto& e : ev_) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -239,98 +248,137 @@ DistEngine::~DistEngine() {
   cudaStreamDestroy(stream_);
 }
 
+void DistEngine::set_pipeline(bool on) {
+  if (on && world_ > 1 && !p2p_) {
+    fail(SD_ERR_CONFIG, "two mini-batches across ranks need the peer exchange (sd_dist_p2p_connect)");
+  }
+  pipelined_ = on;
+  plan_key_.clear();
+}
+
 void DistEngine::ensure(int B) {
   if (B <= cap_) return;
   DeviceGuard dg(device_);
   SD_CUDA(cudaStreamSynchronize(stream_));
-  for (void* p : {static_cast<void*>(x_), static_cast<void*>(qkv_h_), static_cast<void*>(qkv_s_),
-                  static_cast<void*>(o_s_), static_cast<void*>(o_h_), static_cast<void*>(y_),
-                  static_cast<void*>(h_), static_cast<void*>(logits_), static_cast<void*>(xb_),
-                  static_cast<void*>(ob_), static_cast<void*>(yb_), static_cast<void*>(hb_),
-                  static_cast<void*>(tok_), static_cast<void*>(all_tok_), static_cast<void*>(home_idx_),
-                  static_cast<void*>(amax_)}) {
-    if (p) cudaFree(p);
-  }
+  if (all_tok_) cudaFree(all_tok_);
+  all_tok_ = nullptr;
   const size_t bp = (static_cast<size_t>(B) + 127) / 128 * 128;
   const Spec& s = spec_;
-  auto zalloc = [&](void** p, size_t bytes) {
-    SD_CUDA(cudaMalloc(p, bytes));
+  auto zalloc = [&](auto** p, size_t bytes) {
+    SD_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
     SD_CUDA(cudaMemset(*p, 0, bytes));
   };
-  zalloc(reinterpret_cast<void**>(&x_), bp * s.D * 4);
-  zalloc(reinterpret_cast<void**>(&qkv_h_), bp * s.qkv_width() * 4);
-  zalloc(reinterpret_cast<void**>(&qkv_s_), bp * s.qkv_width() * 4);
-  zalloc(reinterpret_cast<void**>(&o_s_), bp * s.D * 4);
-  zalloc(reinterpret_cast<void**>(&o_h_), bp * s.D * 4);
-  zalloc(reinterpret_cast<void**>(&y_), bp * s.D * 4);
-  zalloc(reinterpret_cast<void**>(&h_), bp * s.F * 4);
-  zalloc(reinterpret_cast<void**>(&logits_), bp * s.V * 4);
-  zalloc(reinterpret_cast<void**>(&xb_), bp * s.D * 2);
-  zalloc(reinterpret_cast<void**>(&ob_), bp * s.D * 2);
-  zalloc(reinterpret_cast<void**>(&yb_), bp * s.D * 2);
-  zalloc(reinterpret_cast<void**>(&hb_), bp * s.F * 2);
-  zalloc(reinterpret_cast<void**>(&tok_), bp * 4);
-  zalloc(reinterpret_cast<void**>(&all_tok_), bp * 4);
-  zalloc(reinterpret_cast<void**>(&home_idx_), bp * 4);
-  zalloc(reinterpret_cast<void**>(&amax_), bp * 8);
+  for (Group& G : groups_) {  // either mini-batch may hold the whole batch (merged)
+    free_group(G);
+    zalloc(&G.x, bp * s.D * 4);
+    zalloc(&G.qkv_h, bp * s.qkv_width() * 4);
+    zalloc(&G.qkv_s, bp * s.qkv_width() * 4);
+    zalloc(&G.o_s, bp * s.D * 4);
+    zalloc(&G.o_h, bp * s.D * 4);
+    zalloc(&G.y, bp * s.D * 4);
+    zalloc(&G.h, bp * s.F * 4);
+    zalloc(&G.logits, bp * s.V * 4);
+    zalloc(&G.xb, bp * s.D * 2);
+    zalloc(&G.ob, bp * s.D * 2);
+    zalloc(&G.yb, bp * s.D * 2);
+    zalloc(&G.hb, bp * s.F * 2);
+    zalloc(&G.tok, bp * 4);
+    zalloc(&G.home_idx, bp * 4);
+    zalloc(&G.amax, bp * 8);
+    G.cap = B;
+  }
+  zalloc(&all_tok_, bp * 4);
   SD_CUDA(cudaDeviceSynchronize());  // legacy-stream memsets before non-blocking-stream use
   cap_ = B;
 }
 
+// Mini-batches (workers.cpp:405-420) and each one's row plan. Every rank
+// derives the same groups and plans from the batch.
 void DistEngine::plan_for(int B, const uint64_t* seqs) {
   if (plan_key_.size() == static_cast<size_t>(B) && std::equal(plan_key_.begin(), plan_key_.end(), seqs)) return;
-  make_plan(world_, rank_, s_ranks_, B, seqs, plan_, mode_ | home_flags_, spec_.Hkv);
-  home_set_.clear();
-  for (int32_t i : plan_.home_rows) home_set_.insert(seqs[i]);
-  if (!plan_.home_rows.empty()) {
-    SD_CUDA(cudaMemcpyAsync(home_idx_, plan_.home_rows.data(), plan_.home_rows.size() * 4, cudaMemcpyHostToDevice,
-                            stream_));
-  }
-  plan_key_.assign(seqs, seqs + B);
   if (mode_ != SD_SHARD_BY_SEQUENCE && !p2p_) {
     fail(SD_ERR_CONFIG, "by-head / hybrid sharding needs the peer exchange (sd_dist_p2p_connect)");
   }
   if (world_ > 1 && !comm_ && !p2p_) {
     fail(SD_ERR_CONFIG, "a distributed engine without an NCCL id needs the peer exchange (sd_dist_p2p_connect)");
   }
-  if (p2p_) {
-    // where this rank's rows land in each peer's receive buffers (every rank
-    // derives every plan from the same batch)
-    peer_qkv_off_.assign(static_cast<size_t>(world_), 0);
-    peer_o_off_.assign(static_cast<size_t>(world_), 0);
-    DistPlan q;
-    for (int d = 0; d < world_; ++d) {
-      make_plan(world_, d, s_ranks_, B, seqs, q, mode_ | home_flags_, spec_.Hkv);
-      peer_qkv_off_[static_cast<size_t>(d)] = q.recv_off[static_cast<size_t>(rank_)];
-      peer_o_off_[static_cast<size_t>(d)] = q.send_off[static_cast<size_t>(rank_)];
-      if (static_cast<int>(q.home_rows.size()) > p2p_cap_ || static_cast<int>(q.shard_rows.size()) > p2p_cap_) {
-        fail(SD_ERR_CAPACITY, "peer exchange: batch exceeds the p2p_setup row capacity");
-      }
-    }
-    if (fused_) build_routes();
+  for (Group& G : groups_) {
+    G.rows.clear();
+    G.seqs.clear();
   }
+  if (pipelined_) {
+    for (int b = 0; b < B; ++b) groups_[seqs[b] % 2].rows.push_back(b);
+  }
+  if (!pipelined_ || groups_[0].rows.empty() || groups_[1].rows.empty()) {
+    groups_[0].rows.resize(static_cast<size_t>(B));
+    std::iota(groups_[0].rows.begin(), groups_[0].rows.end(), 0);
+    groups_[1].rows.clear();
+  }
+  ngroups_ = groups_[1].rows.empty() ? 1 : 2;
+  home_set_.clear();
+  std::vector<int32_t> hidx;
+  for (int g = 0; g < ngroups_; ++g) {
+    Group& G = groups_[g];
+    for (int32_t r : G.rows) G.seqs.push_back(seqs[r]);
+    const int n = static_cast<int>(G.rows.size());
+    make_plan(world_, rank_, s_ranks_, n, G.seqs.data(), G.plan, mode_ | home_flags_, spec_.Hkv);
+    hidx.clear();
+    for (int32_t i : G.plan.home_rows) {
+      home_set_.insert(G.seqs[static_cast<size_t>(i)]);
+      hidx.push_back(G.rows[static_cast<size_t>(i)]);
+    }
+    if (!hidx.empty()) {
+      SD_CUDA(cudaMemcpyAsync(G.home_idx, hidx.data(), hidx.size() * 4, cudaMemcpyHostToDevice, stream_));
+      SD_CUDA(cudaStreamSynchronize(stream_));  // hidx is reused by the next group
+    }
+    G.pos.resize(static_cast<size_t>(n));
+    G.to_shards = G.from_homes = G.to_homes = G.from_shards = 0;
+    for (int d = 0; d < world_; ++d) {
+      if (d == rank_) continue;
+      if (G.plan.send_cnt[static_cast<size_t>(d)] > 0) G.to_shards |= 1u << d, G.from_shards |= 1u << d;
+      if (G.plan.recv_cnt[static_cast<size_t>(d)] > 0) G.from_homes |= 1u << d, G.to_homes |= 1u << d;
+    }
+    if (p2p_) {
+      // where this rank's rows land in each peer's receive region of this
+      // mini-batch (every rank derives every plan from the same batch)
+      G.peer_qkv_off.assign(static_cast<size_t>(world_), 0);
+      G.peer_o_off.assign(static_cast<size_t>(world_), 0);
+      DistPlan q;
+      for (int d = 0; d < world_; ++d) {
+        make_plan(world_, d, s_ranks_, n, G.seqs.data(), q, mode_ | home_flags_, spec_.Hkv);
+        G.peer_qkv_off[static_cast<size_t>(d)] = q.recv_off[static_cast<size_t>(rank_)];
+        G.peer_o_off[static_cast<size_t>(d)] = q.send_off[static_cast<size_t>(rank_)];
+        if (static_cast<int>(q.home_rows.size()) > p2p_cap_ || static_cast<int>(q.shard_rows.size()) > p2p_cap_) {
+          fail(SD_ERR_CAPACITY, "peer exchange: batch exceeds the p2p_setup row capacity");
+        }
+      }
+      if (fused_) build_routes(G);
+    }
+  }
+  plan_key_.assign(seqs, seqs + B);
 }
 
 // device tables of the fused exchange: home row -> (shard rank, row in its
-// receive buffer) and shard row -> (home rank, row in its receive buffer)
-void DistEngine::build_routes() {
-  const size_t nh = plan_.home_rows.size(), ns = plan_.shard_rows.size();
+// receive region) and shard row -> (home rank, row in its receive region)
+void DistEngine::build_routes(Group& G) {
+  const DistPlan& P = G.plan;
+  const size_t nh = P.home_rows.size(), ns = P.shard_rows.size();
   std::vector<int32_t> t(2 * nh + 2 * ns + 1, 0);
   for (int d = 0; d < world_; ++d) {
     const size_t u = static_cast<size_t>(d);
-    for (int j = 0; j < plan_.send_cnt[u]; ++j) {
-      const size_t i = static_cast<size_t>(plan_.send_off[u] + j);
+    for (int j = 0; j < P.send_cnt[u]; ++j) {
+      const size_t i = static_cast<size_t>(P.send_off[u] + j);
       t[i] = d;
-      t[nh + i] = peer_qkv_off_[u] + j;
+      t[nh + i] = G.peer_qkv_off[u] + j;
     }
-    for (int j = 0; j < plan_.recv_cnt[u]; ++j) {
-      const size_t i = static_cast<size_t>(plan_.recv_off[u] + j);
+    for (int j = 0; j < P.recv_cnt[u]; ++j) {
+      const size_t i = static_cast<size_t>(P.recv_off[u] + j);
       t[2 * nh + i] = d;
-      t[2 * nh + ns + i] = peer_o_off_[u] + j;
+      t[2 * nh + ns + i] = G.peer_o_off[u] + j;
     }
   }
-  route_.get(t.size() * 4);
-  SD_CUDA(cudaMemcpy(route_.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+  G.route.get(t.size() * 4);
+  SD_CUDA(cudaMemcpy(G.route.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
 }
 
 void DistEngine::p2p_setup(int max_rows, void* handles_out) {
@@ -339,14 +387,14 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   DeviceGuard dg(device_);
   SD_CUDA(cudaStreamSynchronize(stream_));
   for (void* p : {static_cast<void*>(rx_qkv_), static_cast<void*>(rx_o_), static_cast<void*>(flags_),
-                  static_cast<void*>(done_), static_cast<void*>(gemm_done_),
-                  static_cast<void*>(attn_done_), static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_)}) {
+                  static_cast<void*>(done_), static_cast<void*>(gemm_done_), static_cast<void*>(attn_done_),
+                  static_cast<void*>(rx_ob_), static_cast<void*>(rx_tok_)}) {
     if (p) cudaFree(p);
   }
-  const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;
-  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_qkv_), rows * spec_.qkv_width() * 4));
-  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), rows * spec_.D * 4));
-  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_ob_), rows * spec_.D * 2));
+  const size_t rows = (static_cast<size_t>(max_rows) + 127) / 128 * 128;  // per mini-batch region
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_qkv_), 2 * rows * spec_.qkv_width() * 4));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_o_), 2 * rows * spec_.D * 4));
+  SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_ob_), 2 * rows * spec_.D * 2));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&rx_tok_), 2 * rows * sizeof(int32_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), kFlagSlots * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&done_), sizeof(int32_t)));
@@ -354,26 +402,27 @@ void DistEngine::p2p_setup(int max_rows, void* handles_out) {
   SD_CUDA(cudaMalloc(reinterpret_cast<void**>(&attn_done_), sizeof(int32_t)));
   SD_CUDA(cudaMemset(gemm_done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaMemset(attn_done_, 0, sizeof(int32_t)));
-  SD_CUDA(cudaMemset(rx_qkv_, 0, rows * spec_.qkv_width() * 4));
-  SD_CUDA(cudaMemset(rx_o_, 0, rows * spec_.D * 4));
+  SD_CUDA(cudaMemset(rx_qkv_, 0, 2 * rows * spec_.qkv_width() * 4));
+  SD_CUDA(cudaMemset(rx_o_, 0, 2 * rows * spec_.D * 4));
+  SD_CUDA(cudaMemset(rx_ob_, 0, 2 * rows * spec_.D * 2));
   SD_CUDA(cudaMemset(flags_, 0, kFlagSlots * kMaxWorld * sizeof(int64_t)));
   SD_CUDA(cudaMemset(rx_tok_, 0, 2 * rows * sizeof(int32_t)));
   SD_CUDA(cudaMemset(done_, 0, sizeof(int32_t)));
   SD_CUDA(cudaDeviceSynchronize());
-  SD_CUDA(cudaMemset(rx_ob_, 0, rows * spec_.D * 2));
   cudaIpcMemHandle_t h[kIpcHandles];
-  SD_CUDA(cudaIpcGetMemHandle(&h[4], rx_tok_));
   SD_CUDA(cudaIpcGetMemHandle(&h[0], rx_qkv_));
   SD_CUDA(cudaIpcGetMemHandle(&h[1], rx_o_));
   SD_CUDA(cudaIpcGetMemHandle(&h[2], flags_));
   SD_CUDA(cudaIpcGetMemHandle(&h[3], rx_ob_));
+  SD_CUDA(cudaIpcGetMemHandle(&h[4], rx_tok_));
   std::memset(handles_out, 0, kIpcBytes);
   std::memcpy(handles_out, h, sizeof(h));
   const int32_t mode = w_ ? w_->mode() : -1;
   std::memcpy(static_cast<uint8_t*>(handles_out) + sizeof(h), &mode, sizeof(mode));
   p2p_cap_ = max_rows;
+  rx_rows_ = static_cast<int>(rows);
   tok_rows_ = static_cast<int>(rows);
-  epoch_ = 0;
+  steps_run_ = 0;
   tok_epoch_ = 0;
 }
 
@@ -410,66 +459,49 @@ void DistEngine::p2p_connect(const void* all_handles) {
   plan_key_.clear();  // recompute the peer offsets
 }
 
-void DistEngine::exchange_p2p(int kind) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (timing_) {
-    SD_CUDA(cudaEventCreate(&e0));
-    SD_CUDA(cudaEventCreate(&e1));
-    SD_CUDA(cudaEventRecord(e0, stream_));
-  }
-  const int hd = spec_.hd, G = spec_.H / spec_.Hkv, D = spec_.D, kvw = spec_.kv_width();
-  const int my_hc = plan_.head_count[static_cast<size_t>(rank_)], my_h0 = plan_.head_start[static_cast<size_t>(rank_)];
+// the scatter kernel's send of one exchange of mini-batch g (no wait): kind
+// 0 home rows (full q|k|v width) -> each worker's head slice packed as
+// [q slice | k slice | v slice]; kind 1 shard rows (this worker's o slice)
+// -> the home rows' o columns. Publishes `epoch` to every destination.
+void DistEngine::scatter_p2p(int g, int kind, int64_t epoch) {
+  Group& G = groups_[g];
+  const DistPlan& P = G.plan;
+  const int hd = spec_.hd, Gq = spec_.H / spec_.Hkv, D = spec_.D, kvw = spec_.kv_width();
+  const int my_hc = P.head_count[static_cast<size_t>(rank_)], my_h0 = P.head_start[static_cast<size_t>(rank_)];
   P2PScatter a{};
   a.world = world_;
   a.self = rank_;
-  a.slot = kind;
-  a.epoch = ++epoch_;
+  a.slot = slot(kind, g);
+  a.epoch = epoch;
   a.done = done_;
-  const std::vector<int32_t>& sc = kind == 0 ? plan_.send_cnt : plan_.recv_cnt;
-  const std::vector<int32_t>& so = kind == 0 ? plan_.send_off : plan_.recv_off;
-  const std::vector<int32_t>& rc = kind == 0 ? plan_.recv_cnt : plan_.send_cnt;
-  // kind 0: home rows (full q|k|v width) -> each worker's head slice packed
-  //         as [q slice | k slice | v slice];
-  // kind 1: shard rows (this worker's o slice) -> the home rows' o columns
-  a.src = kind == 0 ? qkv_h_ : o_s_;
-  a.src_stride = kind == 0 ? spec_.qkv_width() : static_cast<int64_t>(my_hc) * G * hd;
-  double bytes = 0;
-  uint32_t expect = 0;
+  const std::vector<int32_t>& sc = kind == 0 ? P.send_cnt : P.recv_cnt;
+  const std::vector<int32_t>& so = kind == 0 ? P.send_off : P.recv_off;
+  a.src = kind == 0 ? G.qkv_h : G.o_s;
+  a.src_stride = kind == 0 ? spec_.qkv_width() : static_cast<int64_t>(my_hc) * Gq * hd;
+  const size_t region = static_cast<size_t>(g) * rx_rows_;
   for (int d = 0; d < world_; ++d) {
     const size_t u = static_cast<size_t>(d);
-    const int h0 = plan_.head_start[u], hc = plan_.head_count[u];
+    const int h0 = P.head_start[u], hc = P.head_count[u];
     a.cnt[d] = sc[u];
     a.src_off[d] = so[u];
-    a.dst_off[d] = kind == 0 ? peer_qkv_off_[u] : peer_o_off_[u];
-    a.dst[d] = kind == 0 ? peer_qkv_[d] : peer_o_[d];
+    a.dst_off[d] = kind == 0 ? G.peer_qkv_off[u] : G.peer_o_off[u];
+    a.dst[d] = kind == 0 ? peer_qkv_[d] + region * spec_.qkv_width() : peer_o_[d] + region * D;
     a.flag[d] = peer_flags_[d];
     if (kind == 0) {
-      const int qw = hc * G * hd, kw = hc * hd;
+      const int qw = hc * Gq * hd, kw = hc * hd;
       a.dst_stride[d] = qw + 2 * kw;
       a.nseg[d] = 3;
-      a.seg_src[d][0] = h0 * G * hd, a.seg_dst[d][0] = 0, a.seg_n[d][0] = qw;
+      a.seg_src[d][0] = h0 * Gq * hd, a.seg_dst[d][0] = 0, a.seg_n[d][0] = qw;
       a.seg_src[d][1] = D + h0 * hd, a.seg_dst[d][1] = qw, a.seg_n[d][1] = kw;
       a.seg_src[d][2] = D + kvw + h0 * hd, a.seg_dst[d][2] = qw + kw, a.seg_n[d][2] = kw;
     } else {
       a.dst_stride[d] = D;
       a.nseg[d] = 1;
-      a.seg_src[d][0] = 0, a.seg_dst[d][0] = my_h0 * G * hd, a.seg_n[d][0] = my_hc * G * hd;
+      a.seg_src[d][0] = 0, a.seg_dst[d][0] = my_h0 * Gq * hd, a.seg_n[d][0] = my_hc * Gq * hd;
     }
-    if (d != rank_ && sc[u] > 0) {
-      a.notify |= 1u << d;
-      int w = 0;
-      for (int q = 0; q < a.nseg[d]; ++q) w += a.seg_n[d][q];
-      bytes += static_cast<double>(sc[u]) * w * 4;
-    }
-    if (d != rank_ && rc[u] > 0) expect |= 1u << d;
+    if (d != rank_ && sc[u] > 0) a.notify |= 1u << d;
   }
   launch_p2p_scatter(a, stream_);
-  launch_p2p_wait(flags_, kind, expect, world_, a.epoch, stream_);
-  if (timing_) {
-    SD_CUDA(cudaEventRecord(e1, stream_));
-    ev_.emplace_back(e0, e1);
-    ev_bytes_.push_back(bytes);
-  }
 }
 
 // per-destination grouped send/recv (the scatter of send_layer and the
@@ -516,8 +548,8 @@ void DistEngine::exchange(const float* send, const std::vector<int32_t>& sc, con
 }
 
 // bytes this rank sends to peers in one exchange (kind 0: q|k|v rows, 1: o rows)
-double DistEngine::kind_bytes(int kind) const {
-  const std::vector<int32_t>& sc = kind == 0 ? plan_.send_cnt : plan_.recv_cnt;
+double DistEngine::kind_bytes(const Group& G, int kind) const {
+  const std::vector<int32_t>& sc = kind == 0 ? G.plan.send_cnt : G.plan.recv_cnt;
   const int w = kind == 0 ? spec_.qkv_width() : spec_.D;
   double b = 0;
   for (int d = 0; d < world_; ++d) {
@@ -526,16 +558,16 @@ double DistEngine::kind_bytes(int kind) const {
   return b;
 }
 
-// the receive side of a producer-fused exchange; under timing, the wait is
-// what remains of the exchange once the stores overlapped the producer
-void DistEngine::fused_wait(int slot, uint32_t expect, int64_t epoch, double bytes) {
+// the receive side of a peer exchange; under timing, the wait is what
+// remains of the exchange once the stores overlapped the producers
+void DistEngine::timed_wait(int sl, uint32_t expect, int64_t epoch, double bytes) {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (timing_) {
     SD_CUDA(cudaEventCreate(&e0));
     SD_CUDA(cudaEventCreate(&e1));
     SD_CUDA(cudaEventRecord(e0, stream_));
   }
-  launch_p2p_wait(flags_, slot, expect, world_, epoch, stream_);
+  launch_p2p_wait(flags_, sl, expect, world_, epoch, stream_);
   if (timing_) {
     SD_CUDA(cudaEventRecord(e1, stream_));
     ev_.emplace_back(e0, e1);
@@ -584,141 +616,181 @@ void DistEngine::read_timing(double* ms, double* bytes, bool reset) {
   if (reset) x_ms_ = x_bytes_ = 0;
 }
 
-// one decode step with the home tokens already in tok_ (home order)
+// project_qkv of mini-batch g's home rows for layer l, and send_layer
+// (workers.cpp:324-351): the routed GEMM stores every row into its shard's
+// receive region and publishes the epoch; otherwise the scatter kernel
+// sends (peer exchange) or shard_part's grouped send/recv does (NCCL).
+void DistEngine::layer_in(int g, int l) {
+  Group& G = groups_[g];
+  const Spec& s = spec_;
+  const int D = s.D, qkvw = s.qkv_width();
+  const int nh = static_cast<int>(G.plan.home_rows.size());
+  mark(0);
+  if (!nh) return;
+  if (p2p_ && fused_ && w_->mode() != SD_DENSE_EXACT_F32) {
+    const int32_t* tbl = static_cast<const int32_t*>(G.route.p);
+    RowRoute r{};
+    r.rank = tbl;
+    r.row = tbl + nh;
+    r.ld = qkvw;
+    r.rows = rx_rows_;  // one mini-batch region of every rank's rx_qkv_ (p2p_setup)
+    for (int d = 0; d < world_; ++d) {
+      r.base[d] = peer_qkv_[d] + static_cast<size_t>(g) * rx_rows_ * qkvw;
+      r.flag[d] = peer_flags_[d];
+    }
+    r.done = gemm_done_;
+    r.epoch = epoch_of(l);
+    r.notify = G.to_shards;
+    r.slot = slot(0, g);
+    r.self = rank_;
+    GemmArgs ga = w_->gemm_args(l, 0, nh, G.x, D, G.xb, D, nullptr, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
+    ga.route = &r;
+    launch_gemm_sm100(ga, stream_);
+  } else {
+    w_->linear(l, 0, nh, G.x, D, G.xb, D, G.qkv_h, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    if (p2p_) scatter_p2p(g, 0, epoch_of(l));
+  }
+  mark(1);
+}
+
+// this shard's part of layer l for mini-batch g: receive its Q/K/V rows,
+// append_request + attend (the R-worker's QKV handler, workers.cpp:110-111),
+// send the attention rows back to their homes
+void DistEngine::shard_part(int g, int l) {
+  Group& G = groups_[g];
+  const Spec& s = spec_;
+  const int D = s.D, qkvw = s.qkv_width();
+  const DistPlan& P = G.plan;
+  const int ns = static_cast<int>(P.shard_rows.size());
+  const size_t region = static_cast<size_t>(g) * rx_rows_;
+  float* qkv_s = p2p_ ? rx_qkv_ + region * qkvw : G.qkv_s;
+  if (p2p_) {
+    timed_wait(slot(0, g), G.from_homes, epoch_of(l), kind_bytes(G, 0));
+  } else {
+    exchange(G.qkv_h, P.send_cnt, P.send_off, qkv_s, P.recv_cnt, P.recv_off, qkvw);
+  }
+  mark(2);
+  // this worker's head slice of a shard row: [q | k | v] (full width when by-sequence)
+  const int Gq = s.H / s.Hkv;
+  const int hc = P.head_count[static_cast<size_t>(rank_)];
+  const int sq = hc * Gq * s.hd, sk = hc * s.hd, srow = p2p_ ? sq + 2 * sk : qkvw;
+  const bool fused = p2p_ && fused_;
+  ORoute orr{};
+  if (fused) {  // attention rows straight into their home rank's region
+    const int nh = static_cast<int>(P.home_rows.size());
+    const int32_t* tbl = static_cast<const int32_t*>(G.route.p);
+    orr.rank = tbl + 2 * nh;
+    orr.row = tbl + 2 * nh + ns;
+    orr.ld = D;
+    for (int d = 0; d < world_; ++d) {
+      // a kind::f16 home takes its W_o operand straight from the attention
+      if (peer_mode_[d] == SD_DENSE_BF16 || peer_mode_[d] == SD_DENSE_F16) {
+        orr.bbase[d] = peer_ob_[d] + region * D;
+        if (peer_mode_[d] == SD_DENSE_F16) orr.f16_mask |= 1u << d;
+      } else {
+        orr.base[d] = peer_o_[d] + region * D;
+      }
+      orr.flag[d] = peer_flags_[d];
+    }
+    orr.bld = D;
+    orr.done = attn_done_;
+    orr.epoch = epoch_of(l);
+    orr.notify = G.to_homes;
+    orr.slot = slot(1, g);
+    orr.self = rank_;
+  }
+  if (ns) {
+    for (int i = 0; i < ns; ++i) {
+      G.pos[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(P.shard_seqs[static_cast<size_t>(i)], l));
+    }
+    kv_->append(l, ns, P.shard_seqs.data(), G.pos.data(), qkv_s + sq, srow, qkv_s + sq + sk, srow, stream_);
+    mark(3);
+    kv_->attend(l, ns, P.shard_seqs.data(), qkv_s, srow, G.o_s, p2p_ ? sq : D, stream_, g, nullptr, 0,
+                fused ? &orr : nullptr);
+    if (p2p_ && !fused) scatter_p2p(g, 1, epoch_of(l));
+  }
+  mark(4);
+}
+
+// receive_layer (workers.cpp:353-391) + finish_block (dense.cpp:51-70) of
+// mini-batch g's home rows
+void DistEngine::layer_out(int g, int l) {
+  Group& G = groups_[g];
+  const Spec& s = spec_;
+  const int D = s.D, F = s.F;
+  const DistPlan& P = G.plan;
+  const int nh = static_cast<int>(P.home_rows.size());
+  const size_t region = static_cast<size_t>(g) * rx_rows_;
+  float* o_h = p2p_ ? rx_o_ + region * D : G.o_h;
+  if (p2p_) {
+    timed_wait(slot(1, g), G.from_shards, epoch_of(l), kind_bytes(G, 1));
+  } else {
+    exchange(G.o_s, P.recv_cnt, P.recv_off, o_h, P.send_cnt, P.send_off, D);
+  }
+  mark(5);
+  if (!nh) return;
+  // kind::f16 homes keep 16-bit copies of the GEMM A operands (bf16 or fp16)
+  const bool bf = w_->mode() == SD_DENSE_BF16 || w_->mode() == SD_DENSE_F16;
+  const int f16 = w_->mode() == SD_DENSE_F16 ? 1 : 0;
+  const bool fused = p2p_ && fused_;
+  act16* ob = fused && bf ? rx_ob_ + region * D : G.ob;  // fused: the attention wrote it
+  if (bf && !fused) launch_to_16(nh, D, o_h, D, G.ob, D, f16, stream_);
+  mark(6);
+  w_->linear(l, 4, nh, o_h, D, ob, D, G.y, D, bf ? G.yb : nullptr, D, kEpiResidual, G.x, D, stream_);
+  mark(7);
+  w_->linear(l, 5, nh, G.y, D, G.yb, D, bf ? nullptr : G.h, F, bf ? G.hb : nullptr, F, kEpiSilu, nullptr, 0, stream_);
+  mark(8);
+  w_->linear(l, 6, nh, G.h, F, G.hb, F, G.x, D, bf ? G.xb : nullptr, D, kEpiResidual, G.y, D, stream_);
+  mark(9);
+}
+
+// output_logits + argmax_token (dense.cpp:72-88) of mini-batch g's home rows
+void DistEngine::head(int g) {
+  Group& G = groups_[g];
+  const Spec& s = spec_;
+  const int D = s.D;
+  const int nh = static_cast<int>(G.plan.home_rows.size());
+  if (!nh) return;
+  if (w_->mode() != SD_DENSE_EXACT_F32 && tuning().fused_argmax) {
+    // argmax_token in the head GEMM's epilogue: no logits round trip
+    GemmArgs ga = w_->gemm_args(0, 7, nh, G.x, D, G.xb, D, nullptr, s.V, nullptr, 0, kEpiNone, nullptr, 0);
+    ga.amax = G.amax;
+    launch_gemm_sm100(ga, stream_);
+    launch_argmax_keys(nh, G.amax, G.tok, stream_);
+  } else {
+    w_->linear(0, 7, nh, G.x, D, G.xb, D, G.logits, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
+    launch_argmax(nh, s.V, G.logits, s.V, G.tok, stream_);
+  }
+}
+
+// One decode step with the home tokens already in each mini-batch's tok, in
+// the reference's order (DistributedComputation::compute, workers.cpp:399-452):
+// dense_in + send of every mini-batch, then per layer and mini-batch
+// receive + dense_out + dense_in + send; each rank runs its shard's part of
+// a mini-batch right before that mini-batch's receive.
 void DistEngine::run_step() {
   const Spec& s = spec_;
-  const int D = s.D, F = s.F, qkvw = s.qkv_width(), kvw = s.kv_width();
-  const int nh = static_cast<int>(plan_.home_rows.size());
-  const int ns = static_cast<int>(plan_.shard_rows.size());
-  // kind::f16 homes keep 16-bit copies of the GEMM A operands (bf16 or fp16)
+  const int D = s.D;
+  ++steps_run_;
   const bool bf = w_ && (w_->mode() == SD_DENSE_BF16 || w_->mode() == SD_DENSE_F16);
   const int f16 = w_ && w_->mode() == SD_DENSE_F16 ? 1 : 0;
-  if (nh) launch_embed(nh, D, tok_, w_->embedding(), x_, D, bf ? xb_ : nullptr, f16, stream_);
-  const bool fused = p2p_ && fused_;
-  const bool route_qkv = fused && nh && w_->mode() != SD_DENSE_EXACT_F32;  // exact mode: scatter kernel
-  const int32_t* tbl = static_cast<const int32_t*>(route_.p);
-  uint32_t to_shards = 0, from_homes = 0, to_homes = 0, from_shards = 0;
-  for (int d = 0; d < world_; ++d) {
-    if (d == rank_) continue;
-    if (plan_.send_cnt[static_cast<size_t>(d)] > 0) to_shards |= 1u << d, from_shards |= 1u << d;
-    if (plan_.recv_cnt[static_cast<size_t>(d)] > 0) from_homes |= 1u << d, to_homes |= 1u << d;
+  for (int g = 0; g < ngroups_; ++g) {
+    Group& G = groups_[g];
+    const int nh = static_cast<int>(G.plan.home_rows.size());
+    if (nh) launch_embed(nh, D, G.tok, w_->embedding(), G.x, D, bf ? G.xb : nullptr, f16, stream_);
+    ph_on_ = phases_;
+    layer_in(g, 0);
   }
   for (int l = 0; l < s.L; ++l) {
     ph_on_ = phases_ && l % 8 == 0;
-    mark(0);
-    if (route_qkv) {
-      // project_qkv with the exchange in its epilogue: every home row lands in
-      // its shard's receive buffer; the last CTA publishes the epoch
-      RowRoute r{};
-      r.rank = tbl;
-      r.row = tbl + nh;
-      r.ld = qkvw;
-      r.rows = (p2p_cap_ + 127) / 128 * 128;  // every rank's rx_qkv_ (p2p_setup)
-      for (int d = 0; d < world_; ++d) {
-        r.base[d] = peer_qkv_[d];
-        r.flag[d] = peer_flags_[d];
-      }
-      r.done = gemm_done_;
-      r.epoch = ++epoch_;
-      r.notify = to_shards;
-      r.slot = 0;
-      r.self = rank_;
-      GemmArgs ga = w_->gemm_args(l, 0, nh, x_, D, xb_, D, nullptr, qkvw, nullptr, 0, kEpiNone, nullptr, 0);
-      ga.route = &r;
-      launch_gemm_sm100(ga, stream_);
-      mark(1);
-      fused_wait(0, from_homes, r.epoch, kind_bytes(0));
-      mark(2);
-    } else if (nh) {
-      w_->linear(l, 0, nh, x_, D, xb_, D, qkv_h_, qkvw, nullptr, 0, kEpiNone, nullptr, 0, stream_);
-      mark(1);
-    }
-    if (fused && !route_qkv) {  // nothing to send (or exact mode): the same flags / epochs
-      if (nh) {
-        exchange_p2p(0);
-      } else {
-        launch_p2p_wait(flags_, 0, from_homes, world_, ++epoch_, stream_);
-      }
-    }
-    float* qkv_s = p2p_ ? rx_qkv_ : qkv_s_;
-    float* o_h = p2p_ ? rx_o_ : o_h_;
-    // this worker's head slice of a shard row: [q | k | v] (full width when by-sequence)
-    const int G = s.H / s.Hkv;
-    const int hc = plan_.head_count[static_cast<size_t>(rank_)];
-    const int sq = hc * G * s.hd, sk = hc * s.hd, srow = p2p_ ? sq + 2 * sk : qkvw;
-    if (fused) {
-      // (sent above)
-    } else if (p2p_) {
-      exchange_p2p(0);
-      mark(2);
-    } else {
-      exchange(qkv_h_, plan_.send_cnt, plan_.send_off, qkv_s, plan_.recv_cnt, plan_.recv_off, qkvw);
-    }
-    ORoute orr{};
-    if (fused) {  // attention rows straight into their home rank's buffer
-      orr.rank = tbl + 2 * nh;
-      orr.row = tbl + 2 * nh + ns;
-      orr.ld = D;
-      for (int d = 0; d < world_; ++d) {
-        // a kind::f16 home takes its W_o operand straight from the attention
-        if (peer_mode_[d] == SD_DENSE_BF16 || peer_mode_[d] == SD_DENSE_F16) {
-          orr.bbase[d] = peer_ob_[d];
-          if (peer_mode_[d] == SD_DENSE_F16) orr.f16_mask |= 1u << d;
-        } else {
-          orr.base[d] = peer_o_[d];
-        }
-        orr.flag[d] = peer_flags_[d];
-      }
-      orr.bld = D;
-      orr.done = attn_done_;
-      orr.epoch = ++epoch_;
-      orr.notify = to_homes;
-      orr.slot = 1;
-      orr.self = rank_;
-    }
-    if (ns) {
-      for (int i = 0; i < ns; ++i) {
-        pos_[static_cast<size_t>(i)] = static_cast<uint32_t>(kv_->stored(plan_.shard_seqs[static_cast<size_t>(i)], l));
-      }
-      kv_->append(l, ns, plan_.shard_seqs.data(), pos_.data(), qkv_s + sq, srow, qkv_s + sq + sk, srow, stream_);
-      mark(3);
-      kv_->attend(l, ns, plan_.shard_seqs.data(), qkv_s, srow, o_s_, p2p_ ? sq : D, stream_, 0, nullptr, 0,
-                  fused ? &orr : nullptr);
-      mark(4);
-    }
-    if (fused) {
-      fused_wait(1, from_shards, orr.epoch, kind_bytes(1));
-      mark(5);
-    } else if (p2p_) {
-      exchange_p2p(1);
-      mark(5);
-    } else {
-      exchange(o_s_, plan_.recv_cnt, plan_.recv_off, o_h, plan_.send_cnt, plan_.send_off, D);
-    }
-    if (nh) {
-      act16* ob = fused && bf ? rx_ob_ : ob_;  // fused: the attention wrote it
-      if (bf && !fused) launch_to_16(nh, D, o_h, D, ob_, D, f16, stream_);
-      mark(6);
-      w_->linear(l, 4, nh, o_h, D, ob, D, y_, D, bf ? yb_ : nullptr, D, kEpiResidual, x_, D, stream_);
-      mark(7);
-      w_->linear(l, 5, nh, y_, D, yb_, D, bf ? nullptr : h_, F, bf ? hb_ : nullptr, F, kEpiSilu, nullptr, 0, stream_);
-      mark(8);
-      w_->linear(l, 6, nh, h_, F, hb_, F, x_, D, bf ? xb_ : nullptr, D, kEpiResidual, y_, D, stream_);
-      mark(9);
+    for (int g = 0; g < ngroups_; ++g) {
+      shard_part(g, l);
+      layer_out(g, l);
+      if (l + 1 < s.L) layer_in(g, l + 1);
     }
   }
-  if (nh) {
-    if (w_->mode() != SD_DENSE_EXACT_F32 && tuning().fused_argmax) {
-      // argmax_token in the head GEMM's epilogue: no logits round trip
-      GemmArgs ga = w_->gemm_args(0, 7, nh, x_, D, xb_, D, nullptr, s.V, nullptr, 0, kEpiNone, nullptr, 0);
-      ga.amax = amax_;
-      launch_gemm_sm100(ga, stream_);
-      launch_argmax_keys(nh, amax_, tok_, stream_);
-    } else {
-      w_->linear(0, 7, nh, x_, D, xb_, D, logits_, s.V, nullptr, 0, kEpiNone, nullptr, 0, stream_);
-      launch_argmax(nh, s.V, logits_, s.V, tok_, stream_);
-    }
-  }
+  ph_on_ = false;
+  for (int g = 0; g < ngroups_; ++g) head(g);
 }
 
 // validate_batch (core.cpp:37-54): a repeated sequence id is a ConfigError
@@ -735,32 +807,36 @@ static void check_unique(int B, const uint64_t* seqs) {
 
 void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int32_t* next, float* final_x) {
   check_unique(B, seqs);
+  for (int i = 0; i < B; ++i) {
+    if (tokens[i] < 0 || tokens[i] >= spec_.V) fail(SD_ERR_CONFIG, "token out of the vocabulary");
+  }
   DeviceGuard dg(device_);
   ensure(B);
   plan_for(B, seqs);
-  pos_.resize(static_cast<size_t>(B));
-  const int nh = static_cast<int>(plan_.home_rows.size());
-  host_tok_.resize(static_cast<size_t>(nh));
-  for (int i = 0; i < nh; ++i) {
-    const int32_t t = tokens[plan_.home_rows[static_cast<size_t>(i)]];
-    if (t < 0 || t >= spec_.V) fail(SD_ERR_CONFIG, "token out of the vocabulary");
-    host_tok_[static_cast<size_t>(i)] = t;
+  for (int g = 0; g < ngroups_; ++g) {
+    Group& G = groups_[g];
+    const int nh = static_cast<int>(G.plan.home_rows.size());
+    G.host_tok.resize(static_cast<size_t>(nh));
+    for (int i = 0; i < nh; ++i) {
+      G.host_tok[static_cast<size_t>(i)] = tokens[G.rows[static_cast<size_t>(G.plan.home_rows[static_cast<size_t>(i)])]];
+    }
+    if (nh) SD_CUDA(cudaMemcpyAsync(G.tok, G.host_tok.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
   }
-  if (nh) SD_CUDA(cudaMemcpyAsync(tok_, host_tok_.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
   run_step();
   // every rank returns the whole batch's next tokens: a row's home can move
   // between steps (balanced homes follow the batch), so each rank's caller
-  // keeps every sequence's last token. Homes write their rows into a zeroed
-  // batch vector, summed across ranks (B int32 per step).
+  // keeps every sequence's last token
   if (world_ > 1 && p2p_) {
     // peer stores of the home rows' tokens into every rank's batch vector
     // (double-buffered by step parity: a rank can be at most one step ahead)
     const int64_t ep = ++tok_epoch_;
     const int half = static_cast<int>(ep & 1) * tok_rows_;
     P2PTokens a{};
-    a.idx = home_idx_;
-    a.src = tok_;
-    a.n = nh;
+    for (int g = 0; g < ngroups_; ++g) {
+      a.idx[g] = groups_[g].home_idx;
+      a.src[g] = groups_[g].tok;
+      a.n[g] = static_cast<int>(groups_[g].plan.home_rows.size());
+    }
     a.world = world_;
     a.self = rank_;
     a.slot = kTokSlot;
@@ -776,26 +852,38 @@ void DistEngine::compute(int B, const uint64_t* seqs, const int32_t* tokens, int
     launch_p2p_wait(flags_, kTokSlot, others, world_, ep, stream_);
     SD_CUDA(cudaMemcpyAsync(next, rx_tok_ + half, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
   } else if (world_ > 1) {
+    // homes write their rows into a zeroed batch vector, summed across ranks
     SD_CUDA(cudaMemsetAsync(all_tok_, 0, static_cast<size_t>(B) * 4, stream_));
-    launch_scatter_i32(nh, home_idx_, tok_, all_tok_, stream_);
+    for (int g = 0; g < ngroups_; ++g) {
+      launch_scatter_i32(static_cast<int>(groups_[g].plan.home_rows.size()), groups_[g].home_idx, groups_[g].tok,
+                         all_tok_, stream_);
+    }
     nccl_check(Nccl::get().AllReduce(all_tok_, all_tok_, static_cast<size_t>(B), ncclInt32, ncclSum, comm_, stream_),
                "ncclAllReduce");
     SD_CUDA(cudaMemcpyAsync(next, all_tok_, static_cast<size_t>(B) * 4, cudaMemcpyDeviceToHost, stream_));
-  } else if (nh) {
-    SD_CUDA(cudaMemcpyAsync(host_tok_.data(), tok_, static_cast<size_t>(nh) * 4, cudaMemcpyDeviceToHost, stream_));
+  } else {
+    for (int g = 0; g < ngroups_; ++g) {
+      Group& G = groups_[g];
+      const int nh = static_cast<int>(G.plan.home_rows.size());
+      if (nh) SD_CUDA(cudaMemcpyAsync(G.host_tok.data(), G.tok, static_cast<size_t>(nh) * 4, cudaMemcpyDeviceToHost, stream_));
+    }
   }
-  std::vector<float> fx;
-  if (nh && final_x) {
-    fx.resize(static_cast<size_t>(nh) * spec_.D);
-    SD_CUDA(cudaMemcpyAsync(fx.data(), x_, fx.size() * 4, cudaMemcpyDeviceToHost, stream_));
+  std::vector<float> fx[2];
+  for (int g = 0; g < ngroups_ && final_x; ++g) {
+    Group& G = groups_[g];
+    fx[g].resize(G.plan.home_rows.size() * static_cast<size_t>(spec_.D));
+    if (!fx[g].empty()) SD_CUDA(cudaMemcpyAsync(fx[g].data(), G.x, fx[g].size() * 4, cudaMemcpyDeviceToHost, stream_));
   }
   SD_CUDA(cudaStreamSynchronize(stream_));
-  for (int i = 0; i < nh; ++i) {
-    const int row = plan_.home_rows[static_cast<size_t>(i)];
-    if (world_ == 1) next[row] = host_tok_[static_cast<size_t>(i)];
-    if (final_x) {
-      std::memcpy(final_x + static_cast<size_t>(row) * spec_.D, fx.data() + static_cast<size_t>(i) * spec_.D,
-                  static_cast<size_t>(spec_.D) * 4);
+  for (int g = 0; g < ngroups_; ++g) {
+    Group& G = groups_[g];
+    for (size_t i = 0; i < G.plan.home_rows.size(); ++i) {
+      const int row = G.rows[static_cast<size_t>(G.plan.home_rows[i])];
+      if (world_ == 1) next[row] = G.host_tok[i];
+      if (final_x) {
+        std::memcpy(final_x + static_cast<size_t>(row) * spec_.D, fx[g].data() + i * spec_.D,
+                    static_cast<size_t>(spec_.D) * 4);
+      }
     }
   }
 }
@@ -805,17 +893,21 @@ double DistEngine::bench(int B, const uint64_t* seqs, const int32_t* tokens, int
   DeviceGuard dg(device_);
   ensure(B);
   plan_for(B, seqs);
-  pos_.resize(static_cast<size_t>(B));
-  const int nh = static_cast<int>(plan_.home_rows.size());
-  host_tok_.resize(static_cast<size_t>(nh));
-  for (int i = 0; i < nh; ++i) host_tok_[static_cast<size_t>(i)] = tokens[plan_.home_rows[static_cast<size_t>(i)]];
-  if (nh) SD_CUDA(cudaMemcpyAsync(tok_, host_tok_.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
+  for (int g = 0; g < ngroups_; ++g) {
+    Group& G = groups_[g];
+    const int nh = static_cast<int>(G.plan.home_rows.size());
+    G.host_tok.resize(static_cast<size_t>(nh));
+    for (int i = 0; i < nh; ++i) {
+      G.host_tok[static_cast<size_t>(i)] = tokens[G.rows[static_cast<size_t>(G.plan.home_rows[static_cast<size_t>(i)])]];
+    }
+    if (nh) SD_CUDA(cudaMemcpyAsync(G.tok, G.host_tok.data(), static_cast<size_t>(nh) * 4, cudaMemcpyHostToDevice, stream_));
+  }
   cudaEvent_t e0, e1;
   SD_CUDA(cudaEventCreate(&e0));
   SD_CUDA(cudaEventCreate(&e1));
   SD_CUDA(cudaStreamSynchronize(stream_));
   SD_CUDA(cudaEventRecord(e0, stream_));
-  for (int i = 0; i < steps; ++i) run_step();
+  for (int i = 0; i < steps; ++i) run_step();  // tokens fed back on device
   SD_CUDA(cudaEventRecord(e1, stream_));
   SD_CUDA(cudaEventSynchronize(e1));
   float ms = 0;

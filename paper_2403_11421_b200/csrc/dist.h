@@ -70,28 +70,64 @@ class DistEngine : public StepComputation {
   double bench(int B, const uint64_t* seqs, const int32_t* tokens, int steps);
   void set_timing(bool on) { timing_ = on; }
   void read_timing(double* exch_ms, double* exch_bytes, bool reset);
+  // The reference's two interleaved mini-batches (workers.cpp:405-452):
+  // rows split by seq % 2 (merged when one is empty); every rank runs, per
+  // layer and mini-batch, its shard's attention, then the S-Part of that
+  // mini-batch's home rows, then its next QKV, so one mini-batch's attention
+  // on the R-shards overlaps the other's dense work on the S-ranks. Needs
+  // the peer exchange (sends never block there) when world > 1.
+  void set_pipeline(bool on);
   // Peer-memory exchange (dist_p2p.cu): allocate fixed receive buffers for
-  // up to `max_rows` rows and export their CUDA IPC handles (kIpcBytes);
-  // connect() maps every rank's buffers (world x kIpcBytes, rank order).
+  // up to `max_rows` rows per mini-batch and export their CUDA IPC handles
+  // (kIpcBytes); connect() maps every rank's buffers (world x kIpcBytes, rank
+  // order).
   // [rx_qkv | rx_o | flags | rx_ob | rx_tok handles][int32 dense mode of this rank, -1 none][pad]
   static constexpr int kIpcHandles = 5;
   static constexpr size_t kIpcBytes = kIpcHandles * sizeof(cudaIpcMemHandle_t) + 64;
-  // flag slots: 0 Q/K/V rows, 1 attention rows, 2 next tokens
-  static constexpr int kFlagSlots = 3, kTokSlot = 2;
+  // flag slots: kind + 3 * mini-batch (kind 0 Q/K/V rows, 1 attention rows); 2 next tokens
+  static constexpr int kFlagSlots = 6, kTokSlot = 2;
+  static int slot(int kind, int g) { return kind + 3 * g; }
   void p2p_setup(int max_rows, void* handles_out);
   void p2p_connect(const void* all_handles);
   bool p2p() const { return p2p_; }
 
  private:
+  // one mini-batch of the step (DistributedComputation::GroupState)
+  struct Group {
+    std::vector<int32_t> rows;  // batch rows, in batch order
+    std::vector<uint64_t> seqs;
+    DistPlan plan;              // over this mini-batch's rows
+    int cap = 0;
+    float *x = nullptr, *qkv_h = nullptr, *qkv_s = nullptr, *o_s = nullptr, *o_h = nullptr, *y = nullptr,
+          *h = nullptr, *logits = nullptr;
+    act16 *xb = nullptr, *ob = nullptr, *yb = nullptr, *hb = nullptr;
+    int32_t* tok = nullptr;               // next tokens of the home rows (home order)
+    int32_t* home_idx = nullptr;          // batch row of each home row
+    unsigned long long* amax = nullptr;   // fused-argmax keys of the head GEMM
+    std::vector<uint32_t> pos;
+    std::vector<int32_t> host_tok;
+    // peer exchange: this rank's rows' offsets in each peer's region of this
+    // mini-batch, the fused routes, and who exchanges with whom
+    std::vector<int32_t> peer_qkv_off, peer_o_off;
+    DevBuf route;  // [qkv rank | qkv row | o rank | o row] int32 tables
+    uint32_t to_shards = 0, from_homes = 0, to_homes = 0, from_shards = 0;
+  };
   void ensure(int B);
+  void free_group(Group& g);
   void plan_for(int B, const uint64_t* seqs);
   void run_step();
+  // the reference's per-mini-batch phases (workers.cpp:405-452)
+  void layer_in(int g, int l);    // project_qkv (+ embedding at l = 0 outside) and send_layer
+  void shard_part(int g, int l);  // receive Q/K/V, append + attend this shard's rows, send O
+  void layer_out(int g, int l);   // receive_layer + finish_block
+  void head(int g);
+  int64_t epoch_of(int l) const { return (steps_run_ - 1) * spec_.L + l + 1; }
   void exchange(const float* send, const std::vector<int32_t>& sc, const std::vector<int32_t>& so,
                 float* recv, const std::vector<int32_t>& rc, const std::vector<int32_t>& ro, int width);
   // kind 0: Q/K/V rows home -> shard; kind 1: attention rows shard -> home
-  double kind_bytes(int kind) const;
-  void fused_wait(int slot, uint32_t expect, int64_t epoch, double bytes);
-  void exchange_p2p(int kind);
+  double kind_bytes(const Group& G, int kind) const;
+  void timed_wait(int slot, uint32_t expect, int64_t epoch, double bytes);
+  void scatter_p2p(int g, int kind, int64_t epoch);
   // SD_DIST_PHASES=1: per-phase CUDA events on every 8th layer, summed into
   // ph_ms_ and printed to stderr per rank when the engine is destroyed
   void mark(int phase);
@@ -107,39 +143,34 @@ class DistEngine : public StepComputation {
   int rank_, world_, s_ranks_, device_, mode_ = 0;
   ncclComm_t comm_ = nullptr;
   cudaStream_t stream_ = nullptr;
-  DistPlan plan_;
+  Group groups_[2];
+  int ngroups_ = 1;
+  bool pipelined_ = false;
+  int64_t steps_run_ = 0;
   int home_flags_ = 0;  // SD_HOME_MODULO or 0
   std::unordered_set<uint64_t> home_set_;
   std::vector<uint64_t> plan_key_;
   int cap_ = 0;
-  float *x_ = nullptr, *qkv_h_ = nullptr, *qkv_s_ = nullptr, *o_s_ = nullptr, *o_h_ = nullptr,
-        *y_ = nullptr, *h_ = nullptr, *logits_ = nullptr;
-  act16 *xb_ = nullptr, *ob_ = nullptr, *yb_ = nullptr, *hb_ = nullptr;
-  int32_t* tok_ = nullptr;
-  int32_t* all_tok_ = nullptr;   // [B] next tokens of the whole batch (compute)
-  int32_t* home_idx_ = nullptr;  // [home rows] batch row of each home row
-  unsigned long long* amax_ = nullptr;  // fused-argmax keys of the head GEMM
-  std::vector<uint32_t> pos_;
-  std::vector<int32_t> host_tok_;
+  int32_t* all_tok_ = nullptr;   // [B] next tokens of the whole batch (NCCL path)
   bool timing_ = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_;
   std::vector<double> ev_bytes_;
   double x_ms_ = 0, x_bytes_ = 0;
-  // peer-memory exchange state
+  // peer-memory exchange state: receive buffers hold two regions (one per
+  // mini-batch) of rx_rows_ rows
   bool p2p_ = false;
-  int p2p_cap_ = 0;
+  int p2p_cap_ = 0, rx_rows_ = 0;
   float *rx_qkv_ = nullptr, *rx_o_ = nullptr;  // receive buffers (shard rows / home rows)
-  act16* rx_ob_ = nullptr;             // home rows' attention output as the bf16 W_o operand
+  act16* rx_ob_ = nullptr;                     // home rows' attention output as the 16-bit W_o operand
   // fused exchange: the QKV GEMM and the attention store rows straight into
   // the peers' buffers (RowRoute / ORoute) and publish the epoch themselves.
   // Decided from rank-independent facts (a sender may still use the scatter
   // kernel, e.g. an exact-mode S-rank: receivers only see buffers and flags)
   bool fused_ = false;
-  DevBuf route_;                   // [qkv rank | qkv row | o rank | o row] int32 tables
-  int32_t* gemm_done_ = nullptr;   // arrival counters of the routed launches
+  int32_t* gemm_done_ = nullptr;  // arrival counters of the routed launches
   int32_t* attn_done_ = nullptr;
-  void build_routes();
-  int64_t* flags_ = nullptr;                   // [2][kMaxWorld] epochs published by sources
+  void build_routes(Group& G);
+  int64_t* flags_ = nullptr;  // [kFlagSlots][kMaxWorld] epochs published by sources
   int32_t* done_ = nullptr;
   float* peer_qkv_[kMaxWorld] = {};
   float* peer_o_[kMaxWorld] = {};
@@ -151,8 +182,6 @@ class DistEngine : public StepComputation {
   int tok_rows_ = 0;
   int64_t tok_epoch_ = 0;
   std::vector<void*> opened_;
-  int64_t epoch_ = 0;
-  std::vector<int32_t> peer_qkv_off_, peer_o_off_;  // row offset of this rank's rows in each peer's buffer
 };
 
 }  // namespace sd

@@ -86,9 +86,11 @@ __global__ void p2p_wait_kernel(const int64_t* flags, int slot, uint32_t expect,
 __global__ void p2p_tokens_kernel(const P2PTokens a) {
   pdl_trigger();
   pdl_wait();
-  for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
-    const int32_t t = a.src[i], r = a.idx[i];
-    for (int d = 0; d < a.world; ++d) a.dst[d][r] = t;
+  for (int j = 0; j < 2; ++j) {
+    for (int i = threadIdx.x; i < a.n[j]; i += blockDim.x) {
+      const int32_t t = a.src[j][i], r = a.idx[j][i];
+      for (int d = 0; d < a.world; ++d) a.dst[d][r] = t;
+    }
   }
   __threadfence_system();
   __syncthreads();

@@ -37,12 +37,14 @@ void launch_p2p_scatter(const P2PScatter& a, cudaStream_t s);
 void launch_scatter_i32(int n, const int32_t* idx, const int32_t* src, int32_t* dst, cudaStream_t s);
 // The next-token gather of a distributed step over peer memory: every rank
 // stores its home rows' tokens at their batch rows into every rank's token
-// buffer (dst[d] + idx[i] = src[i]), then publishes flag[d][slot][self] =
-// epoch for every d in `notify` (one block; B int32 per step).
+// buffer (dst[d] + idx[j][i] = src[j][i] for each mini-batch j), then
+// publishes flag[d][slot][self] = epoch for every d in `notify` (one block;
+// B int32 per step).
 struct P2PTokens {
-  const int32_t* idx;
-  const int32_t* src;
-  int n, world, self, slot;
+  const int32_t* idx[2];
+  const int32_t* src[2];
+  int n[2];
+  int world, self, slot;
   int64_t epoch;
   uint32_t notify;
   int32_t* dst[kMaxWorld];

@@ -619,6 +619,13 @@ int sd_dist_create(sd_weights* w, sd_kv* kv, int rank, int world, const void* nc
   });
 }
 
+int sd_dist_pipeline(sd_dist* d, int enable) {
+  return guard([&] {
+    need(d, "dist");
+    d->d->set_pipeline(enable != 0);
+  });
+}
+
 int sd_dist_destroy(sd_dist* d) {
   return guard([&] { delete d; });
 }

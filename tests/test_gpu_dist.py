@@ -28,7 +28,8 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence", drain=False):
+def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence", drain=False,
+            pipeline=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -56,6 +57,8 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mo
     eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks, shard_mode=shard_mode)
     if exchange.startswith("p2p"):
         eng.enable_p2p(64)
+    if pipeline:
+        eng.pipeline(True)
     recs, acts, _ = sd.run_generation(eng, *cfg, seed=0, record_activations=True)
     rows = [(r, acts[i].tolist()) for i, r in enumerate(recs)]
     # after a run to completion every sequence has retired on every rank
@@ -75,8 +78,9 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mo
 @pytest.mark.skipif(_ngpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("s_ranks", [1, 2])
 @pytest.mark.parametrize("cfg", [(8, 32, 32, 32), (8, 16, 4, 48)], ids=["batch", "stabilized"])
-@pytest.mark.parametrize("exchange,shard_mode", [("nccl", "sequence"), ("p2p", "sequence"), ("p2p", "head")])
-def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, exchange, shard_mode):
+@pytest.mark.parametrize("exchange,shard_mode,pipeline", [("nccl", "sequence", False), ("p2p", "sequence", False),
+                                                          ("p2p", "head", False), ("p2p", "sequence", True)])
+def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, exchange, shard_mode, pipeline):
     """`exchange`: NCCL grouped send/recv, or direct NVLink stores into the
     peers' receive buffers with epoch flags (dist_p2p.cu). `shard_mode`
     "head": each rank attends every sequence for its half of the heads
@@ -84,7 +88,8 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
     back into the S-rank's rows."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode, False, pipeline), nprocs=2,
+             join=True)
     _check_rows(oracle, out, cfg)
 
 
@@ -191,19 +196,22 @@ def test_two_gpu_fused_exchange_is_bitwise_equal(tmp_path, s_ranks):
 
 
 @pytest.mark.skipif(_ngpus() < 1, reason="needs a GPU")
+@pytest.mark.parametrize("pipeline", [False, True], ids=["one-batch", "two-minibatches"])
 @pytest.mark.parametrize("s_ranks", [1, 2])
 @pytest.mark.parametrize("shard_mode", ["sequence", "head", "hybrid"])
-def test_two_ranks_one_device_distributed_equals_monolithic(oracle, tmp_path, s_ranks, shard_mode):
+def test_two_ranks_one_device_distributed_equals_monolithic(oracle, tmp_path, s_ranks, shard_mode, pipeline):
     """DistributedComputation with two ranks on ONE device (two processes,
     no NCCL: the per-layer Q/K/V and O exchange and the next-token gather are
     CUDA-IPC peer stores with epoch flags), run to completion: tokens equal
     the monolithic oracle's, activations <= 1e-5 (test_workers.cpp:280-321),
     and every rank's shard is empty afterwards with no drop warnings, in all
-    three ShardMap modes (retire routing, workers.cpp:482-501)."""
+    three ShardMap modes (retire routing, workers.cpp:482-501). With the
+    reference's two interleaved mini-batches (seq % 2, workers.cpp:405-452)
+    the transcript is the same."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
     cfg = (8, 16, 4, 0)
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True),
+    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, pipeline),
              nprocs=2, join=True)
     left = _check_rows(oracle, out, cfg)
     assert left == [(0, 0), (0, 0)]
