@@ -327,6 +327,30 @@ int sd_dist_plan(int world, int rank, int s_ranks, int shard_mode, int heads, in
                  int32_t* home_rows, int32_t* n_home, int32_t* shard_rows, int32_t* n_shard,
                  int32_t* send_counts, int32_t* recv_counts);
 
+/* ------------------------------------------------ SDWP attention worker
+ * A B200 R-worker speaking the reference's wire protocol (SDWP frames:
+ * "SDWP" | version u8 | type u8 | payload_len u32 | payload, little-endian;
+ * transport.hpp / transport.cpp:105-301), as AttentionWorkerSession
+ * (workers.cpp:40-160): HELLO, CONFIG (JSON: model, head_start, head_count,
+ * wire_precision single|half) -> ack, QKV_BATCH -> append_request + attend
+ * on a KvShard in HBM -> O_BATCH, DROP_SEQ (no reply), SHUTDOWN -> stats,
+ * typed ERROR replies (codes = the status numbering). The reference's
+ * DistributedComputation can use it as a remote R-worker. */
+typedef struct sd_rworker sd_rworker;
+/* AttentionWorkerConfig: capacity_tokens, storage format (enum sd_kv_format) */
+int sd_rworker_create(int64_t capacity_tokens, int kv_format, int device, sd_rworker** out);
+int sd_rworker_destroy(sd_rworker* w);
+/* Feed stream bytes (any split); every complete frame is handled and the
+ * reply frames are returned in *replies (valid until the next call). A bad
+ * magic or oversized frame is fatal for the stream: SD_ERR_PROTOCOL. */
+int sd_rworker_feed(sd_rworker* w, const uint8_t* bytes, size_t n, const uint8_t** replies, size_t* replies_len);
+int sd_rworker_shutdown_requested(const sd_rworker* w, int32_t* out);
+/* serve_attention_worker (workers.cpp:162-214): blocking TCP loop on
+ * "host:port" (port 0 = any; the bound port is written to port_file when
+ * non-NULL); once != 0 returns after the first connection ends. */
+int sd_rworker_serve(const char* listen_addr, const char* port_file, int64_t capacity_tokens, int kv_format,
+                     int device, int once);
+
 /* ------------------------------------------- planner inputs and planner
  * The planner's measured inputs on the B200, with the reference bench
  * definitions: T(B) = seconds of one block's S-Part (project_qkv +

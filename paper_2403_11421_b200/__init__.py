@@ -9,7 +9,8 @@ from .api import (AdmissionError, AttentionItem, AttentionRequest, CapacityError
                   CudaError, InfeasiblePlanError, DeviceWeights, DistEngine, Engine, dist_plan, nccl_unique_id, KvShard, LogicError, ProtocolError, ShardMap,
                   SplitDecodeError, UnknownSequenceError, apply_linear, cold_start_schedule,
                   finish_block, gemm_dev, launch_count, make_model_spec, micro_batch_size, mix64, output_logits_argmax,
-                  project_qkv, prompt_token, run_generation, transcript_csv, tune, tuned)
+                  project_qkv, prompt_token, run_generation, transcript_csv, tune, tuned, RWorker,
+                  serve_rworker)
 from ._lib import LIB_PATH, ModelSpec, lib
 
 __all__ = [n for n in dir() if not n.startswith("_")]

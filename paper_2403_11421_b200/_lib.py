@@ -124,6 +124,11 @@ SIGNATURES = {
     "sd_weights_seed_random": (C.c_int, [SPEC_P, C.c_uint64, C.c_int, C.c_int, PP]),
     "sd_tune": (C.c_int, [C.c_char_p, C.c_int]),
     "sd_dist_pipeline": (C.c_int, [C.c_void_p, C.c_int]),
+    "sd_rworker_create": (C.c_int, [C.c_int64, C.c_int, C.c_int, PP]),
+    "sd_rworker_destroy": (C.c_int, [C.c_void_p]),
+    "sd_rworker_feed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
+    "sd_rworker_shutdown_requested": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
+    "sd_rworker_serve": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, C.c_int, C.c_int]),
     "sd_weights_export_embedding": (C.c_int, [C.c_void_p, FP, C.c_size_t]),
     "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_drive_count": (C.c_int64, [P]),

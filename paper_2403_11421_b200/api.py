@@ -627,6 +627,41 @@ def run_generation(engine, batch: int, target_len: int, interval: int, steps: in
         lib.sd_drive_destroy(h)
 
 
+class RWorker:
+    """A B200 attention worker speaking the reference's SDWP wire protocol
+    (AttentionWorkerSession, workers.cpp:40-160): feed() takes stream bytes
+    and returns the reply frames' bytes."""
+
+    def __init__(self, capacity_tokens: int, fmt: str = "single", device: int = 0):
+        self.h = C.c_void_p()
+        _check(lib.sd_rworker_create(capacity_tokens, FORMATS[fmt], device, C.byref(self.h)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sd_rworker_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def feed(self, data: bytes) -> bytes:
+        buf = C.create_string_buffer(bytes(data), len(data)) if data else None
+        p, n = C.c_void_p(), C.c_size_t()
+        _check(lib.sd_rworker_feed(self.h, buf, len(data), C.byref(p), C.byref(n)))
+        return C.string_at(p, n.value) if n.value else b""
+
+    def shutdown_requested(self) -> bool:
+        v = C.c_int32()
+        _check(lib.sd_rworker_shutdown_requested(self.h, C.byref(v)))
+        return bool(v.value)
+
+
+def serve_rworker(listen_addr: str, capacity_tokens: int, fmt: str = "single", device: int = 0,
+                  port_file: str | None = None, once: bool = True):
+    """serve_attention_worker (workers.cpp:162-214) on this process (blocking)."""
+    _check(lib.sd_rworker_serve(listen_addr.encode(), port_file.encode() if port_file else None,
+                                capacity_tokens, FORMATS[fmt], device, int(once)))
+
+
 def transcript_csv(recs) -> str:
     """transcript_csv (workers.cpp:746-755)."""
     return "step,seq_id,token_id\n" + "".join(f"{s},{q},{t}\n" for s, q, t in recs)

@@ -131,13 +131,16 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_h2(x0 - hf.x, x1 - hf.y);
 }
 
-// four int8 (one 32-bit word) -> two fp16 pairs holding the exact integers:
-// byte b becomes fp16 1024 + (b + 128) (0x64xx), minus 1152
-__device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
-  const uint32_t biased = __byte_perm(u, 0x64646464u, sel);
-  __half2 h = *reinterpret_cast<const __half2*>(&biased);
-  h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
-  return *reinterpret_cast<const uint32_t*>(&h);
+// four int8 (one 32-bit word, sign bits flipped: b + 128) -> two fp16 pairs
+// holding the exact integers b + 1152 (0x64xx = 1024 + (b + 128)). The bias
+// is not subtracted per element: it is linear in the MMAs, so 1152 times the
+// sum of the other operand's column is taken off the accumulators instead
+// (once per stage for the scores, once per piece for the outputs).
+constexpr float kI8Bias = 1152.0f;
+__device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) { return __byte_perm(u, 0x64646464u, sel); }
+__device__ __forceinline__ float h2sum(uint32_t h) {
+  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h));
+  return f.x + f.y;
 }
 constexpr int kVPitch = kHD * 2 + 16;
 __device__ __forceinline__ void named_bar(int id, int threads) {
@@ -283,6 +286,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         }
       }
     }
+    // int8: the scores' bias correction per accumulator column, 1152 x the
+    // sum of the fp16 q parts that column's MMAs multiply (lanes tq of group
+    // gq hold column gq's k rows)
+    float kcorr[2] = {0.0f, 0.0f};
+    if (I8) {
+      float ps = 0.0f;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ps += h2sum(qb[kk][h][0]) + (PACK ? 0.0f : h2sum(qb[kk][h][1]));
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      kcorr[0] = kI8Bias * __shfl_sync(0xffffffffu, ps, 4 * (2 * tq));
+      kcorr[1] = kI8Bias * __shfl_sync(0xffffffffu, ps, 4 * (2 * tq + 1));
+    }
+    float vcorr[2] = {0.0f, 0.0f};  // int8: sums of the fp16 P^T parts per column
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
@@ -320,13 +339,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
           if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
-        // per-(position, head) K scales: S = scale * (q . k_int)
+        // per-(position, head) K scales: S = scale * (q . k_int), with the
+        // bias taken off first: q . (k_int + 1152) - 1152 sum(q)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
         const float k0 = ksc[(2 * gq) * g.hc + hk], k1 = ksc[(2 * gq + 1) * g.hc + hk];
-        s[0] *= k0;
-        s[1] *= k0;
-        s[2] *= k1;
-        s[3] *= k1;
+        s[0] = (s[0] - kcorr[0]) * k0;
+        s[1] = (s[1] - kcorr[1]) * k0;
+        s[2] = (s[2] - kcorr[0]) * k1;
+        s[3] = (s[3] - kcorr[1]) * k1;
         // V tile of this head -> exact fp16 integers in the warp's scratch
         // lane l converts word l (4 head dims) of every row: conflict-free
         // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
@@ -377,12 +397,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       const float p2 = fast_exp2(s[2] - mn0), p3 = fast_exp2(s[3] - mn1);
       l[0] = fmaf(l[0], c0, p0 + p2);
       l[1] = fmaf(l[1], c1, p1 + p3);
+      // the running max rarely moves after the first stages: rescale only
+      // when it did in some lane (c = exp2(0) = 1 exactly otherwise)
+      if (__any_sync(0xffffffffu, c0 != 1.0f || c1 != 1.0f)) {
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        o[mt][0] *= c0;
-        o[mt][2] *= c0;
-        o[mt][1] *= c1;
-        o[mt][3] *= c1;
+        for (int mt = 0; mt < 8; ++mt) {
+          o[mt][0] *= c0;
+          o[mt][2] *= c0;
+          o[mt][1] *= c1;
+          o[mt][3] *= c1;
+        }
+        vcorr[0] *= c0;
+        vcorr[1] *= c1;
       }
       // ---- P^T B-fragments via transposes of the S^T accumulator layout
       // (int8: the V scale of each position is folded into p)
@@ -398,6 +424,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (lo_role) {  // PACK: this lane's columns take the lo parts
         h01 = l01;
         h23 = l23;
+      }
+      if (I8) {  // the V bias: (v + 1152) . p - 1152 sum(p), per column
+        const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&h01));
+        const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&h23));
+        vcorr[0] += a0.x + a1.x;
+        vcorr[1] += a0.y + a1.y;
+        if (!PACK) {
+          const float2 b0 = __half22float2(*reinterpret_cast<const __half2*>(&l01));
+          const float2 b1 = __half22float2(*reinterpret_cast<const __half2*>(&l23));
+          vcorr[0] += b0.x + b1.x;
+          vcorr[1] += b0.y + b1.y;
+        }
       }
       const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
       const uint32_t bl0 = PACK ? 0u : movm_t(l01), bl1 = PACK ? 0u : movm_t(l23);
@@ -421,6 +459,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
 
     // ---- finalize: full row sums, then direct output or partial
+    if (I8) {  // O^T = (V + 1152)^T P^T - 1152 sum(P) per column
+#pragma unroll
+      for (int sh = 4; sh < 32; sh <<= 1) {
+        vcorr[0] += __shfl_xor_sync(0xffffffffu, vcorr[0], sh);
+        vcorr[1] += __shfl_xor_sync(0xffffffffu, vcorr[1], sh);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        o[mt][0] = fmaf(-kI8Bias, vcorr[0], o[mt][0]);
+        o[mt][2] = fmaf(-kI8Bias, vcorr[0], o[mt][2]);
+        o[mt][1] = fmaf(-kI8Bias, vcorr[1], o[mt][1]);
+        o[mt][3] = fmaf(-kI8Bias, vcorr[1], o[mt][3]);
+      }
+    }
     if (PACK) {  // O^T columns [G, 2G) hold V . P_lo: add them to the hi columns
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)

@@ -11,9 +11,15 @@
 #include "perf_bench.h"
 #include "planner.h"
 #include "engine.h"
+#include "sdwp.h"
 #include "kv_store.h"
 #include "sd_common.h"
 
+struct sd_rworker {
+  std::unique_ptr<sd::sdwp::WorkerSession> s;
+  sd::sdwp::FrameDecoder dec;
+  std::vector<uint8_t> out;  // reply frames of the last feed
+};
 struct sd_kv {
   std::unique_ptr<sd::KvStore> s;
   sd::DevBuf qb, kb, vb, ob;  // staging for host-pointer calls
@@ -751,6 +757,60 @@ int sd_cold_start_schedule(int batch, int target_len, int interval, int mode, in
       triples[3 * i + 1] = a[i].size;
       triples[3 * i + 2] = a[i].target;
     }
+  });
+}
+
+// ------------------------------------------------- SDWP attention worker
+int sd_rworker_create(int64_t capacity_tokens, int kv_format, int device, sd_rworker** out) {
+  return guard([&] {
+    need(out, "out");
+    auto h = std::make_unique<sd_rworker>();
+    h->s = std::make_unique<sd::sdwp::WorkerSession>(capacity_tokens, kv_format, device);
+    *out = h.release();
+  });
+}
+
+int sd_rworker_destroy(sd_rworker* w) {
+  return guard([&] { delete w; });
+}
+
+int sd_rworker_feed(sd_rworker* w, const uint8_t* bytes, size_t n, const uint8_t** replies, size_t* replies_len) {
+  return guard([&] {
+    need(w, "worker");
+    w->out.clear();
+    if (n) {
+      need(bytes, "bytes");
+      w->dec.feed(bytes, n);
+    }
+    sd::sdwp::Message m;
+    for (;;) {
+      const auto st = w->dec.poll(m);
+      if (st == sd::sdwp::FrameDecoder::kNeedMore) break;
+      if (st == sd::sdwp::FrameDecoder::kFatal) sd::fail(SD_ERR_PROTOCOL, "fatal protocol error: " + w->dec.error());
+      for (const sd::sdwp::Message& r : w->s->handle(m)) {
+        const std::vector<uint8_t> f = sd::sdwp::encode_frame(r);
+        w->out.insert(w->out.end(), f.begin(), f.end());
+      }
+      if (w->s->shutdown_requested()) break;
+    }
+    if (replies) *replies = w->out.data();
+    if (replies_len) *replies_len = w->out.size();
+  });
+}
+
+int sd_rworker_shutdown_requested(const sd_rworker* w, int32_t* out) {
+  return guard([&] {
+    need(w, "worker");
+    need(out, "out");
+    *out = w->s->shutdown_requested() ? 1 : 0;
+  });
+}
+
+int sd_rworker_serve(const char* listen_addr, const char* port_file, int64_t capacity_tokens, int kv_format,
+                     int device, int once) {
+  return guard([&] {
+    need(listen_addr, "listen_addr");
+    sd::sdwp::serve(listen_addr, port_file ? port_file : "", capacity_tokens, kv_format, device, once != 0);
   });
 }
 
