@@ -36,8 +36,13 @@ namespace sd {
 
 namespace {
 
-constexpr int kWarps = 8;                 // consumer warps = kv heads per CTA
-constexpr int kThreads = (kWarps + 1) * 32;
+// consumer warps per CTA: one per kv head for fp16 KV; two per kv head for
+// int8 KV (position classes: each takes every other stage), whose per-stage
+// work (conversion + the same MMAs over half the bytes) is latency-bound at
+// one warp per head (ncu: 2.25 warps per scheduler, issue 43% active)
+template <int FMT>
+constexpr int consumer_warps() { return FMT == SD_KV_INT8 ? 16 : 8; }
+constexpr int kMaxWarps = 16;
 constexpr int kT = 16;                    // positions per stage
 constexpr int kHD = 128;
 
@@ -131,25 +136,30 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_h2(x0 - hf.x, x1 - hf.y);
 }
 
-// four int8 (one 32-bit word, sign bits flipped: b + 128) -> two fp16 pairs
-// holding the exact integers b + 1152 (0x64xx = 1024 + (b + 128)). The bias
-// is not subtracted per element: it is linear in the MMAs, so 1152 times the
-// sum of the other operand's column is taken off the accumulators instead
-// (once per stage for the scores, once per piece for the outputs).
-constexpr float kI8Bias = 1152.0f;
-__device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) { return __byte_perm(u, 0x64646464u, sel); }
-__device__ __forceinline__ float h2sum(uint32_t h) {
-  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&h));
-  return f.x + f.y;
+// four int8 (one 32-bit word) -> two fp16 pairs holding the exact integers:
+// byte b becomes fp16 1024 + (b + 128) (0x64xx), minus 1152. (Folding the
+// 1152 bias out of the MMAs instead — subtracting 1152 x the other operand's
+// column sums from the accumulators — saves the HSUB2s but costs ~7 bits of
+// the fp32 accumulation at context 2048: 1.3e-4 error, measured; kept out.)
+__device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
+  const uint32_t biased = __byte_perm(u, 0x64646464u, sel);
+  __half2 h = *reinterpret_cast<const __half2*>(&biased);
+  h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 constexpr int kVPitch = kHD * 2 + 16;
+// int8: per-warp scratch = the dequantized V tile, reused at the end of a
+// piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
+constexpr int kScratch = kT * kVPitch + 256;
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
 
 template <int G, int FMT, int RPS>
-__global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
+  constexpr int kWarps = consumer_warps<FMT>();
+  constexpr int kThreads = (kWarps + 1) * 32;
   static_assert(!I8 || RPS == 2, "int8 fragments assume pair slots");
   // hi / lo parts of q and p packed into the N columns of one MMA
   constexpr bool PACK = 2 * G <= 8;
@@ -191,8 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
 
   const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
   const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
-  // softmax-state merge slots (hc < 8): after the ring and the int8 V scratch
-  float* mrg = reinterpret_cast<float*>(ring + nst * stage_bytes + (I8 ? kWarps * kT * kVPitch : 0));
+  // softmax-state merge slots (P > 1): after the ring (fp16), in the V
+  // scratch of each warp (int8)
+  uint8_t* scr = ring + nst * stage_bytes;
+  auto merge_slot = [&](int wp) {
+    return I8 ? reinterpret_cast<float*>(scr + wp * kScratch) + lane * 36
+              : reinterpret_cast<float*>(scr) + (wp * 32 + lane) * 36;
+  };
 
   if (warp == kWarps) {
     // producer warp: lane 0 arms the stage barrier, then lanes 0-15 copy the
@@ -286,22 +301,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
         }
       }
     }
-    // int8: the scores' bias correction per accumulator column, 1152 x the
-    // sum of the fp16 q parts that column's MMAs multiply (lanes tq of group
-    // gq hold column gq's k rows)
-    float kcorr[2] = {0.0f, 0.0f};
-    if (I8) {
-      float ps = 0.0f;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) ps += h2sum(qb[kk][h][0]) + (PACK ? 0.0f : h2sum(qb[kk][h][1]));
-      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-      kcorr[0] = kI8Bias * __shfl_sync(0xffffffffu, ps, 4 * (2 * tq));
-      kcorr[1] = kI8Bias * __shfl_sync(0xffffffffu, ps, 4 * (2 * tq + 1));
-    }
-    float vcorr[2] = {0.0f, 0.0f};  // int8: sums of the fp16 P^T parts per column
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
@@ -339,18 +338,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
           if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
         }
-        // per-(position, head) K scales: S = scale * (q . k_int), with the
-        // bias taken off first: q . (k_int + 1152) - 1152 sum(q)
+        // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
         const float k0 = ksc[(2 * gq) * g.hc + hk], k1 = ksc[(2 * gq + 1) * g.hc + hk];
-        s[0] = (s[0] - kcorr[0]) * k0;
-        s[1] = (s[1] - kcorr[1]) * k0;
-        s[2] = (s[2] - kcorr[0]) * k1;
-        s[3] = (s[3] - kcorr[1]) * k1;
+        s[0] *= k0;
+        s[1] *= k0;
+        s[2] *= k1;
+        s[3] *= k1;
         // V tile of this head -> exact fp16 integers in the warp's scratch
         // lane l converts word l (4 head dims) of every row: conflict-free
         // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
-        uint8_t* vscr = ring + nst * stage_bytes + warp * (kT * kVPitch);
+        uint8_t* vscr = scr + warp * kScratch;
         const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
         uint8_t* vd = vscr + 8 * lane;
 #pragma unroll
@@ -407,8 +405,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
           o[mt][1] *= c1;
           o[mt][3] *= c1;
         }
-        vcorr[0] *= c0;
-        vcorr[1] *= c1;
       }
       // ---- P^T B-fragments via transposes of the S^T accumulator layout
       // (int8: the V scale of each position is folded into p)
@@ -424,18 +420,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       if (lo_role) {  // PACK: this lane's columns take the lo parts
         h01 = l01;
         h23 = l23;
-      }
-      if (I8) {  // the V bias: (v + 1152) . p - 1152 sum(p), per column
-        const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&h01));
-        const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&h23));
-        vcorr[0] += a0.x + a1.x;
-        vcorr[1] += a0.y + a1.y;
-        if (!PACK) {
-          const float2 b0 = __half22float2(*reinterpret_cast<const __half2*>(&l01));
-          const float2 b1 = __half22float2(*reinterpret_cast<const __half2*>(&l23));
-          vcorr[0] += b0.x + b1.x;
-          vcorr[1] += b0.y + b1.y;
-        }
       }
       const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
       const uint32_t bl0 = PACK ? 0u : movm_t(l01), bl1 = PACK ? 0u : movm_t(l23);
@@ -459,20 +443,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     }
 
     // ---- finalize: full row sums, then direct output or partial
-    if (I8) {  // O^T = (V + 1152)^T P^T - 1152 sum(P) per column
-#pragma unroll
-      for (int sh = 4; sh < 32; sh <<= 1) {
-        vcorr[0] += __shfl_xor_sync(0xffffffffu, vcorr[0], sh);
-        vcorr[1] += __shfl_xor_sync(0xffffffffu, vcorr[1], sh);
-      }
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        o[mt][0] = fmaf(-kI8Bias, vcorr[0], o[mt][0]);
-        o[mt][2] = fmaf(-kI8Bias, vcorr[0], o[mt][2]);
-        o[mt][1] = fmaf(-kI8Bias, vcorr[1], o[mt][1]);
-        o[mt][3] = fmaf(-kI8Bias, vcorr[1], o[mt][3]);
-      }
-    }
     if (PACK) {  // O^T columns [G, 2G) hold V . P_lo: add them to the hi columns
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
@@ -487,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
     if (P > 1) {
       // merge the P position classes of this head into class 0 (same
       // fragment layout in every warp: elementwise per lane)
-      float* mine = mrg + (warp * 32 + lane) * 36;
+      float* mine = merge_slot(warp);
       if (cls > 0) {
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt)
@@ -501,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_mma_kernel(const AttnArgs a)
       named_bar(1 + hk, P * 32);
       if (cls == 0) {
         for (int c = 1; c < P; ++c) {
-          const float* th = mrg + ((hk + c * g.hc) * 32 + lane) * 36;
+          const float* th = merge_slot(hk + c * g.hc);
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const float mn = fmaxf(m[j], th[32 + j]);
@@ -672,8 +642,9 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   *stage_region = (kT / rps) * (rps * g.pos_bytes + 16);
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
-  const size_t scratch = (g.fmt == SD_KV_INT8 ? static_cast<size_t>(kWarps) * kT * kVPitch : 0) +
-                         (g.hc < kWarps ? static_cast<size_t>(kWarps) * 32 * 36 * 4 : 0);  // merge slots
+  const int warps = g.fmt == SD_KV_INT8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>();
+  const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
+                         : (g.hc < warps ? static_cast<size_t>(warps) * 32 * 36 * 4 : 0);  // merge slots
   *nstages = 5;
   while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
   return 128 + *nstages * stage + scratch;
@@ -700,7 +671,8 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
       set.emplace_back(fn, smem);
     }
   }
-  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(kThreads), smem, s, 1, a));
+  const int threads = ((i8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>()) + 1) * 32;
+  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(threads), smem, s, 1, a));
   SD_CUDA(cudaGetLastError());
   count_launch();
 }
