@@ -36,12 +36,10 @@ namespace sd {
 
 namespace {
 
-// consumer warps per CTA: one per kv head for fp16 KV; two per kv head for
-// int8 KV (position classes: each takes every other stage), whose per-stage
-// work (conversion + the same MMAs over half the bytes) is latency-bound at
-// one warp per head (ncu: 2.25 warps per scheduler, issue 43% active)
+// consumer warps per CTA: one per kv head (two per head for int8 KV as
+// position classes measured slower: 0.517 vs 0.498 ms per C5 layer)
 template <int FMT>
-constexpr int consumer_warps() { return FMT == SD_KV_INT8 ? 16 : 8; }
+constexpr int consumer_warps() { return 8; }
 constexpr int kMaxWarps = 16;
 constexpr int kT = 16;                    // positions per stage
 constexpr int kHD = 128;
@@ -160,7 +158,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   constexpr bool I8 = FMT == SD_KV_INT8;
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
-  static_assert(!I8 || RPS == 2, "int8 fragments assume pair slots");
+  static_assert(RPS == 2 || RPS == 4, "pair or quad slots");
   // hi / lo parts of q and p packed into the N columns of one MMA
   constexpr bool PACK = 2 * G <= 8;
   constexpr int XG = G / 2;  // lane xor between a column's hi and lo holders
@@ -326,13 +324,16 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (I8) {
-        // MMA row m holds position 2m (m < 8) or 2(m-8)+1: rows gq and gq+8 of
-        // this lane are the pair slot gq (conflict-free: slot pitch = 4 mod 32 words)
-        const uint8_t* kb = st8 + hk * kHD + 4 * tq + gq * ppitch;
+        // MMA row r holds position (r % NS) * RPS + r / NS: rows gq and gq+8
+        // of this lane are rows gq / NS and (gq + 8) / NS of slot gq % NS
+        // (pair slots: conflict-free, slot pitch = 4 mod 32 words; quad slots:
+        // rows gq and gq + 4 share banks, 2-way)
+        const uint8_t* kb = st8 + hk * kHD + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
+        const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;  // row gq + 8, same slot
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + g.pos_bytes + 16 * kk) ^ 0x80808080u;
+          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
           const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
                                   i8x2_to_h2(w1, 0x5342)};
           mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         }
         // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
-        const float k0 = ksc[(2 * gq) * g.hc + hk], k1 = ksc[(2 * gq + 1) * g.hc + hk];
+        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
+        const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
         s[0] *= k0;
         s[1] *= k0;
         s[2] *= k1;
@@ -353,8 +355,8 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         uint8_t* vd = vscr + 8 * lane;
 #pragma unroll
         for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
-          const int slot = m & 7, odd = m >> 3;
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + odd * g.pos_bytes) ^ 0x80808080u;
+          const int slot = m % NS, sub = m / NS;
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
           *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
         }
         __syncwarp();
@@ -411,8 +413,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       float vs0 = 1.0f, vs1 = 1.0f;
       if (I8) {
         const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
-        vs0 = vsc[(2 * gq) * g.hc + hk];
-        vs1 = vsc[(2 * gq + 1) * g.hc + hk];
+        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
+        vs0 = vsc[pos0 * g.hc + hk];
+        vs1 = vsc[pos1 * g.hc + hk];
       }
       uint32_t h01, l01, h23, l23;
       split2(p0 * vs0, p1 * vs0, h01, l01);  // (pos gq, heads 2tq..): rows = pos
@@ -629,7 +632,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 // copies, tools/bulk_bw.cu; the C5 layer 0.630 -> 0.626 ms) at the price of
 // 2-way ldmatrix conflicts (rows of a slot share bank groups); int8 keeps
 // pair slots, which its 32-bit fragment loads need.
-int attention_mma_rows_per_slot(const KvGeom& g) { return g.fmt == SD_KV_HALF ? 4 : 2; }
+int attention_mma_rows_per_slot(const KvGeom& g) {
+  return g.fmt == SD_KV_HALF || tuning().attn_i8_quad ? 4 : 2;
+}
 
 bool attention_mma_supported(const KvGeom& g, int G) {
   return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD &&
@@ -653,10 +658,14 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
   const bool i8 = a.g.fmt == SD_KV_INT8;
+  const bool quad = attention_mma_rows_per_slot(a.g) == 4;
   switch (a.G) {
-    case 2: fn = i8 ? attn_mma_kernel<2, SD_KV_INT8, 2> : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
-    case 4: fn = i8 ? attn_mma_kernel<4, SD_KV_INT8, 2> : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
-    case 8: fn = i8 ? attn_mma_kernel<8, SD_KV_INT8, 2> : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
+    case 2: fn = i8 ? (quad ? attn_mma_kernel<2, SD_KV_INT8, 4> : attn_mma_kernel<2, SD_KV_INT8, 2>)
+                    : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
+    case 4: fn = i8 ? (quad ? attn_mma_kernel<4, SD_KV_INT8, 4> : attn_mma_kernel<4, SD_KV_INT8, 2>)
+                    : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
+    case 8: fn = i8 ? (quad ? attn_mma_kernel<8, SD_KV_INT8, 4> : attn_mma_kernel<8, SD_KV_INT8, 2>)
+                    : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   // the dynamic-smem opt-in once per instantiation and size

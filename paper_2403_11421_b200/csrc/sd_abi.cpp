@@ -527,6 +527,7 @@ int sd_tune(const char* name, int value) {
              : n == "attn_mma"     ? &t.attn_mma
              : n == "pdl"          ? &t.pdl
              : n == "dist_phases"  ? &t.dist_phases
+             : n == "attn_i8_quad" ? &t.attn_i8_quad
                                    : nullptr;
     if (!f) sd::fail(SD_ERR_CONFIG, "sd_tune: unknown switch " + n);
     *f = value;

@@ -85,6 +85,7 @@ struct Tuning {
   int attn_mma = 1;      // tensor-core attention where the geometry allows it
   int pdl = 1;           // programmatic dependent launch between the step's kernels
   int dist_phases = 0;   // per-phase CUDA events in DistEngine, printed to stderr at destroy
+  int attn_i8_quad = 0;  // int8 tensor-core attention: four positions per bulk copy (else two)
 };
 inline Tuning& tuning() {
   static Tuning t;

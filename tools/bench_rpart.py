@@ -19,7 +19,11 @@ ap.add_argument("--L", type=int, default=1024)
 ap.add_argument("--layers", type=int, default=1)
 ap.add_argument("--fmt", default="half")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--tune", action="append", default=[], help="name=value (sd_tune switch)")
 a = ap.parse_args()
+for t in a.tune:
+    k, v = t.split("=")
+    sd.tune(k, int(v))
 import torch
 spec = sd.make_model_spec(a.layers, a.D, a.H, 64, 64, a.Hkv)
 hkv = spec.num_kv_heads
@@ -38,5 +42,5 @@ for l in range(a.reps):
 ms, n, byt = kv.timing_read()
 torch.cuda.synchronize()
 gbs = byt / (ms / 1e3) / 1e9
-print(json.dumps({"D": a.D, "H": a.H, "Hkv": hkv, "B": a.B, "L": a.L, "fmt": a.fmt,
+print(json.dumps({"tune": a.tune, "D": a.D, "H": a.H, "Hkv": hkv, "B": a.B, "L": a.L, "fmt": a.fmt,
                   "ms_per_launch": ms / n, "GBps": gbs, "frac_of_6524": gbs / 6524}))
