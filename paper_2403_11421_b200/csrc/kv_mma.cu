@@ -321,8 +321,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       const uint32_t Ks = smem_u32(st8) + hk * kHD * (I8 ? 1 : 2);
       uint32_t Vs = Ks + a.stage_region;
       int vpitch = 0;  // 0: fp16 rows in the ring's pair slots; else the int8 scratch pitch
-      // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q
-      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q; two
+      // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
+      float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if (I8) {
         // MMA row r holds position (r % NS) * RPS + r / NS: rows gq and gq+8
         // of this lane are rows gq / NS and (gq + 8) / NS of slot gq % NS
@@ -336,9 +337,12 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
           const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
                                   i8x2_to_h2(w1, 0x5342)};
-          mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
-          if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+          float(&acc)[4] = (kk & 1) ? s2 : s;
+          mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
+          if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
         // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
         const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
@@ -370,9 +374,12 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           // matrix rows are MMA rows lr (+8): positions 2lr / 2lr+1 -> slot lr
           const int mr = lr + 8 * (lm & 1);  // MMA row: slot mr % NS, row mr / NS of the slot
           ldsm_x4(Ks + (mr % NS) * ppitch + (mr / NS) * g.pos_bytes + (16 * kk + 8 * (lm >> 1)) * 2, ka);
-          mma16816(s, ka, qb[kk][0][0], qb[kk][1][0]);
-          if (!PACK) mma16816(s, ka, qb[kk][0][1], qb[kk][1][1]);
+          float(&acc)[4] = (kk & 1) ? s2 : s;
+          mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
+          if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
         }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s[i] += s2[i];
       }
       if (PACK) {  // hi + lo columns: every lane of the pair holds the full score
 #pragma unroll
