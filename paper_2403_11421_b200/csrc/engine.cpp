@@ -93,6 +93,11 @@ int Weights::out_dim(int which) const {
 
 int Weights::in_dim(int which) const { return which == 6 ? spec_.F : spec_.D; }
 
+int64_t Weights::weight_bytes(int which) const {
+  const int64_t es = mode_ == SD_DENSE_BF16 || mode_ == SD_DENSE_F16 ? 2 : 4;
+  return es * out_dim(which) * in_dim(which);
+}
+
 void Weights::alloc() {
   DeviceGuard dg(device_);
   const size_t es = mode_ == SD_DENSE_BF16 || mode_ == SD_DENSE_F16 ? 2 : 4;

@@ -48,6 +48,9 @@ class Weights {
               int64_t ldyb, int epi, const float* res, int64_t ldr, cudaStream_t s,
               int max_ctas = 0) const;
   const float* embedding() const { return emb_; }  // fp32 D x V column-major (the reference storage)
+  // the device tensor of (layer, which) and its bytes (L2 prefetch of the next GEMM's weights)
+  const void* weight_ptr(int layer, int which) const { return tensor(layer, which); }
+  int64_t weight_bytes(int which) const;
   int out_dim(int which) const;
   int in_dim(int which) const;
 

@@ -248,7 +248,11 @@ void Engine::run(int ng, bool embed) {
         }
         kv_->append(l, n, g.seqs.data(), g.pos.data(), g.qkv + D, qkvw, g.qkv + D + kvw, qkvw, rs);
       }
-      // the attention also writes the 16-bit copy of o that W_o consumes
+      // the attention also writes the 16-bit copy of o that W_o consumes, and
+      // prefetches W_o's weights into L2 at its end
+      if (tuning().attn_l2_prefetch && w_->mode() != SD_DENSE_EXACT_F32) {
+        kv_->set_l2_prefetch(w_->weight_ptr(l, 4), w_->weight_bytes(4));
+      }
       kv_->attend(l, n, g.seqs.data(), g.qkv, qkvw, g.o, D, rs, gi, bf ? g.ob : nullptr, D, nullptr, f16);
       if (pipeline_) {
         SD_CUDA(cudaEventRecord(g.ev_r, rs));

@@ -139,8 +139,11 @@ struct Fmt<SD_KV_INT8> {
 // in batches of PB positions per head: all K dots of a batch are issued
 // before any reduction (ILP), the online softmax rescales once per batch, in
 // the log2 domain, fp32 throughout.
-template <int FMT, int LPR, int EPL, int MAXH, int G>
-__global__ void __launch_bounds__(kThreads, 1) attn_kernel(const AttnArgs a) {
+// CW consumer warps (8, or 10 for 40-head shards: 40 row groups of 8 lanes,
+// one head each, instead of 16 row groups carrying 2-3 heads)
+template <int FMT, int LPR, int EPL, int MAXH, int G, int CW = kConsumerWarps>
+__global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a) {
+  constexpr int kConsumerWarps = CW;
   constexpr int E = Fmt<FMT>::kBytes;
   constexpr int HD = LPR * EPL;
   constexpr int RGW = 32 / LPR;              // row groups per warp
@@ -737,6 +740,7 @@ AttnFn pick_mh(int maxh, int G) {
 
 template <int FMT>
 AttnFn pick_fmt(const AttnConfig& c, int G) {
+  if (c.cw == 10) return c.epl == 16 && c.lpr == 8 && c.maxh == 1 && G == 1 ? attn_kernel<FMT, 8, 16, 1, 1, 10> : nullptr;
   if (c.epl == 16) {
     switch (c.lpr) {
       case 8: return pick_mh<FMT, 8, 16>(c.maxh, G);
@@ -771,23 +775,28 @@ AttnFn pick(const KvGeom& g, int G) {
 // balances the heads over the row groups at least as well as EPL = 8 (fewer
 // shuffles per element), else 8. Heads per row group MAXH <= 3, G <= 4.
 AttnConfig choose_attn_config(const KvGeom& g, int G) {
-  AttnConfig best{false, 0, 0, 0, 0};
+  AttnConfig best{false, 0, 0, 0, 0, kConsumerWarps};
   if (g.hd % 8 != 0 || g.pos_bytes % 16 != 0) return best;
   double best_eff = -1.0;
-  for (int epl : {16, 8}) {
-    if (g.hd % epl != 0) continue;
-    const int lpr = g.hd / epl;
-    if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) continue;
-    // EPL 16 with grouped heads needs ~220 registers: over the 168 a thread
-    // may hold when 9 warps share 4 SM sub-partitions
-    if (epl == 16 && (G != 1 || (lpr != 8 && lpr != 16))) continue;
-    const int rg = kConsumerWarps * (32 / lpr);
-    const int maxh = g.hc >= rg ? (g.hc + rg - 1) / rg : 1;
-    if (maxh > 3 || (G > 1 && maxh != 1) || (G != 1 && G != 2 && G != 4)) continue;
-    const double eff = g.hc >= rg ? static_cast<double>(g.hc) / (rg * maxh) : 1.0;
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      best = AttnConfig{true, lpr, epl, maxh, rg};
+  for (int cw : {kConsumerWarps, 10}) {
+    for (int epl : {16, 8}) {
+      if (g.hd % epl != 0) continue;
+      const int lpr = g.hd / epl;
+      if (lpr < 2 || lpr > 32 || (lpr & (lpr - 1))) continue;
+      // EPL 16 with grouped heads needs ~220 registers: over the 168 a thread
+      // may hold when 9 warps share 4 SM sub-partitions
+      if (epl == 16 && (G != 1 || (lpr != 8 && lpr != 16))) continue;
+      if (cw != kConsumerWarps && (epl != 16 || lpr != 8 || G != 1)) continue;  // the one 10-warp instantiation
+      const int rg = cw * (32 / lpr);
+      const int maxh = g.hc >= rg ? (g.hc + rg - 1) / rg : 1;
+      if (maxh > 3 || (G > 1 && maxh != 1) || (G != 1 && G != 2 && G != 4)) continue;
+      if (cw != kConsumerWarps && maxh != 1) continue;
+      const double eff = g.hc >= rg ? static_cast<double>(g.hc) / (rg * maxh) : 1.0;
+      // the wider CTA only when it balances strictly better (e.g. 40 heads: 1.0 vs 0.83)
+      if (eff > best_eff + 1e-9 && (cw == kConsumerWarps || eff > best_eff + 0.05)) {
+        best_eff = eff;
+        best = AttnConfig{true, lpr, epl, maxh, rg, cw};
+      }
     }
   }
   return best;
@@ -818,7 +827,8 @@ bool launch_attention(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) 
     SD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   }
-  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(kThreads), smem, s, 1, a));
+  const int threads = (choose_attn_config(a.g, a.G).cw + 1) * 32;
+  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(threads), smem, s, 1, a));
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFuncAttributes fa{};

@@ -102,12 +102,15 @@ struct AttnArgs {
   int ob_f16;                 // the copy is fp16 (else bf16)
   int routed;                 // o rows go to the home ranks (oroute), o/ob unused
   ORoute oroute;
+  const uint8_t* l2pf;        // optional: bytes to prefetch into L2 at the end (the next GEMM's weights)
+  int64_t l2pf_bytes;
 };
 
 // Static shape of the fast attention kernel for a geometry (kv_kernels.cu).
 struct AttnConfig {
   bool supported;
   int lpr, epl, maxh, rg;
+  int cw;  // consumer warps per CTA (8, or 10 for 40-head shards)
 };
 AttnConfig choose_attn_config(const KvGeom& g, int G);
 

@@ -259,6 +259,19 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         }
       }
     }
+    // the next GEMM's weights into L2 while the consumers drain the last
+    // stages (this CTA's slice, in 32-KB requests over the lanes): W_o then
+    // reads its B operand from L2 instead of streaming it at the ring's
+    // bytes-in-flight limit
+    if (a.l2pf_bytes > 0) {
+      const int64_t per = ((a.l2pf_bytes + gridDim.x - 1) / gridDim.x + 15) & ~int64_t{15};
+      const int64_t b0 = per * blockIdx.x, b1 = min(a.l2pf_bytes, b0 + per);
+      for (int64_t o = b0 + static_cast<int64_t>(lane) * 32768; o < b1; o += 32 * 32768) {
+        const int64_t left = b1 - o;
+        const uint32_t n = static_cast<uint32_t>(left < 32768 ? left : 32768);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.l2pf + o), "r"(n) : "memory");
+      }
+    }
     return;
   }
 
@@ -321,6 +334,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       const uint32_t Ks = smem_u32(st8) + hk * kHD * (I8 ? 1 : 2);
       uint32_t Vs = Ks + a.stage_region;
       int vpitch = 0;  // 0: fp16 rows in the ring's pair slots; else the int8 scratch pitch
+      float vs0 = 1.0f, vs1 = 1.0f;  // int8: the V scales of MMA rows gq, gq + 8
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q; two
       // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -363,7 +377,17 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
           *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
         }
+        // the V scales too, then the ring slot is free: everything after this
+        // reads registers and the warp's scratch, so the producer can refill
+        // the slot while the softmax and the value product run
+        {
+          const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
+          const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
+          vs0 = vsc[pos0 * g.hc + hk];
+          vs1 = vsc[pos1 * g.hc + hk];
+        }
         __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
         Vs = smem_u32(vscr);
         vpitch = kVPitch;
       } else {
@@ -417,13 +441,6 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       }
       // ---- P^T B-fragments via transposes of the S^T accumulator layout
       // (int8: the V scale of each position is folded into p)
-      float vs0 = 1.0f, vs1 = 1.0f;
-      if (I8) {
-        const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
-        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
-        vs0 = vsc[pos0 * g.hc + hk];
-        vs1 = vsc[pos1 * g.hc + hk];
-      }
       uint32_t h01, l01, h23, l23;
       split2(p0 * vs0, p1 * vs0, h01, l01);  // (pos gq, heads 2tq..): rows = pos
       split2(p2 * vs1, p3 * vs1, h23, l23);  // (pos gq+8, ...)
@@ -445,7 +462,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         if (!PACK) mma16816(o[mt], va, bl0, bl1);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (!I8 && lane == 0) mbar_arrive(&empty[stage]);  // (int8 released the slot after its loads)
       if (++stage == nst) {
         stage = 0;
         phase ^= 1;

@@ -573,6 +573,10 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   a.ob = fused ? ob : nullptr;
   a.ob_stride = obs;
   a.ob_f16 = ob_f16;
+  a.l2pf = l2pf_;
+  a.l2pf_bytes = use_mma_ ? l2pf_bytes_ : 0;
+  l2pf_ = nullptr;  // one launch
+  l2pf_bytes_ = 0;
   if (oroute) {
     if (!fused) fail(SD_ERR_INTERNAL, "routed attention output needs the fused combine");
     a.routed = 1;

@@ -68,6 +68,12 @@ class KvStore {
   // SM budget of the attention grid (0 = every SM): the R-Part's share when
   // it runs beside the S-Part of the other mini-batch
   void set_grid_limit(int sms) { grid_limit_ = sms; }
+  // bytes the next attend() launch prefetches into L2 at its end (the
+  // following GEMM's weights; tensor-core path only)
+  void set_l2_prefetch(const void* p, int64_t bytes) {
+    l2pf_ = static_cast<const uint8_t*>(p);
+    l2pf_bytes_ = bytes;
+  }
   // KvShard::drop_sequence (attention.cpp:284-294)
   void drop(uint64_t seq);
   int64_t export_lane(uint64_t seq, int layer, int which, void* host, size_t host_bytes,
@@ -144,6 +150,8 @@ class KvStore {
   };
   Fast fast_[2];
   Fast* fused_pending_ = nullptr;
+  const uint8_t* l2pf_ = nullptr;
+  int64_t l2pf_bytes_ = 0;
   int fused_prev_layer_ = -1;
   uint64_t fast_clock_ = 0;
   const Fast* fast_match(int n, const uint64_t* seqs) const;
