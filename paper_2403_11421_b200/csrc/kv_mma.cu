@@ -146,12 +146,9 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 constexpr int kVPitch = kHD * 2 + 16;
-// int8: per-warp scratch = two dequantized V tiles (the stage being
-// finished and the next one, software-pipelined), reused at the end of a
+// int8: per-warp scratch = the dequantized V tile, reused at the end of a
 // piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
-constexpr int kVTile = kT * kVPitch;
-constexpr int kScratch = 2 * kVTile;
-static_assert(kScratch >= 32 * 36 * 4, "merge slot fits the scratch");
+constexpr int kScratch = kT * kVPitch + 256;
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
@@ -322,143 +319,6 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
     m[0] = m[1] = -INFINITY;
     l[0] = l[1] = 0.0f;
 
-    if constexpr (I8) {
-      // Software-pipelined int8 stages: the scores and the dequantized V tile
-      // of this warp's next stage are produced (and its ring slot released)
-      // before the softmax and the value product of the current one, so the
-      // HMMA / conversion chain of one overlaps the shuffle / exp / ldmatrix
-      // chain of the other (ncu: the one-stage-at-a-time loop issued 43% of
-      // cycles at 2.25 warps per scheduler).
-      int pos = pc.p0;
-      auto step_fwd = [&]() {
-        pos += kT;
-        ++jst;
-        if (++stage == nst) {
-          stage = 0;
-          phase ^= 1;
-        }
-      };
-      auto skip_other = [&]() {  // another class's stages (warp-uniform)
-        while (P > 1 && pos < pc.p1 && jst % P != cls) step_fwd();
-      };
-      struct Pre {
-        float s[4];
-        float vs0, vs1;
-        int cnt;
-      };
-      const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
-      uint8_t* const vtile0 = scr + warp * kScratch;
-      auto prep = [&](Pre& r, int buf) {
-        r.cnt = min(kT, pc.p1 - pos);
-        mbar_wait(&full[stage], phase);
-        __syncwarp();
-        const uint8_t* st8 = ring + stage * stage_bytes;
-        float sa[4] = {0.0f, 0.0f, 0.0f, 0.0f}, sb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-        // MMA row r holds position (r % NS) * RPS + r / NS: rows gq and gq+8
-        // of this lane are rows gq / NS and (gq + 8) / NS of slot gq % NS
-        const uint8_t* kb = st8 + hk * kHD + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
-        const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
-          const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
-                                  i8x2_to_h2(w1, 0x5342)};
-          float(&acc)[4] = (kk & 1) ? sb : sa;
-          mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
-          if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
-        }
-        // per-(position, head) K scales: S = scale * (q . k_int)
-        const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
-        const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
-        r.s[0] = (sa[0] + sb[0]) * k0;
-        r.s[1] = (sa[1] + sb[1]) * k0;
-        r.s[2] = (sa[2] + sb[2]) * k1;
-        r.s[3] = (sa[3] + sb[3]) * k1;
-        // V tile of this head -> exact fp16 integers in the warp's scratch
-        // buffer `buf` (lane l converts word l of every row: conflict-free)
-        const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
-        uint8_t* vd = vtile0 + buf * kVTile + 8 * lane;
-#pragma unroll
-        for (int mm = 0; mm < kT; ++mm) {
-          const int slot = mm % NS, sub = mm / NS;
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
-          *reinterpret_cast<uint2*>(vd + mm * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
-        }
-        const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
-        r.vs0 = vsc[pos0 * g.hc + hk];
-        r.vs1 = vsc[pos1 * g.hc + hk];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);  // the ring slot is free; the rest is registers + scratch
-      };
-      auto finish = [&](const Pre& r, int buf) {
-        float sc[4] = {r.s[0], r.s[1], r.s[2], r.s[3]};
-        if (PACK) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) sc[i] += __shfl_xor_sync(0xffffffffu, sc[i], XG);
-        }
-        if (pos0 >= r.cnt) sc[0] = sc[1] = -INFINITY;
-        if (pos1 >= r.cnt) sc[2] = sc[3] = -INFINITY;
-        float mx0 = fmaxf(sc[0], sc[2]), mx1 = fmaxf(sc[1], sc[3]);
-#pragma unroll
-        for (int sh = 4; sh < 32; sh <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
-        }
-        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
-        const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
-        m[0] = mn0;
-        m[1] = mn1;
-        const float p0 = fast_exp2(sc[0] - mn0), p1 = fast_exp2(sc[1] - mn1);
-        const float p2 = fast_exp2(sc[2] - mn0), p3 = fast_exp2(sc[3] - mn1);
-        l[0] = fmaf(l[0], c0, p0 + p2);
-        l[1] = fmaf(l[1], c1, p1 + p3);
-        if (__any_sync(0xffffffffu, c0 != 1.0f || c1 != 1.0f)) {
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            o[mt][0] *= c0;
-            o[mt][2] *= c0;
-            o[mt][1] *= c1;
-            o[mt][3] *= c1;
-          }
-        }
-        uint32_t h01, l01, h23, l23;
-        split2(p0 * r.vs0, p1 * r.vs0, h01, l01);
-        split2(p2 * r.vs1, p3 * r.vs1, h23, l23);
-        if (lo_role) {
-          h01 = l01;
-          h23 = l23;
-        }
-        const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
-        const uint32_t bl0 = PACK ? 0u : movm_t(l01), bl1 = PACK ? 0u : movm_t(l23);
-        const uint32_t Vs = smem_u32(vtile0 + buf * kVTile);
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t va[4];
-          const int vrow = lr + 8 * (lm >> 1);
-          ldsm_x4_t(Vs + vrow * kVPitch + (16 * mt + 8 * (lm & 1)) * 2, va);
-          mma16816(o[mt], va, bh0, bh1);
-          if (!PACK) mma16816(o[mt], va, bl0, bl1);
-        }
-        __syncwarp();  // the tile's reads are done before a later prep overwrites it
-      };
-      skip_other();
-      if (pos < pc.p1) {
-        Pre cur, nxt;
-        int buf = 0;
-        prep(cur, 0);
-        for (;;) {
-          step_fwd();
-          skip_other();
-          const bool more = pos < pc.p1;
-          if (more) prep(nxt, buf ^ 1);
-          finish(cur, buf);
-          if (!more) break;
-          cur = nxt;
-          buf ^= 1;
-        }
-      }
-    } else
     for (int pos = pc.p0; pos < pc.p1; pos += kT, ++jst) {
       if (P > 1 && jst % P != cls) {  // another class's stage (warp-uniform)
         if (++stage == nst) {
