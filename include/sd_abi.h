@@ -84,7 +84,14 @@ typedef struct sd_model_spec {
 } sd_model_spec;
 
 /* Physical KV store sizing (no reference counterpart: the reference grows
- * std::vectors). All zero = defaults documented in DESIGN.md. */
+ * std::vectors). All zero = defaults documented in DESIGN.md. The default
+ * pool (ceil(capacity / page_positions) + max_sequences page groups, each
+ * spanning every layer) always suffices for lockstep decode, where every
+ * layer of a sequence advances together. A caller appending layers unevenly
+ * (the reference accepts up to capacity * num_layers positions in any
+ * spread, attention.cpp:148) can run out of page groups first and gets
+ * SD_ERR_CAPACITY ("physical KV pool exhausted"); size pool_pages for its
+ * spread (up to capacity * num_layers / page_positions) in that case. */
 typedef struct sd_kv_options {
   int32_t max_sequences;  /* live sequences (slots); 0 = min(capacity, 4096) */
   int32_t max_seq_len;    /* positions per sequence; 0 = min(capacity, 32768) */
