@@ -28,8 +28,11 @@ def _free_port():
     return p
 
 
+TOY = (2, 64, 4, 256, 128)
+
+
 def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence", drain=False,
-            pipeline=False):
+            pipeline=False, spec_args=TOY):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -45,14 +48,15 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mo
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     obj = [sd.nccl_unique_id() if rank == 0 and exchange != "p2p-one-device" else None]
     dist.broadcast_object_list(obj, src=0)
-    W = o.Weights(o.make_spec(2, 64, 4, 256, 128), 0)
+    W = o.Weights(o.make_spec(*spec_args), 0)
     is_s = s_ranks == world or rank == 0
     dw = upload_oracle_weights(W, "exact", device=dev) if is_s else None
-    spec = sd.make_model_spec(2, 64, 4, 256, 128)
+    spec = sd.make_model_spec(*spec_args)
+    heads = spec.num_kv_heads
     if shard_mode == "sequence":
-        h0, hc = 0, 4
+        h0, hc = 0, heads
     else:
-        h0, hc = sd.ShardMap(shard_mode, 4, world).head_range(rank)
+        h0, hc = sd.ShardMap(shard_mode, heads, world).head_range(rank)
     kv = sd.KvShard(spec, h0, hc, 1 << 16, "single", dev)
     eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks, shard_mode=shard_mode)
     if exchange.startswith("p2p"):
@@ -93,9 +97,9 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
     _check_rows(oracle, out, cfg)
 
 
-def _check_rows(oracle, out, cfg):
+def _check_rows(oracle, out, cfg, spec_args=TOY):
     rows, left = pickle.load(open(out, "rb"))
-    W = oracle.Weights(oracle.make_spec(2, 64, 4, 256, 128), 0)
+    W = oracle.Weights(oracle.make_spec(*spec_args), 0)
     orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
     ref = {(s, q): (t, oacts[i]) for i, (s, q, t) in enumerate(orecs)}
     assert len(rows) == len(ref)
@@ -215,3 +219,21 @@ def test_two_ranks_one_device_distributed_equals_monolithic(oracle, tmp_path, s_
              nprocs=2, join=True)
     left = _check_rows(oracle, out, cfg)
     assert left == [(0, 0), (0, 0)]
+
+
+@pytest.mark.skipif(_ngpus() < 1, reason="needs a GPU")
+@pytest.mark.parametrize("s_ranks", [1, 4])
+def test_four_ranks_one_device_hybrid_shardmap(oracle, tmp_path, s_ranks):
+    """ShardMap hybrid with two sequence groups (4 workers over 2 kv heads:
+    HG = gcd(4, 2) = 2 head groups x SG = 2 sequence groups,
+    transport.cpp:354-376): four ranks on one device, run to completion,
+    tokens equal the monolithic oracle, activations <= 1e-5, every shard
+    empty afterwards."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rows.pkl")
+    cfg = (8, 12, 4, 0)
+    spec_args = (2, 64, 2, 256, 128)
+    mp.spawn(_worker, args=(4, _free_port(), s_ranks, cfg, out, "p2p-one-device", "hybrid", True, False, spec_args),
+             nprocs=4, join=True)
+    left = _check_rows(oracle, out, cfg, spec_args)
+    assert left == [(0, 0)] * 4
