@@ -146,12 +146,9 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 constexpr int kVPitch = kHD * 2 + 16;
-// int8: per-warp scratch = the dequantized V tiles of a unit of kU stages,
-// reused at the end of a piece as the warp's softmax-state merge slot (32
-// lanes x 36 floats)
-constexpr int kU = 2;
-constexpr int kScratch = kU * kT * kVPitch;
-static_assert(kScratch >= 32 * 36 * 4, "merge slot fits the scratch");
+// int8: per-warp scratch = the dequantized V tile, reused at the end of a
+// piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
+constexpr int kScratch = kT * kVPitch + 256;
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
@@ -322,140 +319,6 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
     m[0] = m[1] = -INFINITY;
     l[0] = l[1] = 0.0f;
 
-    if (I8 && P == 1) {
-      // int8, one warp per kv head: stages are consumed kU at a time (a
-      // 32-position unit): the kU score chains and V conversions are
-      // independent work for the scheduler, and the max / exp / rescale /
-      // transpose steps of the online softmax run once per unit
-      for (int pos = pc.p0; pos < pc.p1;) {
-        const int nt = min(kU, (pc.p1 - pos + kT - 1) / kT);  // stages in this unit (warp-uniform)
-        float sc[kU][4], vsu[kU][2];
-        uint8_t* vscr = scr + warp * kScratch;
-        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          sc[u][0] = sc[u][1] = sc[u][2] = sc[u][3] = -INFINITY;
-          vsu[u][0] = vsu[u][1] = 0.0f;
-          if (u >= nt) continue;
-          const int su = (stage + u) % nst;
-          const uint32_t phu = phase ^ static_cast<uint32_t>((stage + u) / nst);
-          const int cnt = min(kT, pc.p1 - pos - u * kT);
-          mbar_wait(&full[su], phu);
-          __syncwarp();
-          const uint8_t* st8 = ring + su * stage_bytes;
-          float sa[4] = {0.0f, 0.0f, 0.0f, 0.0f}, sb[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          const uint8_t* kb = st8 + hk * kHD + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
-          const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
-            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
-            const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
-                                    i8x2_to_h2(w1, 0x5342)};
-            float(&acc)[4] = (kk & 1) ? sb : sa;
-            mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
-            if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
-          }
-          const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
-          const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
-          float t[4] = {(sa[0] + sb[0]) * k0, (sa[1] + sb[1]) * k0, (sa[2] + sb[2]) * k1, (sa[3] + sb[3]) * k1};
-          if (PACK) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) t[i] += __shfl_xor_sync(0xffffffffu, t[i], XG);
-          }
-          sc[u][0] = pos0 < cnt ? t[0] : -INFINITY;
-          sc[u][1] = pos0 < cnt ? t[1] : -INFINITY;
-          sc[u][2] = pos1 < cnt ? t[2] : -INFINITY;
-          sc[u][3] = pos1 < cnt ? t[3] : -INFINITY;
-          const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
-          uint8_t* vd = vscr + u * kT * kVPitch + 8 * lane;
-#pragma unroll
-          for (int mm = 0; mm < kT; ++mm) {
-            const int slot = mm % NS, sub = mm / NS;
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
-            *reinterpret_cast<uint2*>(vd + mm * kVPitch) = make_uint2(i8x2_to_h2(w, 0x5140), i8x2_to_h2(w, 0x5342));
-          }
-          const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
-          vsu[u][0] = vsc[pos0 * g.hc + hk];
-          vsu[u][1] = vsc[pos1 * g.hc + hk];
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[su]);  // the slot is free: the rest is registers + scratch
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          mx0 = fmaxf(mx0, fmaxf(sc[u][0], sc[u][2]));
-          mx1 = fmaxf(mx1, fmaxf(sc[u][1], sc[u][3]));
-        }
-#pragma unroll
-        for (int sh = 4; sh < 32; sh <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
-        }
-        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
-        const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
-        m[0] = mn0;
-        m[1] = mn1;
-        float pu[kU][4];
-        float ls0 = 0.0f, ls1 = 0.0f;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          pu[u][0] = fast_exp2(sc[u][0] - mn0);
-          pu[u][1] = fast_exp2(sc[u][1] - mn1);
-          pu[u][2] = fast_exp2(sc[u][2] - mn0);
-          pu[u][3] = fast_exp2(sc[u][3] - mn1);
-          ls0 += pu[u][0] + pu[u][2];
-          ls1 += pu[u][1] + pu[u][3];
-        }
-        l[0] = fmaf(l[0], c0, ls0);
-        l[1] = fmaf(l[1], c1, ls1);
-        if (__any_sync(0xffffffffu, c0 != 1.0f || c1 != 1.0f)) {
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            o[mt][0] *= c0;
-            o[mt][2] *= c0;
-            o[mt][1] *= c1;
-            o[mt][3] *= c1;
-          }
-        }
-        uint32_t bh[kU][2], bl[kU][2];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          uint32_t h01, l01, h23, l23;
-          split2(pu[u][0] * vsu[u][0], pu[u][1] * vsu[u][0], h01, l01);
-          split2(pu[u][2] * vsu[u][1], pu[u][3] * vsu[u][1], h23, l23);
-          if (lo_role) {
-            h01 = l01;
-            h23 = l23;
-          }
-          bh[u][0] = movm_t(h01);
-          bh[u][1] = movm_t(h23);
-          bl[u][0] = PACK ? 0u : movm_t(l01);
-          bl[u][1] = PACK ? 0u : movm_t(l23);
-        }
-        const uint32_t Vs0 = smem_u32(vscr);
-        const int vrow = lr + 8 * (lm >> 1);
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-#pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            if (u >= nt) continue;
-            uint32_t va[4];
-            ldsm_x4_t(Vs0 + (u * kT + vrow) * kVPitch + (16 * mt + 8 * (lm & 1)) * 2, va);
-            mma16816(o[mt], va, bh[u][0], bh[u][1]);
-            if (!PACK) mma16816(o[mt], va, bl[u][0], bl[u][1]);
-          }
-        }
-        __syncwarp();  // the tiles' reads are done before the next unit overwrites them
-        pos += nt * kT;
-        jst += nt;
-        stage += nt;
-        if (stage >= nst) {
-          stage -= nst;
-          phase ^= 1;
-        }
-      }
-    } else
     for (int pos = pc.p0; pos < pc.p1; pos += kT, ++jst) {
       if (P > 1 && jst % P != cls) {  // another class's stage (warp-uniform)
         if (++stage == nst) {
