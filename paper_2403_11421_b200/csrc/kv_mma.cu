@@ -674,7 +674,7 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   const int warps = g.fmt == SD_KV_INT8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>();
   const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
                          : (g.hc < warps ? static_cast<size_t>(warps) * 32 * 36 * 4 : 0);  // merge slots
-  *nstages = 5;
+  *nstages = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : 5;
   while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
   return 128 + *nstages * stage + scratch;
 }

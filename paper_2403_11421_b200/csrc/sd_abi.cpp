@@ -529,6 +529,7 @@ int sd_tune(const char* name, int value) {
              : n == "dist_phases"  ? &t.dist_phases
              : n == "attn_i8_quad" ? &t.attn_i8_quad
              : n == "attn_l2_prefetch" ? &t.attn_l2_prefetch
+             : n == "attn_max_stages" ? &t.attn_max_stages
                                    : nullptr;
     if (!f) sd::fail(SD_ERR_CONFIG, "sd_tune: unknown switch " + n);
     *f = value;

@@ -87,6 +87,7 @@ struct Tuning {
   int dist_phases = 0;   // per-phase CUDA events in DistEngine, printed to stderr at destroy
   int attn_i8_quad = 0;  // int8 tensor-core attention: four positions per bulk copy (else two)
   int attn_l2_prefetch = 0;  // the attention prefetches the W_o weights into L2 at its end
+  int attn_max_stages = 0;   // tensor-core attention ring depth cap (0: as many as fit, up to 5)
 };
 inline Tuning& tuning() {
   static Tuning t;
