@@ -674,7 +674,11 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   const int warps = g.fmt == SD_KV_INT8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>();
   const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
                          : (g.hc < warps ? static_cast<size_t>(warps) * 32 * 36 * 4 : 0);  // merge slots
-  *nstages = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : 5;
+  // fp16: two 64-KB stages stream faster than three (0.605 vs 0.643 ms per C5
+  // layer, tools/bench_rpart.py, round 2); int8 (34-KB stages) is flat from
+  // three to five stages and slower at two
+  const int dflt = g.fmt == SD_KV_HALF ? 2 : 5;
+  *nstages = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : dflt;
   while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
   return 128 + *nstages * stage + scratch;
 }
