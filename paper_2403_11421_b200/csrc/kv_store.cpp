@@ -105,7 +105,7 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   T_ = 1;
   while (T_ * 2 <= P && 2 * (T_ * 2) * g.pos_bytes <= 64 * 1024) T_ *= 2;
   int region = 0, sregion = 0;
-  nstages_ = 8;
+  nstages_ = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : 8;
   while (nstages_ > 2 && attention_smem_bytes(g, T_, nstages_, G_, &region, &sregion) > 210 * 1024) {
     --nstages_;
   }
