@@ -109,12 +109,6 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
-// 16 x 16 int8 tile, transposed (sm_100a): lane l receives, for matrix
-// columns c = l / 4 and c + 8, the bytes of rows 4 (l % 4) .. 4 (l % 4) + 3;
-// lanes 0-15 give the row addresses (layout probed: tools/ldsm_b8_probe.cu)
-__device__ __forceinline__ void ldsm_b8_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
-  asm volatile("ldmatrix.sync.aligned.m16n16.x1.trans.shared.b8 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
-}
 __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   uint32_t y;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
@@ -152,9 +146,9 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 constexpr int kVPitch = kHD * 2 + 16;
-// per-warp softmax-state merge slot (32 lanes x 36 floats), used when a kv
-// head's stages are split over position classes
-constexpr int kScratch = 32 * 36 * 4;
+// int8: per-warp scratch = the dequantized V tile, reused at the end of a
+// piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
+constexpr int kScratch = kT * kVPitch + 256;
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
@@ -205,9 +199,13 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 
   const int cb = a.cta_begin[blockIdx.x], ce = a.cta_begin[blockIdx.x + 1];
   const uint8_t* layer_base = g.pool + static_cast<int64_t>(a.layer) * g.layer_bytes;
-  // softmax-state merge slots (P > 1), after the ring
+  // softmax-state merge slots (P > 1): after the ring (fp16), in the V
+  // scratch of each warp (int8)
   uint8_t* scr = ring + nst * stage_bytes;
-  auto merge_slot = [&](int wp) { return reinterpret_cast<float*>(scr + wp * kScratch) + lane * 36; };
+  auto merge_slot = [&](int wp) {
+    return I8 ? reinterpret_cast<float*>(scr + wp * kScratch) + lane * 36
+              : reinterpret_cast<float*>(scr) + (wp * 32 + lane) * 36;
+  };
 
   if (warp == kWarps) {
     // producer warp: lane 0 arms the stage barrier, then lanes 0-15 copy the
@@ -335,9 +333,8 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       const uint8_t* st8 = ring + stage * stage_bytes;
       const uint32_t Ks = smem_u32(st8) + hk * kHD * (I8 ? 1 : 2);
       uint32_t Vs = Ks + a.stage_region;
+      int vpitch = 0;  // 0: fp16 rows in the ring's pair slots; else the int8 scratch pitch
       float vs0 = 1.0f, vs1 = 1.0f;  // int8: the V scales of MMA rows gq, gq + 8
-      // stage positions of MMA rows gq and gq + 8 (row r: slot r % NS, row r / NS of the slot)
-      const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q; two
       // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -362,17 +359,37 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         for (int i = 0; i < 4; ++i) s[i] += s2[i];
         // per-(position, head) K scales: S = scale * (q . k_int)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
+        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
         const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
         s[0] *= k0;
         s[1] *= k0;
         s[2] *= k1;
         s[3] *= k1;
-        // the V scales (the V tile itself is read by the value product below)
+        // V tile of this head -> exact fp16 integers in the warp's scratch
+        // lane l converts word l (4 head dims) of every row: conflict-free
+        // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
+        uint8_t* vscr = scr + warp * kScratch;
+        const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
+        uint8_t* vd = vscr + 8 * lane;
+#pragma unroll
+        for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
+          const int slot = m % NS, sub = m / NS;
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
+          *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
+        }
+        // the V scales too, then the ring slot is free: everything after this
+        // reads registers and the warp's scratch, so the producer can refill
+        // the slot while the softmax and the value product run
         {
           const float* vsc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region + a.sc_region);
+          const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
           vs0 = vsc[pos0 * g.hc + hk];
           vs1 = vsc[pos1 * g.hc + hk];
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        Vs = smem_u32(vscr);
+        vpitch = kVPitch;
       } else {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -434,39 +451,18 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       const uint32_t bh0 = movm_t(h01), bh1 = movm_t(h23);
       const uint32_t bl0 = PACK ? 0u : movm_t(l01), bl1 = PACK ? 0u : movm_t(l23);
       // ---- O^T += V^T . P^T  (8 tiles of 16 head-dims)
-      if (I8) {
-        // A = V^T straight from the int8 ring: one transposed 16 x 16 byte
-        // tile per 16 head dims gives this lane positions 4tq..4tq+3 of dims
-        // gq and gq + 8. Matrix row i is the stage row of S-row sigma(i), with
-        // sigma(4t + {0,1,2,3}) = {2t, 2t+1, 2t+8, 2t+9}: exactly the k slots
-        // {2tq, 2tq+1, 2tq+8, 2tq+9} the P^T fragments carry.
-        const int i = lane & 15;
-        const int srow = (i >> 2) * 2 + ((i & 3) < 2 ? (i & 3) : 6 + (i & 3));
-        const uint32_t vrow_addr = Vs + (srow % NS) * ppitch + (srow / NS) * g.pos_bytes;
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t r0, r1;
-          ldsm_b8_t(vrow_addr + 16 * mt, r0, r1);
-          r0 ^= 0x80808080u;
-          r1 ^= 0x80808080u;
-          const uint32_t va[4] = {i8x2_to_h2(r0, 0x5140), i8x2_to_h2(r1, 0x5140), i8x2_to_h2(r0, 0x5342),
-                                  i8x2_to_h2(r1, 0x5342)};
-          mma16816(o[mt], va, bh0, bh1);
-          if (!PACK) mma16816(o[mt], va, bl0, bl1);
-        }
-      } else {
-#pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t va[4];
-          // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
-          const int vrow = lr + 8 * (lm >> 1);  // MMA k row (position mapping as for K)
-          ldsm_x4_t(Vs + (vrow % NS) * ppitch + (vrow / NS) * g.pos_bytes + (16 * mt + 8 * (lm & 1)) * 2, va);
-          mma16816(o[mt], va, bh0, bh1);
-          if (!PACK) mma16816(o[mt], va, bl0, bl1);
-        }
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t va[4];
+        // A = V^T: matrices (pos 0-7, d 0-7), (pos 0-7, d 8-15), (pos 8-15, d 0-7), (pos 8-15, d 8-15)
+        const int vrow = lr + 8 * (lm >> 1);  // MMA k row (position mapping as for K)
+        const uint32_t vaddr = vpitch ? Vs + vrow * vpitch : Vs + (vrow % NS) * ppitch + (vrow / NS) * g.pos_bytes;
+        ldsm_x4_t(vaddr + (16 * mt + 8 * (lm & 1)) * 2, va);
+        mma16816(o[mt], va, bh0, bh1);
+        if (!PACK) mma16816(o[mt], va, bl0, bl1);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (!I8 && lane == 0) mbar_arrive(&empty[stage]);  // (int8 released the slot after its loads)
       if (++stage == nst) {
         stage = 0;
         phase ^= 1;
@@ -676,7 +672,8 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
   const int warps = g.fmt == SD_KV_INT8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>();
-  const size_t scratch = g.hc < warps ? static_cast<size_t>(warps) * kScratch : 0;  // merge slots
+  const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
+                         : (g.hc < warps ? static_cast<size_t>(warps) * 32 * 36 * 4 : 0);  // merge slots
   // fp16: two 64-KB stages stream faster than three (0.605 vs 0.643 ms per C5
   // layer, tools/bench_rpart.py, round 2); int8 (34-KB stages) is flat from
   // three to five stages and slower at two
