@@ -354,9 +354,11 @@ int sd_rworker_feed(sd_rworker* w, const uint8_t* bytes, size_t n, const uint8_t
 int sd_rworker_shutdown_requested(const sd_rworker* w, int32_t* out);
 /* serve_attention_worker (workers.cpp:162-214): blocking TCP loop on
  * "host:port" (port 0 = any; the bound port is written to port_file when
- * non-NULL); once != 0 returns after the first connection ends. */
+ * non-NULL); once != 0 returns after the first connection ends; a connection
+ * idle for recv_timeout_seconds (> 0) ends its session. The `sd_rworker
+ * serve` binary is the reference CLI's `serve` subcommand over this. */
 int sd_rworker_serve(const char* listen_addr, const char* port_file, int64_t capacity_tokens, int kv_format,
-                     int device, int once);
+                     int device, int once, double recv_timeout_seconds);
 
 /* ------------------------------------------- planner inputs and planner
  * The planner's measured inputs on the B200, with the reference bench

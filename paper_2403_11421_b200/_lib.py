@@ -128,7 +128,7 @@ SIGNATURES = {
     "sd_rworker_destroy": (C.c_int, [C.c_void_p]),
     "sd_rworker_feed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]),
     "sd_rworker_shutdown_requested": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32)]),
-    "sd_rworker_serve": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, C.c_int, C.c_int]),
+    "sd_rworker_serve": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_double]),
     "sd_weights_export_embedding": (C.c_int, [C.c_void_p, FP, C.c_size_t]),
     "sd_drive": (C.c_int, [P, C.POINTER(DriveConfig), PP]),
     "sd_drive_count": (C.c_int64, [P]),

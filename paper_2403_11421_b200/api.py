@@ -657,10 +657,10 @@ class RWorker:
 
 
 def serve_rworker(listen_addr: str, capacity_tokens: int, fmt: str = "single", device: int = 0,
-                  port_file: str | None = None, once: bool = True):
+                  port_file: str | None = None, once: bool = True, recv_timeout: float = 0.0):
     """serve_attention_worker (workers.cpp:162-214) on this process (blocking)."""
     _check(lib.sd_rworker_serve(listen_addr.encode(), port_file.encode() if port_file else None,
-                                capacity_tokens, FORMATS[fmt], device, int(once)))
+                                capacity_tokens, FORMATS[fmt], device, int(once), float(recv_timeout)))
 
 
 def transcript_csv(recs) -> str:

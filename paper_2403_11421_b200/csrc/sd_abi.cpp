@@ -810,10 +810,11 @@ int sd_rworker_shutdown_requested(const sd_rworker* w, int32_t* out) {
 }
 
 int sd_rworker_serve(const char* listen_addr, const char* port_file, int64_t capacity_tokens, int kv_format,
-                     int device, int once) {
+                     int device, int once, double recv_timeout_seconds) {
   return guard([&] {
     need(listen_addr, "listen_addr");
-    sd::sdwp::serve(listen_addr, port_file ? port_file : "", capacity_tokens, kv_format, device, once != 0);
+    sd::sdwp::serve(listen_addr, port_file ? port_file : "", capacity_tokens, kv_format, device, once != 0,
+                    recv_timeout_seconds);
   });
 }
 

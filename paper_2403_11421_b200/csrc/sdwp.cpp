@@ -4,6 +4,7 @@
 #include <arpa/inet.h>
 #include <netinet/in.h>
 #include <netinet/tcp.h>
+#include <poll.h>
 #include <sys/socket.h>
 #include <unistd.h>
 
@@ -542,7 +543,7 @@ std::vector<Message> WorkerSession::handle_inner(const Message& m) {
 
 // ---------------------------------------------------------------- serve ---
 int serve(const std::string& listen_addr, const std::string& port_file, int64_t capacity_tokens, int kv_format,
-          int device, bool once) {
+          int device, bool once, double recv_timeout_seconds) {
   const size_t colon = listen_addr.rfind(':');
   if (colon == std::string::npos) fail(SD_ERR_CONFIG, "listen address must be host:port");
   const std::string host = listen_addr.substr(0, colon);
@@ -585,6 +586,14 @@ int serve(const std::string& listen_addr, const std::string& port_file, int64_t 
     bool over = false;
     while (!over) {
       const auto t0 = std::chrono::steady_clock::now();
+      if (recv_timeout_seconds > 0) {
+        pollfd pfd{fd, POLLIN, 0};
+        const int pr = ::poll(&pfd, 1, static_cast<int>(recv_timeout_seconds * 1000.0));
+        if (pr == 0) {
+          std::fprintf(stderr, "worker: receive timed out after %.1f s\n", recv_timeout_seconds);
+          break;
+        }
+      }
       const ssize_t n = ::recv(fd, buf.data(), buf.size(), 0);
       session.note_idle(seconds_since(t0));
       if (n <= 0) break;  // peer closed (or error)

@@ -111,8 +111,10 @@ class WorkerSession {
 // listen on host:port (port 0 = any), write the bound port to port_file
 // when given, serve one connection at a time; once = return after the first
 // session ends. Returns 0, or throws sd::Error.
+// recv_timeout_seconds > 0: a connection idle that long ends its session
+// (ServeOptions::recv_timeout_seconds); 0 blocks forever.
 int serve(const std::string& listen_addr, const std::string& port_file, int64_t capacity_tokens, int kv_format,
-          int device, bool once);
+          int device, bool once, double recv_timeout_seconds = 0);
 
 }  // namespace sdwp
 }  // namespace sd

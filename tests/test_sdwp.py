@@ -220,3 +220,97 @@ def test_worker_serves_over_tcp(w, oracle, tmp_path):
     okv.append_request(0, seqs, P, k, v)
     _, _, _, _, oseqs, o = w.decode_o(fr[2][2], 64)
     assert oseqs == seqs and np.abs(o - okv.attend(0, seqs, q)).max() <= 2e-5
+
+
+# ------------------------------------------ the `serve` drop-in binary
+RWORKER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2403_11421_b200",
+                       "sd_rworker")
+
+
+def test_rworker_cli_rejects_bad_options():
+    """The reference CLI's argument errors (splitdecode_main.cpp serve:
+    --capacity required, --storage single|half|int8): exit 2, no socket."""
+    import subprocess
+    assert os.access(RWORKER, os.X_OK), "sd_rworker not built (make -C paper_2403_11421_b200/csrc)"
+    for args, msg in ((["serve"], "usage"), (["serve", "--capacity", "16", "--storage", "fp8"], "unknown kv storage"),
+                      (["serve", "--capacity"], "needs a value"), (["bogus"], "usage")):
+        r = subprocess.run([RWORKER, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 2 and msg in r.stderr, (args, r.stderr)
+
+
+def _start_rworker(tmp_path, *extra):
+    import subprocess
+    import time
+    port_file = str(tmp_path / "port")
+    p = subprocess.Popen([RWORKER, "serve", "--listen", "127.0.0.1:0", "--port-file", port_file, "--once", *extra],
+                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+    for _ in range(1200):
+        if os.path.exists(port_file) and open(port_file).read().strip():
+            return p, int(open(port_file).read())
+        if p.poll() is not None:
+            break
+        time.sleep(0.05)
+    p.kill()
+    raise AssertionError("sd_rworker did not come up: " + p.communicate()[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("storage", ["half", "int8"])
+def test_rworker_binary_serves_a_session(w, oracle, tmp_path, storage):
+    """`sd_rworker serve --once` as its own process: the dense side connects
+    over TCP, runs HELLO / CONFIG / two steps of QKV_BATCH / SHUTDOWN, gets
+    the oracle KvShard's outputs back, and the worker exits 0."""
+    import json
+    import socket
+    p, port = _start_rworker(tmp_path, "--capacity", "4096", "--storage", storage)
+    try:
+        c = socket.create_connection(("127.0.0.1", port), timeout=60)
+        okv = oracle.KvShard(oracle.make_spec(2, 64, 4, 256, 128), 0, 4, 4096, storage)
+        rng = np.random.default_rng(3)
+        seqs = [21, 22, 23, 24]
+        c.sendall(w.encode_frame(w.HELLO) + w.encode_frame(w.CONFIG, w.config_payload(2, 64, 4, 256, 128, 0, 4)))
+        sent, want = [], []
+        for step in range(2):
+            for layer in range(2):
+                q, k, v = (rng.uniform(-1, 1, (4, 64)).astype(np.float32) for _ in range(3))
+                sent.append(w.encode_frame(w.QKV_BATCH, w.encode_qkv(layer, step, 0, 4, seqs, [step] * 4, q, k, v)))
+                okv.append_request(layer, seqs, [step] * 4, k, v)
+                want.append(okv.attend(layer, seqs, q))
+        c.sendall(b"".join(sent) + w.encode_frame(w.SHUTDOWN))
+        data = b""
+        while True:
+            fr, _ = w.frames(data)
+            if len(fr) == 7:
+                break
+            chunk = c.recv(1 << 16)
+            assert chunk, "connection closed early"
+            data += chunk
+        c.close()
+        assert p.wait(timeout=60) == 0, p.communicate()[1]
+    finally:
+        if p.poll() is None:
+            p.kill()
+    assert [f[1] for f in fr] == [w.HELLO, w.CONFIG] + [w.O_BATCH] * 4 + [w.SHUTDOWN]
+    assert json.loads(fr[1][2])["storage_format"] == storage
+    for f, ref in zip(fr[2:6], want):
+        assert np.abs(w.decode_o(f[2], 64)[5] - ref).max() <= 2e-5
+    assert json.loads(fr[6][2])["tokens_processed"] == 4 * 2 * 2
+
+
+@pytest.mark.gpu
+def test_rworker_binary_receive_timeout(w, tmp_path):
+    """--timeout (ServeOptions::recv_timeout_seconds): an idle connection
+    ends its session; with --once the worker then exits 0."""
+    import socket
+    import time
+    p, port = _start_rworker(tmp_path, "--capacity", "64", "--timeout", "1")
+    try:
+        c = socket.create_connection(("127.0.0.1", port), timeout=60)
+        c.sendall(w.encode_frame(w.HELLO))
+        t0 = time.time()
+        assert p.wait(timeout=60) == 0
+        assert time.time() - t0 < 30 and "timed out" in p.communicate()[1]
+        c.close()
+    finally:
+        if p.poll() is None:
+            p.kill()
