@@ -24,6 +24,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   if (threadIdx.x == 0) {
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], g.hc);  // the hc warps of the stage's position class
+      mbar_init(&empty[s], g.hc);  // the hc warps of the stage's position class (nst % P == 0: one class per slot)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -678,9 +679,18 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   // layer, tools/bench_rpart.py, round 2); int8 (34-KB stages) is flat from
   // three to five stages and slower at two
   const int dflt = g.fmt == SD_KV_HALF ? 2 : 5;
-  *nstages = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : dflt;
-  while (*nstages > 2 && 128 + *nstages * stage + scratch > 215 * 1024) --*nstages;
-  return 128 + *nstages * stage + scratch;
+  // The ring depth is a multiple of the P = warps / hc position classes, so
+  // every fill of a slot is consumed by the same class: a class then waits on
+  // a slot's full barrier only after it consumed the slot's previous fill, and
+  // the parity wait cannot alias the phase before it (with P > depth a class
+  // could see the previous fill's parity and read a stage not yet landed).
+  const int P = warps / g.hc;
+  int n = tuning().attn_max_stages > 1 ? tuning().attn_max_stages : dflt;
+  n = std::max(P, (n + P - 1) / P * P);
+  while (n > std::max(P, 2) && 128 + n * stage + scratch > 215 * 1024) n -= P;
+  if (128 + n * stage + scratch > 227 * 1024) fail(SD_ERR_INTERNAL, "attention_mma: ring does not fit shared memory");
+  *nstages = n;
+  return 128 + n * stage + scratch;
 }
 
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
