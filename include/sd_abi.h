@@ -55,8 +55,11 @@ enum sd_status {
   SD_ERR_INFEASIBLE = 12 /* InfeasiblePlanError (planner.hpp:18-23) */
 };
 
-/* KvFormat (attention.hpp:24) */
-enum sd_kv_format { SD_KV_SINGLE = 0, SD_KV_HALF = 1, SD_KV_INT8 = 2 };
+/* KvFormat (attention.hpp:24). SD_KV_INT4 is an extension: the paper's 4-bit
+ * quantization hook with quantize_int8's rules at +-7
+ * (per-(position, head) fp32 scale max|x| / 7, round half to even), two
+ * values per byte, element 2i in the low nibble; needs an even head_dim. */
+enum sd_kv_format { SD_KV_SINGLE = 0, SD_KV_HALF = 1, SD_KV_INT8 = 2, SD_KV_INT4 = 3 };
 
 /* S-Part arithmetic (dense.hpp:16-20 fixes fp32, k-ascending). */
 enum sd_dense_mode {

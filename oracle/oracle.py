@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "libsd_oracle.so")
 
-FORMATS = {"single": 0, "half": 1, "int8": 2}
+FORMATS = {"single": 0, "half": 1, "int8": 2, "int4": 3}
 ERR_NAMES = {3: "ProtocolError", 4: "CapacityError", 5: "UnknownSequenceError",
              6: "InternalError", 7: "LogicError", 8: "ConfigError", 11: "AdmissionError"}
 
@@ -73,6 +73,7 @@ _sig("orc_prompt_token", C.c_int, C.c_uint64, C.c_uint64, C.c_int)
 _sig("orc_f2h", C.c_uint16, C.c_float)
 _sig("orc_h2f", C.c_float, C.c_uint16)
 _sig("orc_quantize_int8", C.c_float, FP, C.c_int, C.POINTER(C.c_int8))
+_sig("orc_quantize_int4", C.c_float, FP, C.c_int, C.POINTER(C.c_uint8))
 _sig("orc_eigen_dot", C.c_float, FP, FP, C.c_int)
 _sig("orc_synth_value", C.c_float, C.c_uint64)
 _sig("orc_weights_create", C.c_int, C.POINTER(Spec), C.c_uint64, PP)
@@ -173,6 +174,21 @@ def quantize_int8(x) -> tuple[np.ndarray, float]:
     q = np.zeros(x.size, dtype=np.int8)
     s = _lib.orc_quantize_int8(_f(x), x.size, q.ctypes.data_as(C.POINTER(C.c_int8)))
     return q, float(np.float32(s))
+
+
+def quantize_int4(x) -> tuple[np.ndarray, float]:
+    """The 4-bit extension codec (sd_oracle.cpp quantize_int4): packed bytes, scale."""
+    x = f32(x)
+    q = np.zeros((x.size + 1) // 2, dtype=np.uint8)
+    s = _lib.orc_quantize_int4(_f(x), x.size, q.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return q, float(np.float32(s))
+
+
+def unpack_int4(packed, n) -> np.ndarray:
+    """Packed nibbles (element 2i low) -> signed integers."""
+    b = np.asarray(packed, dtype=np.uint8)
+    nib = np.stack([b & 0xF, b >> 4], axis=-1).reshape(*b.shape[:-1], -1)[..., :n].astype(np.int8)
+    return np.where(nib >= 8, nib - 16, nib).astype(np.int8)
 
 
 def eigen_dot(a, b) -> float:
@@ -291,7 +307,7 @@ class KvShard:
             _check(int(-n))
         buf = np.zeros(n, dtype=np.uint8)
         L = self.stored_length(seq, layer)
-        scales = np.zeros(L * self.head_count, dtype=np.float32) if self.fmt == "int8" else None
+        scales = np.zeros(L * self.head_count, dtype=np.float32) if self.fmt in ("int8", "int4") else None
         _lib.orc_kv_export_lane(self.h, seq, layer, which, buf.ctypes.data_as(C.c_void_p), n,
                                 _f(scales) if scales is not None else None,
                                 scales.size if scales is not None else 0)

@@ -22,6 +22,9 @@
 // Extension (NOT in the reference, parity unpinned): grouped-query attention
 // via ModelSpec.num_kv_heads (query head h reads kv head h / (H / Hkv)).
 // With num_kv_heads == num_heads every function is the reference's.
+// Extension (NOT in the reference, parity unpinned): int4 KV storage, the
+// paper's 4-bit quantization hook, following
+// quantize_int8's rules with a +-7 range (quantize_int4 below).
 //
 // Layout at this C ABI: activations are row-major [rows][width]; weights
 // keep the reference's Eigen column-major (out x in) storage, i.e. element
@@ -274,6 +277,32 @@ float quantize_int8(const float* x, int n, int8_t* q) {
   return scale;
 }
 
+// quantize_int4: the paper's quantization hook ("suppose
+// that 4-bit integers are used to store K and V") in the shape of
+// quantize_int8 — per-(position, head) scale max|x| / 7, round half to even,
+// clamp to +-7 — stored two per byte, element 2i in the low nibble of byte
+// i (two's complement). The reference has no 4-bit format: this extension is
+// pinned to its int8 codec's rules, not to reference vectors.
+float quantize_int4(const float* x, int n, uint8_t* packed) {
+  float max_abs = 0.0f;
+  for (int i = 0; i < n; ++i) max_abs = std::max(max_abs, std::fabs(x[i]));
+  for (int i = 0; i < (n + 1) / 2; ++i) packed[i] = 0;
+  if (max_abs == 0.0f) return 0.0f;
+  const float scale = max_abs / 7.0f;
+  const double inv = 1.0 / static_cast<double>(scale);
+  for (int i = 0; i < n; ++i) {
+    double r = std::nearbyint(static_cast<double>(x[i]) * inv);
+    r = std::clamp(r, -7.0, 7.0);
+    const uint8_t nib = static_cast<uint8_t>(static_cast<int>(r) & 0xF);
+    packed[i / 2] = static_cast<uint8_t>(packed[i / 2] | (i & 1 ? nib << 4 : nib));
+  }
+  return scale;
+}
+int int4_at(const uint8_t* packed, int i) {
+  const int nib = (packed[i / 2] >> (i & 1 ? 4 : 0)) & 0xF;
+  return nib >= 8 ? nib - 16 : nib;
+}
+
 // ---------------------------------------------------------- dot products ---
 // Eigen 3.x `a.dot(b)` for dynamic float vectors on an SSE2 build: linear
 // vectorized redux with alignedStart 0 (the product expression has no
@@ -311,7 +340,7 @@ float eigen_dot(const float* a, const float* b, int n) {
 }
 
 // ---------------------------------------------------------------- KvShard ---
-enum Fmt : int { kSingle = 0, kHalf = 1, kInt8 = 2 };
+enum Fmt : int { kSingle = 0, kHalf = 1, kInt8 = 2, kInt4 = 3 };
 
 // KvShard (attention.hpp:68-140; attention.cpp:62-305). head_start /
 // head_count index the shard's kv heads; the q width is derived from them.
@@ -325,7 +354,8 @@ class KvShard {
       throw Error(kConfig, "shard head range outside the model's heads");
     }
     if (cap < 1) throw Error(kConfig, "shard capacity must be >= 1");
-    if (fmt < 0 || fmt > 2) throw Error(kConfig, "unknown kv storage format");
+    if (fmt < 0 || fmt > 3) throw Error(kConfig, "unknown kv storage format");
+    if (fmt == kInt4 && s.head_dim % 2) throw Error(kConfig, "int4 kv storage needs an even head_dim");
   }
   int width() const { return hc_ * s_.head_dim; }  // kv width
   int head_start() const { return h0_; }
@@ -344,6 +374,7 @@ class KvShard {
     switch (fmt_) {
       case kSingle: return 2 * w * sizeof(float);
       case kHalf: return 2 * w * sizeof(uint16_t);
+      case kInt4: return 2 * (w / 2 + static_cast<size_t>(hc_) * sizeof(float));
       default: return 2 * (w + static_cast<size_t>(hc_) * sizeof(float));
     }
   }
@@ -477,10 +508,11 @@ class KvShard {
     switch (fmt_) {
       case kSingle: bytes = ln.f32.size() * 4; src = ln.f32.data(); break;
       case kHalf: bytes = ln.f16.size() * 2; src = ln.f16.data(); break;
+      case kInt4: bytes = ln.i4.size(); src = ln.i4.data(); break;
       default: bytes = ln.i8.size(); src = ln.i8.data(); break;
     }
     if (out && bytes <= cap && bytes) std::memcpy(out, src, bytes);
-    if (scales && fmt_ == kInt8 && ln.i8s.size() <= scap && !ln.i8s.empty()) {
+    if (scales && (fmt_ == kInt8 || fmt_ == kInt4) && ln.i8s.size() <= scap && !ln.i8s.empty()) {
       std::memcpy(scales, ln.i8s.data(), ln.i8s.size() * 4);
     }
     return bytes;
@@ -491,7 +523,8 @@ class KvShard {
     std::vector<float> f32;
     std::vector<uint16_t> f16;
     std::vector<int8_t> i8;
-    std::vector<float> i8s;
+    std::vector<uint8_t> i4;  // int4: [pos][head][hd / 2] packed nibbles
+    std::vector<float> i8s;   // int8 / int4 scales [pos][head]
     int positions = 0;
   };
   struct SeqLayer {
@@ -511,6 +544,16 @@ class KvShard {
       case kHalf:
         for (int i = 0; i < w; ++i) ln.f16.push_back(f2h(x[i]));
         break;
+      case kInt4: {
+        const int hd = s_.head_dim;
+        std::vector<uint8_t> q(static_cast<size_t>(hd / 2));
+        for (int h = 0; h < hc_; ++h) {
+          const float sc = quantize_int4(x + h * hd, hd, q.data());
+          ln.i4.insert(ln.i4.end(), q.begin(), q.end());
+          ln.i8s.push_back(sc);
+        }
+        break;
+      }
       default: {
         const int hd = s_.head_dim;
         std::vector<int8_t> q(static_cast<size_t>(hd));
@@ -532,6 +575,12 @@ class KvShard {
       case kHalf:
         for (int i = 0; i < hd; ++i) out[i] = h2f(ln.f16[off + i]);
         return out;
+      case kInt4: {
+        const float sc = ln.i8s[static_cast<size_t>(pos) * hc_ + head];
+        const uint8_t* row = ln.i4.data() + off / 2;
+        for (int i = 0; i < hd; ++i) out[i] = static_cast<float>(int4_at(row, i)) * sc;
+        return out;
+      }
       default: {
         const float sc = ln.i8s[static_cast<size_t>(pos) * hc_ + head];
         for (int i = 0; i < hd; ++i) out[i] = static_cast<float>(ln.i8[off + i]) * sc;
@@ -1069,6 +1118,7 @@ int orc_prompt_token(uint64_t seed, uint64_t id, int vocab) { return prompt_toke
 uint16_t orc_f2h(float f) { return f2h(f); }
 float orc_h2f(uint16_t h) { return h2f(h); }
 float orc_quantize_int8(const float* x, int n, int8_t* q) { return quantize_int8(x, n, q); }
+float orc_quantize_int4(const float* x, int n, uint8_t* packed) { return quantize_int4(x, n, packed); }
 float orc_eigen_dot(const float* a, const float* b, int n) { return eigen_dot(a, b, n); }
 float orc_synth_value(uint64_t idx) { return synth_value(idx); }
 

@@ -66,7 +66,7 @@ def _check(rc: int):
         raise _BY_CODE.get(rc, SplitDecodeError)(msg)
 
 
-FORMATS = {"single": 0, "half": 1, "int8": 2}
+FORMATS = {"single": 0, "half": 1, "int8": 2, "int4": 3}
 DENSE_MODES = {"exact": 0, "bf16": 1, "tf32": 2, "fp16": 3}
 SHARD_MODES = {"by-sequence": 0, "by-head": 1, "hybrid": 2, "sequence": 0, "head": 1}
 # home (S-Part) placement with data-parallel S-ranks (SD_HOME_MODULO, include/sd_abi.h)
@@ -276,13 +276,13 @@ class KvShard:
 
     def export_lane(self, seq: int, layer: int, which: int):
         """Stored bytes of lane K (0) / V (1) in the reference [pos][head][d]
-        order, plus int8 scales [pos][head]."""
+        order, plus int8 / int4 scales [pos][head]."""
         n = lib.sd_kv_export_lane(self.h, seq, layer, which, None, 0, None, 0)
         if n < 0:
             _check(int(-n))
         buf = np.zeros(n, dtype=np.uint8)
         L = self.stored_length(seq, layer)
-        sc = np.zeros(L * self._head_count, np.float32) if self._fmt == "int8" else None
+        sc = np.zeros(L * self._head_count, np.float32) if self._fmt in ("int8", "int4") else None
         r = lib.sd_kv_export_lane(self.h, seq, layer, which, buf.ctypes.data_as(C.c_void_p), n,
                                   _fp(sc) if sc is not None else None,
                                   sc.size if sc is not None else 0)

@@ -125,6 +125,16 @@ struct Fmt<SD_KV_INT8> {
     cvt4(r.y, x + 4);
   }
 };
+template <>
+struct Fmt<SD_KV_INT4> {
+  // eight nibbles (element 2i low) -> fp32: nibble n (two's complement q)
+  // xor 8 is q + 8; the float 2^23 + (q + 8) minus 2^23 + 8 is exactly q
+  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p) ^ 0x88888888u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(0x4B000000u | ((u >> (4 * i)) & 0xFu)) - 8388616.0f;
+  }
+};
 
 // --------------------------------------------------------------- K2 ------
 // Persistent split-K decode attention. One CTA per SM walks a contiguous,
@@ -144,7 +154,7 @@ struct Fmt<SD_KV_INT8> {
 template <int FMT, int LPR, int EPL, int MAXH, int G, int CW = kConsumerWarps>
 __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a) {
   constexpr int kConsumerWarps = CW;
-  constexpr int E = Fmt<FMT>::kBytes;
+  constexpr bool QNT = kv_quantized(FMT);
   constexpr int HD = LPR * EPL;
   constexpr int RGW = 32 / LPR;              // row groups per warp
   constexpr int RG = kConsumerWarps * RGW;   // row groups per CTA
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
     nh = cls < ncls ? 1 : 0;
   }
   const int Hq = hkv * G;
-  constexpr int row_bytes = HD * E;
+  constexpr int row_bytes = kv_row_bytes(FMT, HD);
   const int tstep = ncls * PB;
 
   float q[MAXQ][EPL], acc[MAXQ][EPL], m[MAXQ], l[MAXQ];
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
       const uint8_t* Vs = Ks + a.stage_region;
       const float* ksc = nullptr;
       const float* vsc = nullptr;
-      if (FMT == SD_KV_INT8) {
+      if (QNT) {
         if (a.sc_region) {
           ksc = reinterpret_cast<const float*>(Ks + 2 * a.stage_region);
           vsc = reinterpret_cast<const float*>(Ks + 2 * a.stage_region + a.sc_region);
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
                 float kx[8];
-                Fmt<FMT>::load8(kr + (c * LPR + li) * 8 * E, kx);
+                Fmt<FMT>::load8(kr + kv_row_bytes(FMT, (c * LPR + li) * 8), kx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
             const bool act = t < cnt && hh < nh;
             float ks = 1.0f;
             vs[hh][i] = 1.0f;
-            if (FMT == SD_KV_INT8 && act) {
+            if (QNT && act) {
               ks = ksc[t * hkv + hk];
               vs[hh][i] = vsc[t * hkv + hk];
             }
@@ -386,10 +396,10 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
                 float vx[8];
-                Fmt<FMT>::load8(vr + (c * LPR + li) * 8 * E, vx);
+                Fmt<FMT>::load8(vr + kv_row_bytes(FMT, (c * LPR + li) * 8), vx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                  const float pv = FMT == SD_KV_INT8 ? p[hh][i][gg] * vs[hh][i] : p[hh][i][gg];
+                  const float pv = QNT ? p[hh][i][gg] * vs[hh][i] : p[hh][i][gg];
 #pragma unroll
                   for (int e = 0; e < 8; ++e) acc[hh * G + gg][c * 8 + e] = fmaf(pv, vx[e], acc[hh * G + gg][c * 8 + e]);
                 }
@@ -496,6 +506,11 @@ __device__ __forceinline__ float load_elem(const KvGeom& g, const uint8_t* lb, i
   switch (g.fmt) {
     case SD_KV_SINGLE: return reinterpret_cast<const float*>(rows)[idx];
     case SD_KV_HALF: return __half2float(reinterpret_cast<const __half*>(rows)[idx]);
+    case SD_KV_INT4: {
+      const float sc = reinterpret_cast<const float*>(lb + (is_v ? g.vs_off : g.ks_off))[off * g.hc + hk];
+      const int nib = (rows[idx >> 1] >> ((idx & 1) * 4)) & 0xF;
+      return static_cast<float>(nib >= 8 ? nib - 16 : nib) * sc;
+    }
     default: {
       const float sc = reinterpret_cast<const float*>(lb + (is_v ? g.vs_off : g.ks_off))[off * g.hc + hk];
       return static_cast<float>(reinterpret_cast<const int8_t*>(rows)[idx]) * sc;
@@ -599,10 +614,31 @@ __global__ void combine_kernel(const CombineArgs a) {
 }
 
 // --------------------------------------------------------------- K1 ------
+// One warp quantizes one head row (hd values from get(e)): int8 follows
+// quantize_int8 (attention.cpp:28-46) bit for bit — scale = max|x| / 127.0f
+// (IEEE fp32 division), q = clamp(rint((double)x * (1.0 / (double)scale)),
+// +-127); int4 the same rules at +-7, two per byte, element 2i low.
+template <class Get>
+__device__ __forceinline__ void quantize_head(int fmt, int hd, const Get& get, uint8_t* dst, float* scale,
+                                              int lane) {
+  float mx = 0.0f;
+  for (int e = lane; e < hd; e += 32) mx = fmaxf(mx, fabsf(get(e)));
+#pragma unroll
+  for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
+  const double qmax = fmt == SD_KV_INT4 ? 7.0 : 127.0;
+  const float sc = mx == 0.0f ? 0.0f : __fdiv_rn(mx, static_cast<float>(qmax));
+  const double inv = sc == 0.0f ? 0.0 : 1.0 / static_cast<double>(sc);
+  auto q = [&](int e) { return static_cast<int>(fmin(fmax(rint(static_cast<double>(get(e)) * inv), -qmax), qmax)); };
+  if (fmt == SD_KV_INT4) {
+    for (int e = lane; e < hd / 2; e += 32) dst[e] = static_cast<uint8_t>((q(2 * e) & 0xF) | ((q(2 * e + 1) & 0xF) << 4));
+  } else {
+    for (int e = lane; e < hd; e += 32) dst[e] = static_cast<uint8_t>(static_cast<int8_t>(q(e)));
+  }
+  if (lane == 0) *scale = sc;
+}
+
 // One block per (item, K|V) row: convert the fp32 row into the storage
-// format at (slot, layer, position). int8 follows quantize_int8
-// (attention.cpp:28-46) bit for bit: scale = max|x| / 127.0f (IEEE fp32
-// division), q = clamp(rint((double)x * (1.0 / (double)scale)), +-127).
+// format at (slot, layer, position).
 __global__ void append_kernel(const AppendArgs a) {
   pdl_trigger();
   pdl_wait();
@@ -640,26 +676,9 @@ __global__ void append_kernel(const AppendArgs a) {
     // one warp per head
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float* scales = reinterpret_cast<float*>(lb + (is_v ? g.vs_off : g.ks_off)) + off * g.hc;
-    int8_t* d = reinterpret_cast<int8_t*>(row);
     for (int h = warp; h < g.hc; h += nw) {
       const float* x = src + h * g.hd;
-      float mx = 0.0f;
-      for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(x[e]));
-#pragma unroll
-      for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
-      if (mx == 0.0f) {
-        for (int e = lane; e < g.hd; e += 32) d[h * g.hd + e] = 0;
-        if (lane == 0) scales[h] = 0.0f;
-      } else {
-        const float sc = __fdiv_rn(mx, 127.0f);
-        const double inv = 1.0 / static_cast<double>(sc);
-        for (int e = lane; e < g.hd; e += 32) {
-          double r = rint(static_cast<double>(x[e]) * inv);
-          r = fmin(fmax(r, -127.0), 127.0);
-          d[h * g.hd + e] = static_cast<int8_t>(r);
-        }
-        if (lane == 0) scales[h] = sc;
-      }
+      quantize_head(g.fmt, g.hd, [&](int e) { return x[e]; }, row + kv_row_bytes(g.fmt, h * g.hd), scales + h, lane);
     }
   }
 }
@@ -698,20 +717,10 @@ __global__ void prefill_kernel(const KvGeom g, int num_layers, const int32_t* sl
     } else {
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       float* scales = reinterpret_cast<float*>(lb + (kv ? g.vs_off : g.ks_off)) + off * g.hc;
-      int8_t* d = reinterpret_cast<int8_t*>(row);
       for (int h = warp; h < g.hc; h += nw) {
-        float mx = 0.0f;
-        for (int e = lane; e < g.hd; e += 32) mx = fmaxf(mx, fabsf(synth_value(salt ^ (base + h * g.hd + e))));
-#pragma unroll
-        for (int sh = 16; sh > 0; sh >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, sh));
-        const float sc = mx == 0.0f ? 0.0f : __fdiv_rn(mx, 127.0f);
-        const double inv = sc == 0.0f ? 0.0 : 1.0 / static_cast<double>(sc);
-        for (int e = lane; e < g.hd; e += 32) {
-          double rr = rint(static_cast<double>(synth_value(salt ^ (base + h * g.hd + e))) * inv);
-          rr = fmin(fmax(rr, -127.0), 127.0);
-          d[h * g.hd + e] = static_cast<int8_t>(rr);
-        }
-        if (lane == 0) scales[h] = sc;
+        const uint64_t hb = base + static_cast<uint64_t>(h) * g.hd;
+        quantize_head(g.fmt, g.hd, [&](int e) { return synth_value(salt ^ (hb + e)); },
+                      row + kv_row_bytes(g.fmt, h * g.hd), scales + h, lane);
       }
     }
   }
@@ -765,6 +774,7 @@ AttnFn pick(const KvGeom& g, int G) {
     case SD_KV_SINGLE: return pick_fmt<SD_KV_SINGLE>(c, G);
     case SD_KV_HALF: return pick_fmt<SD_KV_HALF>(c, G);
     case SD_KV_INT8: return pick_fmt<SD_KV_INT8>(c, G);
+    case SD_KV_INT4: return pick_fmt<SD_KV_INT4>(c, G);
     default: return nullptr;
   }
 }
@@ -809,7 +819,7 @@ size_t attention_smem_bytes(const KvGeom& g, int T, int nstages, int G, int* sta
   const int region = ((T * g.pos_bytes + 127) / 128) * 128;
   *stage_region = region;
   *sc_region = 0;
-  if (g.fmt == SD_KV_INT8 && g.hc % 4 == 0) *sc_region = ((T * g.hc * 4 + 127) / 128) * 128;
+  if (kv_quantized(g.fmt) && g.hc % 4 == 0) *sc_region = ((T * g.hc * 4 + 127) / 128) * 128;
   size_t bytes = 128 * ((16 * nstages + 127) / 128) +
                  static_cast<size_t>(nstages) * (2 * region + 2 * *sc_region);
   const AttnConfig c = choose_attn_config(g, G);

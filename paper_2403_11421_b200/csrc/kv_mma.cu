@@ -146,6 +146,24 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// eight int4 (one word, element 2i in the low nibble, each biased to q + 8
+// by an xor with 0x88888888) -> four fp16 pairs holding the exact integers
+// q: h[0] = (q0, q4), h[1] = (q1, q5), h[2] = (q2, q6), h[3] = (q3, q7).
+// A nibble or'ed under 0x6400 is fp16 1024 + n (low nibble of a half) or
+// 1024 + 16 n (high nibble): one LOP3 each, then a subtract or an FMA.
+__device__ __forceinline__ void i4x8_to_h2(uint32_t u, uint32_t (&h)[4]) {
+  const uint32_t t = u >> 8;
+  const uint32_t r[4] = {(u & 0x000F000Fu) | 0x64006400u, (u & 0x00F000F0u) | 0x64006400u,
+                         (t & 0x000F000Fu) | 0x64006400u, (t & 0x00F000F0u) | 0x64006400u};
+  const __half2 b_lo = __floats2half2_rn(1032.0f, 1032.0f), m_hi = __floats2half2_rn(0.0625f, 0.0625f),
+                b_hi = __floats2half2_rn(-72.0f, -72.0f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 x = *reinterpret_cast<const __half2*>(&r[i]);
+    const __half2 y = (i & 1) ? __hfma2(x, m_hi, b_hi) : __hsub2(x, b_lo);
+    h[i] = *reinterpret_cast<const uint32_t*>(&y);
+  }
+}
 constexpr int kVPitch = kHD * 2 + 16;
 // int8: per-warp scratch = the dequantized V tile, reused at the end of a
 // piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
@@ -157,6 +175,8 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 template <int G, int FMT, int RPS>
 __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
+  constexpr bool I4 = FMT == SD_KV_INT4;
+  constexpr bool QNT = I8 || I4;  // quantized: scales in the stage, V dequantized into scratch
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
   static_assert(RPS == 2 || RPS == 4, "pair or quad slots");
@@ -173,7 +193,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   // holds position 2m (m < 8) or 2(m-8)+1, i.e. slot m & 7, row m >> 3
   const int ppitch = RPS * a.g.pos_bytes + 16;
   // int8: [K rows][V rows][K scales kT x hc][V scales kT x hc]
-  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + (I8 ? 2 * a.sc_region : 0);
+  const size_t stage_bytes = static_cast<size_t>(2) * a.stage_region + (QNT ? 2 * a.sc_region : 0);
   const KvGeom& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -204,7 +224,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   // scratch of each warp (int8)
   uint8_t* scr = ring + nst * stage_bytes;
   auto merge_slot = [&](int wp) {
-    return I8 ? reinterpret_cast<float*>(scr + wp * kScratch) + lane * 36
+    return QNT ? reinterpret_cast<float*>(scr + wp * kScratch) + lane * 36
               : reinterpret_cast<float*>(scr) + (wp * 32 + lane) * 36;
   };
 
@@ -231,7 +251,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
                               static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
         // scale block rounded up to the bulk-copy granule (16 B): stages start
         // 16-aligned in a page group, so the extra scales stay inside its region
-        const uint32_t scb = I8 ? (static_cast<uint32_t>(cnt * g.hc * 4) + 15u) & ~15u : 0u;
+        const uint32_t scb = QNT ? (static_cast<uint32_t>(cnt * g.hc * 4) + 15u) & ~15u : 0u;
         if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], 2u * cnt * g.pos_bytes + 2u * scb);
@@ -248,7 +268,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
             bulk_g2s(dst, base + (lane >= 16 ? g.v_off : 0) + RPS * pr * g.pos_bytes, nb, &full[stage], pol);
           }
         }
-        if (I8 && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
+        if (QNT && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
           const uint8_t* lb = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes;
           const int off = pos & (g.P - 1);
           uint8_t* dst = ring + stage * stage_bytes + 2 * a.stage_region + (lane ? a.sc_region : 0);
@@ -305,9 +325,15 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           float2 x = make_float2(0.0f, 0.0f);
           // int8 K fragments take 4 contiguous d per lane (a permutation of
           // the dot's k index); Q^T uses the same permutation
-          const int d = I8 ? 16 * kk + 4 * tq + 2 * h : 16 * kk + 8 * h + 2 * tq;
+          // int4: a word of 8 nibbles feeds k-steps 2j, 2j+1 as pairs (d, d + 4)
+          const int d = I8   ? 16 * kk + 4 * tq + 2 * h
+                        : I4 ? 32 * (kk >> 1) + 8 * tq + 2 * (kk & 1) + h
+                             : 16 * kk + 8 * h + 2 * tq;
           const int hq = PACK && gq >= G ? gq - G : gq;  // PACK: column gq >= G is head gq - G's lo part
-          if (hq < G && gq < (PACK ? 2 * G : G)) x = *reinterpret_cast<const float2*>(qrow + hq * kHD + d);
+          if (hq < G && gq < (PACK ? 2 * G : G)) {
+            x = I4 ? make_float2(qrow[hq * kHD + d], qrow[hq * kHD + d + 4])
+                   : *reinterpret_cast<const float2*>(qrow + hq * kHD + d);
+          }
           split2(x.x * a.qscale, x.y * a.qscale, qb[kk][h][0], qb[kk][h][1]);
           if (PACK && gq >= G) qb[kk][h][0] = qb[kk][h][1];  // the MMA's B column gets the lo part
         }
@@ -339,22 +365,39 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q; two
       // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-      if (I8) {
+      if (QNT) {
         // MMA row r holds position (r % NS) * RPS + r / NS: rows gq and gq+8
         // of this lane are rows gq / NS and (gq + 8) / NS of slot gq % NS
         // (pair slots: conflict-free, slot pitch = 4 mod 32 words; quad slots:
         // rows gq and gq + 4 share banks, 2-way)
-        const uint8_t* kb = st8 + hk * kHD + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
+        const uint8_t* kb = st8 + hk * (I4 ? kHD / 2 : kHD) + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
         const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;  // row gq + 8, same slot
+        if (I8) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
-          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
-          const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
-                                  i8x2_to_h2(w1, 0x5342)};
-          float(&acc)[4] = (kk & 1) ? s2 : s;
-          mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
-          if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
+            const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
+                                    i8x2_to_h2(w1, 0x5342)};
+            float(&acc)[4] = (kk & 1) ? s2 : s;
+            mma16816(acc, ka, qb[kk][0][0], qb[kk][1][0]);
+            if (!PACK) mma16816(acc, ka, qb[kk][0][1], qb[kk][1][1]);
+          }
+        } else {
+          // one word per row and lane covers two k-steps (32 head dims per
+          // word column): pairs (q0, q4), (q1, q5) for the even one,
+          // (q2, q6), (q3, q7) for the odd one
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t h0[4], h1[4];
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + 16 * j) ^ 0x88888888u, h0);
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * j) ^ 0x88888888u, h1);
+            const uint32_t ka0[4] = {h0[0], h1[0], h0[1], h1[1]}, ka1[4] = {h0[2], h1[2], h0[3], h1[3]};
+            mma16816(s, ka0, qb[2 * j][0][0], qb[2 * j][1][0]);
+            if (!PACK) mma16816(s, ka0, qb[2 * j][0][1], qb[2 * j][1][1]);
+            mma16816(s2, ka1, qb[2 * j + 1][0][0], qb[2 * j + 1][1][0]);
+            if (!PACK) mma16816(s2, ka1, qb[2 * j + 1][0][1], qb[2 * j + 1][1][1]);
+          }
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) s[i] += s2[i];
@@ -370,13 +413,30 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         // lane l converts word l (4 head dims) of every row: conflict-free
         // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
         uint8_t* vscr = scr + warp * kScratch;
-        const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
-        uint8_t* vd = vscr + 8 * lane;
+        if (I8) {
+          const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
+          uint8_t* vd = vscr + 8 * lane;
 #pragma unroll
-        for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
-          const int slot = m % NS, sub = m / NS;
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
-          *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
+          for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
+            const int slot = m % NS, sub = m / NS;
+            const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
+            *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
+          }
+        } else {
+          // int4: a row is 16 words; half-warps take alternate rows, lane
+          // converts one word (8 head dims) and stores them in d order
+          const uint8_t* vb = st8 + a.stage_region + hk * (kHD / 2) + 4 * (lane & 15);
+          uint8_t* vd = vscr + 16 * (lane & 15);
+#pragma unroll
+          for (int i = 0; i < kT / 2; ++i) {
+            const int m = 2 * i + (lane >> 4);
+            const int slot = m % NS, sub = m / NS;
+            uint32_t h[4];
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x88888888u, h);
+            *reinterpret_cast<uint4*>(vd + m * kVPitch) =
+                make_uint4(__byte_perm(h[0], h[1], 0x5410), __byte_perm(h[2], h[3], 0x5410),
+                           __byte_perm(h[0], h[1], 0x7632), __byte_perm(h[2], h[3], 0x7632));
+          }
         }
         // the V scales too, then the ring slot is free: everything after this
         // reads registers and the warp's scratch, so the producer can refill
@@ -463,7 +523,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         if (!PACK) mma16816(o[mt], va, bl0, bl1);
       }
       __syncwarp();
-      if (!I8 && lane == 0) mbar_arrive(&empty[stage]);  // (int8 released the slot after its loads)
+      if (!QNT && lane == 0) mbar_arrive(&empty[stage]);  // (int8 / int4 released the slot after their loads)
       if (++stage == nst) {
         stage = 0;
         phase ^= 1;
@@ -658,11 +718,11 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 // 2-way ldmatrix conflicts (rows of a slot share bank groups); int8 keeps
 // pair slots, which its 32-bit fragment loads need.
 int attention_mma_rows_per_slot(const KvGeom& g) {
-  return g.fmt == SD_KV_HALF || tuning().attn_i8_quad ? 4 : 2;
+  return g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT4 || tuning().attn_i8_quad ? 4 : 2;
 }
 
 bool attention_mma_supported(const KvGeom& g, int G) {
-  return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8) && g.hd == kHD &&
+  return (g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT8 || g.fmt == SD_KV_INT4) && g.hd == kHD &&
          (g.hc == 8 || g.hc == 4 || g.hc == 2 || g.hc == 1) && (G == 2 || G == 4 || G == 8) && g.P % kT == 0;
 }
 
@@ -670,15 +730,16 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   // kT/2 pair slots of two rows + a 16-B pad
   const int rps = attention_mma_rows_per_slot(g);
   *stage_region = (kT / rps) * (rps * g.pos_bytes + 16);
-  *sc_region = g.fmt == SD_KV_INT8 ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
+  const bool qnt = kv_quantized(g.fmt);
+  *sc_region = qnt ? ((kT * g.hc * 4 + 127) / 128) * 128 : 0;
   const size_t stage = 2 * static_cast<size_t>(*stage_region) + 2 * static_cast<size_t>(*sc_region);
-  const int warps = g.fmt == SD_KV_INT8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>();
-  const size_t scratch = g.fmt == SD_KV_INT8 ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
+  const int warps = consumer_warps<SD_KV_HALF>();
+  const size_t scratch = qnt ? static_cast<size_t>(warps) * kScratch  // V tiles + merge slots
                          : (g.hc < warps ? static_cast<size_t>(warps) * 32 * 36 * 4 : 0);  // merge slots
   // fp16: two 64-KB stages stream faster than three (0.605 vs 0.643 ms per C5
   // layer, tools/bench_rpart.py, round 2); int8 (34-KB stages) is flat from
   // three to five stages and slower at two
-  const int dflt = g.fmt == SD_KV_HALF ? 2 : 5;
+  const int dflt = g.fmt == SD_KV_HALF ? 2 : g.fmt == SD_KV_INT8 ? 5 : 8;
   // The ring depth is a multiple of the P = warps / hc position classes, so
   // every fill of a slot is consumed by the same class: a class then waits on
   // a slot's full barrier only after it consumed the slot's previous fill, and
@@ -695,15 +756,18 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
-  const bool i8 = a.g.fmt == SD_KV_INT8;
+  const bool i8 = a.g.fmt == SD_KV_INT8, i4 = a.g.fmt == SD_KV_INT4;
   const bool quad = attention_mma_rows_per_slot(a.g) == 4;
   switch (a.G) {
-    case 2: fn = i8 ? (quad ? attn_mma_kernel<2, SD_KV_INT8, 4> : attn_mma_kernel<2, SD_KV_INT8, 2>)
-                    : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
-    case 4: fn = i8 ? (quad ? attn_mma_kernel<4, SD_KV_INT8, 4> : attn_mma_kernel<4, SD_KV_INT8, 2>)
-                    : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
-    case 8: fn = i8 ? (quad ? attn_mma_kernel<8, SD_KV_INT8, 4> : attn_mma_kernel<8, SD_KV_INT8, 2>)
-                    : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
+    case 2: fn = i4 ? attn_mma_kernel<2, SD_KV_INT4, 4>
+                 : i8 ? (quad ? attn_mma_kernel<2, SD_KV_INT8, 4> : attn_mma_kernel<2, SD_KV_INT8, 2>)
+                      : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
+    case 4: fn = i4 ? attn_mma_kernel<4, SD_KV_INT4, 4>
+                 : i8 ? (quad ? attn_mma_kernel<4, SD_KV_INT8, 4> : attn_mma_kernel<4, SD_KV_INT8, 2>)
+                      : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
+    case 8: fn = i4 ? attn_mma_kernel<8, SD_KV_INT4, 4>
+                 : i8 ? (quad ? attn_mma_kernel<8, SD_KV_INT8, 4> : attn_mma_kernel<8, SD_KV_INT8, 2>)
+                      : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   // the dynamic-smem opt-in once per instantiation and size
@@ -718,7 +782,7 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
       set.emplace_back(fn, smem);
     }
   }
-  const int threads = ((i8 ? consumer_warps<SD_KV_INT8>() : consumer_warps<SD_KV_HALF>()) + 1) * 32;
+  const int threads = (consumer_warps<SD_KV_HALF>() + 1) * 32;
   SD_CUDA(launch_pdl(fn, dim3(grid), dim3(threads), smem, s, 1, a));
   SD_CUDA(cudaGetLastError());
   count_launch();

@@ -16,7 +16,6 @@ namespace {
 
 int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
-int elem_bytes(int fmt) { return fmt == SD_KV_SINGLE ? 4 : fmt == SD_KV_HALF ? 2 : 1; }
 
 }  // namespace
 
@@ -29,7 +28,8 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
     fail(SD_ERR_CONFIG, "shard head range outside the model's heads");
   }
   if (capacity_tokens < 1) fail(SD_ERR_CONFIG, "shard capacity must be >= 1");
-  if (fmt < SD_KV_SINGLE || fmt > SD_KV_INT8) fail(SD_ERR_CONFIG, "unknown kv storage format");
+  if (fmt < SD_KV_SINGLE || fmt > SD_KV_INT4) fail(SD_ERR_CONFIG, "unknown kv storage format");
+  if (fmt == SD_KV_INT4 && spec.hd % 2) fail(SD_ERR_CONFIG, "int4 kv storage needs an even head_dim");
   G_ = spec.H / spec.Hkv;
   DeviceGuard dg(device);
   SD_CUDA(cudaDeviceGetAttribute(&nsm_, cudaDevAttrMultiProcessorCount, device));
@@ -58,11 +58,11 @@ KvStore::KvStore(const Spec& spec, int head_start, int head_count, int64_t capac
   g.log2P = 0;
   while ((1 << g.log2P) < P) ++g.log2P;
   g.max_pages = max_pages;
-  g.pos_bytes = g.width * elem_bytes(fmt);
+  g.pos_bytes = kv_row_bytes(fmt, g.width);
   const int64_t lane_bytes = round_up(static_cast<int64_t>(P) * g.pos_bytes, 128);
   g.v_off = lane_bytes;
   int64_t lb = 2 * lane_bytes;
-  if (fmt == SD_KV_INT8) {
+  if (kv_quantized(fmt)) {
     const int64_t sb = round_up(static_cast<int64_t>(P) * head_count * 4, 128);
     g.ks_off = lb;
     g.vs_off = lb + sb;
@@ -149,6 +149,7 @@ int64_t KvStore::bytes_per_token() const {  // attention.cpp:296-305
   switch (geom_.fmt) {
     case SD_KV_SINGLE: return 2 * w * 4;
     case SD_KV_HALF: return 2 * w * 2;
+    case SD_KV_INT4: return 2 * (w / 2 + static_cast<int64_t>(head_count_) * 4);
     default: return 2 * (w + static_cast<int64_t>(head_count_) * 4);
   }
 }
@@ -608,9 +609,8 @@ void KvStore::launch_attention_plan(Plan& P, int layer, const float* q, int64_t 
   if (timed) {
     SD_CUDA(cudaEventRecord(e1, s));
     ev_pending_.emplace_back(e0, e1);
-    const double e = geom_.fmt == SD_KV_SINGLE ? 4 : geom_.fmt == SD_KV_HALF ? 2 : 1;
-    double bytes = static_cast<double>(P.positions) * 2 * geom_.width * e;
-    if (geom_.fmt == SD_KV_INT8) bytes += static_cast<double>(P.positions) * 2 * geom_.hc * 4;
+    double bytes = static_cast<double>(P.positions) * 2 * geom_.pos_bytes;
+    if (kv_quantized(geom_.fmt)) bytes += static_cast<double>(P.positions) * 2 * geom_.hc * 4;
     bytes += static_cast<double>(P.slots.size()) * q_width() * 4 * 2;  // q in, o out
     ev_bytes_.push_back(bytes);
   }
@@ -671,7 +671,7 @@ int64_t KvStore::export_lane(uint64_t seq, int layer, int which, void* host, siz
                          static_cast<size_t>(cnt) * geom_.pos_bytes, cudaMemcpyDeviceToHost));
     }
   }
-  if (scales && geom_.fmt == SD_KV_INT8 &&
+  if (scales && kv_quantized(geom_.fmt) &&
       static_cast<size_t>(len) * head_count_ <= scales_count) {
     for (int p0 = 0; p0 < len; p0 += geom_.P) {
       const int cnt = std::min(geom_.P, len - p0);

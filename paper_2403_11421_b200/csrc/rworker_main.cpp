@@ -13,7 +13,7 @@
 
 static int usage() {
   std::fprintf(stderr,
-               "usage: sd_rworker serve --capacity TOKENS [--listen HOST:PORT] [--storage single|half|int8]\n"
+               "usage: sd_rworker serve --capacity TOKENS [--listen HOST:PORT] [--storage single|half|int8|int4]\n"
                "                        [--port-file PATH] [--once] [--timeout SECONDS] [--device N]\n");
   return 2;
 }
@@ -52,7 +52,11 @@ int main(int argc, char** argv) {
     }
   }
   if (capacity < 1) return usage();
-  const int fmt = storage == "single" ? SD_KV_SINGLE : storage == "half" ? SD_KV_HALF : storage == "int8" ? SD_KV_INT8 : -1;
+  const int fmt = storage == "single" ? SD_KV_SINGLE
+                  : storage == "half" ? SD_KV_HALF
+                  : storage == "int8" ? SD_KV_INT8
+                  : storage == "int4" ? SD_KV_INT4  // extension (sd_abi.h)
+                                      : -1;
   if (fmt < 0) {
     std::fprintf(stderr, "sd_rworker: unknown kv storage format: %s\n", storage.c_str());
     return 2;

@@ -106,6 +106,13 @@ __device__ __forceinline__ uint32_t pack16x2(float lo, float hi, int f16) {
   return static_cast<uint32_t>(to16(lo, f16)) | (static_cast<uint32_t>(to16(hi, f16)) << 16);
 }
 
+// KV storage formats: the quantized ones carry per-(position, head) fp32
+// scales; bytes of n elements of a row (int4: two per byte)
+__host__ __device__ constexpr bool kv_quantized(int fmt) { return fmt == SD_KV_INT8 || fmt == SD_KV_INT4; }
+__host__ __device__ constexpr int kv_row_bytes(int fmt, int n) {
+  return fmt == SD_KV_SINGLE ? 4 * n : fmt == SD_KV_HALF ? 2 * n : fmt == SD_KV_INT8 ? n : n / 2;
+}
+
 // Counter-based synthetic value in [-1, 1) (SURVEY §8d bench prefill)
 __host__ __device__ inline float synth_value(uint64_t idx) {
   return 2.0f * (static_cast<float>(mix64(0x5EEDull ^ idx) >> 40) * 0x1p-24f) - 1.0f;

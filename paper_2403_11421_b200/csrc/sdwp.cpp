@@ -198,7 +198,9 @@ int json_int(const Json& j, const char* key) {
   return static_cast<int>(v->num);
 }
 
-const char* format_name(int fmt) { return fmt == SD_KV_SINGLE ? "single" : fmt == SD_KV_HALF ? "half" : "int8"; }
+const char* format_name(int fmt) {
+  return fmt == SD_KV_SINGLE ? "single" : fmt == SD_KV_HALF ? "half" : fmt == SD_KV_INT8 ? "int8" : "int4";
+}
 
 // nlohmann::json::dump() of a flat object: keys sorted, no spaces
 std::string dump_sorted(const std::map<std::string, std::string>& kv) {
@@ -414,7 +416,7 @@ Message make_error(uint16_t code, const std::string& message) {
 WorkerSession::WorkerSession(int64_t capacity_tokens, int kv_format, int device)
     : cap_(capacity_tokens), fmt_(kv_format), device_(device) {
   if (capacity_tokens < 1) fail(SD_ERR_CONFIG, "shard capacity must be >= 1");
-  if (kv_format < SD_KV_SINGLE || kv_format > SD_KV_INT8) fail(SD_ERR_CONFIG, "unknown kv storage format");
+  if (kv_format < SD_KV_SINGLE || kv_format > SD_KV_INT4) fail(SD_ERR_CONFIG, "unknown kv storage format");
 }
 
 std::vector<Message> WorkerSession::handle(const Message& m) {

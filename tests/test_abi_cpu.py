@@ -36,6 +36,17 @@ def test_spec_and_errors_match_reference():
         sd.make_model_spec(0, 64, 4, 256, 128)
 
 
+def test_kv_format_validation_before_any_device_work():
+    """Storage formats: unknown ones and int4 over an odd head_dim are
+    config errors, raised before the store touches a device."""
+    import paper_2403_11421_b200 as sd
+    odd = sd.make_model_spec(1, 12, 4, 8, 8)  # head_dim 3
+    with pytest.raises(sd.ConfigError, match="even head_dim"):
+        sd.KvShard(odd, 0, 4, 8, "int4")
+    with pytest.raises(KeyError):
+        sd.KvShard(odd, 0, 4, 8, "int2")
+
+
 def test_mix64_prompt_tokens_match_oracle(oracle):
     import paper_2403_11421_b200 as sd
     for x in [0, 1, 42, 2**63 + 5, 2**64 - 1]:

@@ -117,6 +117,11 @@ CASES = [
     (1, 4096, 32, 0, "half", 3, 90),       # Llama-2-7B head geometry
     (1, 5120, 40, 0, "half", 3, 70),       # Llama-2-13B head geometry (3 heads per row group)
     (1, 4096, 32, 8, "half", 3, 90),       # Llama-3-8B GQA geometry
+    # int4 KV (extension: the paper's 4-bit hook)
+    (2, 64, 4, 0, "int4", 5, 40),          # hd 16, CUDA-core K2
+    (1, 48, 4, 0, "int4", 4, 30),          # hd 12: rows not 16-B multiples, generic path
+    (1, 4096, 32, 0, "int4", 3, 90),       # Llama-2-7B heads, K2
+    (1, 2048, 16, 4, "int4", 6, 150),      # GQA hd 128, tensor-core K2m
 ]
 
 
@@ -155,7 +160,7 @@ def test_ragged_batch_parity_vs_oracle(sd, oracle, case):
             bg, sg = gpu.export_lane(seqs[i], 0, which)
             bc, sc = cpu.export_lane(seqs[i], 0, which)
             assert np.array_equal(bg, bc)
-            if fmt == "int8":
+            if fmt in ("int8", "int4"):
                 assert np.array_equal(sg.view(np.uint32), sc.view(np.uint32))
 
 
@@ -181,7 +186,7 @@ def test_many_sequences_split_and_combine(sd, oracle):
 
 
 @pytest.mark.parametrize("stages", [0, 2, 3])
-@pytest.mark.parametrize("fmt", ["half", "int8"])
+@pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
 @pytest.mark.parametrize("h0,hc", [(4, 4), (2, 2), (7, 1)])
 def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages):
     """Shards holding 4 / 2 / 1 of 8 kv heads (by-head / hybrid ShardMap):
@@ -215,7 +220,7 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages):
     assert err < 2e-5, err
 
 
-@pytest.mark.parametrize("fmt", ["half", "int8"])
+@pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt):
     """fp16 / int8 KV, hd 128, 8 kv heads: the mma.sync attention path

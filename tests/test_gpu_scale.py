@@ -96,7 +96,25 @@ def test_c5_prefill_is_sequence_keyed_and_bit_exact(sd, oracle):
         assert lane[pos, h, d] == np.float32(np.float16(v))
 
 
-@pytest.mark.parametrize("fmt,bar", [("half", 2e-5), ("int8", 2e-5)])
+@pytest.mark.parametrize("fmt", ["int8", "int4"])
+def test_c5_quantized_prefill_bit_exact(sd, oracle, fmt):
+    """The synthetic prefill in the quantized formats: bytes and scales equal
+    the oracle's quantize_int8 / quantize_int4 of the same values."""
+    spec = sd.make_model_spec(*C5)
+    seqs = [5, 9]
+    kv = sd.KvShard(spec, 0, 8, 2 * 40, fmt, max_sequences=2, max_seq_len=40)
+    kv.prefill_synthetic(seqs, 33)
+    okv = oracle.KvShard(oracle.make_spec(*C5), 0, 8, 2 * 40, fmt)
+    okv.prefill_synthetic(seqs, 33)
+    for q in seqs:
+        for layer in range(2):
+            for which in (0, 1):
+                (bg, sg), (bc, sc) = kv.export_lane(q, layer, which), okv.export_lane(q, layer, which)
+                assert bg.size == 33 * 8 * (128 if fmt == "int8" else 64)
+                assert np.array_equal(bg, bc) and np.array_equal(sg.view(np.uint32), sc.view(np.uint32))
+
+
+@pytest.mark.parametrize("fmt,bar", [("half", 2e-5), ("int8", 2e-5), ("int4", 2e-5)])
 def test_c5_attention_at_bench_scale(sd, oracle, fmt, bar):
     """The tensor-core GQA attention (K2m) over the bench's batch and context
     (512 sequences x 2048 positions, 8 kv heads, G=4), one shared q: sampled

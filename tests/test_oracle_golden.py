@@ -210,6 +210,46 @@ def test_bytes_per_token(oracle):
     assert oracle.KvShard(s, 0, 4, 8, "single").bytes_per_token() == 2 * 32 * 4
     assert oracle.KvShard(s, 0, 4, 8, "half").bytes_per_token() == 2 * 32 * 2
     assert oracle.KvShard(s, 0, 4, 8, "int8").bytes_per_token() == 2 * (32 + 4 * 4)
+    assert oracle.KvShard(s, 0, 4, 8, "int4").bytes_per_token() == 2 * (16 + 4 * 4)
+
+
+def test_int4_codec_follows_the_int8_rules(oracle):
+    """The 4-bit extension restated independently in
+    numpy: scale = fp32(max|x| / 7), q = clamp(round-half-even(x * (1 / scale)
+    in double), +-7), element 2i in the low nibble; zeros give scale 0."""
+    rng = np.random.default_rng(4)
+    cases = [rng.uniform(-1, 1, 128).astype(np.float32), np.zeros(16, np.float32),
+             np.array([7, -7, 3.5, -3.5, 0.5, -0.5, 1e-30, 6.999], np.float32)]
+    for x in cases:
+        packed, sc = oracle.quantize_int4(x)
+        mx = np.float32(np.abs(x).max())
+        want_sc = np.float32(mx / np.float32(7.0)) if mx else np.float32(0)
+        assert np.float32(sc) == want_sc
+        inv = 1.0 / float(want_sc) if want_sc else 0.0
+        want = np.clip(np.rint(x.astype(np.float64) * inv), -7, 7).astype(np.int8)
+        assert np.array_equal(oracle.unpack_int4(packed, x.size), want)
+        nib = (want & 0xF).astype(np.uint8)
+        assert np.array_equal(packed, nib[0::2] | (nib[1::2] << 4))
+
+
+def test_int4_storage_within_bounds(oracle):
+    """int4 attention against fp32 storage on the reference's bounds test
+    inputs (test_attention.cpp:165-203): 4 bits of mantissa per element."""
+    vec = rnd_stream(13)
+    s = oracle.make_spec(1, 32, 4, 8, 8)
+    w4 = 0.0
+    for trial in range(30):
+        sh = {f: oracle.KvShard(s, 0, 4, 256, f) for f in ("single", "int4")}
+        n = 1 + oracle.mix64(1000 + trial) % 32
+        for pos in range(n):
+            q, k, v = vec(32), vec(32), vec(32)
+            for kv in sh.values():
+                kv.append_request(0, [1], [pos], k[None], v[None])
+        base = sh["single"].attend(0, [1], q[None])
+        w4 = max(w4, float(np.abs(sh["int4"].attend(0, [1], q[None]) - base).max()))
+    assert 1e-3 < w4 < 0.5
+    with pytest.raises(oracle.OracleError, match="even head_dim"):
+        oracle.KvShard(oracle.make_spec(1, 12, 4, 8, 8), 0, 4, 8, "int4")
 
 
 def test_shardmap_cases(oracle):
