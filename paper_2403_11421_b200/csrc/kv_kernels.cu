@@ -110,10 +110,10 @@ struct Fmt<SD_KV_HALF> {
 template <>
 struct Fmt<SD_KV_INT8> {
   static constexpr int kBytes = 1;
-  // int8 -> fp32 without I2F: byte b becomes the float 2^23 + (b + 128)
-  // (one PRMT into 0x4B0000xx), minus 2^23 + 128: exact, equal to (float)b
-  __device__ static __forceinline__ void cvt4(uint32_t w, float* x) {
-    const uint32_t u = w ^ 0x80808080u;
+  // int8 -> fp32 without I2F: the pool stores q + 128 (kv_store.h), so
+  // byte u becomes the float 2^23 + u (one PRMT into 0x4B0000xx), minus
+  // 2^23 + 128: exact, equal to (float)q
+  __device__ static __forceinline__ void cvt4(uint32_t u, float* x) {
     x[0] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7650)) - 8388736.0f;
     x[1] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7651)) - 8388736.0f;
     x[2] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7652)) - 8388736.0f;
@@ -127,10 +127,10 @@ struct Fmt<SD_KV_INT8> {
 };
 template <>
 struct Fmt<SD_KV_INT4> {
-  // eight nibbles (element 2i low) -> fp32: nibble n (two's complement q)
-  // xor 8 is q + 8; the float 2^23 + (q + 8) minus 2^23 + 8 is exactly q
+  // eight nibbles (element 2i low) holding q + 8 -> fp32: the float
+  // 2^23 + (q + 8) minus 2^23 + 8 is exactly q
   __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
-    const uint32_t u = *reinterpret_cast<const uint32_t*>(p) ^ 0x88888888u;
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(0x4B000000u | ((u >> (4 * i)) & 0xFu)) - 8388616.0f;
   }
@@ -508,12 +508,11 @@ __device__ __forceinline__ float load_elem(const KvGeom& g, const uint8_t* lb, i
     case SD_KV_HALF: return __half2float(reinterpret_cast<const __half*>(rows)[idx]);
     case SD_KV_INT4: {
       const float sc = reinterpret_cast<const float*>(lb + (is_v ? g.vs_off : g.ks_off))[off * g.hc + hk];
-      const int nib = (rows[idx >> 1] >> ((idx & 1) * 4)) & 0xF;
-      return static_cast<float>(nib >= 8 ? nib - 16 : nib) * sc;
+      return static_cast<float>(static_cast<int>((rows[idx >> 1] >> ((idx & 1) * 4)) & 0xF) - 8) * sc;
     }
     default: {
       const float sc = reinterpret_cast<const float*>(lb + (is_v ? g.vs_off : g.ks_off))[off * g.hc + hk];
-      return static_cast<float>(reinterpret_cast<const int8_t*>(rows)[idx]) * sc;
+      return static_cast<float>(static_cast<int>(rows[idx]) - 128) * sc;
     }
   }
 }
@@ -617,7 +616,10 @@ __global__ void combine_kernel(const CombineArgs a) {
 // One warp quantizes one head row (hd values from get(e)): int8 follows
 // quantize_int8 (attention.cpp:28-46) bit for bit — scale = max|x| / 127.0f
 // (IEEE fp32 division), q = clamp(rint((double)x * (1.0 / (double)scale)),
-// +-127); int4 the same rules at +-7, two per byte, element 2i low.
+// +-127); int4 the same rules at +-7, two per byte, element 2i low. Stored
+// offset-binary: q + 128 (int8), q + 8 (int4 nibbles), so the readers turn
+// bytes into exact fp16 / fp32 integers without an xor; export_lane gives
+// the reference's two's-complement bytes back.
 template <class Get>
 __device__ __forceinline__ void quantize_head(int fmt, int hd, const Get& get, uint8_t* dst, float* scale,
                                               int lane) {
@@ -630,9 +632,9 @@ __device__ __forceinline__ void quantize_head(int fmt, int hd, const Get& get, u
   const double inv = sc == 0.0f ? 0.0 : 1.0 / static_cast<double>(sc);
   auto q = [&](int e) { return static_cast<int>(fmin(fmax(rint(static_cast<double>(get(e)) * inv), -qmax), qmax)); };
   if (fmt == SD_KV_INT4) {
-    for (int e = lane; e < hd / 2; e += 32) dst[e] = static_cast<uint8_t>((q(2 * e) & 0xF) | ((q(2 * e + 1) & 0xF) << 4));
+    for (int e = lane; e < hd / 2; e += 32) dst[e] = static_cast<uint8_t>((q(2 * e) + 8) | ((q(2 * e + 1) + 8) << 4));
   } else {
-    for (int e = lane; e < hd; e += 32) dst[e] = static_cast<uint8_t>(static_cast<int8_t>(q(e)));
+    for (int e = lane; e < hd; e += 32) dst[e] = static_cast<uint8_t>(q(e) + 128);
   }
   if (lane == 0) *scale = sc;
 }

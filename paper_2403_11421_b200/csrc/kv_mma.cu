@@ -135,8 +135,8 @@ __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_
   lo = pack_h2(x0 - hf.x, x1 - hf.y);
 }
 
-// four int8 (one 32-bit word) -> two fp16 pairs holding the exact integers:
-// byte b becomes fp16 1024 + (b + 128) (0x64xx), minus 1152. (Folding the
+// four int8 (one 32-bit word, stored q + 128) -> two fp16 pairs holding the
+// exact integers: byte u becomes fp16 1024 + u (0x64xx), minus 1152. (Folding the
 // 1152 bias out of the MMAs instead — subtracting 1152 x the other operand's
 // column sums from the accumulators — saves the HSUB2s but costs ~7 bits of
 // the fp32 accumulation at context 2048: 1.3e-4 error, measured; kept out.)
@@ -146,8 +146,8 @@ __device__ __forceinline__ uint32_t i8x2_to_h2(uint32_t u, uint32_t sel) {
   h = __hsub2(h, __floats2half2_rn(1152.0f, 1152.0f));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
-// eight int4 (one word, element 2i in the low nibble, each biased to q + 8
-// by an xor with 0x88888888) -> four fp16 pairs holding the exact integers
+// eight int4 (one word, element 2i in the low nibble, each stored q + 8)
+// -> four fp16 pairs holding the exact integers
 // q: h[0] = (q0, q4), h[1] = (q1, q5), h[2] = (q2, q6), h[3] = (q3, q7).
 // A nibble or'ed under 0x6400 is fp16 1024 + n (low nibble of a half) or
 // 1024 + 16 n (high nibble): one LOP3 each, then a subtract or an FMA.
@@ -375,8 +375,8 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         if (I8) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk) ^ 0x80808080u;
-            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk) ^ 0x80808080u;
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk);
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * kk);
             const uint32_t ka[4] = {i8x2_to_h2(w0, 0x5140), i8x2_to_h2(w1, 0x5140), i8x2_to_h2(w0, 0x5342),
                                     i8x2_to_h2(w1, 0x5342)};
             float(&acc)[4] = (kk & 1) ? s2 : s;
@@ -390,8 +390,8 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             uint32_t h0[4], h1[4];
-            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + 16 * j) ^ 0x88888888u, h0);
-            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * j) ^ 0x88888888u, h1);
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + 16 * j), h0);
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * j), h1);
             const uint32_t ka0[4] = {h0[0], h1[0], h0[1], h1[1]}, ka1[4] = {h0[2], h1[2], h0[3], h1[3]};
             mma16816(s, ka0, qb[2 * j][0][0], qb[2 * j][1][0]);
             if (!PACK) mma16816(s, ka0, qb[2 * j][0][1], qb[2 * j][1][1]);
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 #pragma unroll
           for (int m = 0; m < kT; ++m) {  // scratch row m = MMA row m (position pair mapping)
             const int slot = m % NS, sub = m / NS;
-            const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x80808080u;
+            const uint32_t u = *reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes);
             *reinterpret_cast<uint2*>(vd + m * kVPitch) = make_uint2(i8x2_to_h2(u, 0x5140), i8x2_to_h2(u, 0x5342));
           }
         } else {
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
             const int m = 2 * i + (lane >> 4);
             const int slot = m % NS, sub = m / NS;
             uint32_t h[4];
-            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes) ^ 0x88888888u, h);
+            i4x8_to_h2(*reinterpret_cast<const uint32_t*>(vb + slot * ppitch + sub * g.pos_bytes), h);
             *reinterpret_cast<uint4*>(vd + m * kVPitch) =
                 make_uint4(__byte_perm(h[0], h[1], 0x5410), __byte_perm(h[2], h[3], 0x5410),
                            __byte_perm(h[0], h[1], 0x7632), __byte_perm(h[2], h[3], 0x7632));

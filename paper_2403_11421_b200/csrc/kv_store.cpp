@@ -670,6 +670,13 @@ int64_t KvStore::export_lane(uint64_t seq, int layer, int which, void* host, siz
       SD_CUDA(cudaMemcpy(static_cast<uint8_t*>(host) + static_cast<int64_t>(p0) * geom_.pos_bytes, src,
                          static_cast<size_t>(cnt) * geom_.pos_bytes, cudaMemcpyDeviceToHost));
     }
+    // the pool holds offset-binary codes (q + 128, nibbles q + 8): give the
+    // reference's two's-complement bytes back
+    if (kv_quantized(geom_.fmt)) {
+      const uint8_t flip = geom_.fmt == SD_KV_INT8 ? 0x80 : 0x88;
+      uint8_t* h = static_cast<uint8_t*>(host);
+      for (int64_t i = 0; i < bytes; ++i) h[i] ^= flip;
+    }
   }
   if (scales && kv_quantized(geom_.fmt) &&
       static_cast<size_t>(len) * head_count_ <= scales_count) {
