@@ -251,8 +251,10 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
  * separate KV append kernel), "fused_argmax" (0: logits + argmax kernel),
  * "dist_fuse" (0: scatter kernel for the peer exchange), "attn_mma" (0:
  * CUDA-core attention), "pdl" (0: no programmatic dependent launch),
- * "dist_phases" (1: per-phase DistEngine timing on stderr). Unknown names
- * return SD_ERR_CONFIG. */
+ * "dist_phases" (1: per-phase DistEngine timing on stderr), "attn_i8_quad",
+ * "attn_l2_prefetch", "attn_max_stages" (attention copy / prefetch / ring
+ * depth variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
+ * instead of integer ones). Unknown names return SD_ERR_CONFIG. */
 int sd_tune(const char* name, int value);
 /* Kernel launches issued by this library in this process (all devices). */
 int64_t sd_launch_count(void);

@@ -164,6 +164,17 @@ __device__ __forceinline__ void i4x8_to_h2(uint32_t u, uint32_t (&h)[4]) {
     h[i] = *reinterpret_cast<const uint32_t*>(&y);
   }
 }
+// D (+)= A . B, m16n8k32, A unsigned bytes (offset-binary K codes), B signed
+// bytes (a q limb), exact int32 accumulate
+__device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// the low byte of x as a signed value
+__device__ __forceinline__ int sbyte(int x) { return static_cast<int>(static_cast<int8_t>(x & 0xFF)); }
 constexpr int kVPitch = kHD * 2 + 16;
 // int8: per-warp scratch = the dequantized V tile, reused at the end of a
 // piece as the warp's softmax-state merge slot (32 lanes x 36 floats)
@@ -172,11 +183,21 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }  // bytes per row of a warp's dequantized V tile
 
-template <int G, int FMT, int RPS>
+// IM (quantized KV only): the scores on integer tensor cores. K codes are
+// exact unsigned bytes (int4: nibbles unpacked to bytes with two LOP3s) and
+// q is carried as a 22-bit fixed-point integer per head (scale 2^(22-E),
+// E = exponent of the head's max |q|) split into three signed byte limbs:
+// three m16n8k32 IMMAs per 32 head dims give the exact int32 dot of each
+// limb, the codes' offset (128 / 8 x the limb's column sum) preloaded into
+// the accumulators; the limbs recombine in fp32. No per-element conversion
+// of K at all, where the fp16 path spends a byte permute and a subtract per
+// two values.
+template <int G, int FMT, int RPS, bool IM = false>
 __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
   constexpr bool I4 = FMT == SD_KV_INT4;
   constexpr bool QNT = I8 || I4;  // quantized: scales in the stage, V dequantized into scratch
+  static_assert(!IM || QNT, "integer scores need quantized KV");
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
   static_assert(RPS == 2 || RPS == 4, "pair or quad slots");
@@ -309,6 +330,11 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   float o[8][4];      // O^T fragments: hd rows 16*mt + {gq, gq+8}, heads {2tq, 2tq+1}
   float m[2], l[2];   // per head 2tq, 2tq+1 (replicated over gq lanes; l partial per lane)
   uint32_t qb[8][2][2];  // Q^T B-fragments: [k-step][b0|b1][hi|lo]
+  // IM: q limbs as B fragments [limb][k32-step][b0|b1]; per output column
+  // (heads 2tq', 2tq'+1) the accumulator preload and the fixed-point scale
+  uint32_t ql[3][4][2];
+  int qinit[3][2];
+  float qdown[2];
   int stage = 0;
   uint32_t phase = 0;
   // ldmatrix lane address components
@@ -316,7 +342,62 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 
   for (int w = cb; w < ce; ++w) {
     const Piece pc = a.pieces[w];
-    {
+    if constexpr (IM) {
+      // B column gq = head gq (< G); k slot i of step s, half h is head dim
+      // 32s + 16h + 4tq + i (int8: a lane's 4 K bytes) or 32s + 8tq + 2i + h
+      // (int4: low / high nibbles of a lane's K word)
+      const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride + static_cast<int64_t>(hk) * G * kHD;
+      const bool colv = gq < G;
+      float xv[4][2][4];
+      float mx = 0.0f;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int d = I8 ? 32 * s + 16 * h + 4 * tq + i : 32 * s + 8 * tq + 2 * i + h;
+            xv[s][h][i] = colv ? qrow[gq * kHD + d] * a.qscale : 0.0f;
+            mx = fmaxf(mx, fabsf(xv[s][h][i]));
+          }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      int E = 0;
+      if (mx > 0.0f) frexpf(mx, &E);  // mx < 2^E
+      const float up = ldexpf(1.0f, 22 - E), down = ldexpf(1.0f, E - 22);
+      int cs[3] = {0, 0, 0};
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[3] = {0u, 0u, 0u};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            // |n| < 2^22: balanced base-256 digits n = l0 * 2^16 + l1 * 2^8 + l2
+            const int n = __float2int_rn(xv[s][h][i] * up);
+            const int l2 = sbyte(n), r = (n - l2) >> 8;
+            const int l1 = sbyte(r), l0 = (r - l1) >> 8;
+            cs[0] += l0;
+            cs[1] += l1;
+            cs[2] += l2;
+            pk[0] |= static_cast<uint32_t>(l0 & 0xFF) << (8 * i);
+            pk[1] |= static_cast<uint32_t>(l1 & 0xFF) << (8 * i);
+            pk[2] |= static_cast<uint32_t>(l2 & 0xFF) << (8 * i);
+          }
+#pragma unroll
+          for (int t = 0; t < 3; ++t) ql[t][s][h] = pk[t];
+        }
+      const int bias = I8 ? 128 : 8;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 1);
+        cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 2);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) qinit[t][j] = -bias * __shfl_sync(0xffffffffu, cs[t], 4 * ((2 * tq + j) & 7));
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) qdown[j] = __shfl_sync(0xffffffffu, down, 4 * ((2 * tq + j) & 7));
+    } else {
       const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride + static_cast<int64_t>(hk) * G * kHD;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
@@ -365,6 +446,49 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       // ---- S^T = K . Q^T  (16 positions x 8 heads), hi + lo parts of q; two
       // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if constexpr (IM) {
+        const uint8_t* kb = st8 + hk * (I4 ? kHD / 2 : kHD) + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
+        const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;  // row gq + 8, same slot
+        int dacc[3][4];
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          dacc[t][0] = dacc[t][2] = qinit[t][0];
+          dacc[t][1] = dacc[t][3] = qinit[t][1];
+        }
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+          uint32_t ka[4];
+          if (I8) {
+            ka[0] = *reinterpret_cast<const uint32_t*>(kb + 32 * st);
+            ka[1] = *reinterpret_cast<const uint32_t*>(kb + krow8 + 32 * st);
+            ka[2] = *reinterpret_cast<const uint32_t*>(kb + 32 * st + 16);
+            ka[3] = *reinterpret_cast<const uint32_t*>(kb + krow8 + 32 * st + 16);
+          } else {
+            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * st);
+            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * st);
+            ka[0] = w0 & 0x0F0F0F0Fu;
+            ka[1] = w1 & 0x0F0F0F0Fu;
+            ka[2] = (w0 >> 4) & 0x0F0F0F0Fu;
+            ka[3] = (w1 >> 4) & 0x0F0F0F0Fu;
+          }
+#pragma unroll
+          for (int t = 0; t < 3; ++t) imma16832(dacc[t], ka, ql[t][st][0], ql[t][st][1]);
+        }
+        // per-(position, head) K scales: S = kscale * 2^(E-22) * (q_int . k)
+        const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
+        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
+        const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float v = fmaf(static_cast<float>(dacc[0][e]), 65536.0f,
+                               fmaf(static_cast<float>(dacc[1][e]), 256.0f, static_cast<float>(dacc[2][e])));
+          s[e] = v * (qdown[e & 1] * (e < 2 ? k0 : k1));
+        }
+        if (PACK) {  // lanes whose columns are past G take the scores of lane tq & (XG - 1)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s[e] = __shfl_sync(0xffffffffu, s[e], (lane & ~3) | (tq & (XG - 1)));
+        }
+      }
       if (QNT) {
         // MMA row r holds position (r % NS) * RPS + r / NS: rows gq and gq+8
         // of this lane are rows gq / NS and (gq + 8) / NS of slot gq % NS
@@ -372,7 +496,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         // rows gq and gq + 4 share banks, 2-way)
         const uint8_t* kb = st8 + hk * (I4 ? kHD / 2 : kHD) + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
         const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;  // row gq + 8, same slot
-        if (I8) {
+        if (IM) {
+          // scores done above on the integer tensor cores
+        } else if (I8) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * kk);
@@ -399,16 +525,18 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
             if (!PACK) mma16816(s2, ka1, qb[2 * j + 1][0][1], qb[2 * j + 1][1][1]);
           }
         }
+        if (!IM) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) s[i] += s2[i];
-        // per-(position, head) K scales: S = scale * (q . k_int)
-        const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
-        const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
-        const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
-        s[0] *= k0;
-        s[1] *= k0;
-        s[2] *= k1;
-        s[3] *= k1;
+          for (int i = 0; i < 4; ++i) s[i] += s2[i];
+          // per-(position, head) K scales: S = scale * (q . k_int)
+          const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
+          const int pos0 = (gq % NS) * RPS + gq / NS, pos1 = ((gq + 8) % NS) * RPS + (gq + 8) / NS;
+          const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
+          s[0] *= k0;
+          s[1] *= k0;
+          s[2] *= k1;
+          s[3] *= k1;
+        }
         // V tile of this head -> exact fp16 integers in the warp's scratch
         // lane l converts word l (4 head dims) of every row: conflict-free
         // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
@@ -466,7 +594,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 #pragma unroll
         for (int i = 0; i < 4; ++i) s[i] += s2[i];
       }
-      if (PACK) {  // hi + lo columns: every lane of the pair holds the full score
+      if (PACK && !IM) {  // hi + lo columns: every lane of the pair holds the full score
 #pragma unroll
         for (int i = 0; i < 4; ++i) s[i] += __shfl_xor_sync(0xffffffffu, s[i], XG);
       }
@@ -754,20 +882,23 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
   return 128 + n * stage + scratch;
 }
 
+template <int G>
+void (*pick_mma(bool i8, bool i4, bool quad, bool im))(const AttnArgs) {
+  if (i4) return im ? attn_mma_kernel<G, SD_KV_INT4, 4, true> : attn_mma_kernel<G, SD_KV_INT4, 4>;
+  if (i8 && quad) return im ? attn_mma_kernel<G, SD_KV_INT8, 4, true> : attn_mma_kernel<G, SD_KV_INT8, 4>;
+  if (i8) return im ? attn_mma_kernel<G, SD_KV_INT8, 2, true> : attn_mma_kernel<G, SD_KV_INT8, 2>;
+  return attn_mma_kernel<G, SD_KV_HALF, 4>;
+}
+
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
   const bool i8 = a.g.fmt == SD_KV_INT8, i4 = a.g.fmt == SD_KV_INT4;
   const bool quad = attention_mma_rows_per_slot(a.g) == 4;
+  const bool im = tuning().attn_imma != 0;
   switch (a.G) {
-    case 2: fn = i4 ? attn_mma_kernel<2, SD_KV_INT4, 4>
-                 : i8 ? (quad ? attn_mma_kernel<2, SD_KV_INT8, 4> : attn_mma_kernel<2, SD_KV_INT8, 2>)
-                      : attn_mma_kernel<2, SD_KV_HALF, 4>; break;
-    case 4: fn = i4 ? attn_mma_kernel<4, SD_KV_INT4, 4>
-                 : i8 ? (quad ? attn_mma_kernel<4, SD_KV_INT8, 4> : attn_mma_kernel<4, SD_KV_INT8, 2>)
-                      : attn_mma_kernel<4, SD_KV_HALF, 4>; break;
-    case 8: fn = i4 ? attn_mma_kernel<8, SD_KV_INT4, 4>
-                 : i8 ? (quad ? attn_mma_kernel<8, SD_KV_INT8, 4> : attn_mma_kernel<8, SD_KV_INT8, 2>)
-                      : attn_mma_kernel<8, SD_KV_HALF, 4>; break;
+    case 2: fn = pick_mma<2>(i8, i4, quad, im); break;
+    case 4: fn = pick_mma<4>(i8, i4, quad, im); break;
+    case 8: fn = pick_mma<8>(i8, i4, quad, im); break;
     default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
   }
   // the dynamic-smem opt-in once per instantiation and size

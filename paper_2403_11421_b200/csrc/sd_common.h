@@ -87,7 +87,8 @@ struct Tuning {
   int dist_phases = 0;   // per-phase CUDA events in DistEngine, printed to stderr at destroy
   int attn_i8_quad = 0;  // int8 tensor-core attention: four positions per bulk copy (else two)
   int attn_l2_prefetch = 0;  // the attention prefetches the W_o weights into L2 at its end
-  int attn_max_stages = 0;   // tensor-core attention ring depth cap (0: as many as fit, up to 5)
+  int attn_max_stages = 0;   // tensor-core attention ring depth (0: the per-format default)
+  int attn_imma = 1;         // int8 / int4 KV: scores on integer tensor cores (q as byte limbs)
 };
 inline Tuning& tuning() {
   static Tuning t;
