@@ -364,6 +364,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       int E = 0;
       if (mx > 0.0f) frexpf(mx, &E);  // mx < 2^E
+      E = max(E, -100);               // keeps 2^(22-E) finite for subnormal-sized heads
       const float up = ldexpf(1.0f, 22 - E), down = ldexpf(1.0f, E - 22);
       int cs[3] = {0, 0, 0};
 #pragma unroll

@@ -113,7 +113,7 @@ def _session(w, sd, fmt, precision, spec=(2, 64, 4, 256, 128), h0=0, hc=4, cap=1
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("fmt", ["single", "half", "int8"])
+@pytest.mark.parametrize("fmt", ["single", "half", "int8", "int4"])
 @pytest.mark.parametrize("precision", ["single", "half"])
 def test_worker_qkv_batches_match_oracle_kvshard(w, oracle, fmt, precision):
     """Several steps x layers of QKV_BATCH frames (new sequences, growing
@@ -255,7 +255,7 @@ def _start_rworker(tmp_path, *extra):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("storage", ["half", "int8"])
+@pytest.mark.parametrize("storage", ["half", "int8", "int4"])
 def test_rworker_binary_serves_a_session(w, oracle, tmp_path, storage):
     """`sd_rworker serve --once` as its own process: the dense side connects
     over TCP, runs HELLO / CONFIG / two steps of QKV_BATCH / SHUTDOWN, gets
