@@ -354,3 +354,33 @@ def test_slot_and_page_reuse_after_drop(sd, oracle):
         for i in ids:
             live[i] += 1
     assert g.token_count() == c.token_count()
+
+
+@pytest.mark.parametrize("fmt", ["int8", "int4"])
+def test_integer_scores_extreme_query_scales(sd, oracle, fmt):
+    """The integer-score path carries q per head as a 22-bit fixed-point
+    integer scaled by the head's max: a zero head, a ~1e-20 head and a
+    sharply peaked (x30) head must match the oracle like an ordinary one."""
+    G = 4
+    H, D = 8 * G, 8 * G * 128
+    s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
+    B, L = 6, 90
+    gpu = sd.KvShard(s, 0, 8, B * L, fmt)
+    cpu = oracle.KvShard(os_, 0, 8, B * L, fmt)
+    rng = _rng(77)
+    seqs = list(range(1, B + 1))
+    for pos in range(L):
+        k = rng.uniform(-1, 1, (B, 1024)).astype(np.float32)
+        v = rng.uniform(-1, 1, (B, 1024)).astype(np.float32)
+        gpu.append_request(0, seqs, [pos] * B, k, v)
+        cpu.append_request(0, seqs, [pos] * B, k, v)
+    q = rng.uniform(-1, 1, (B, H, 128)).astype(np.float32)
+    q[:, 0::4] = 0.0
+    q[:, 1::4] *= 1e-20
+    q[:, 2::4] *= 30.0
+    q = q.reshape(B, D)
+    with sd.tuned(attn_imma=1):
+        og = gpu.attend(0, seqs, q)
+    oc = cpu.attend(0, seqs, q)
+    err = float(np.abs(og - oc).max())
+    assert err < 2e-5, err
