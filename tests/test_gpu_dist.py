@@ -237,3 +237,20 @@ def test_four_ranks_one_device_hybrid_shardmap(oracle, tmp_path, s_ranks):
              nprocs=4, join=True)
     left = _check_rows(oracle, out, cfg, spec_args)
     assert left == [(0, 0)] * 4
+
+
+@pytest.mark.parametrize("shard_mode,s_ranks", [("sequence", 1), ("sequence", 8), ("hybrid", 8)])
+def test_eight_ranks_one_device(oracle, tmp_path, shard_mode, s_ranks):
+    """The full 8-rank geometry of one 8xB200 box (flag slots, peer maps and
+    the token gather at their maximum width) on the driver's one device:
+    by-sequence with one or eight S-ranks, and hybrid (8 workers over 4 kv
+    heads: 4 head groups x 2 sequence groups); tokens equal the monolithic
+    oracle, every shard empty after retirement."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rows.pkl")
+    cfg = (16, 12, 4, 0)
+    spec_args = (2, 64, 4, 256, 128)
+    mp.spawn(_worker, args=(8, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, False, spec_args),
+             nprocs=8, join=True)
+    left = _check_rows(oracle, out, cfg, spec_args)
+    assert left == [(0, 0)] * 8
