@@ -79,31 +79,33 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Eight consecutive elements of a row as four fp32 pairs (the K2 inner
+// loops run on Blackwell's paired FFMA2 / FADD2: two fp32 lanes per issue).
 template <int FMT>
 struct Fmt;
 template <>
 struct Fmt<SD_KV_SINGLE> {
   static constexpr int kBytes = 4;
-  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+  __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const float4 a = *reinterpret_cast<const float4*>(p);
     const float4 b = *reinterpret_cast<const float4*>(p + 16);
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-    x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    x[0] = make_float2(a.x, a.y);
+    x[1] = make_float2(a.z, a.w);
+    x[2] = make_float2(b.x, b.y);
+    x[3] = make_float2(b.z, b.w);
   }
 };
 template <>
 struct Fmt<SD_KV_HALF> {
   static constexpr int kBytes = 2;
-  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+  __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const uint4 r = *reinterpret_cast<const uint4*>(p);
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       __half2 h;
       *reinterpret_cast<uint32_t*>(&h) = w[i];
-      const float2 f = __half22float2(h);
-      x[2 * i] = f.x;
-      x[2 * i + 1] = f.y;
+      x[i] = __half22float2(h);
     }
   }
 };
@@ -112,27 +114,34 @@ struct Fmt<SD_KV_INT8> {
   static constexpr int kBytes = 1;
   // int8 -> fp32 without I2F: the pool stores q + 128 (kv_store.h), so
   // byte u becomes the float 2^23 + u (one PRMT into 0x4B0000xx), minus
-  // 2^23 + 128: exact, equal to (float)q
-  __device__ static __forceinline__ void cvt4(uint32_t u, float* x) {
-    x[0] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7650)) - 8388736.0f;
-    x[1] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7651)) - 8388736.0f;
-    x[2] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7652)) - 8388736.0f;
-    x[3] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7653)) - 8388736.0f;
+  // 2^23 + 128 (one FADD2 per pair): exact, equal to (float)q
+  __device__ static __forceinline__ float2 cvt2(uint32_t u, uint32_t s0, uint32_t s1) {
+    return __fadd2_rn(make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, s0)),
+                                  __uint_as_float(__byte_perm(u, 0x4B000000u, s1))),
+                      make_float2(-8388736.0f, -8388736.0f));
   }
-  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+  __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const uint2 r = *reinterpret_cast<const uint2*>(p);
-    cvt4(r.x, x);
-    cvt4(r.y, x + 4);
+    x[0] = cvt2(r.x, 0x7650, 0x7651);
+    x[1] = cvt2(r.x, 0x7652, 0x7653);
+    x[2] = cvt2(r.y, 0x7650, 0x7651);
+    x[3] = cvt2(r.y, 0x7652, 0x7653);
   }
 };
 template <>
 struct Fmt<SD_KV_INT4> {
-  // eight nibbles (element 2i low) holding q + 8 -> fp32: the float
-  // 2^23 + (q + 8) minus 2^23 + 8 is exactly q
-  __device__ static __forceinline__ void load8(const uint8_t* p, float (&x)[8]) {
+  // eight nibbles (element 2i low) holding q + 8 -> fp32: byte i goes under
+  // 0x4B0000 (one PRMT); masking keeps 2^23 + lo or 2^23 + 16 hi, and one
+  // FFMA2 maps them to lo - 8 and (2^23 + 16 hi) / 16 - (2^19 + 8) = hi - 8,
+  // both exact
+  __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = __uint_as_float(0x4B000000u | ((u >> (4 * i)) & 0xFu)) - 8388616.0f;
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t b = __byte_perm(u, 0x4B000000u, 0x7650 + i);
+      x[i] = __ffma2_rn(make_float2(__uint_as_float(b & 0xFFFFFF0Fu), __uint_as_float(b & 0xFFFFFFF0u)),
+                        make_float2(1.0f, 0.0625f), make_float2(-8388616.0f, -524296.0f));
+    }
   }
 };
 
@@ -320,15 +329,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
             if (act) {
               const uint8_t* kr = Ks + static_cast<size_t>(t * hkv + hk) * row_bytes;
 #pragma unroll
+              float2 d2[G];
+#pragma unroll
+              for (int gg = 0; gg < G; ++gg) d2[gg] = make_float2(0.0f, 0.0f);
+#pragma unroll
               for (int c = 0; c < NC; ++c) {
-                float kx[8];
+                float2 kx[4];
                 Fmt<FMT>::load8(kr + kv_row_bytes(FMT, (c * LPR + li) * 8), kx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) sc[hh][i][gg] = fmaf(q[hh * G + gg][c * 8 + e], kx[e], sc[hh][i][gg]);
+                  for (int e = 0; e < 4; ++e)
+                    d2[gg] = __ffma2_rn(make_float2(q[hh * G + gg][c * 8 + 2 * e], q[hh * G + gg][c * 8 + 2 * e + 1]),
+                                        kx[e], d2[gg]);
                 }
               }
+#pragma unroll
+              for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] = d2[gg].x + d2[gg].y;
             }
           }
         }
@@ -395,13 +412,19 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
               const uint8_t* vr = Vs + static_cast<size_t>(t * hkv + hk) * row_bytes;
 #pragma unroll
               for (int c = 0; c < NC; ++c) {
-                float vx[8];
+                float2 vx[4];
                 Fmt<FMT>::load8(vr + kv_row_bytes(FMT, (c * LPR + li) * 8), vx);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                   const float pv = QNT ? p[hh][i][gg] * vs[hh][i] : p[hh][i][gg];
+                  const float2 pv2 = make_float2(pv, pv);
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) acc[hh * G + gg][c * 8 + e] = fmaf(pv, vx[e], acc[hh * G + gg][c * 8 + e]);
+                  for (int e = 0; e < 4; ++e) {
+                    float* ac = &acc[hh * G + gg][c * 8 + 2 * e];
+                    const float2 r = __ffma2_rn(pv2, vx[e], make_float2(ac[0], ac[1]));
+                    ac[0] = r.x;
+                    ac[1] = r.y;
+                  }
                 }
               }
             }
