@@ -894,7 +894,9 @@ void (*pick_mma(bool i8, bool i4, bool quad, bool im))(const AttnArgs) {
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
   const bool i8 = a.g.fmt == SD_KV_INT8, i4 = a.g.fmt == SD_KV_INT4;
-  const bool quad = attention_mma_rows_per_slot(a.g) == 4;
+  // the slot layout the store was built with (a later attn_i8_quad flip
+  // does not change an existing store's stage geometry)
+  const bool quad = a.stage_region == (kT / 4) * (4 * a.g.pos_bytes + 16);
   const bool im = tuning().attn_imma != 0;
   switch (a.G) {
     case 2: fn = pick_mma<2>(i8, i4, quad, im); break;

@@ -384,3 +384,32 @@ def test_integer_scores_extreme_query_scales(sd, oracle, fmt):
     oc = cpu.attend(0, seqs, q)
     err = float(np.abs(og - oc).max())
     assert err < 2e-5, err
+
+
+@pytest.mark.parametrize("imma", [1, 0])
+def test_int8_quad_slot_variant(sd, oracle, imma):
+    """int8 with four positions per bulk copy (attn_i8_quad, the layout int4
+    always uses) under both score paths: same results as the oracle."""
+    G = 4
+    H, D = 8 * G, 8 * G * 128
+    s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
+    B, Lmax = 12, 300
+    with sd.tuned(attn_i8_quad=1):  # the slot layout is fixed when the store is built
+        gpu = sd.KvShard(s, 0, 8, B * Lmax, "int8")
+    cpu = oracle.KvShard(os_, 0, 8, B * Lmax, "int8")
+    rng = _rng(31)
+    lens = rng.integers(1, Lmax, B)
+    lens[0] = 5
+    seqs = list(range(1, B + 1))
+    for pos in range(int(lens.max())):
+        act = [i for i in range(B) if lens[i] > pos]
+        k = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        v = rng.uniform(-1, 1, (len(act), 1024)).astype(np.float32)
+        ids = [seqs[i] for i in act]
+        gpu.append_request(0, ids, [pos] * len(act), k, v)
+        cpu.append_request(0, ids, [pos] * len(act), k, v)
+    q = rng.uniform(-3, 3, (B, D)).astype(np.float32)
+    with sd.tuned(attn_imma=imma):
+        og = gpu.attend(0, seqs, q)
+    err = float(np.abs(og - cpu.attend(0, seqs, q)).max())
+    assert err < 2e-5, err
