@@ -141,6 +141,10 @@ class Engine : public StepComputation {
   // when the KV store allows it (returns whether it did)
   bool qkv_fused_append(int layer, Group& g);
   bool want_logits_ = false;  // this step returns the logits (else the head's argmax is fused)
+  // step(): the final activations' D2H copy, issued on the R stream as soon
+  // as the last block is done, overlaps the head GEMM (one group only)
+  float* early_final_ = nullptr;
+  cudaEvent_t ev_final_ = nullptr;
 
   bool timing_ = false;
   std::vector<cudaEvent_t> ev_pool_;

@@ -32,6 +32,7 @@ Engine::Engine(Weights* w, KvStore* kv) : w_(w), kv_(kv) {
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_s, cudaEventDisableTiming));
     SD_CUDA(cudaEventCreateWithFlags(&g.ev_r, cudaEventDisableTiming));
   }
+  SD_CUDA(cudaEventCreateWithFlags(&ev_final_, cudaEventDisableTiming));
 }
 
 void Engine::free_group(Group& g) {
@@ -62,6 +63,7 @@ Engine::~Engine() {
     cudaEventDestroy(e.second);
   }
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  cudaEventDestroy(ev_final_);
   cudaStreamDestroy(stream_);
   cudaStreamDestroy(stream_r_);
 }
@@ -272,6 +274,12 @@ void Engine::run(int ng, bool embed) {
       }
     }
   }
+  if (early_final_ && ng == 1) {  // final activations leave while the head runs
+    SD_CUDA(cudaEventRecord(ev_final_, stream_));
+    SD_CUDA(cudaStreamWaitEvent(stream_r_, ev_final_, 0));
+    SD_CUDA(cudaMemcpyAsync(early_final_, groups_[0].x, groups_[0].rows.size() * static_cast<size_t>(D) * 4,
+                            cudaMemcpyDeviceToHost, stream_r_));
+  }
   for (int gi = 0; gi < ng; ++gi) {  // output_logits + argmax_token (dense.cpp:72-88)
     Group& g = groups_[gi];
     const int n = static_cast<int>(g.rows.size());
@@ -333,8 +341,18 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
     }
   }
   want_logits_ = logits_host != nullptr;
-  run(ng, tokens_host != nullptr);
+  early_final_ = ng == 1 ? final_host : nullptr;
+  try {
+    run(ng, tokens_host != nullptr);
+  } catch (...) {
+    early_final_ = nullptr;
+    want_logits_ = false;
+    throw;
+  }
+  const bool final_done = early_final_ != nullptr;
+  early_final_ = nullptr;
   want_logits_ = false;
+  if (final_done) SD_CUDA(cudaStreamSynchronize(stream_r_));
   std::vector<int32_t> nt;
   std::vector<float> buf;
   for (int gi = 0; gi < ng; ++gi) {
@@ -359,7 +377,7 @@ void Engine::step(int B, const uint64_t* seqs, const int32_t* tokens_host, const
                     buf.data() + static_cast<size_t>(i) * width, static_cast<size_t>(width) * 4);
       }
     };
-    if (final_host) scatter(g.x, s.D, final_host);
+    if (final_host && !final_done) scatter(g.x, s.D, final_host);
     if (logits_host) scatter(g.logits, s.V, logits_host);
   }
 }
