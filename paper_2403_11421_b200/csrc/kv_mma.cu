@@ -1,7 +1,8 @@
-// K2 for grouped-query attention over fp16 KV (BASELINE config 5): the G
-// query heads that share a kv head make the R-Part a thin GEMM, so the dot
-// products and the value sum run on tensor cores (mma.sync m16n8k16, fp32
-// accumulate) instead of CUDA-core FMAs.
+// K2 for grouped-query attention over fp16, int8 or int4 KV (BASELINE
+// config 5): the G query heads that share a kv head make the R-Part a thin
+// GEMM, so the dot products and the value sum run on tensor cores
+// (mma.sync m16n8k16, fp32 accumulate; int8 / int4 scores on m16n8k32
+// IMMA, see IM below) instead of CUDA-core FMAs.
 //
 //   S^T[pos][q] = K[pos][:] . Q^T[:][q]     M = 16 positions, N = 8 (G <= 8 heads), K = hd
 //   O^T[d][q]  += V^T[d][pos] . P^T[pos][q]  M = 16 head-dims,  N = 8 heads,         K = 16 pos
@@ -18,7 +19,7 @@
 //
 // Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
-// positions copied four (fp16) or two (int8) per bulk copy (the per-SM copy
+// positions copied four (fp16, int4) or two (int8) per bulk copy (the per-SM copy
 // issue rate, not bytes, limits row-sized copies) into slots with a 16-B pad;
 // MMA row r holds position (r % NS) * RPS + r / NS (NS slots of RPS rows).
 #include <cuda_bf16.h>
