@@ -157,9 +157,11 @@ int sd_kv_warning_count(const sd_kv* kv, int32_t* out);
 int sd_kv_bytes_per_token(const sd_kv* kv, int64_t* out);
 int sd_kv_width(const sd_kv* kv, int32_t* width, int32_t* q_width);
 /* Stored bytes of one lane (which: 0 = K, 1 = V) in the reference's
- * [pos][head][d] order (attention.cpp:117-118) and, for int8, the per
- * (pos, head) scales (attention.cpp:129-130). Returns the byte count (or a
- * negative status); copies when host/scales are large enough. */
+ * [pos][head][d] order (attention.cpp:117-118) and, for int8 / int4, the per
+ * (pos, head) scales (attention.cpp:129-130); quantized codes come back as
+ * the reference's two's-complement bytes (int4: two per byte, element 2i in
+ * the low nibble). Returns the byte count (or a negative status); copies
+ * when host/scales are large enough. */
 int64_t sd_kv_export_lane(const sd_kv* kv, uint64_t seq, int layer, int which, void* host,
                           size_t host_bytes, float* scales, size_t scales_count);
 /* Fills every (slot, layer, position < length) of the listed sequences

@@ -91,7 +91,7 @@ struct AttnArgs {
   int32_t T;                  // positions per pipeline stage
   int32_t nstages;
   int32_t stage_region;       // bytes of one K (or V) stage region (128-B aligned)
-  int32_t sc_region;          // bytes of one int8 scale region per stage (0: scales read from L2)
+  int32_t sc_region;          // bytes of one int8 / int4 scale region per stage (0: scales read from L2)
   // fused combine (kv_mma.cu): the last piece of a split item to finish, per
   // kv head, merges the item's partials in piece order (the combine_kernel
   // arithmetic) and resets its counter
