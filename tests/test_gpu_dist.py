@@ -32,7 +32,7 @@ TOY = (2, 64, 4, 256, 128)
 
 
 def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mode="sequence", drain=False,
-            pipeline=False, spec_args=TOY):
+            pipeline=False, spec_args=TOY, fmt="single"):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path[:0] = [root, os.path.join(root, "oracle"), os.path.join(root, "tests")]
@@ -57,7 +57,7 @@ def _worker(rank, world, port, s_ranks, cfg, out_path, exchange="nccl", shard_mo
         h0, hc = 0, heads
     else:
         h0, hc = sd.ShardMap(shard_mode, heads, world).head_range(rank)
-    kv = sd.KvShard(spec, h0, hc, 1 << 16, "single", dev)
+    kv = sd.KvShard(spec, h0, hc, 1 << 16, fmt, dev)
     eng = sd.DistEngine(dw, kv, rank, world, obj[0], s_ranks, shard_mode=shard_mode)
     if exchange.startswith("p2p"):
         eng.enable_p2p(64)
@@ -97,10 +97,10 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
     _check_rows(oracle, out, cfg)
 
 
-def _check_rows(oracle, out, cfg, spec_args=TOY):
+def _check_rows(oracle, out, cfg, spec_args=TOY, fmt="single", bar=1e-5):
     rows, left = pickle.load(open(out, "rb"))
     W = oracle.Weights(oracle.make_spec(*spec_args), 0)
-    orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, record=True)
+    orecs, oacts = oracle.run_monolithic(W, *cfg, seed=0, fmt=fmt, record=True)
     ref = {(s, q): (t, oacts[i]) for i, (s, q, t) in enumerate(orecs)}
     assert len(rows) == len(ref)
     worst = 0.0
@@ -108,7 +108,7 @@ def _check_rows(oracle, out, cfg, spec_args=TOY):
         rt, rx = ref[(s, q)]
         assert t == rt
         worst = max(worst, float(np.abs(np.asarray(x, np.float32) - rx).max()))
-    assert worst <= 1e-5
+    assert worst <= bar
     return left
 
 
@@ -254,3 +254,18 @@ def test_eight_ranks_one_device(oracle, tmp_path, shard_mode, s_ranks):
              nprocs=8, join=True)
     left = _check_rows(oracle, out, cfg, spec_args)
     assert left == [(0, 0)] * 8
+
+
+@pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
+@pytest.mark.parametrize("shard_mode", ["sequence", "hybrid"])
+def test_two_ranks_one_device_stored_kv_formats(oracle, tmp_path, fmt, shard_mode):
+    """The distributed step over fp16 / int8 / int4 KV shards (two ranks, one
+    device): the same transcript as the oracle's run_monolithic over a
+    KvShard in that format, activations <= 1e-4."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "rows.pkl")
+    cfg = (8, 16, 4, 0)
+    mp.spawn(_worker, args=(2, _free_port(), 2, cfg, out, "p2p-one-device", shard_mode, True, False, TOY, fmt),
+             nprocs=2, join=True)
+    left = _check_rows(oracle, out, cfg, TOY, fmt, 1e-4)
+    assert left == [(0, 0), (0, 0)]
