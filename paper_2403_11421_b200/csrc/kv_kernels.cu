@@ -21,7 +21,6 @@ namespace sd {
 namespace {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -85,7 +84,6 @@ template <int FMT>
 struct Fmt;
 template <>
 struct Fmt<SD_KV_SINGLE> {
-  static constexpr int kBytes = 4;
   __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const float4 a = *reinterpret_cast<const float4*>(p);
     const float4 b = *reinterpret_cast<const float4*>(p + 16);
@@ -97,7 +95,6 @@ struct Fmt<SD_KV_SINGLE> {
 };
 template <>
 struct Fmt<SD_KV_HALF> {
-  static constexpr int kBytes = 2;
   __device__ static __forceinline__ void load8(const uint8_t* p, float2 (&x)[4]) {
     const uint4 r = *reinterpret_cast<const uint4*>(p);
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
@@ -111,7 +108,6 @@ struct Fmt<SD_KV_HALF> {
 };
 template <>
 struct Fmt<SD_KV_INT8> {
-  static constexpr int kBytes = 1;
   // int8 -> fp32 without I2F: the pool stores q + 128 (kv_store.h), so
   // byte u becomes the float 2^23 + u (one PRMT into 0x4B0000xx), minus
   // 2^23 + 128 (one FADD2 per pair): exact, equal to (float)q
@@ -328,7 +324,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1) attn_kernel(const AttnArgs a
             for (int gg = 0; gg < G; ++gg) sc[hh][i][gg] = 0.0f;
             if (act) {
               const uint8_t* kr = Ks + static_cast<size_t>(t * hkv + hk) * row_bytes;
-#pragma unroll
               float2 d2[G];
 #pragma unroll
               for (int gg = 0; gg < G; ++gg) d2[gg] = make_float2(0.0f, 0.0f);

@@ -42,7 +42,6 @@ namespace {
 // position classes measured slower: 0.517 vs 0.498 ms per C5 layer)
 template <int FMT>
 constexpr int consumer_warps() { return 8; }
-constexpr int kMaxWarps = 16;
 constexpr int kT = 16;                    // positions per stage
 constexpr int kHD = 128;
 
@@ -74,22 +73,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
-}
-// bulk copy issued by one elected lane of a converged warp (uniform operands)
-__device__ __forceinline__ void e_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                           uint64_t policy) {
-  asm volatile(
-      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;\n}\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void e_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-               "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
 }
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
