@@ -1,0 +1,253 @@
+// sd_b200.hpp — the reference's R-Part C++ interface (splitdecode/attention.hpp,
+// core.hpp) over the C ABI, header-only: a C++ host sees the same names,
+// argument meanings and exception types as splitdecode::KvShard, backed by
+// the B200 KV store. The reference's Eigen vectors become contiguous float
+// vectors / spans (Eigen is not part of this boundary); everything else —
+// construction, append / append_request (all or nothing), attend (outputs in
+// item order), drop_sequence, the accounting queries, the error types and
+// their messages — follows attention.hpp:68-140 and core.hpp:25-38.
+//
+// The ABI takes packed rows, so vector sizes are checked here, with the
+// reference's messages; a request that is both mis-sized and invalid in
+// another way reports the size first (the reference checks capacity first in
+// append_request and the sequence first in attend).
+//
+// Link with libsd_b200.so; include/sd_abi.h documents each entry point.
+#pragma once
+
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sd_abi.h"
+
+namespace sd_b200 {
+
+// ---- errors (core.hpp:25-38, attention.hpp:19-22)
+class ConfigError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ProtocolError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class UnknownSequenceError : public ProtocolError {
+ public:
+  using ProtocolError::ProtocolError;
+};
+class CapacityError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+// CUDA / internal failures of the B200 backend (no reference counterpart)
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+// status -> the reference's exception type, message from sd_last_error()
+inline void check(int status) {
+  if (status == SD_OK) return;
+  const std::string msg = sd_last_error();
+  switch (status) {
+    case SD_ERR_PROTOCOL: throw ProtocolError(msg);
+    case SD_ERR_CAPACITY: throw CapacityError(msg);
+    case SD_ERR_UNKNOWN_SEQ: throw UnknownSequenceError(msg);
+    case SD_ERR_LOGIC: throw std::logic_error(msg);
+    case SD_ERR_CONFIG: throw ConfigError(msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+using SequenceId = std::uint64_t;
+using Vec = std::vector<float>;
+
+// ---- geometry (core.hpp:43-58): head_dim = model_dim / num_heads;
+// num_kv_heads (the GQA extension) defaults to num_heads
+struct ModelSpec {
+  int num_layers = 0, model_dim = 0, num_heads = 0, head_dim = 0, mlp_dim = 0, vocab_size = 0;
+  int num_kv_heads = 0;
+  sd_model_spec raw() const {
+    return sd_model_spec{num_layers, model_dim, num_heads, head_dim, mlp_dim, vocab_size, num_kv_heads};
+  }
+};
+
+inline ModelSpec make_model_spec(int num_layers, int model_dim, int num_heads, int mlp_dim, int vocab_size,
+                                 int num_kv_heads = 0) {
+  sd_model_spec s{};
+  check(sd_make_model_spec(num_layers, model_dim, num_heads, mlp_dim, vocab_size, num_kv_heads, &s));
+  return ModelSpec{s.num_layers, s.model_dim, s.num_heads, s.head_dim, s.mlp_dim, s.vocab_size, s.num_kv_heads};
+}
+
+inline std::uint64_t mix64(std::uint64_t x) { return sd_mix64(x); }
+
+// ---- KvFormat (attention.hpp:24); kInt4 is the 4-bit hook extension
+enum class KvFormat : std::uint8_t { kSingle, kHalf, kInt8, kInt4 };
+
+// ---- requests (attention.hpp:44-60)
+struct AttentionItem {
+  SequenceId seq = 0;
+  std::uint32_t position = 0;  // stored length before this token is appended
+  Vec q, k, v;                 // q: q_width, k / v: width of the shard's head range
+};
+struct AttentionRequest {
+  int layer = 0;
+  std::vector<AttentionItem> items;
+};
+struct AttentionOutput {
+  SequenceId seq = 0;
+  Vec o;
+};
+struct AttentionResponse {
+  int layer = 0;
+  std::vector<AttentionOutput> outputs;  // same order as the request items
+};
+
+// ---- KvShard (attention.hpp:68-140) on a B200
+class KvShard {
+ public:
+  KvShard(const ModelSpec& spec, int head_start, int head_count, long capacity_tokens,
+          KvFormat format = KvFormat::kSingle, int device = 0)
+      : spec_(spec), head_start_(head_start), head_count_(head_count), capacity_(capacity_tokens),
+        format_(format) {
+    const sd_model_spec s = spec.raw();
+    check(sd_kv_create(&s, head_start, head_count, capacity_tokens, static_cast<int>(format), device, nullptr,
+                       &h_));
+    std::int32_t w = 0, qw = 0;
+    check(sd_kv_width(h_, &w, &qw));
+    width_ = w;
+    q_width_ = qw;
+  }
+  ~KvShard() {
+    if (h_) sd_kv_destroy(h_);
+  }
+  KvShard(const KvShard&) = delete;
+  KvShard& operator=(const KvShard&) = delete;
+  KvShard(KvShard&& o) noexcept { *this = std::move(o); }
+  KvShard& operator=(KvShard&& o) noexcept {
+    if (this != &o) {
+      if (h_) sd_kv_destroy(h_);
+      h_ = o.h_;
+      o.h_ = nullptr;
+      spec_ = o.spec_;
+      head_start_ = o.head_start_;
+      head_count_ = o.head_count_;
+      capacity_ = o.capacity_;
+      format_ = o.format_;
+      width_ = o.width_;
+      q_width_ = o.q_width_;
+    }
+    return *this;
+  }
+
+  int head_start() const { return head_start_; }
+  int head_count() const { return head_count_; }
+  int width() const { return width_; }
+  int q_width() const { return q_width_; }
+  KvFormat format() const { return format_; }
+  long capacity() const { return capacity_; }
+
+  long token_count() const {
+    std::int64_t n = 0;
+    check(sd_kv_token_count(h_, &n));
+    return static_cast<long>(n);
+  }
+  bool has_sequence(SequenceId seq) const {
+    std::int32_t b = 0;
+    check(sd_kv_has_sequence(h_, seq, &b));
+    return b != 0;
+  }
+  int stored_length(SequenceId seq, int layer) const {
+    std::int32_t n = 0;
+    check(sd_kv_stored_length(h_, seq, layer, &n));
+    return n;
+  }
+  int warning_count() const {
+    std::int32_t n = 0;
+    check(sd_kv_warning_count(h_, &n));
+    return n;
+  }
+  std::size_t bytes_per_token() const {
+    std::int64_t n = 0;
+    check(sd_kv_bytes_per_token(h_, &n));
+    return static_cast<std::size_t>(n);
+  }
+
+  // attention.hpp:91-92
+  void append(SequenceId seq, int layer, std::uint32_t position, std::span<const float> k,
+              std::span<const float> v) {
+    if (layer < 0 || layer >= spec_.num_layers) throw ProtocolError("append: layer index out of range");
+    if (static_cast<int>(k.size()) != width_ || static_cast<int>(v.size()) != width_) {
+      throw ProtocolError("append: K/V width does not match the shard's head range");
+    }
+    check(sd_kv_append(h_, seq, layer, position, k.data(), v.data()));
+  }
+
+  // attention.hpp:96: all or nothing
+  void append_request(const AttentionRequest& r) {
+    Packed p(r, width_, q_width_, false);
+    check(sd_kv_append_request(h_, r.layer, p.n, p.seqs.data(), p.pos.data(), p.k.data(), p.v.data()));
+  }
+
+  // attention.hpp:102: one output per item, in item order
+  AttentionResponse attend(const AttentionRequest& r) const {
+    Packed p(r, width_, q_width_, true);
+    std::vector<float> o(static_cast<std::size_t>(p.n) * q_width_);
+    check(sd_kv_attend(h_, r.layer, p.n, p.seqs.data(), p.q.data(), o.data()));
+    AttentionResponse resp;
+    resp.layer = r.layer;
+    resp.outputs.resize(r.items.size());
+    for (std::size_t i = 0; i < r.items.size(); ++i) {
+      resp.outputs[i].seq = r.items[i].seq;
+      resp.outputs[i].o.assign(o.begin() + static_cast<std::ptrdiff_t>(i * q_width_),
+                               o.begin() + static_cast<std::ptrdiff_t>((i + 1) * q_width_));
+    }
+    return resp;
+  }
+
+  // attention.hpp:106
+  void drop_sequence(SequenceId seq) { check(sd_kv_drop(h_, 1, &seq)); }
+
+  sd_kv* handle() const { return h_; }
+
+ private:
+  // items packed row-major for the ABI (the reference's per-item VectorXf)
+  struct Packed {
+    std::int32_t n = 0;
+    std::vector<std::uint64_t> seqs;
+    std::vector<std::uint32_t> pos;
+    std::vector<float> q, k, v;
+    Packed(const AttentionRequest& r, int width, int q_width, bool want_q) {
+      n = static_cast<std::int32_t>(r.items.size());
+      for (const AttentionItem& it : r.items) {
+        seqs.push_back(it.seq);
+        pos.push_back(it.position);
+        if (want_q) {
+          if (static_cast<int>(it.q.size()) != q_width) {
+            throw ProtocolError("attend: Q width does not match the shard's head range");
+          }
+          q.insert(q.end(), it.q.begin(), it.q.end());
+        } else {
+          if (static_cast<int>(it.k.size()) != width || static_cast<int>(it.v.size()) != width) {
+            throw ProtocolError("append: K/V width does not match the shard's head range");
+          }
+          k.insert(k.end(), it.k.begin(), it.k.end());
+          v.insert(v.end(), it.v.begin(), it.v.end());
+        }
+      }
+    }
+  };
+
+  sd_kv* h_ = nullptr;
+  ModelSpec spec_;
+  int head_start_ = 0, head_count_ = 0;
+  long capacity_ = 0;
+  KvFormat format_ = KvFormat::kSingle;
+  int width_ = 0, q_width_ = 0;
+};
+
+}  // namespace sd_b200
