@@ -250,4 +250,166 @@ class KvShard {
   int width_ = 0, q_width_ = 0;
 };
 
+// ---- S-Part (dense.hpp:16-50) over device-resident weights
+
+// the S-Part arithmetic of a WeightSet (sd_dense_mode): kExact is the
+// reference's fp32 per-element order (bitwise), the rest run on tcgen05
+enum class DenseMode : int { kExact = SD_DENSE_EXACT_F32, kBf16 = SD_DENSE_BF16, kTf32 = SD_DENSE_TF32, kFp16 = SD_DENSE_F16 };
+
+// Row-major [rows][cols] float matrix (the reference's MatrixXf rows)
+struct Rows {
+  int rows = 0, cols = 0;
+  std::vector<float> data;
+  Rows() = default;
+  Rows(int r, int c) : rows(r), cols(c), data(static_cast<std::size_t>(r) * c, 0.0f) {}
+  float* row(int r) { return data.data() + static_cast<std::size_t>(r) * cols; }
+  const float* row(int r) const { return data.data() + static_cast<std::size_t>(r) * cols; }
+};
+
+// seed_random_weights (core.cpp:97-127) generated on the device: the
+// reference's mt19937 tensors bit for bit, in the requested dense mode
+class WeightSet {
+ public:
+  WeightSet(const ModelSpec& spec, std::uint64_t seed, DenseMode mode = DenseMode::kExact, int device = 0)
+      : spec_(spec) {
+    const sd_model_spec s = spec.raw();
+    check(sd_weights_seed_random(&s, seed, static_cast<int>(mode), device, &h_));
+  }
+  ~WeightSet() {
+    if (h_) sd_weights_destroy(h_);
+  }
+  WeightSet(const WeightSet&) = delete;
+  WeightSet& operator=(const WeightSet&) = delete;
+  const ModelSpec& spec() const { return spec_; }
+  sd_weights* handle() const { return h_; }
+  // embedding.col(token) (workers.cpp:636)
+  Vec embedding_column(int token) const {
+    if (emb_.empty()) {
+      emb_.resize(static_cast<std::size_t>(spec_.model_dim) * spec_.vocab_size);
+      check(sd_weights_export_embedding(h_, emb_.data(), emb_.size()));
+    }
+    const float* c = emb_.data() + static_cast<std::size_t>(token) * spec_.model_dim;
+    return Vec(c, c + spec_.model_dim);
+  }
+
+ private:
+  ModelSpec spec_;
+  sd_weights* h_ = nullptr;
+  mutable std::vector<float> emb_;
+};
+
+struct QkvProjection {  // dense.hpp:22-27
+  Rows q, k, v;
+};
+// project_qkv (dense.cpp:33-43): features [B][D] -> q [B][q width], k / v [B][kv width]
+inline QkvProjection project_qkv(const WeightSet& w, int layer, const Rows& x) {
+  const ModelSpec& s = w.spec();
+  const int kvw = (s.num_kv_heads > 0 ? s.num_kv_heads : s.num_heads) * s.head_dim;
+  QkvProjection r{Rows(x.rows, s.num_heads * s.head_dim), Rows(x.rows, kvw), Rows(x.rows, kvw)};
+  check(sd_s_project_qkv(w.handle(), layer, x.rows, x.data.data(), r.q.data.data(), r.k.data.data(), r.v.data.data()));
+  return r;
+}
+// finish_block (dense.cpp:51-70): o and the residual [B][D] -> the block's output
+inline Rows finish_block(const WeightSet& w, int layer, const Rows& o, const Rows& residual) {
+  Rows x(o.rows, w.spec().model_dim);
+  check(sd_s_finish_block(w.handle(), layer, o.rows, o.data.data(), residual.data.data(), x.data.data()));
+  return x;
+}
+// output_logits + argmax_token (dense.cpp:72-88)
+inline Rows output_logits(const WeightSet& w, const Rows& x) {
+  Rows l(x.rows, w.spec().vocab_size);
+  std::vector<std::int32_t> t(static_cast<std::size_t>(x.rows));
+  check(sd_s_logits_argmax(w.handle(), x.rows, x.data.data(), l.data.data(), t.data()));
+  return l;
+}
+inline int argmax_token(std::span<const float> logits) {  // first maximum wins
+  int best = 0;
+  for (int j = 1; j < static_cast<int>(logits.size()); ++j)
+    if (logits[static_cast<std::size_t>(j)] > logits[static_cast<std::size_t>(best)]) best = j;
+  return best;
+}
+
+// ---- the runtime seam (workers.hpp:151-158): the GPU StepComputation
+
+struct TokenBatch {  // core.hpp:66-72
+  std::vector<SequenceId> seq_ids;
+  Rows features;  // batch x model_dim
+  int size() const { return static_cast<int>(seq_ids.size()); }
+};
+struct DecodeStepResult {  // dense.hpp:40-43
+  std::vector<int> next_tokens;
+  Rows final_activations;
+};
+
+class StepComputation {
+ public:
+  StepComputation(WeightSet& w, KvShard& kv) : spec_(w.spec()) { check(sd_engine_create(w.handle(), kv.handle(), &h_)); }
+  ~StepComputation() {
+    if (h_) sd_engine_destroy(h_);
+  }
+  StepComputation(const StepComputation&) = delete;
+  StepComputation& operator=(const StepComputation&) = delete;
+  // compute(batch, step) (workers.hpp:155): one decode step of every layer
+  DecodeStepResult compute(const TokenBatch& batch, long /*step*/) {
+    DecodeStepResult r;
+    r.next_tokens.resize(batch.seq_ids.size());
+    r.final_activations = Rows(batch.size(), spec_.model_dim);
+    std::vector<std::int32_t> t(batch.seq_ids.size());
+    check(sd_engine_step_features(h_, batch.size(), batch.seq_ids.data(), batch.features.data.data(), t.data(),
+                                  r.final_activations.data.data(), nullptr));
+    for (std::size_t i = 0; i < t.size(); ++i) r.next_tokens[i] = t[i];
+    return r;
+  }
+  void retire(const std::vector<SequenceId>& seqs) {  // workers.hpp:157
+    check(sd_engine_retire(h_, static_cast<std::int32_t>(seqs.size()), seqs.data()));
+  }
+  sd_engine* handle() const { return h_; }
+
+ private:
+  ModelSpec spec_;
+  sd_engine* h_ = nullptr;
+};
+
+// ---- drive_schedule (workers.cpp:547-684) over a StepComputation, host C++
+struct GenerationConfig {  // workers.hpp:115-129 (the fields drive_schedule reads)
+  int batch = 0, target_len = 0, interval = 0;
+  long steps = 0;  // <= 0: run to completion
+  std::uint64_t seed = 0;
+  int cold_start = 0;  // 0 fixed-interval, 1 ramped-limit
+  long load_limit = 0;
+};
+struct GenerationRecord {  // workers.hpp:131-135
+  long step = 0;
+  SequenceId seq = 0;
+  int token = 0;
+};
+inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, StepComputation& comp) {
+  sd_drive_config cfg{c.batch, c.target_len, c.interval, c.cold_start, c.steps, c.load_limit, c.seed, 0};
+  sd_drive_result* r = nullptr;
+  check(sd_drive(comp.handle(), &cfg, &r));
+  std::vector<GenerationRecord> out(static_cast<std::size_t>(sd_drive_count(r)));
+  for (std::size_t i = 0; i < out.size(); ++i) {
+    std::int64_t st = 0;
+    std::uint64_t sq = 0;
+    std::int32_t tk = 0;
+    const int rc = sd_drive_record(r, static_cast<std::int64_t>(i), &st, &sq, &tk);
+    if (rc != SD_OK) {
+      sd_drive_destroy(r);
+      check(rc);
+    }
+    out[i] = GenerationRecord{static_cast<long>(st), sq, tk};
+  }
+  sd_drive_destroy(r);
+  return out;
+}
+
+// transcript_csv (workers.cpp:746-755): "step,seq_id,token_id" rows
+inline std::string transcript_csv(const std::vector<GenerationRecord>& transcript) {
+  std::string csv = "step,seq_id,token_id\n";
+  for (const GenerationRecord& rec : transcript) {
+    csv += std::to_string(rec.step) + "," + std::to_string(rec.seq) + "," + std::to_string(rec.token) + "\n";
+  }
+  return csv;
+}
+
 }  // namespace sd_b200
