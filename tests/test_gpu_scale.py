@@ -224,3 +224,28 @@ def test_c5_decode_step_matches_oracle(sd, oracle, c5_weights, mode):
     assert kv_err <= REL_BAR[mode]
     assert fx_err <= REL_BAR[mode]
     assert lg_err <= REL_BAR[mode]
+
+
+@pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
+def test_long_context_attention(sd, oracle, fmt):
+    """Context 8192 (the top of BASELINE config 5's sweep) on a few
+    sequences of ragged length: long pieces split across many CTAs and
+    merged, every stored format, against the oracle's KvShard::attend."""
+    import torch
+    spec = sd.make_model_spec(1, 4096, 32, 14336, 128256, 8)
+    lens = [8192, 8191, 4097, 1, 17, 6000]
+    seqs = list(range(101, 101 + len(lens)))
+    cap = sum(lens) + 64
+    kv = sd.KvShard(spec, 0, 8, cap, fmt, max_sequences=len(lens), max_seq_len=8192 + 16)
+    okv = oracle.KvShard(oracle.make_spec(1, 4096, 32, 14336, 128256, 8), 0, 8, cap, fmt)
+    for s, n in zip(seqs, lens):
+        kv.prefill_synthetic([s], n)
+        okv.prefill_synthetic([s], n)
+    g = torch.Generator().manual_seed(9)
+    q = (torch.rand(len(seqs), 4096, generator=g) * 2 - 1).float()
+    qd = q.cuda()
+    o = torch.empty_like(qd)
+    kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
+    torch.cuda.synchronize()
+    err = float(np.abs(o.cpu().numpy() - okv.attend(0, seqs, q.numpy())).max())
+    assert err <= 2e-5, err
