@@ -226,18 +226,20 @@ def test_c5_decode_step_matches_oracle(sd, oracle, c5_weights, mode):
     assert lg_err <= REL_BAR[mode]
 
 
+@pytest.mark.parametrize("hkv", [8, 32], ids=["gqa-tensor-core", "mha-cuda-core"])
 @pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
-def test_long_context_attention(sd, oracle, fmt):
+def test_long_context_attention(sd, oracle, fmt, hkv):
     """Context 8192 (the top of BASELINE config 5's sweep) on a few
     sequences of ragged length: long pieces split across many CTAs and
-    merged, every stored format, against the oracle's KvShard::attend."""
+    merged, every stored format, GQA (K2m) and MHA (K2), against the
+    oracle's KvShard::attend."""
     import torch
-    spec = sd.make_model_spec(1, 4096, 32, 14336, 128256, 8)
+    spec = sd.make_model_spec(1, 4096, 32, 14336, 128256, hkv)
     lens = [8192, 8191, 4097, 1, 17, 6000]
     seqs = list(range(101, 101 + len(lens)))
     cap = sum(lens) + 64
-    kv = sd.KvShard(spec, 0, 8, cap, fmt, max_sequences=len(lens), max_seq_len=8192 + 16)
-    okv = oracle.KvShard(oracle.make_spec(1, 4096, 32, 14336, 128256, 8), 0, 8, cap, fmt)
+    kv = sd.KvShard(spec, 0, hkv, cap, fmt, max_sequences=len(lens), max_seq_len=8192 + 16)
+    okv = oracle.KvShard(oracle.make_spec(1, 4096, 32, 14336, 128256, hkv), 0, hkv, cap, fmt)
     for s, n in zip(seqs, lens):
         kv.prefill_synthetic([s], n)
         okv.prefill_synthetic([s], n)
