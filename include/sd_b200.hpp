@@ -383,10 +383,11 @@ struct GenerationRecord {  // workers.hpp:131-135
   SequenceId seq = 0;
   int token = 0;
 };
-inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, StepComputation& comp) {
-  sd_drive_config cfg{c.batch, c.target_len, c.interval, c.cold_start, c.steps, c.load_limit, c.seed, 0};
-  sd_drive_result* r = nullptr;
-  check(sd_drive(comp.handle(), &cfg, &r));
+namespace detail {
+inline sd_drive_config drive_config(const GenerationConfig& c) {
+  return sd_drive_config{c.batch, c.target_len, c.interval, c.cold_start, c.steps, c.load_limit, c.seed, 0};
+}
+inline std::vector<GenerationRecord> records(sd_drive_result* r) {
   std::vector<GenerationRecord> out(static_cast<std::size_t>(sd_drive_count(r)));
   for (std::size_t i = 0; i < out.size(); ++i) {
     std::int64_t st = 0;
@@ -401,6 +402,72 @@ inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, S
   }
   sd_drive_destroy(r);
   return out;
+}
+}  // namespace detail
+
+inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, StepComputation& comp) {
+  const sd_drive_config cfg = detail::drive_config(c);
+  sd_drive_result* r = nullptr;
+  check(sd_drive(comp.handle(), &cfg, &r));
+  return detail::records(r);
+}
+
+// ---- DistributedComputation (workers.cpp:264-501) on NVLink peer memory:
+// one process per rank (several may share a device). The peer exchange is
+// connected before the first step: setup() writes this rank's CUDA IPC
+// handles (SD_DIST_IPC_BYTES), the caller gathers every rank's in rank order
+// over its own channel, connect() maps the peers.
+enum class ShardMode : int { kBySequence = SD_SHARD_BY_SEQUENCE, kByHead = SD_SHARD_BY_HEAD, kHybrid = SD_SHARD_HYBRID };
+
+// ShardMap::range_of (transport.cpp:354-376): the kv heads a rank's shard holds
+inline std::pair<int, int> shard_head_range(ShardMode mode, int heads, int workers, int rank) {
+  int h0 = 0, hc = 0;
+  check(sd_shardmap_head_range(static_cast<int>(mode), heads, workers, rank, &h0, &hc));
+  return {h0, hc};
+}
+
+class DistributedComputation {
+ public:
+  // weights: the S-ranks' weight set (nullptr on pure R-ranks); s_ranks 1 is
+  // the paper's single S-worker, s_ranks == world data-parallel S-ranks
+  DistributedComputation(WeightSet* weights, KvShard& kv, int rank, int world, int s_ranks,
+                         ShardMode mode = ShardMode::kBySequence)
+      : world_(world) {
+    check(sd_dist_create(weights ? weights->handle() : nullptr, kv.handle(), rank, world, nullptr, s_ranks,
+                         static_cast<int>(mode), &h_));
+  }
+  ~DistributedComputation() {
+    if (h_) sd_dist_destroy(h_);
+  }
+  DistributedComputation(const DistributedComputation&) = delete;
+  DistributedComputation& operator=(const DistributedComputation&) = delete;
+  std::vector<std::uint8_t> setup(int max_rows) {
+    std::vector<std::uint8_t> mine(SD_DIST_IPC_BYTES);
+    check(sd_dist_p2p_setup(h_, max_rows, mine.data()));
+    return mine;
+  }
+  void connect(const std::vector<std::uint8_t>& all_ranks) {
+    if (all_ranks.size() != static_cast<std::size_t>(world_) * SD_DIST_IPC_BYTES) {
+      throw ConfigError("connect: expected world x SD_DIST_IPC_BYTES of handles");
+    }
+    check(sd_dist_p2p_connect(h_, all_ranks.data()));
+  }
+  // the reference's pipelined_ (two interleaved mini-batches, seq % 2)
+  void set_pipelined(bool on) { check(sd_dist_pipeline(h_, on ? 1 : 0)); }
+  sd_dist* handle() const { return h_; }
+
+ private:
+  int world_;
+  sd_dist* h_ = nullptr;
+};
+
+// drive_schedule over the distributed computation: the rows this rank
+// produced (its home rows)
+inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, DistributedComputation& comp) {
+  const sd_drive_config cfg = detail::drive_config(c);
+  sd_drive_result* r = nullptr;
+  check(sd_dist_drive(comp.handle(), &cfg, &r));
+  return detail::records(r);
 }
 
 // transcript_csv (workers.cpp:746-755): "step,seq_id,token_id" rows

@@ -53,3 +53,20 @@ def test_cpp_interface_reference_dense_cases(dense_exe):
     r = subprocess.run([dense_exe, golden], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.fixture(scope="module")
+def dist_exe(tmp_path_factory):
+    return _build(tmp_path_factory, "dist_test")
+
+
+@pytest.mark.gpu
+def test_cpp_interface_reference_distributed_cases(dist_exe):
+    """test_workers.cpp:280-332 through the C++ interface: forked ranks on
+    one device (by sequence with one or two S-ranks, by head, four-rank
+    hybrid, two interleaved mini-batches, the stabilized schedule with
+    retirement) produce the monolithic transcript row for row, and every
+    shard is empty afterwards."""
+    r = subprocess.run([dist_exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
