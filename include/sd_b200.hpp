@@ -470,6 +470,55 @@ inline std::vector<GenerationRecord> drive_schedule(const GenerationConfig& c, D
   return detail::records(r);
 }
 
+// ---- the remote R-worker (workers.hpp:27-112): an AttentionWorkerSession
+// speaking SDWP over a KvShard in HBM, and the blocking serve loop
+struct AttentionWorkerConfig {  // workers.hpp:27-30 (+ the device)
+  long capacity_tokens = 1 << 20;
+  KvFormat storage = KvFormat::kSingle;
+  int device = 0;
+};
+class AttentionWorkerSession {
+ public:
+  explicit AttentionWorkerSession(const AttentionWorkerConfig& c) {
+    check(sd_rworker_create(c.capacity_tokens, static_cast<int>(c.storage), c.device, &h_));
+  }
+  ~AttentionWorkerSession() {
+    if (h_) sd_rworker_destroy(h_);
+  }
+  AttentionWorkerSession(const AttentionWorkerSession&) = delete;
+  AttentionWorkerSession& operator=(const AttentionWorkerSession&) = delete;
+  // stream bytes in (any split), the reply frames' bytes out; a fatal
+  // framing error (bad magic, oversized frame) throws ProtocolError
+  std::vector<std::uint8_t> feed(std::span<const std::uint8_t> bytes) {
+    const std::uint8_t* out = nullptr;
+    std::size_t n = 0;
+    check(sd_rworker_feed(h_, bytes.data(), bytes.size(), &out, &n));
+    return std::vector<std::uint8_t>(out, out + n);
+  }
+  bool shutdown_requested() const {
+    std::int32_t b = 0;
+    check(sd_rworker_shutdown_requested(h_, &b));
+    return b != 0;
+  }
+
+ private:
+  sd_rworker* h_ = nullptr;
+};
+struct ServeOptions {  // workers.hpp:68-74
+  std::string listen_addr = "127.0.0.1:0";
+  std::string port_file;
+  bool once = false;
+  double recv_timeout_seconds = 0;
+  AttentionWorkerConfig worker;
+};
+// serve_attention_worker (workers.cpp:162-214)
+inline int serve_attention_worker(const ServeOptions& o) {
+  check(sd_rworker_serve(o.listen_addr.c_str(), o.port_file.empty() ? nullptr : o.port_file.c_str(),
+                         o.worker.capacity_tokens, static_cast<int>(o.worker.storage), o.worker.device, o.once ? 1 : 0,
+                         o.recv_timeout_seconds));
+  return 0;
+}
+
 // transcript_csv (workers.cpp:746-755): "step,seq_id,token_id" rows
 inline std::string transcript_csv(const std::vector<GenerationRecord>& transcript) {
   std::string csv = "step,seq_id,token_id\n";

@@ -70,3 +70,18 @@ def test_cpp_interface_reference_distributed_cases(dist_exe):
     r = subprocess.run([dist_exe], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.fixture(scope="module")
+def worker_exe(tmp_path_factory):
+    return _build(tmp_path_factory, "worker_test")
+
+
+@pytest.mark.gpu
+def test_cpp_interface_attention_worker_session(worker_exe):
+    """AttentionWorkerSession over SDWP through the C++ interface: HELLO,
+    CONFIG, a first-token QKV_BATCH returning O == V bitwise (also fed one
+    byte at a time), DROP_SEQ, SHUTDOWN stats, fatal bad magic."""
+    r = subprocess.run([worker_exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
