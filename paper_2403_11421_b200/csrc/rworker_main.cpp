@@ -3,13 +3,14 @@
 // speaking SDWP over TCP with its KV shard in HBM. Options mirror the
 // reference's: --listen host:port (port 0 = ephemeral), --capacity tokens
 // (required), --storage single|half|int8, --port-file, --once, --timeout s;
-// plus --device. Built against the C ABI only (include/sd_abi.h).
+// plus --device. Built against the C ABI only, through its C++ face
+// (include/sd_b200.hpp: ServeOptions, serve_attention_worker).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 
-#include "../../include/sd_abi.h"
+#include "../../include/sd_b200.hpp"
 
 static int usage() {
   std::fprintf(stderr,
@@ -52,19 +53,29 @@ int main(int argc, char** argv) {
     }
   }
   if (capacity < 1) return usage();
-  const int fmt = storage == "single" ? SD_KV_SINGLE
-                  : storage == "half" ? SD_KV_HALF
-                  : storage == "int8" ? SD_KV_INT8
-                  : storage == "int4" ? SD_KV_INT4  // extension (sd_abi.h)
-                                      : -1;
-  if (fmt < 0) {
+  sd_b200::ServeOptions opts;
+  opts.listen_addr = listen;
+  opts.port_file = port_file;
+  opts.once = once != 0;
+  opts.recv_timeout_seconds = timeout;
+  opts.worker.capacity_tokens = static_cast<long>(capacity);
+  opts.worker.device = device;
+  if (storage == "single") {
+    opts.worker.storage = sd_b200::KvFormat::kSingle;
+  } else if (storage == "half") {
+    opts.worker.storage = sd_b200::KvFormat::kHalf;
+  } else if (storage == "int8") {
+    opts.worker.storage = sd_b200::KvFormat::kInt8;
+  } else if (storage == "int4") {  // extension (sd_abi.h)
+    opts.worker.storage = sd_b200::KvFormat::kInt4;
+  } else {
     std::fprintf(stderr, "sd_rworker: unknown kv storage format: %s\n", storage.c_str());
     return 2;
   }
-  const int rc = sd_rworker_serve(listen.c_str(), port_file.empty() ? nullptr : port_file.c_str(), capacity, fmt,
-                                  device, once, timeout);
-  if (rc != SD_OK) {
-    std::fprintf(stderr, "sd_rworker: %s\n", sd_last_error());
+  try {
+    sd_b200::serve_attention_worker(opts);
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "sd_rworker: %s\n", e.what());
     return 1;
   }
   return 0;
