@@ -184,7 +184,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   static_assert(!IM || QNT, "integer scores need quantized KV");
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
-  static_assert(RPS == 2 || RPS == 4, "pair or quad slots");
+  static_assert(RPS == 2 || RPS == 4 || RPS == 8, "pair, quad or octet slots");
   // hi / lo parts of q and p packed into the N columns of one MMA
   constexpr bool PACK = 2 * G <= 8;
   constexpr int XG = G / 2;  // lane xor between a column's hi and lo holders
@@ -840,6 +840,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 // 2-way ldmatrix conflicts (rows of a slot share bank groups); int8 keeps
 // pair slots, which its 32-bit fragment loads need.
 int attention_mma_rows_per_slot(const KvGeom& g) {
+  // fp16 shards of 1-2 kv heads have 256-512-B positions: eight per copy
+  // (2-4 KB) instead of four, the per-copy issue cost being the limit there
+  if (g.fmt == SD_KV_HALF && g.hc <= 2 && tuning().attn_rps8) return 8;
   return g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT4 || tuning().attn_i8_quad ? 4 : 2;
 }
 
@@ -888,6 +891,10 @@ void (*pick_mma(bool i8, bool i4, bool quad, bool im))(const AttnArgs) {
   if (i8) return im ? attn_mma_kernel<G, SD_KV_INT8, 2, true> : attn_mma_kernel<G, SD_KV_INT8, 2>;
   return attn_mma_kernel<G, SD_KV_HALF, 4>;
 }
+template <int G>
+void (*pick_mma_half(int rps))(const AttnArgs) {
+  return rps == 8 ? attn_mma_kernel<G, SD_KV_HALF, 8> : attn_mma_kernel<G, SD_KV_HALF, 4>;
+}
 
 void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t s) {
   void (*fn)(const AttnArgs) = nullptr;
@@ -895,13 +902,24 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
   // the slot layout the store was built with (a later attn_i8_quad flip
   // does not change an existing store's stage geometry)
   const bool quad = a.stage_region == (kT / 4) * (4 * a.g.pos_bytes + 16);
+  const bool octet = a.stage_region == (kT / 8) * (8 * a.g.pos_bytes + 16);
   const bool im = tuning().attn_imma != 0;
-  switch (a.G) {
-    case 2: fn = pick_mma<2>(i8, i4, quad, im); break;
-    case 4: fn = pick_mma<4>(i8, i4, quad, im); break;
-    case 8: fn = pick_mma<8>(i8, i4, quad, im); break;
-    default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
+  if (!i8 && !i4 && octet) {
+    switch (a.G) {
+      case 2: fn = pick_mma_half<2>(8); break;
+      case 4: fn = pick_mma_half<4>(8); break;
+      case 8: fn = pick_mma_half<8>(8); break;
+      default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
+    }
+  } else {
+    switch (a.G) {
+      case 2: fn = pick_mma<2>(i8, i4, quad, im); break;
+      case 4: fn = pick_mma<4>(i8, i4, quad, im); break;
+      case 8: fn = pick_mma<8>(i8, i4, quad, im); break;
+      default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
+    }
   }
+
   // the dynamic-smem opt-in once per instantiation and size
   static std::mutex mu;
   static std::vector<std::pair<void (*)(const AttnArgs), size_t>> set;

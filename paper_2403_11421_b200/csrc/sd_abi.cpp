@@ -531,6 +531,7 @@ int sd_tune(const char* name, int value) {
              : n == "attn_l2_prefetch" ? &t.attn_l2_prefetch
              : n == "attn_max_stages" ? &t.attn_max_stages
              : n == "attn_imma"    ? &t.attn_imma
+             : n == "attn_rps8"    ? &t.attn_rps8
                                    : nullptr;
     if (!f) sd::fail(SD_ERR_CONFIG, "sd_tune: unknown switch " + n);
     *f = value;
