@@ -185,21 +185,27 @@ def test_many_sequences_split_and_combine(sd, oracle):
     assert err < 2e-5, err
 
 
-@pytest.mark.parametrize("stages", [0, 2, 3])
+@pytest.mark.parametrize("stages,rps", [(0, 1), (2, 1), (3, 1), (0, 0)],
+                         ids=["default", "ring2", "ring3", "quad-copies"])
 @pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
 @pytest.mark.parametrize("h0,hc", [(4, 4), (2, 2), (7, 1)])
-def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages):
+def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps):
     """Shards holding 4 / 2 / 1 of 8 kv heads (by-head / hybrid ShardMap):
     the tensor-core kernel splits each head's stages over 8/hc warps and
     merges their softmax states per piece. Any requested ring depth (0 =
     default) is rounded to a multiple of those 8/hc position classes: with
     fewer ring slots than classes a class's parity wait could pass on a
-    slot's previous fill (a stage not yet landed) and the kernel hung."""
+    slot's previous fill (a stage not yet landed) and the kernel hung.
+    fp16 shards of 1-2 heads copy 8 positions at a time (attn_rps8 = 1) or
+    4 (0). Ring depth and slot layout are fixed when the store is built."""
+    if rps != 1 and (fmt != "half" or hc > 2):
+        pytest.skip("copy width variants apply to fp16 shards of 1-2 kv heads")
     G = 4
     H, D = 8 * G, 8 * G * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
     B, Lmax = 24, 500
-    gpu = sd.KvShard(s, h0, hc, B * Lmax, fmt)
+    with sd.tuned(attn_max_stages=stages, attn_rps8=rps):
+        gpu = sd.KvShard(s, h0, hc, B * Lmax, fmt)
     cpu = oracle.KvShard(os_, h0, hc, B * Lmax, fmt)
     rng = _rng(100 + hc)
     lens = rng.integers(1, Lmax, B)
@@ -214,8 +220,7 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages):
         gpu.append_request(0, ids, [pos] * len(act), k, v)
         cpu.append_request(0, ids, [pos] * len(act), k, v)
     q = rng.uniform(-3, 3, (B, w * G)).astype(np.float32)
-    with sd.tuned(attn_max_stages=stages):
-        got = gpu.attend(0, seqs, q)
+    got = gpu.attend(0, seqs, q)
     err = float(np.abs(got - cpu.attend(0, seqs, q)).max())
     assert err < 2e-5, err
 
