@@ -843,7 +843,9 @@ int attention_mma_rows_per_slot(const KvGeom& g) {
   // fp16 shards of 1-2 kv heads have 256-512-B positions: eight per copy
   // (2-4 KB) instead of four, the per-copy issue cost being the limit there
   if (g.fmt == SD_KV_HALF && g.hc <= 2 && tuning().attn_rps8) return 8;
-  return g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT4 || tuning().attn_i8_quad ? 4 : 2;
+  // int8: pairs at 8 kv heads (quads measured neutral there), quads on
+  // smaller shards (hc = 4: 0.40 -> 0.53 of the copy peak, hc = 2: 0.21 -> 0.29)
+  return g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT4 || tuning().attn_i8_quad || g.hc < 8 ? 4 : 2;
 }
 
 bool attention_mma_supported(const KvGeom& g, int G) {
