@@ -256,7 +256,10 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
  * "dist_phases" (1: per-phase DistEngine timing on stderr), "attn_i8_quad",
  * "attn_l2_prefetch", "attn_max_stages" (attention copy / prefetch / ring
  * depth variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
- * instead of integer ones). Unknown names return SD_ERR_CONFIG. */
+ * instead of integer ones), "attn_rps8" (0: fp16 shards of 1-2 kv heads copy
+ * four positions at a time instead of eight). Switches that shape a store's
+ * shared-memory layout (attn_max_stages, attn_i8_quad, attn_rps8) take effect
+ * for stores created afterwards. Unknown names return SD_ERR_CONFIG. */
 int sd_tune(const char* name, int value);
 /* Kernel launches issued by this library in this process (all devices). */
 int64_t sd_launch_count(void);
