@@ -166,6 +166,32 @@ def test_c2_mha_attention_at_bench_scale(sd, oracle):
     assert err <= 2e-5
 
 
+def test_c4_13b_attention_at_bench_scale(sd, oracle):
+    """BASELINE config 4's R-Part shape per GPU: Llama-2-13B heads (40 x 128,
+    MHA; the 10-consumer-warp CUDA-core kernel), 512 sequences x 2048
+    positions (2048 rows over 4 GPUs), fp16 KV, sampled rows."""
+    import torch
+    spec = sd.make_model_spec(1, 5120, 40, 13824, 32000)
+    Bc, ctx = 512, 2048
+    seqs = list(range(1, Bc + 1))
+    kv = sd.KvShard(spec, 0, 40, Bc * (ctx + 1), "half", max_sequences=Bc, max_seq_len=ctx + 16)
+    kv.prefill_synthetic(seqs, ctx)
+    g = torch.Generator().manual_seed(8)
+    q = (torch.rand(Bc, 5120, generator=g) * 2 - 1).float()
+    qd = q.cuda()
+    o = torch.empty_like(qd)
+    kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
+    torch.cuda.synchronize()
+    o = o.cpu().numpy()
+    rows = [0, 1, 63, 64, 255, 256, 400, 510, 511]
+    okv = oracle.KvShard(oracle.make_spec(1, 5120, 40, 13824, 32000), 0, 40, len(rows) * (ctx + 1), "half")
+    sample = [seqs[r] for r in rows]
+    okv.prefill_synthetic(sample, ctx)
+    err = float(np.abs(o[rows] - okv.attend(0, sample, q.numpy()[rows])).max())
+    _record(test="c4_attention", fmt="half", max_abs_err=err, rows=len(rows))
+    assert err <= 2e-5
+
+
 @pytest.mark.parametrize("mode", ["fp16", "tf32", "bf16"])
 def test_c5_decode_step_matches_oracle(sd, oracle, c5_weights, mode):
     """One full decode step at the bench's shapes (2 layers): the GPU engine
