@@ -8,8 +8,8 @@ target_len, so KV lengths are ragged (SURVEY §8d synthetic inputs (ii)):
 after the cold start, S/F micro-batches of B*F/S rows sit at every length
 step of F, mean ~ (S+F)/2.
 
-Two drives of the same config at different step counts give the steady
-window by difference: (tokens2 - tokens1) / (wall2 - wall1). With N > 1 the
+After an untimed short drive (one-time setup), two drives of the same
+config at different step counts give the steady window by difference: (tokens2 - tokens1) / (wall2 - wall1). With N > 1 the
 batch is B per GPU (weak scaling, as bench.py), every rank an S-rank (the
 data-parallel topology) unless --s-ranks 1; tokens are summed over ranks,
 wall is the max over ranks.
@@ -96,6 +96,7 @@ def drive(steps):
 
 s1 = a.target + a.interval
 s2 = s1 + a.extra
+drive(2 * a.interval)  # untimed: first-touch allocations and one-time setup stay out of drive 1
 n1, w1, _ = drive(s1)
 n2, w2, ps2 = drive(s2)
 steady_rows = [ps2[s] for s in range(s1 + 1, s2 + 1) if s in ps2] if world == 1 else []
