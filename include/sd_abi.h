@@ -253,11 +253,16 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
  * separate KV append kernel), "fused_argmax" (0: logits + argmax kernel),
  * "dist_fuse" (0: scatter kernel for the peer exchange), "attn_mma" (0:
  * CUDA-core attention), "pdl" (0: no programmatic dependent launch),
- * "dist_phases" (1: per-phase DistEngine timing on stderr), "attn_i8_quad",
- * "attn_l2_prefetch", "attn_max_stages" (attention copy / prefetch / ring
- * depth variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
+ * "dist_phases" (1: per-phase DistEngine timing on stderr), "attn_i8_quad"
+ * (0: int8 stages copy two positions at a time instead of four),
+ * "attn_l2_prefetch", "attn_max_stages" (attention prefetch / ring depth
+ * variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
  * instead of integer ones), "attn_rps8" (0: fp16 shards of 1-2 kv heads copy
- * four positions at a time instead of eight). Switches that shape a store's
+ * four positions at a time instead of eight), "attn_ivalue" (0: int8 KV
+ * with G <= 4 runs the value product on fp16 tensor cores over a dequantized
+ * V tile instead of integer ones with p as fixed-point byte limbs; a value
+ * > 1 also forces the integer path's int32 -> fp32 flush every that many
+ * stages, a test hook). Switches that shape a store's
  * shared-memory layout (attn_max_stages, attn_i8_quad, attn_rps8) take effect
  * for stores created afterwards. Unknown names return SD_ERR_CONFIG. */
 int sd_tune(const char* name, int value);

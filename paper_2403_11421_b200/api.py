@@ -102,9 +102,9 @@ def launch_count() -> int:
 
 
 _TUNED = {"gemm_bn": 0, "gemm_pair": 1, "fused_append": 1, "fused_argmax": 1, "dist_fuse": 1,
-          "attn_mma": 1, "pdl": 1, "dist_phases": 0, "attn_i8_quad": 0,
+          "attn_mma": 1, "pdl": 1, "dist_phases": 0, "attn_i8_quad": 1,
           "attn_l2_prefetch": 0, "attn_max_stages": 0, "attn_imma": 1,
-          "attn_rps8": 1}
+          "attn_rps8": 1, "attn_ivalue": 1}
 
 
 def tune(name: str, value: int):

@@ -104,6 +104,7 @@ struct AttnArgs {
   ORoute oroute;
   const uint8_t* l2pf;        // optional: bytes to prefetch into L2 at the end (the next GEMM's weights)
   int64_t l2pf_bytes;
+  int32_t iv_flush;           // kv_mma.cu IV: stages between forced flushes (set at launch)
 };
 
 // Static shape of the fast attention kernel for a geometry (kv_kernels.cu).

@@ -157,6 +157,20 @@ __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], u
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// D (+)= A . B, m16n8k16, both unsigned bytes (V codes, p limbs), exact int32 accumulate
+__device__ __forceinline__ void imma16816u(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(b));
+}
+// 16 x 16 byte tile, transposed (sm_100a): lane l receives, for matrix
+// columns c = l / 4 and c + 8, the bytes of rows 4 (l % 4) .. 4 (l % 4) + 3 —
+// the A fragment of an m16n8k16 byte MMA whose rows are the tile's columns;
+// lanes 0-15 give the row addresses (layout probed on the B200)
+__device__ __forceinline__ void ldsm_b8_t(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m16n16.x1.trans.shared.b8 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
 // the low byte of x as a signed value
 __device__ __forceinline__ int sbyte(int x) { return static_cast<int>(static_cast<int8_t>(x & 0xFF)); }
 constexpr int kVPitch = kHD * 2 + 16;
@@ -176,12 +190,25 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 // the accumulators; the limbs recombine in fp32. No per-element conversion
 // of K at all, where the fp16 path spends a byte permute and a subtract per
 // two values.
-template <int G, int FMT, int RPS, bool IM = false>
+//
+// IV (int8 KV, G <= 4): the value product on integer tensor cores too. V^T
+// comes straight from the ring as the A operand of u8 x u8 m16n8k16 IMMAs
+// (transposed byte ldmatrix, no dequantized scratch tile); P^T is carried as
+// a 23-bit fixed-point integer W = p * vscale * 2^22 / Sb in three byte limbs
+// (3G <= 12 B columns: limb-major, 8 per tile). The int32 accumulators live
+// across stages: p is taken against a reference max mref that moves only
+// when a stage's max passes mref + 1 (so p <= 2), and Sb bounds the warp's V
+// scales, so the integers are converted into the fp32 O (offset 128 x the
+// limb column sums removed exactly in int32, limbs recombined, rescaled to the
+// new mref) only when mref or Sb moves or before 2000 stages could overflow.
+// Resolution 2^-22 of Sb per term: ~1e-6 of max|v| against the 2e-5 bar.
+template <int G, int FMT, int RPS, bool IM = false, bool IV = false>
 __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_kernel(const AttnArgs a) {
   constexpr bool I8 = FMT == SD_KV_INT8;
   constexpr bool I4 = FMT == SD_KV_INT4;
   constexpr bool QNT = I8 || I4;  // quantized: scales in the stage, V dequantized into scratch
   static_assert(!IM || QNT, "integer scores need quantized KV");
+  static_assert(!IV || (I8 && 2 * G <= 8), "integer value product: int8 KV, G <= 4");
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
   static_assert(RPS == 2 || RPS == 4 || RPS == 8, "pair, quad or octet slots");
@@ -323,6 +350,64 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   uint32_t phase = 0;
   // ldmatrix lane address components
   const int lm = lane >> 3, lr = lane & 7;
+  // IV: int32 O^T accumulators [B tile][hd tile] (B column c = limb * G + head),
+  // per-lane partial column sums of the B fragments, the V scale bound Sb and
+  // the fixed-point factor 2^22 / Sb, stages accumulated since the last flush
+  constexpr int NT = IV ? (3 * G + 7) / 8 : 1;
+  int vacc[NT][8][4];
+  uint32_t vcs[NT];
+  float sb = 1.0f, fs = 4194288.0f;
+  int nacc = 0;
+  // this lane's B column gq in tile k holds limb (8k + gq) / G of head gq % G;
+  // row 4tq + i of the fragment is MMA row sigma(4tq + i) = 2tq + {0, 1, 8, 9}
+  uint32_t vrow_addr_off = 0;
+  if constexpr (IV) {
+    const int i = lane & 15;
+    const int srow = (i >> 2) * 2 + ((i & 3) < 2 ? (i & 3) : 6 + (i & 3));
+    vrow_addr_off = (srow % NS) * ppitch + (srow / NS) * g.pos_bytes;
+  }
+  // IV: the fp32 O^T lives in the warp's scratch ([element][lane], conflict
+  // free) while the int32 sums hold the registers; it is only touched by the
+  // (rare) flushes and read back into o at the end of a piece
+  auto ivo = [&]() { return reinterpret_cast<float*>(scr + warp * kScratch) + lane; };
+  // IV flush: int32 accumulators -> fp32 O (o = (o + W-sum * Sb / 2^22) * c),
+  // then cleared. Lanes tq < XG own heads 2tq, 2tq + 1; the other lanes keep 0
+  // so the PACK finalize adds nothing from them.
+  auto iv_flush = [&](float c0, float c1) {
+    if constexpr (IV) {
+      int cs[NT][2];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        uint32_t t = vcs[k] + __shfl_xor_sync(0xffffffffu, vcs[k], 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);  // lanes 4c..4c+3: column c's sum
+        cs[k][0] = static_cast<int>(__shfl_sync(0xffffffffu, t, 4 * (2 * tq)));
+        cs[k][1] = static_cast<int>(__shfl_sync(0xffffffffu, t, 4 * (2 * tq + 1)));
+        vcs[k] = 0u;
+      }
+      const float kf = sb * (1.0f / 4194288.0f);
+      const bool own = tq < XG;
+      float* os = ivo();
+      const int sl1 = (lane & ~3) | (((G % 8) / 2) + (tq & (XG - 1)));        // limb 1's holder
+      const int sl2 = (lane & ~3) | (((2 * G) % 8) / 2 + (tq & (XG - 1)));  // limb 2's holder
+      constexpr int T1 = G / 8, T2 = (2 * G) / 8;                           // their tiles
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          int d[NT];
+#pragma unroll
+          for (int k = 0; k < NT; ++k) {
+            d[k] = vacc[k][mt][e] - 128 * cs[k][e & 1];  // exact: the codes are q + 128
+            vacc[k][mt][e] = 0;
+          }
+          const int d1 = __shfl_sync(0xffffffffu, d[T1], sl1), d2 = __shfl_sync(0xffffffffu, d[T2], sl2);
+          const float v = fmaf(static_cast<float>(d2), 65536.0f, fmaf(static_cast<float>(d1), 256.0f, static_cast<float>(d[0])));
+          float& x = os[(4 * mt + e) * 32];
+          x = own ? (x + v * kf) * ((e & 1) ? c1 : c0) : 0.0f;
+        }
+      nacc = 0;
+    }
+  };
 
   for (int w = cb; w < ce; ++w) {
     const Piece pc = a.pieces[w];
@@ -405,12 +490,28 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         }
       }
     }
+    if constexpr (!IV) {
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
+      for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) o[mt][i] = 0.0f;
+        for (int i = 0; i < 4; ++i) o[mt][i] = 0.0f;
+    }
     m[0] = m[1] = -INFINITY;
     l[0] = l[1] = 0.0f;
+    if constexpr (IV) {
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        vcs[k] = 0u;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) vacc[k][mt][i] = 0;
+      }
+      nacc = 0;
+      float* os = ivo();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) os[32 * i] = 0.0f;
+    }
 
     for (int pos = pc.p0; pos < pc.p1; pos += kT, ++jst) {
       if (P > 1 && jst % P != cls) {  // another class's stage (warp-uniform)
@@ -526,7 +627,9 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         // lane l converts word l (4 head dims) of every row: conflict-free
         // 32-bit loads (pitch = 4 mod 32 words) and full-wavefront 64-bit stores
         uint8_t* vscr = scr + warp * kScratch;
-        if (I8) {
+        if (IV) {
+          // the value product reads the codes from the ring itself
+        } else if (I8) {
           const uint8_t* vb = st8 + a.stage_region + hk * kHD + 4 * lane;
           uint8_t* vd = vscr + 8 * lane;
 #pragma unroll
@@ -569,10 +672,12 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           vs0 = vsc[pos0 * g.hc + hk];
           vs1 = vsc[pos1 * g.hc + hk];
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
-        Vs = smem_u32(vscr);
-        vpitch = kVPitch;
+        if (!IV) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          Vs = smem_u32(vscr);
+          vpitch = kVPitch;
+        }
       } else {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -602,6 +707,63 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       for (int sh = 4; sh < 32; sh <<= 1) {
         mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, sh));
         mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, sh));
+      }
+      if constexpr (IV) {
+        // flush when the stage's max passes mref + 1 (p would exceed 2), a
+        // valid row's V scale passes Sb, or the int32 sums could overflow
+        // (iv_flush <= 2000 stages: 2000 x 16 rows x 255 x 255 < 2^31)
+        const float vl = fmaxf(v0 ? vs0 : 0.0f, v1 ? vs1 : 0.0f);
+        if (__any_sync(0xffffffffu, mx0 > m[0] + 1.0f || mx1 > m[1] + 1.0f || vl > sb || nacc == a.iv_flush)) {
+          float vm = vl;
+#pragma unroll
+          for (int sh = 4; sh < 32; sh <<= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, sh));
+          const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: position 0 of a piece is valid
+          const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
+          iv_flush(c0, c1);
+          l[0] *= c0;
+          l[1] *= c1;
+          m[0] = mn0;
+          m[1] = mn1;
+          sb = fmaxf(vm * 1.0625f, 1e-30f);  // a little headroom: fewer flushes, 0.09 bit
+          fs = 4194288.0f / sb;               // (2^22 - 16) / Sb: W < 2^23 for p <= 2
+        }
+        ++nacc;
+        const float p0 = fast_exp2(s[0] - m[0]), p1 = fast_exp2(s[1] - m[1]);
+        const float p2 = fast_exp2(s[2] - m[0]), p3 = fast_exp2(s[3] - m[1]);
+        l[0] += p0 + p2;
+        l[1] += p1 + p3;
+        // W = rn(p * vscale * fs) in the low 23 bits of the float 2^23 + W
+        const float f0 = v0 ? vs0 * fs : 0.0f, f1 = v1 ? vs1 * fs : 0.0f;
+        const uint32_t w0 = __float_as_uint(fmaf(p0, f0, 8388608.0f)), w1 = __float_as_uint(fmaf(p1, f0, 8388608.0f));
+        const uint32_t w2 = __float_as_uint(fmaf(p2, f1, 8388608.0f)), w3 = __float_as_uint(fmaf(p3, f1, 8388608.0f));
+        // transposes of the (limb 0 | limb 1) and (limb 2 | exponent) 16-bit
+        // planes: lane (gq, tq) gets head gq % G at MMA rows 2tq, 2tq + 1 (x01)
+        // and 2tq + 8, 2tq + 9 (x23)
+        const uint32_t lo01 = movm_t(__byte_perm(w0, w1, 0x5410)), lo23 = movm_t(__byte_perm(w2, w3, 0x5410));
+        const uint32_t hi01 = movm_t(__byte_perm(w0, w1, 0x7632)), hi23 = movm_t(__byte_perm(w2, w3, 0x7632));
+        uint32_t bf[NT];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          const int limb = (8 * k + gq) / G;
+          const uint32_t x = limb == 2 ? __byte_perm(hi01, hi23, 0x6420) : __byte_perm(lo01, lo23, limb ? 0x7531 : 0x6420);
+          bf[k] = limb <= 2 ? x : 0u;
+          vcs[k] = __dp4a(bf[k], 0x01010101u, vcs[k]);
+        }
+        // ---- O^T(int) += V^T . P^T, V^T codes straight from the ring
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          uint32_t r0, r1;
+          ldsm_b8_t(Vs + vrow_addr_off + 16 * mt, r0, r1);
+#pragma unroll
+          for (int k = 0; k < NT; ++k) imma16816u(vacc[k][mt], r0, r1, bf[k]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == nst) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
       }
       const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: position 0 of a piece is valid
       const float c0 = fast_exp2(m[0] - mn0), c1 = fast_exp2(m[1] - mn1);
@@ -653,6 +815,15 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
     }
 
     // ---- finalize: full row sums, then direct output or partial
+    if constexpr (IV) {
+      iv_flush(1.0f, 1.0f);  // the integer sums since the last flush, same mref
+      const float* os = ivo();
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[mt][e] = os[(4 * mt + e) * 32];
+      __syncwarp();  // the scratch becomes the merge slot below
+    }
     if (PACK) {  // O^T columns [G, 2G) hold V . P_lo: add them to the hi columns
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
@@ -843,8 +1014,11 @@ int attention_mma_rows_per_slot(const KvGeom& g) {
   // fp16 shards of 1-2 kv heads have 256-512-B positions: eight per copy
   // (2-4 KB) instead of four, the per-copy issue cost being the limit there
   if (g.fmt == SD_KV_HALF && g.hc <= 2 && tuning().attn_rps8) return 8;
-  // int8: pairs at 8 kv heads (quads measured neutral there), quads on
-  // smaller shards (hc = 4: 0.40 -> 0.53 of the copy peak, hc = 2: 0.21 -> 0.29)
+  // int8: quads. With the value product on integer tensor cores (IV) the
+  // consumers keep up and the copy count is the limit: 0.448 -> 0.351 ms per
+  // C5 layer with quads (0.975 of the copy peak); with fp16 values (G = 8) quads
+  // are neutral at 8 kv heads and faster on smaller shards (hc = 4: 0.40 ->
+  // 0.53 of the copy peak, hc = 2: 0.21 -> 0.29). attn_i8_quad = 0: pairs.
   return g.fmt == SD_KV_HALF || g.fmt == SD_KV_INT4 || tuning().attn_i8_quad || g.hc < 8 ? 4 : 2;
 }
 
@@ -887,8 +1061,11 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 }
 
 template <int G>
-void (*pick_mma(bool i8, bool i4, bool quad, bool im))(const AttnArgs) {
+void (*pick_mma(bool i8, bool i4, bool quad, bool im, bool iv))(const AttnArgs) {
   if (i4) return im ? attn_mma_kernel<G, SD_KV_INT4, 4, true> : attn_mma_kernel<G, SD_KV_INT4, 4>;
+  if constexpr (G <= 4) {  // the integer value product (scores on integer tensor cores too)
+    if (i8 && iv && im) return quad ? attn_mma_kernel<G, SD_KV_INT8, 4, true, true> : attn_mma_kernel<G, SD_KV_INT8, 2, true, true>;
+  }
   if (i8 && quad) return im ? attn_mma_kernel<G, SD_KV_INT8, 4, true> : attn_mma_kernel<G, SD_KV_INT8, 4>;
   if (i8) return im ? attn_mma_kernel<G, SD_KV_INT8, 2, true> : attn_mma_kernel<G, SD_KV_INT8, 2>;
   return attn_mma_kernel<G, SD_KV_HALF, 4>;
@@ -906,6 +1083,7 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
   const bool quad = a.stage_region == (kT / 4) * (4 * a.g.pos_bytes + 16);
   const bool octet = a.stage_region == (kT / 8) * (8 * a.g.pos_bytes + 16);
   const bool im = tuning().attn_imma != 0;
+  const bool iv = tuning().attn_ivalue != 0;
   if (!i8 && !i4 && octet) {
     switch (a.G) {
       case 2: fn = pick_mma_half<2>(8); break;
@@ -915,9 +1093,9 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
     }
   } else {
     switch (a.G) {
-      case 2: fn = pick_mma<2>(i8, i4, quad, im); break;
-      case 4: fn = pick_mma<4>(i8, i4, quad, im); break;
-      case 8: fn = pick_mma<8>(i8, i4, quad, im); break;
+      case 2: fn = pick_mma<2>(i8, i4, quad, im, iv); break;
+      case 4: fn = pick_mma<4>(i8, i4, quad, im, iv); break;
+      case 8: fn = pick_mma<8>(i8, i4, quad, im, iv); break;
       default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
     }
   }
@@ -935,7 +1113,11 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
     }
   }
   const int threads = (consumer_warps<SD_KV_HALF>() + 1) * 32;
-  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(threads), smem, s, 1, a));
+  AttnArgs b = a;
+  // attn_ivalue > 1: forced flushes every that many stages (tests reach the
+  // overflow guard's path without 32,000-position pieces)
+  b.iv_flush = tuning().attn_ivalue > 1 ? std::min(tuning().attn_ivalue, 2000) : 2000;
+  SD_CUDA(launch_pdl(fn, dim3(grid), dim3(threads), smem, s, 1, b));
   SD_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -532,6 +532,7 @@ int sd_tune(const char* name, int value) {
              : n == "attn_max_stages" ? &t.attn_max_stages
              : n == "attn_imma"    ? &t.attn_imma
              : n == "attn_rps8"    ? &t.attn_rps8
+             : n == "attn_ivalue"  ? &t.attn_ivalue
                                    : nullptr;
     if (!f) sd::fail(SD_ERR_CONFIG, "sd_tune: unknown switch " + n);
     *f = value;

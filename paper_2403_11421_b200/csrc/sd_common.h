@@ -85,11 +85,13 @@ struct Tuning {
   int attn_mma = 1;      // tensor-core attention where the geometry allows it
   int pdl = 1;           // programmatic dependent launch between the step's kernels
   int dist_phases = 0;   // per-phase CUDA events in DistEngine, printed to stderr at destroy
-  int attn_i8_quad = 0;  // int8 tensor-core attention: four positions per bulk copy (else two)
+  int attn_i8_quad = 1;  // int8 tensor-core attention: four positions per bulk copy (else two; set when a store is built)
   int attn_l2_prefetch = 0;  // the attention prefetches the W_o weights into L2 at its end
   int attn_max_stages = 0;   // tensor-core attention ring depth (0: the per-format default)
-  int attn_imma = 1;
-  int attn_rps8 = 1;         // fp16 shards of <= 2 kv heads copy 8 positions at a time (set when a store is built)         // int8 / int4 KV: scores on integer tensor cores (q as byte limbs)
+  int attn_imma = 1;          // int8 / int4 KV: scores on integer tensor cores (q as byte limbs)
+  int attn_rps8 = 1;          // fp16 shards of <= 2 kv heads copy 8 positions at a time (set when a store is built)
+  int attn_ivalue = 1;        // int8 KV, G <= 4, with attn_imma: the value product on integer tensor cores
+                              // too; > 1 also forces its int32 -> fp32 flush every that many stages (tests)
 };
 inline Tuning& tuning() {
   static Tuning t;

@@ -25,6 +25,19 @@ def test_library_exports_every_declared_symbol():
     assert sd.lib.sd_abi_version() == 1
 
 
+def test_every_tuning_switch_is_known_and_documented():
+    """sd_tune accepts each switch the Python mirror restores (api._TUNED)
+    and sd_abi.h documents it; an unknown name is a ConfigError."""
+    import paper_2403_11421_b200 as sd
+    from paper_2403_11421_b200 import api
+    doc = open(os.path.join(ROOT, "include", "sd_abi.h")).read()
+    for name, default in api._TUNED.items():
+        sd.tune(name, default)
+        assert f'"{name}"' in doc, name
+    with pytest.raises(sd.ConfigError):
+        sd.tune("no_such_switch", 1)
+
+
 def test_spec_and_errors_match_reference():
     import paper_2403_11421_b200 as sd
     s = sd.make_model_spec(2, 64, 4, 256, 128)

@@ -187,9 +187,10 @@ def test_many_sequences_split_and_combine(sd, oracle):
 
 @pytest.mark.parametrize("stages,rps", [(0, 1), (2, 1), (3, 1), (0, 0)],
                          ids=["default", "ring2", "ring3", "quad-copies"])
+@pytest.mark.parametrize("iv", [0, 1], ids=["fp16-values", "int-values"])
 @pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
 @pytest.mark.parametrize("h0,hc", [(4, 4), (2, 2), (7, 1)])
-def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps):
+def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps, iv):
     """Shards holding 4 / 2 / 1 of 8 kv heads (by-head / hybrid ShardMap):
     the tensor-core kernel splits each head's stages over 8/hc warps and
     merges their softmax states per piece. Any requested ring depth (0 =
@@ -200,6 +201,8 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps):
     4 (0). Ring depth and slot layout are fixed when the store is built."""
     if rps != 1 and (fmt != "half" or hc > 2):
         pytest.skip("copy width variants apply to fp16 shards of 1-2 kv heads")
+    if iv and fmt != "int8":
+        pytest.skip("the integer value product is int8 only")
     G = 4
     H, D = 8 * G, 8 * G * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
@@ -220,21 +223,28 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps):
         gpu.append_request(0, ids, [pos] * len(act), k, v)
         cpu.append_request(0, ids, [pos] * len(act), k, v)
     q = rng.uniform(-3, 3, (B, w * G)).astype(np.float32)
-    got = gpu.attend(0, seqs, q)
+    with sd.tuned(attn_ivalue=iv):
+        got = gpu.attend(0, seqs, q)
     err = float(np.abs(got - cpu.attend(0, seqs, q)).max())
     assert err < 2e-5, err
 
 
+@pytest.mark.parametrize("iv", [0, 1, 3], ids=["fp16-values", "int-values", "int-values-flush3"])
 @pytest.mark.parametrize("imma", [1, 0], ids=["int-scores", "fp16-scores"])
 @pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
 @pytest.mark.parametrize("G", [2, 4, 8])
-def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt, imma):
+def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt, imma, iv):
     """fp16 / int8 KV, hd 128, 8 kv heads: the mma.sync attention path
     (kv_mma.cu), with ragged lengths (tails of 16-position stages) and split
     pieces. int8 keys enter the MMA as exact fp16 integers with the K scale
-    applied to the scores and the V scale folded into p; same bar as fp16."""
+    applied to the scores and the V scale folded into p; same bar as fp16.
+    iv: int8 values on integer tensor cores too (p as 23-bit fixed point in
+    byte limbs, int32 sums flushed to fp32 when the reference max or the
+    scale bound moves; flush3 forces a flush every 3 stages)."""
     if fmt == "half" and not imma:
         pytest.skip("fp16 KV has one score path")
+    if iv and (fmt != "int8" or not imma or G > 4):
+        pytest.skip("the integer value product: int8 KV, integer scores, G <= 4")
     H = 8 * G
     D = H * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
@@ -253,7 +263,7 @@ def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt, imma):
         gpu.append_request(0, ids, [pos] * len(act), k, v)
         cpu.append_request(0, ids, [pos] * len(act), k, v)
     q = rng.uniform(-3, 3, (B, D)).astype(np.float32)
-    with sd.tuned(attn_imma=imma):
+    with sd.tuned(attn_imma=imma, attn_ivalue=iv):
         og = gpu.attend(0, seqs, q)
     oc = cpu.attend(0, seqs, q)
     err = float(np.abs(og - oc).max())
@@ -361,8 +371,8 @@ def test_slot_and_page_reuse_after_drop(sd, oracle):
     assert g.token_count() == c.token_count()
 
 
-@pytest.mark.parametrize("fmt", ["int8", "int4"])
-def test_integer_scores_extreme_query_scales(sd, oracle, fmt):
+@pytest.mark.parametrize("fmt,iv", [("int8", 0), ("int4", 0), ("int8", 1), ("int8", 2)])
+def test_integer_scores_extreme_query_scales(sd, oracle, fmt, iv):
     """The integer-score path carries q per head as a 22-bit fixed-point
     integer scaled by the head's max: a zero head, a ~1e-20 head and a
     sharply peaked (x30) head must match the oracle like an ordinary one."""
@@ -384,22 +394,24 @@ def test_integer_scores_extreme_query_scales(sd, oracle, fmt):
     q[:, 1::4] *= 1e-20
     q[:, 2::4] *= 30.0
     q = q.reshape(B, D)
-    with sd.tuned(attn_imma=1):
+    with sd.tuned(attn_imma=1, attn_ivalue=iv):
         og = gpu.attend(0, seqs, q)
     oc = cpu.attend(0, seqs, q)
     err = float(np.abs(og - oc).max())
     assert err < 2e-5, err
 
 
+@pytest.mark.parametrize("iv", [1, 0], ids=["int-values", "fp16-values"])
 @pytest.mark.parametrize("imma", [1, 0])
-def test_int8_quad_slot_variant(sd, oracle, imma):
-    """int8 with four positions per bulk copy (attn_i8_quad, the layout int4
-    always uses) under both score paths: same results as the oracle."""
+def test_int8_pair_slot_variant(sd, oracle, imma, iv):
+    """int8 with two positions per bulk copy (attn_i8_quad = 0; the default
+    is four, the layout int4 always uses) under both score and value paths:
+    same results as the oracle."""
     G = 4
     H, D = 8 * G, 8 * G * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
     B, Lmax = 12, 300
-    with sd.tuned(attn_i8_quad=1):  # the slot layout is fixed when the store is built
+    with sd.tuned(attn_i8_quad=0):  # the slot layout is fixed when the store is built
         gpu = sd.KvShard(s, 0, 8, B * Lmax, "int8")
     cpu = oracle.KvShard(os_, 0, 8, B * Lmax, "int8")
     rng = _rng(31)
@@ -414,7 +426,7 @@ def test_int8_quad_slot_variant(sd, oracle, imma):
         gpu.append_request(0, ids, [pos] * len(act), k, v)
         cpu.append_request(0, ids, [pos] * len(act), k, v)
     q = rng.uniform(-3, 3, (B, D)).astype(np.float32)
-    with sd.tuned(attn_imma=imma):
+    with sd.tuned(attn_imma=imma, attn_ivalue=iv):
         og = gpu.attend(0, seqs, q)
     err = float(np.abs(og - cpu.attend(0, seqs, q)).max())
     assert err < 2e-5, err

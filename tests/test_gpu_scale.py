@@ -114,11 +114,12 @@ def test_c5_quantized_prefill_bit_exact(sd, oracle, fmt):
                 assert np.array_equal(bg, bc) and np.array_equal(sg.view(np.uint32), sc.view(np.uint32))
 
 
-@pytest.mark.parametrize("fmt,bar", [("half", 2e-5), ("int8", 2e-5), ("int4", 2e-5)])
-def test_c5_attention_at_bench_scale(sd, oracle, fmt, bar):
+@pytest.mark.parametrize("fmt,bar,iv", [("half", 2e-5, 0), ("int8", 2e-5, 0), ("int4", 2e-5, 0), ("int8", 2e-5, 1)])
+def test_c5_attention_at_bench_scale(sd, oracle, fmt, bar, iv):
     """The tensor-core GQA attention (K2m) over the bench's batch and context
     (512 sequences x 2048 positions, 8 kv heads, G=4), one shared q: sampled
-    rows against the oracle's KvShard::attend (attention.cpp:204-282)."""
+    rows against the oracle's KvShard::attend (attention.cpp:204-282).
+    iv: int8 values on integer tensor cores (attn_ivalue)."""
     import torch
     spec = sd.make_model_spec(1, 4096, 32, 14336, 128256, 8)
     seqs = list(range(1, B + 1))
@@ -128,7 +129,8 @@ def test_c5_attention_at_bench_scale(sd, oracle, fmt, bar):
     q = (torch.rand(B, 4096, generator=g) * 2 - 1).float()
     qd = q.cuda()
     o = torch.empty_like(qd)
-    kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
+    with sd.tuned(attn_ivalue=iv):
+        kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
     torch.cuda.synchronize()
     o = o.cpu().numpy()
     okv = oracle.KvShard(oracle.make_spec(1, 4096, 32, 14336, 128256, 8), 0, 8, len(SAMPLE_ROWS) * (CTX + 1), fmt)
@@ -136,7 +138,7 @@ def test_c5_attention_at_bench_scale(sd, oracle, fmt, bar):
     okv.prefill_synthetic(sample, CTX)
     ref = okv.attend(0, sample, q.numpy()[SAMPLE_ROWS])
     err = float(np.abs(o[SAMPLE_ROWS] - ref).max())
-    _record(test="c5_attention", fmt=fmt, max_abs_err=err, rows=len(SAMPLE_ROWS))
+    _record(test="c5_attention", fmt=fmt, ivalue=iv, max_abs_err=err, rows=len(SAMPLE_ROWS))
     assert err <= bar
 
 
@@ -252,13 +254,16 @@ def test_c5_decode_step_matches_oracle(sd, oracle, c5_weights, mode):
     assert lg_err <= REL_BAR[mode]
 
 
+@pytest.mark.parametrize("iv", [0, 1], ids=["fp16-values", "int-values"])
 @pytest.mark.parametrize("hkv", [8, 32], ids=["gqa-tensor-core", "mha-cuda-core"])
 @pytest.mark.parametrize("fmt", ["half", "int8", "int4"])
-def test_long_context_attention(sd, oracle, fmt, hkv):
+def test_long_context_attention(sd, oracle, fmt, hkv, iv):
     """Context 8192 (the top of BASELINE config 5's sweep) on a few
     sequences of ragged length: long pieces split across many CTAs and
     merged, every stored format, GQA (K2m) and MHA (K2), against the
     oracle's KvShard::attend."""
+    if iv and (fmt != "int8" or hkv != 8):
+        pytest.skip("the integer value product: int8 GQA")
     import torch
     spec = sd.make_model_spec(1, 4096, 32, 14336, 128256, hkv)
     lens = [8192, 8191, 4097, 1, 17, 6000]
@@ -273,7 +278,8 @@ def test_long_context_attention(sd, oracle, fmt, hkv):
     q = (torch.rand(len(seqs), 4096, generator=g) * 2 - 1).float()
     qd = q.cuda()
     o = torch.empty_like(qd)
-    kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
+    with sd.tuned(attn_ivalue=iv):
+        kv.attend_dev(0, seqs, qd.data_ptr(), o.data_ptr())
     torch.cuda.synchronize()
     err = float(np.abs(o.cpu().numpy() - okv.attend(0, seqs, q.numpy())).max())
     assert err <= 2e-5, err
