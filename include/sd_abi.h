@@ -258,8 +258,8 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
  * "attn_l2_prefetch", "attn_max_stages" (attention prefetch / ring depth
  * variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
  * instead of integer ones), "attn_rps8" (0: fp16 shards of 1-2 kv heads copy
- * four positions at a time instead of eight), "attn_ivalue" (0: int8 KV
- * with G <= 4 runs the value product on fp16 tensor cores over a dequantized
+ * four positions at a time instead of eight), "attn_ivalue" (0: int8 /
+ * int4 KV with G <= 4 runs the value product on fp16 tensor cores over a dequantized
  * V tile instead of integer ones with p as fixed-point byte limbs; a value
  * > 1 also forces the integer path's int32 -> fp32 flush every that many
  * stages, a test hook). Switches that shape a store's

@@ -19,8 +19,9 @@
 //
 // Work split, TMA bulk-copy producer, mbarrier ring and piece/partial
 // protocol are those of attn_kernel (kv_kernels.cu); stages hold 16
-// positions copied four (fp16, int4) or two (int8) per bulk copy (the per-SM copy
-// issue rate, not bytes, limits row-sized copies) into slots with a 16-B pad;
+// positions copied four per bulk copy (int8: two with attn_i8_quad = 0; fp16
+// shards of 1-2 kv heads: eight) — the per-SM copy issue rate, not bytes,
+// limits row-sized copies — into slots with a 16-B pad;
 // MMA row r holds position (r % NS) * RPS + r / NS (NS slots of RPS rows).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -191,9 +192,10 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 // of K at all, where the fp16 path spends a byte permute and a subtract per
 // two values.
 //
-// IV (int8 KV, G <= 4): the value product on integer tensor cores too. V^T
-// comes straight from the ring as the A operand of u8 x u8 m16n8k16 IMMAs
-// (transposed byte ldmatrix, no dequantized scratch tile); P^T is carried as
+// IV (int8 / int4 KV, G <= 4): the value product on integer tensor cores
+// too. V^T comes straight from the ring as the A operand of u8 x u8 m16n8k16
+// IMMAs (transposed byte ldmatrix, no dequantized scratch tile; int4: one AND
+// / shift-AND per word splits a byte column into its two head dims); P^T is carried as
 // a 23-bit fixed-point integer W = p * vscale * 2^22 / Sb in three byte limbs
 // (3G <= 12 B columns: limb-major, 8 per tile). The int32 accumulators live
 // across stages: p is taken against a reference max mref that moves only
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   constexpr bool I4 = FMT == SD_KV_INT4;
   constexpr bool QNT = I8 || I4;  // quantized: scales in the stage, V dequantized into scratch
   static_assert(!IM || QNT, "integer scores need quantized KV");
-  static_assert(!IV || (I8 && 2 * G <= 8), "integer value product: int8 KV, G <= 4");
+  static_assert(!IV || (QNT && 2 * G <= 8), "integer value product: quantized KV, G <= 4");
   constexpr int kWarps = consumer_warps<FMT>();
   constexpr int kThreads = (kWarps + 1) * 32;
   static_assert(RPS == 2 || RPS == 4 || RPS == 8, "pair, quad or octet slots");
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           int d[NT];
 #pragma unroll
           for (int k = 0; k < NT; ++k) {
-            d[k] = vacc[k][mt][e] - 128 * cs[k][e & 1];  // exact: the codes are q + 128
+            d[k] = vacc[k][mt][e] - (I8 ? 128 : 8) * cs[k][e & 1];  // exact: the codes are q + 128 (q + 8)
             vacc[k][mt][e] = 0;
           }
           const int d1 = __shfl_sync(0xffffffffu, d[T1], sl1), d2 = __shfl_sync(0xffffffffu, d[T2], sl2);
@@ -750,12 +752,31 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           vcs[k] = __dp4a(bf[k], 0x01010101u, vcs[k]);
         }
         // ---- O^T(int) += V^T . P^T, V^T codes straight from the ring
+        if constexpr (I8) {
 #pragma unroll
-        for (int mt = 0; mt < 8; ++mt) {
-          uint32_t r0, r1;
-          ldsm_b8_t(Vs + vrow_addr_off + 16 * mt, r0, r1);
+          for (int mt = 0; mt < 8; ++mt) {
+            uint32_t r0, r1;
+            ldsm_b8_t(Vs + vrow_addr_off + 16 * mt, r0, r1);
 #pragma unroll
-          for (int k = 0; k < NT; ++k) imma16816u(vacc[k][mt], r0, r1, bf[k]);
+            for (int k = 0; k < NT; ++k) imma16816u(vacc[k][mt], r0, r1, bf[k]);
+          }
+        } else {
+          // int4: byte column c of a 16 x 16 tile is head dims (2c, 2c + 1) of
+          // 32; its low / high nibbles make the A rows of tiles 2j (dims
+          // 32j + 2g, 32j + 2g + 16) and 2j + 1 (the same + 1)
+          const uint32_t vb4 = smem_u32(st8) + a.stage_region + hk * (kHD / 2) + vrow_addr_off;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t r0, r1;
+            ldsm_b8_t(vb4 + 16 * j, r0, r1);
+            const uint32_t a0 = r0 & 0x0F0F0F0Fu, a1 = r1 & 0x0F0F0F0Fu;
+            const uint32_t b0 = (r0 >> 4) & 0x0F0F0F0Fu, b1 = (r1 >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+            for (int k = 0; k < NT; ++k) {
+              imma16816u(vacc[k][2 * j], a0, a1, bf[k]);
+              imma16816u(vacc[k][2 * j + 1], b0, b1, bf[k]);
+            }
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
@@ -823,6 +844,24 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 #pragma unroll
         for (int e = 0; e < 4; ++e) o[mt][e] = os[(4 * mt + e) * 32];
       __syncwarp();  // the scratch becomes the merge slot below
+      if constexpr (I4) {
+        // back to the standard fragment layout (tile mt = head dims 16 mt ..
+        // 16 mt + 15) through the scratch as O^T[dim][column]
+        float* t = reinterpret_cast<float*>(scr + warp * kScratch);
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int dim = 32 * (mt >> 1) + 2 * gq + 16 * (e >> 1) + (mt & 1);
+            t[dim * 8 + 2 * tq + (e & 1)] = o[mt][e];
+          }
+        __syncwarp();
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[mt][e] = t[(16 * mt + gq + 8 * (e >> 1)) * 8 + 2 * tq + (e & 1)];
+        __syncwarp();
+      }
     }
     if (PACK) {  // O^T columns [G, 2G) hold V . P_lo: add them to the hi columns
 #pragma unroll
@@ -1062,10 +1101,11 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 
 template <int G>
 void (*pick_mma(bool i8, bool i4, bool quad, bool im, bool iv))(const AttnArgs) {
-  if (i4) return im ? attn_mma_kernel<G, SD_KV_INT4, 4, true> : attn_mma_kernel<G, SD_KV_INT4, 4>;
   if constexpr (G <= 4) {  // the integer value product (scores on integer tensor cores too)
+    if (i4 && iv && im) return attn_mma_kernel<G, SD_KV_INT4, 4, true, true>;
     if (i8 && iv && im) return quad ? attn_mma_kernel<G, SD_KV_INT8, 4, true, true> : attn_mma_kernel<G, SD_KV_INT8, 2, true, true>;
   }
+  if (i4) return im ? attn_mma_kernel<G, SD_KV_INT4, 4, true> : attn_mma_kernel<G, SD_KV_INT4, 4>;
   if (i8 && quad) return im ? attn_mma_kernel<G, SD_KV_INT8, 4, true> : attn_mma_kernel<G, SD_KV_INT8, 4>;
   if (i8) return im ? attn_mma_kernel<G, SD_KV_INT8, 2, true> : attn_mma_kernel<G, SD_KV_INT8, 2>;
   return attn_mma_kernel<G, SD_KV_HALF, 4>;

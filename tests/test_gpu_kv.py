@@ -201,8 +201,8 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps, iv):
     4 (0). Ring depth and slot layout are fixed when the store is built."""
     if rps != 1 and (fmt != "half" or hc > 2):
         pytest.skip("copy width variants apply to fp16 shards of 1-2 kv heads")
-    if iv and fmt != "int8":
-        pytest.skip("the integer value product is int8 only")
+    if iv and fmt == "half":
+        pytest.skip("the integer value product: quantized KV")
     G = 4
     H, D = 8 * G, 8 * G * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
@@ -240,11 +240,12 @@ def test_gqa_tensor_core_path_parity(sd, oracle, G, fmt, imma, iv):
     applied to the scores and the V scale folded into p; same bar as fp16.
     iv: int8 values on integer tensor cores too (p as 23-bit fixed point in
     byte limbs, int32 sums flushed to fp32 when the reference max or the
-    scale bound moves; flush3 forces a flush every 3 stages)."""
+    scale bound moves; flush3 forces a flush every 3 stages; int4 splits a
+    byte column's nibbles into two head dims)."""
     if fmt == "half" and not imma:
         pytest.skip("fp16 KV has one score path")
-    if iv and (fmt != "int8" or not imma or G > 4):
-        pytest.skip("the integer value product: int8 KV, integer scores, G <= 4")
+    if iv and (fmt == "half" or not imma or G > 4):
+        pytest.skip("the integer value product: quantized KV, integer scores, G <= 4")
     H = 8 * G
     D = H * 128
     s, os_ = _specs(sd, oracle, 1, D, H, 8, 8, 8)
@@ -371,7 +372,7 @@ def test_slot_and_page_reuse_after_drop(sd, oracle):
     assert g.token_count() == c.token_count()
 
 
-@pytest.mark.parametrize("fmt,iv", [("int8", 0), ("int4", 0), ("int8", 1), ("int8", 2)])
+@pytest.mark.parametrize("fmt,iv", [("int8", 0), ("int4", 0), ("int8", 1), ("int8", 2), ("int4", 1), ("int4", 2)])
 def test_integer_scores_extreme_query_scales(sd, oracle, fmt, iv):
     """The integer-score path carries q per head as a 22-bit fixed-point
     integer scaled by the head's max: a zero head, a ~1e-20 head and a
