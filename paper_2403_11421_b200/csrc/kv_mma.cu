@@ -416,9 +416,12 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
     if constexpr (IM) {
       // B column gq = head gq (< G); k slot i of step s, half h is head dim
       // 32s + 16h + 4tq + i (int8: a lane's 4 K bytes) or 32s + 8tq + 2i + h
-      // (int4: low / high nibbles of a lane's K word)
+      // (int4: low / high nibbles of a lane's K word). PACK (G <= 4): limbs 0
+      // and 1 share one MMA (columns [0, G) and [G, 2G)), limb 2 takes a
+      // second: two IMMAs per k-step instead of three
       const float* qrow = a.q + static_cast<int64_t>(pc.item) * a.q_stride + static_cast<int64_t>(hk) * G * kHD;
-      const bool colv = gq < G;
+      const bool colv = gq < (PACK ? 2 * G : G);
+      const int hcol = PACK && gq >= G ? gq - G : gq;
       float xv[4][2][4];
       float mx = 0.0f;
 #pragma unroll
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int d = I8 ? 32 * s + 16 * h + 4 * tq + i : 32 * s + 8 * tq + 2 * i + h;
-            xv[s][h][i] = colv ? qrow[gq * kHD + d] * a.qscale : 0.0f;
+            xv[s][h][i] = colv ? qrow[hcol * kHD + d] * a.qscale : 0.0f;
             mx = fmaxf(mx, fabsf(xv[s][h][i]));
           }
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -456,14 +459,27 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
             pk[1] |= static_cast<uint32_t>(l1 & 0xFF) << (8 * i);
             pk[2] |= static_cast<uint32_t>(l2 & 0xFF) << (8 * i);
           }
+          if constexpr (PACK) {
+            ql[0][s][h] = gq < G ? pk[0] : pk[1];  // (columns >= 2G: zero q, zero limbs)
+            ql[1][s][h] = gq < G ? pk[2] : 0u;
+          } else {
 #pragma unroll
-          for (int t = 0; t < 3; ++t) ql[t][s][h] = pk[t];
+            for (int t = 0; t < 3; ++t) ql[t][s][h] = pk[t];
+          }
         }
       const int bias = I8 ? 128 : 8;
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 1);
         cs[t] += __shfl_xor_sync(0xffffffffu, cs[t], 2);
+      }
+      if constexpr (PACK) {
+        const int ca = gq < G ? cs[0] : cs[1], cb2 = gq < G ? cs[2] : 0;
+        cs[0] = ca;
+        cs[1] = cb2;
+      }
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) qinit[t][j] = -bias * __shfl_sync(0xffffffffu, cs[t], 4 * ((2 * tq + j) & 7));
       }
@@ -560,7 +576,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
             ka[3] = (w1 >> 4) & 0x0F0F0F0Fu;
           }
 #pragma unroll
-          for (int t = 0; t < 3; ++t) imma16832(dacc[t], ka, ql[t][st][0], ql[t][st][1]);
+          for (int t = 0; t < (PACK ? 2 : 3); ++t) imma16832(dacc[t], ka, ql[t][st][0], ql[t][st][1]);
         }
         // per-(position, head) K scales: S = kscale * 2^(E-22) * (q_int . k)
         const float* ksc = reinterpret_cast<const float*>(st8 + 2 * a.stage_region);
@@ -568,8 +584,12 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
         const float k0 = ksc[pos0 * g.hc + hk], k1 = ksc[pos1 * g.hc + hk];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
+          // PACK: limb 1 of this lane's heads sits XG lanes over (columns + G),
+          // limb 2 in the second accumulator (lanes tq >= XG: filled below)
+          const int l1 = PACK ? __shfl_xor_sync(0xffffffffu, dacc[0][e], XG) : dacc[1][e];
+          const int l2 = PACK ? dacc[1][e] : dacc[2][e];
           const float v = fmaf(static_cast<float>(dacc[0][e]), 65536.0f,
-                               fmaf(static_cast<float>(dacc[1][e]), 256.0f, static_cast<float>(dacc[2][e])));
+                               fmaf(static_cast<float>(l1), 256.0f, static_cast<float>(l2)));
           s[e] = v * (qdown[e & 1] * (e < 2 ? k0 : k1));
         }
         if (PACK) {  // lanes whose columns are past G take the scores of lane tq & (XG - 1)
