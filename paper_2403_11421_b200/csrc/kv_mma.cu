@@ -362,6 +362,11 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
   int nacc = 0;
   // this lane's B column gq in tile k holds limb (8k + gq) / G of head gq % G;
   // row 4tq + i of the fragment is MMA row sigma(4tq + i) = 2tq + {0, 1, 8, 9}
+  // IM int8: ldmatrix x4 row addresses of the K tile (lanes 0-15: MMA rows
+  // 0-15 at k bytes 0-15 of a k-step, lanes 16-31: the same rows at 16-31)
+  // (int4: 16-B chunks 2j and 2j + 1 of a row, two k32-steps per LDSM)
+  const uint32_t klsm_off = hk * (I4 ? kHD / 2 : kHD) + ((lane & 15) % NS) * ppitch + ((lane & 15) / NS) * g.pos_bytes +
+                            (lane >> 4) * 16;
   uint32_t vrow_addr_off = 0;
   if constexpr (IV) {
     const int i = lane & 15;
@@ -551,25 +556,23 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
       // accumulator chains (even / odd k-steps) halve the dependent HMMA depth
       float s[4] = {0.0f, 0.0f, 0.0f, 0.0f}, s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       if constexpr (IM) {
-        const uint8_t* kb = st8 + hk * (I4 ? kHD / 2 : kHD) + 4 * tq + (gq % NS) * ppitch + (gq / NS) * g.pos_bytes;
-        const int krow8 = ((gq + 8) / NS - gq / NS) * g.pos_bytes;  // row gq + 8, same slot
         int dacc[3][4];
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
           dacc[t][0] = dacc[t][2] = qinit[t][0];
           dacc[t][1] = dacc[t][3] = qinit[t][1];
         }
+        uint32_t kw4[4];  // int4: rows gq, gq + 8 of two 16-B chunks
 #pragma unroll
         for (int st = 0; st < 4; ++st) {
           uint32_t ka[4];
           if (I8) {
-            ka[0] = *reinterpret_cast<const uint32_t*>(kb + 32 * st);
-            ka[1] = *reinterpret_cast<const uint32_t*>(kb + krow8 + 32 * st);
-            ka[2] = *reinterpret_cast<const uint32_t*>(kb + 32 * st + 16);
-            ka[3] = *reinterpret_cast<const uint32_t*>(kb + krow8 + 32 * st + 16);
+            // the m16n8k32 byte A fragment is the b16 ldmatrix x4 layout read
+            // as bytes: one LDSM per k-step instead of four 32-bit loads
+            ldsm_x4(smem_u32(st8) + klsm_off + 32 * st, ka);
           } else {
-            const uint32_t w0 = *reinterpret_cast<const uint32_t*>(kb + 16 * st);
-            const uint32_t w1 = *reinterpret_cast<const uint32_t*>(kb + krow8 + 16 * st);
+            if ((st & 1) == 0) ldsm_x4(smem_u32(st8) + klsm_off + 16 * st, kw4);
+            const uint32_t w0 = kw4[2 * (st & 1)], w1 = kw4[2 * (st & 1) + 1];
             ka[0] = w0 & 0x0F0F0F0Fu;
             ka[1] = w1 & 0x0F0F0F0Fu;
             ka[2] = (w0 >> 4) & 0x0F0F0F0Fu;
