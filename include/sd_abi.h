@@ -257,7 +257,7 @@ int sd_engine_pipeline(sd_engine* e, int enable, int r_sms);
  * (0: int8 stages copy two positions at a time instead of four),
  * "attn_l2_prefetch", "attn_max_stages" (attention prefetch / ring depth
  * variants), "attn_imma" (0: int8 / int4 scores on fp16 tensor cores
- * instead of integer ones), "attn_rps8" (0: fp16 shards of 1-2 kv heads copy
+ * instead of integer ones), "attn_rps8" (0: shards of 1-2 kv heads copy
  * four positions at a time instead of eight), "attn_ivalue" (0: int8 /
  * int4 KV with G <= 4 runs the value product on fp16 tensor cores over a dequantized
  * V tile instead of integer ones with p as fixed-point byte limbs; a value

@@ -273,15 +273,22 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
     for (int w = cb; w < ce; ++w) {
       const Piece pc = a.pieces[w];
       const int32_t* pt = g.page_table + static_cast<int64_t>(a.item_slot[pc.item]) * g.max_pages;
+      // the page of the next stage is loaded one stage ahead, so its latency
+      // overlaps the wait for a free slot (small shards: ~1,000 cycles per stage
+      // of producer latency otherwise)
+      int32_t pg_next = pc.p0 < pc.p1 ? pt[pc.p0 >> g.log2P] : 0;
       for (int pos = pc.p0; pos < pc.p1; pos += kT) {
         // a stage ending before the piece's last position cannot hold the
         // position being appended (the item's last) nor a page opened for it
         if (!waited && pos + kT >= pc.p1) {
           pdl_wait();
           waited = true;
+          pg_next = pt[pos >> g.log2P];  // (re-read after the wait: the appended position's page)
         }
+        const int32_t pg = pg_next;
+        if (pos + kT < pc.p1) pg_next = pt[(pos + kT) >> g.log2P];
         const int cnt = min(kT, pc.p1 - pos);
-        const uint8_t* base = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes +
+        const uint8_t* base = layer_base + static_cast<int64_t>(pg) * g.group_bytes +
                               static_cast<int64_t>(pos & (g.P - 1)) * g.pos_bytes;
         // scale block rounded up to the bulk-copy granule (16 B): stages start
         // 16-aligned in a page group, so the extra scales stay inside its region
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__((consumer_warps<FMT>() + 1) * 32, 1) attn_mma_
           }
         }
         if (QNT && (lane == 0 || lane == 16)) {  // the stage's scales (one page group: contiguous)
-          const uint8_t* lb = layer_base + static_cast<int64_t>(pt[pos >> g.log2P]) * g.group_bytes;
+          const uint8_t* lb = layer_base + static_cast<int64_t>(pg) * g.group_bytes;
           const int off = pos & (g.P - 1);
           uint8_t* dst = ring + stage * stage_bytes + 2 * a.stage_region + (lane ? a.sc_region : 0);
           bulk_g2s(dst, lb + (lane ? g.vs_off : g.ks_off) + off * g.hc * 4, scb, &full[stage], pol);
@@ -1076,6 +1083,10 @@ int attention_mma_rows_per_slot(const KvGeom& g) {
   // fp16 shards of 1-2 kv heads have 256-512-B positions: eight per copy
   // (2-4 KB) instead of four, the per-copy issue cost being the limit there
   if (g.fmt == SD_KV_HALF && g.hc <= 2 && tuning().attn_rps8) return 8;
+  // quantized shards of <= 2 kv heads (128-256 B int8 positions, half that
+  // int4): the ten copies per stage bound them at every width, so eight
+  // positions per copy there too
+  if (kv_quantized(g.fmt) && g.hc <= 2 && tuning().attn_rps8) return 8;
   // int8: quads. With the value product on integer tensor cores (IV) the
   // consumers keep up and the copy count is the limit: 0.448 -> 0.351 ms per
   // C5 layer with quads (0.975 of the copy peak); with fp16 values (G = 8) quads
@@ -1123,7 +1134,14 @@ size_t attention_mma_smem(const KvGeom& g, int* stage_region, int* sc_region, in
 }
 
 template <int G>
-void (*pick_mma(bool i8, bool i4, bool quad, bool im, bool iv))(const AttnArgs) {
+void (*pick_mma(bool i8, bool i4, bool quad, bool octet, bool im, bool iv))(const AttnArgs) {
+  if (octet) {  // quantized shards of 1-2 kv heads: eight positions per copy
+    if constexpr (G <= 4) {
+      if (iv && im) return i4 ? attn_mma_kernel<G, SD_KV_INT4, 8, true, true> : attn_mma_kernel<G, SD_KV_INT8, 8, true, true>;
+    }
+    if (i4) return im ? attn_mma_kernel<G, SD_KV_INT4, 8, true> : attn_mma_kernel<G, SD_KV_INT4, 8>;
+    return im ? attn_mma_kernel<G, SD_KV_INT8, 8, true> : attn_mma_kernel<G, SD_KV_INT8, 8>;
+  }
   if constexpr (G <= 4) {  // the integer value product (scores on integer tensor cores too)
     if (i4 && iv && im) return attn_mma_kernel<G, SD_KV_INT4, 4, true, true>;
     if (i8 && iv && im) return quad ? attn_mma_kernel<G, SD_KV_INT8, 4, true, true> : attn_mma_kernel<G, SD_KV_INT8, 2, true, true>;
@@ -1156,9 +1174,9 @@ void launch_attention_mma(const AttnArgs& a, int grid, size_t smem, cudaStream_t
     }
   } else {
     switch (a.G) {
-      case 2: fn = pick_mma<2>(i8, i4, quad, im, iv); break;
-      case 4: fn = pick_mma<4>(i8, i4, quad, im, iv); break;
-      case 8: fn = pick_mma<8>(i8, i4, quad, im, iv); break;
+      case 2: fn = pick_mma<2>(i8, i4, quad, octet, im, iv); break;
+      case 4: fn = pick_mma<4>(i8, i4, quad, octet, im, iv); break;
+      case 8: fn = pick_mma<8>(i8, i4, quad, octet, im, iv); break;
       default: fail(SD_ERR_INTERNAL, "attention_mma: unsupported group size");
     }
   }

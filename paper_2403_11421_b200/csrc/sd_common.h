@@ -89,7 +89,7 @@ struct Tuning {
   int attn_l2_prefetch = 0;  // the attention prefetches the W_o weights into L2 at its end
   int attn_max_stages = 0;   // tensor-core attention ring depth (0: the per-format default)
   int attn_imma = 1;          // int8 / int4 KV: scores on integer tensor cores (q as byte limbs)
-  int attn_rps8 = 1;          // fp16 shards of <= 2 kv heads copy 8 positions at a time (set when a store is built)
+  int attn_rps8 = 1;          // shards of <= 2 kv heads copy 8 positions at a time (set when a store is built)
   int attn_ivalue = 1;        // int8 / int4 KV, G <= 4, with attn_imma: the value product on integer tensor cores
                               // too; > 1 also forces its int32 -> fp32 flush every that many stages (tests)
 };

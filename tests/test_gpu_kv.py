@@ -197,10 +197,11 @@ def test_gqa_tensor_core_head_slices(sd, oracle, fmt, h0, hc, stages, rps, iv):
     default) is rounded to a multiple of those 8/hc position classes: with
     fewer ring slots than classes a class's parity wait could pass on a
     slot's previous fill (a stage not yet landed) and the kernel hung.
-    fp16 shards of 1-2 heads copy 8 positions at a time (attn_rps8 = 1) or
-    4 (0). Ring depth and slot layout are fixed when the store is built."""
-    if rps != 1 and (fmt != "half" or hc > 2):
-        pytest.skip("copy width variants apply to fp16 shards of 1-2 kv heads")
+    Shards of 1-2 heads copy 8 positions at a time (attn_rps8 = 1) or 4
+    (0), in every format. Ring depth and slot layout are fixed when the
+    store is built."""
+    if rps != 1 and hc > 2:
+        pytest.skip("copy width variants apply to shards of 1-2 kv heads")
     if iv and fmt == "half":
         pytest.skip("the integer value product: quantized KV")
     G = 4
