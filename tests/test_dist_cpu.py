@@ -17,6 +17,19 @@ def _free_port():
     return p
 
 
+def _spawn(fn, args, nprocs, **kw):
+    """mp.spawn whose rendezvous port (args[1]) is drawn again when another
+    process took it between _free_port() and the bind (EADDRINUSE)."""
+    import torch.multiprocessing as mp
+    for attempt in range(3):
+        try:
+            return mp.spawn(fn, args=args, nprocs=nprocs, **kw)
+        except Exception as e:  # ProcessRaisedException carrying the rank's DistNetworkError
+            if "EADDRINUSE" not in str(e) or attempt == 2:
+                raise
+            args = (args[0], _free_port()) + tuple(args[2:])
+
+
 def _affinity_homes(world, seqs, oracle):
     """Restatement of the balanced shard-affine home assignment
     (dist.cpp assign_homes): quotas floor/ceil(B / world), rows fill their
@@ -200,7 +213,7 @@ def test_gloo_two_ranks_equal_monolithic(oracle, tmp_path, s_ranks):
     import pickle
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
-    mp.spawn(_gloo_worker, args=(2, _free_port(), s_ranks, out), nprocs=2, join=True)
+    _spawn(_gloo_worker, args=(2, _free_port(), s_ranks, out), nprocs=2, join=True)
     rows = pickle.load(open(out, "rb"))
     # monolithic oracle over the same batch and steps
     spec = oracle.make_spec(2, 64, 4, 256, 128)

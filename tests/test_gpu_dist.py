@@ -28,6 +28,19 @@ def _free_port():
     return p
 
 
+def _spawn(fn, args, nprocs, **kw):
+    """mp.spawn whose rendezvous port (args[1]) is drawn again when another
+    process took it between _free_port() and the bind (EADDRINUSE)."""
+    import torch.multiprocessing as mp
+    for attempt in range(3):
+        try:
+            return mp.spawn(fn, args=args, nprocs=nprocs, **kw)
+        except Exception as e:  # ProcessRaisedException carrying the rank's DistNetworkError
+            if "EADDRINUSE" not in str(e) or attempt == 2:
+                raise
+            args = (args[0], _free_port()) + tuple(args[2:])
+
+
 TOY = (2, 64, 4, 256, 128)
 
 
@@ -92,7 +105,7 @@ def test_two_gpu_distributed_equals_monolithic(oracle, tmp_path, s_ranks, cfg, e
     back into the S-rank's rows."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode, False, pipeline), nprocs=2,
+    _spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, exchange, shard_mode, False, pipeline), nprocs=2,
              join=True)
     _check_rows(oracle, out, cfg)
 
@@ -195,7 +208,7 @@ def test_two_gpu_fused_exchange_is_bitwise_equal(tmp_path, s_ranks):
     bf16 S-Part's relative precision."""
     import torch.multiprocessing as mp
     out = str(tmp_path / "fused.txt")
-    mp.spawn(_fused_worker, args=(2, _free_port(), out, s_ranks), nprocs=2, join=True)
+    _spawn(_fused_worker, args=(2, _free_port(), out, s_ranks), nprocs=2, join=True)
     assert open(out).read() == "ok"
 
 
@@ -215,7 +228,7 @@ def test_two_ranks_one_device_distributed_equals_monolithic(oracle, tmp_path, s_
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
     cfg = (8, 16, 4, 0)
-    mp.spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, pipeline),
+    _spawn(_worker, args=(2, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, pipeline),
              nprocs=2, join=True)
     left = _check_rows(oracle, out, cfg)
     assert left == [(0, 0), (0, 0)]
@@ -233,7 +246,7 @@ def test_four_ranks_one_device_hybrid_shardmap(oracle, tmp_path, s_ranks):
     out = str(tmp_path / "rows.pkl")
     cfg = (8, 12, 4, 0)
     spec_args = (2, 64, 2, 256, 128)
-    mp.spawn(_worker, args=(4, _free_port(), s_ranks, cfg, out, "p2p-one-device", "hybrid", True, False, spec_args),
+    _spawn(_worker, args=(4, _free_port(), s_ranks, cfg, out, "p2p-one-device", "hybrid", True, False, spec_args),
              nprocs=4, join=True)
     left = _check_rows(oracle, out, cfg, spec_args)
     assert left == [(0, 0)] * 4
@@ -250,7 +263,7 @@ def test_eight_ranks_one_device(oracle, tmp_path, shard_mode, s_ranks):
     out = str(tmp_path / "rows.pkl")
     cfg = (16, 12, 4, 0)
     spec_args = (2, 64, 4, 256, 128)
-    mp.spawn(_worker, args=(8, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, False, spec_args),
+    _spawn(_worker, args=(8, _free_port(), s_ranks, cfg, out, "p2p-one-device", shard_mode, True, False, spec_args),
              nprocs=8, join=True)
     left = _check_rows(oracle, out, cfg, spec_args)
     assert left == [(0, 0)] * 8
@@ -265,7 +278,7 @@ def test_two_ranks_one_device_stored_kv_formats(oracle, tmp_path, fmt, shard_mod
     import torch.multiprocessing as mp
     out = str(tmp_path / "rows.pkl")
     cfg = (8, 16, 4, 0)
-    mp.spawn(_worker, args=(2, _free_port(), 2, cfg, out, "p2p-one-device", shard_mode, True, False, TOY, fmt),
+    _spawn(_worker, args=(2, _free_port(), 2, cfg, out, "p2p-one-device", shard_mode, True, False, TOY, fmt),
              nprocs=2, join=True)
     left = _check_rows(oracle, out, cfg, TOY, fmt, 1e-4)
     assert left == [(0, 0), (0, 0)]
